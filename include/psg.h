@@ -1,0 +1,207 @@
+/*
+ * psg — perfslice-gpu: the thin C ABI between the perfslice host layer and the
+ * hand-written sm_100a kernels of the trace query path (SURVEY.md §8(b) "New
+ * thin C ABI into CUDA").  Plain C types only; no exceptions cross it.
+ *
+ * Status codes are the reference's ps_status values (perfslice.h:24-40,
+ * reproduced in perfslice_gpu.h) so callers map errors exactly as they do for
+ * the reference C API; CUDA / NCCL failures map to PS_E_INTERNAL with the CUDA
+ * error string in psg_last_error() (thread-local, like capi.cpp:33).
+ *
+ * Ownership (SURVEY.md §8(b) "Ownership"): every device buffer belongs to the
+ * psg_context; results stay resident in HBM until the next query of the same
+ * kind and are copied out through the psg_get_* calls into caller-allocated
+ * host arrays (sizes are reported by the query call first — the two-call
+ * pattern).  A context is single-threaded (serialise like a ps_session) and
+ * issues all work on one CUDA stream; every call returns after its outputs
+ * are complete on that stream unless documented otherwise.
+ *
+ * Multi-GPU: one process per GPU.  Each rank opens a context on its device,
+ * loads (or generates) its own shard of traces, and joins a communicator with
+ * psg_comm_init(); queries then all-reduce only the per-shard summaries
+ * (iteration counts, per-(iteration,node) cross-rank sums, per-node outlier
+ * sums) over NCCL.  Trace events never cross GPUs.
+ */
+#ifndef PSG_H
+#define PSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "perfslice_gpu.h" /* ps_status */
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct psg_context psg_context;
+
+/* ---- context ------------------------------------------------------------ */
+const char* psg_version(void);
+const char* psg_last_error(void);
+/* stream: a cudaStream_t to issue on, or NULL for a context-owned stream. */
+ps_status psg_open(int device, void* stream, psg_context** out);
+void psg_close(psg_context* ctx);
+/* The cudaStream_t every kernel of this context is launched on. */
+void* psg_stream(psg_context* ctx);
+/* Device bytes currently held by the context (traces + results). */
+uint64_t psg_device_bytes(const psg_context* ctx);
+
+/* ---- multi-GPU (NCCL over NVLink; loaded at runtime) ------ */
+ps_status psg_comm_unique_id(uint8_t out_id[128]);
+ps_status psg_comm_init(psg_context* ctx, int nranks, int rank, const uint8_t id[128]);
+
+/* ---- calling-context tree (meta.bin contexts, store.hpp:70-75) ----------- */
+/* parent[0] must be 0xFFFFFFFF; parent[c] < c for c > 0 (topological ids). */
+ps_status psg_set_cct(psg_context* ctx, const uint32_t* parent, uint32_t n_ctx);
+
+/* ---- trace loading ------------------------------------------------------ */
+/* Replaces db_handle::read_trace_full's per-event decode (store.cpp:573-580,
+ * 678-692): `body` holds the packed 12-byte little-endian trace.db events
+ * {u64 ts, u32 ctx} of n_traces traces back to back (host memory, pinned or
+ * pageable), event_off[n_traces+1] their event offsets, profile_ids and
+ * t_end_ns the trace.db index fields.  Copies to HBM, transposes to SoA and
+ * validates (non-decreasing ts, ctx < n_ctx, t_end >= last ts); an invalid
+ * body fails with PS_E_FORMAT like validate_database (store.cpp:713-764). */
+ps_status psg_load_traces_aos(psg_context* ctx, const void* body, uint64_t n_events,
+                              const uint64_t* event_off, const uint32_t* profile_ids,
+                              const uint64_t* t_end_ns, uint32_t n_traces);
+/* The mmap reader path: opens <dir>/meta.bin + trace.db (format store.hpp:5-23)
+ * and loads the traces whose profile id is listed (NULL = every trace),
+ * setting the CCT and the rank->host mapping from meta.bin as well. */
+ps_status psg_load_trace_db(psg_context* ctx, const char* dir, const uint32_t* pids,
+                            uint32_t n_pids);
+
+/* Device synthetic generator: byte-identical to the reference
+ * synthgen::generate_iterative_scenario (synthgen.cpp:146-246) for ranks
+ * [rank_lo, rank_hi) of an n_ranks scenario (the xorshift64* stream of
+ * util.hpp:18-42 is jumped ahead on the GPU).  spread is
+ * [n_kernels][n_ranks] (spread_rank_stride = n_ranks) or one shared
+ * [n_ranks] ladder (spread_rank_stride = 0 → index by rank only); NULL means
+ * factor 1.0.  Also installs the scenario's CCT. */
+typedef struct psg_iter_scenario {
+  uint32_t n_ranks;
+  uint32_t n_iterations;
+  uint32_t n_kernels;
+  const double* mean_time_s;   /* [n_kernels] */
+  const double* jitter_frac;   /* [n_kernels] */
+  const double* spread;        /* see above, may be NULL */
+  uint64_t spread_kernel_stride; /* 0: the same ladder for every kernel */
+  double copy_segment_s;
+  uint64_t seed;
+} psg_iter_scenario;
+ps_status psg_generate_iterative(psg_context* ctx, const psg_iter_scenario* s,
+                                 uint32_t rank_lo, uint32_t rank_hi);
+
+/* Rank -> node (hostname) mapping for node_correlate / topology: node_of_trace
+ * is indexed by loaded-trace position; rack/chassis per node are the parsed
+ * x<rack>c<chassis>... coordinates (topology.cpp:33-46). */
+ps_status psg_set_nodes(psg_context* ctx, const uint32_t* node_of_trace, uint32_t n_nodes,
+                        const uint32_t* node_rack, const uint32_t* node_chassis);
+
+/* Loaded shard shape. */
+typedef struct psg_shard_info {
+  uint32_t n_traces;
+  uint32_t n_ctx;
+  uint64_t n_events;
+  uint64_t t_min;      /* min first timestamp */
+  uint64_t t_max;      /* max t_end */
+} psg_shard_info;
+ps_status psg_shard(psg_context* ctx, psg_shard_info* out);
+/* Copies the loaded SoA back (tests): ts[n_events], ctx[n_events], event_off[n+1],
+ * t_end[n], profile_ids[n]; any pointer may be NULL. */
+ps_status psg_get_traces(psg_context* ctx, uint64_t* ts, uint32_t* ctx_ids, uint64_t* event_off,
+                         uint64_t* t_end, uint32_t* profile_ids);
+
+/* ---- query ------------------------------------------------------------- */
+enum {
+  PSG_Q_WINDOW = 1u << 0,      /* (1)+(2): window filter + per-(trace,ctx) aggregates */
+  PSG_Q_CUBE = 1u << 1,        /* (3): iteration detection + trace x iteration x node cube */
+  PSG_Q_STATS = 1u << 2,       /* cross-rank savings / CV over the cube (needs CUBE) */
+  PSG_Q_OUTLIERS = 1u << 3,    /* (4): balance ratios, node means, z-score / top-k, topology (needs WINDOW) */
+  PSG_Q_NO_CUBE_STORE = 1u << 8, /* stream cube rows into STATS without materialising them */
+  PSG_Q_CLAMP_TEND = 1u << 9,    /* window end = min(t1, trace t_end) per trace: whole-trace
+                                    integration equals the trace's profile record exactly */
+  PSG_Q_ALL = PSG_Q_WINDOW | PSG_Q_CUBE | PSG_Q_STATS | PSG_Q_OUTLIERS
+};
+
+typedef struct psg_query_spec {
+  uint32_t flags;
+  uint64_t t0_ns, t1_ns;         /* window [t0, t1); t0 > t1 is PS_E_INVALID_ARGUMENT */
+  uint32_t anchor_ctx;           /* explicit anchor (itermodel anchor_policy::explicit_ctx) */
+  /* outliers: candidate call-site contexts (the worst balance ratio wins,
+   * workflows.cpp:442-459), then node means of its per-rank window-inclusive
+   * time, z-scores, and the top-k (value desc, node id asc) among z >= z_min
+   * (k = 0: no cap). */
+  const uint32_t* site_ctx;
+  uint32_t n_sites;
+  uint32_t top_k;
+  double z_min;
+} psg_query_spec;
+
+typedef struct psg_query_info {
+  /* window */
+  uint64_t n_window_groups;      /* rows of the group_aggregate result (count > 0) */
+  uint64_t n_window_rows;        /* events with t0 <= ts < t1 */
+  /* cube (global over all ranks where noted) */
+  uint32_t n_nodes;              /* anchor subtree size */
+  uint32_t n_kept;               /* local traces with >= 1 iteration */
+  uint32_t n_skipped;            /* local traces without iterations */
+  uint32_t min_iterations;       /* global ordinal intersection (diagnostics use it) */
+  uint32_t n_kept_global;
+  uint64_t n_cells;              /* local cube cells (sum iter_counts * n_nodes) */
+  uint32_t n_leaves;
+  /* outliers */
+  uint32_t worst_site;           /* ctx id */
+  double worst_ratio;
+  uint32_t n_outliers;
+  uint32_t n_racks;
+  /* timing of the last query on the device (CUDA events on psg_stream) */
+  float ms_total;
+  float ms_main;                 /* the fused window+cube kernel */
+} psg_query_info;
+
+ps_status psg_query(psg_context* ctx, const psg_query_spec* spec, psg_query_info* info);
+
+/* ---- result copy-out (caller-allocated host arrays; NULL skips a column) -- */
+/* Dense per-(trace, ctx) window aggregates, trace-major [n_traces][n_ctx]:
+ * count, sum/min/max of clipped row durations (ns), mean = sum/count,
+ * excl/incl = time-integrated exclusive/inclusive ns incl. the carry-in
+ * segment (itermodel::rematerialize over [t0,t1)). */
+ps_status psg_get_window(psg_context* ctx, uint64_t* count, int64_t* sum, int64_t* min,
+                         int64_t* max, double* mean, int64_t* excl, int64_t* incl);
+/* Per trace carry-in (store.cpp:667-670): has (0/1), ts, ctx. */
+ps_status psg_get_carry(psg_context* ctx, uint8_t* has, uint64_t* ts, uint32_t* ctx_ids);
+/* tri_model (itermodel.hpp:78-116): node_ids[n_nodes], per loaded trace
+ * iter_counts[n_traces] (0 = skipped), block_offset[n_kept], dense cube
+ * incl/excl[n_cells] (iteration-major, node-minor per kept trace, kept traces
+ * in load order) and gap rows [n_kept][n_nodes]. */
+ps_status psg_get_cube(psg_context* ctx, uint32_t* node_ids, uint32_t* iter_counts,
+                       uint64_t* block_offset, int64_t* incl, int64_t* excl,
+                       int64_t* gap_incl, int64_t* gap_excl);
+/* savings_report / iteration_cv_report per subtree leaf (diagnostics.cpp:100-158):
+ * leaves[n_leaves]; savings rows [n_leaves][4] = avg_mean_s, avg_max_s,
+ * savings_per_iter_s, total_reduction_s; summary[4] = n_iterations,
+ * total_savings_s, total_time_s (as given), speedup_frac; cv [n_leaves][2] =
+ * across, within; cv_ok[n_leaves] (0 = the reference would raise). */
+ps_status psg_get_stats(psg_context* ctx, double total_time_s, uint32_t* leaves, double* savings,
+                        double* summary, double* cv, int32_t* cv_ok);
+/* Outliers: per site balance ratio [n_sites]; node means [n_nodes] (s);
+ * node z-scores; selected node ids [n_outliers] (value desc, id asc); topology
+ * rows [n_racks][3] = rack, affected nodes, n_chassis and chassis masks per
+ * rack: affected [n_racks], fully affected [n_racks] (bit c = chassis c). */
+ps_status psg_get_outliers(psg_context* ctx, double* site_ratio, double* node_mean, double* node_z,
+                           uint32_t* selected, uint32_t* rack_rows, uint64_t* chassis_mask,
+                           uint64_t* full_mask);
+
+/* ingest::ingest_traces (ingest.cpp:178-208) on the device: the events with
+ * t0 <= ts < t1 of every loaded trace in load order, as SoA rows, plus the
+ * carry-ins.  Call with NULL arrays to get *n_rows, then again to copy. */
+ps_status psg_window_rows(psg_context* ctx, uint64_t t0_ns, uint64_t t1_ns, uint64_t* n_rows,
+                          uint32_t* row_pid, uint64_t* row_ts, uint32_t* row_ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSG_H */

@@ -1,0 +1,287 @@
+"""TEST INFRASTRUCTURE ONLY (checker, never the thing measured or shipped).
+
+Python bindings of
+  * oracle/liboracle.so       — the CPU restatement (oracle/psg_oracle.c);
+  * oracle/_ref/libps_refharness.so — the UNMODIFIED reference core plus our
+    harness (oracle/ref_harness.cpp), built by oracle/build_ref.sh.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_DIR = os.path.join(HERE, "_ref")
+REF_SO = os.path.join(REF_DIR, "libps_refharness.so")
+
+U8P, U32P, U64P = C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+I32P, I64P, F64P = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_double)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(C.POINTER(t))
+
+
+def build_oracle() -> str:
+    if not os.path.exists(ORACLE_SO) or os.path.getmtime(ORACLE_SO) < os.path.getmtime(
+            os.path.join(HERE, "psg_oracle.c")):
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return ORACLE_SO
+
+
+_orc = None
+
+
+def orc():
+    global _orc
+    if _orc is None:
+        lib = C.CDLL(build_oracle())
+        lib.orc_window.restype = None
+        lib.orc_window.argtypes = [U64P, U64P, U32P, C.c_uint32, U32P, C.c_uint32, C.c_uint64,
+                                   C.c_uint64, U64P, I64P, I64P, I64P, F64P, I64P, I64P, U8P, U64P,
+                                   U32P]
+        lib.orc_iter_counts.restype = None
+        lib.orc_iter_counts.argtypes = [U64P, U64P, U32P, U64P, C.c_uint32, U32P, C.c_uint32,
+                                        C.c_uint32, U32P]
+        lib.orc_subtree.restype = C.c_uint32
+        lib.orc_subtree.argtypes = [U32P, C.c_uint32, C.c_uint32, U32P]
+        lib.orc_cube.restype = None
+        lib.orc_cube.argtypes = [U64P, U64P, U32P, U64P, C.c_uint32, U32P, C.c_uint32, C.c_uint32,
+                                 I64P, I64P, I64P, I64P]
+        lib.orc_node_stats.restype = None
+        lib.orc_node_stats.argtypes = [I64P, U64P, U32P, C.c_uint32, C.c_uint32, C.c_uint32, F64P,
+                                       C.POINTER(C.c_int)]
+        lib.orc_outliers.restype = C.c_uint32
+        lib.orc_outliers.argtypes = [I64P, C.c_uint32, C.c_uint32, U32P, C.c_uint32, C.c_uint32,
+                                     C.c_double, F64P, U32P, F64P, F64P, U32P]
+        _orc = lib
+    return _orc
+
+
+# ---- oracle restatement wrappers -------------------------------------------
+
+def window(tr: dict, parent, t0: int, t1: int) -> dict:
+    n = len(tr["off"]) - 1
+    parent = np.ascontiguousarray(parent, np.uint32)
+    nc = len(parent)
+    out = {k: np.zeros((n, nc), dt) for k, dt in [
+        ("count", np.uint64), ("sum", np.int64), ("min", np.int64), ("max", np.int64),
+        ("mean", np.float64), ("excl", np.int64), ("incl", np.int64)]}
+    has, cts, cctx = np.zeros(n, np.uint8), np.zeros(n, np.uint64), np.zeros(n, np.uint32)
+    orc().orc_window(_p(tr["off"], C.c_uint64), _p(tr["ts"], C.c_uint64), _p(tr["ctx"], C.c_uint32),
+                     n, _p(parent, C.c_uint32), nc, t0, t1, _p(out["count"], C.c_uint64),
+                     _p(out["sum"], C.c_int64), _p(out["min"], C.c_int64), _p(out["max"], C.c_int64),
+                     _p(out["mean"], C.c_double), _p(out["excl"], C.c_int64),
+                     _p(out["incl"], C.c_int64), _p(has, C.c_uint8), _p(cts, C.c_uint64),
+                     _p(cctx, C.c_uint32))
+    out["carry"] = {"has": has, "ts": cts, "ctx": cctx}
+    return out
+
+
+def cube(tr: dict, parent, anchor: int) -> dict:
+    n = len(tr["off"]) - 1
+    parent = np.ascontiguousarray(parent, np.uint32)
+    nc = len(parent)
+    ic = np.zeros(n, np.uint32)
+    args = (_p(tr["off"], C.c_uint64), _p(tr["ts"], C.c_uint64), _p(tr["ctx"], C.c_uint32),
+            _p(tr["t_end"], C.c_uint64), n, _p(parent, C.c_uint32), nc, anchor)
+    orc().orc_iter_counts(*args, _p(ic, C.c_uint32))
+    nn = orc().orc_subtree(_p(parent, C.c_uint32), nc, anchor, None)
+    node_ids = np.zeros(nn, np.uint32)
+    orc().orc_subtree(_p(parent, C.c_uint32), nc, anchor, _p(node_ids, C.c_uint32))
+    kept = ic[ic > 0]
+    cells = int(kept.astype(np.uint64).sum()) * nn
+    incl, excl = np.zeros(cells, np.int64), np.zeros(cells, np.int64)
+    gi, ge = np.zeros(len(kept) * nn, np.int64), np.zeros(len(kept) * nn, np.int64)
+    orc().orc_cube(*args, _p(incl, C.c_int64), _p(excl, C.c_int64), _p(gi, C.c_int64),
+                   _p(ge, C.c_int64))
+    bo = np.zeros(len(kept), np.uint64)
+    if len(kept):
+        bo[1:] = np.cumsum(kept.astype(np.uint64) * nn)[:-1]
+    return {"node_ids": node_ids, "iter_counts": ic, "block_offset": bo, "incl": incl,
+            "excl": excl, "gap_incl": gi, "gap_excl": ge}
+
+
+def node_stats(cb: dict, npos: int) -> tuple[np.ndarray, bool]:
+    kept = cb["iter_counts"][cb["iter_counts"] > 0].astype(np.uint32)
+    nn = len(cb["node_ids"])
+    out = np.zeros(6, np.float64)
+    ok = C.c_int(0)
+    bo = np.ascontiguousarray(cb["block_offset"], np.uint64)
+    orc().orc_node_stats(_p(cb["incl"], C.c_int64), _p(bo, C.c_uint64), _p(kept, C.c_uint32),
+                         len(kept), nn, npos, _p(out, C.c_double), C.byref(ok))
+    return out, bool(ok.value)
+
+
+def outliers(values: np.ndarray, node_of_rank, n_nodes: int, top_k: int, z_min: float) -> dict:
+    values = np.ascontiguousarray(values, np.int64)
+    ns, nr = values.shape
+    nor = np.ascontiguousarray(node_of_rank, np.uint32)
+    ratio = np.zeros(ns)
+    worst = C.c_uint32(0)
+    mean, z = np.zeros(n_nodes), np.zeros(n_nodes)
+    sel = np.zeros(n_nodes, np.uint32)
+    k = orc().orc_outliers(_p(values, C.c_int64), ns, nr, _p(nor, C.c_uint32), n_nodes, top_k,
+                           z_min, _p(ratio, C.c_double), C.byref(worst), _p(mean, C.c_double),
+                           _p(z, C.c_double), _p(sel, C.c_uint32))
+    return {"site_ratio": ratio, "worst": worst.value, "node_mean": mean, "node_z": z,
+            "selected": sel[:k]}
+
+
+# ---- the reference (oracle/_ref) --------------------------------------------
+
+_ref = None
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise RuntimeError(f"{REF_SO} missing: run oracle/build_ref.sh where /root/reference exists")
+        lib = C.CDLL(REF_SO)
+        lib.refh_last_error.restype = C.c_char_p
+        lib.refh_free.argtypes = [C.c_void_p]
+        lib.refh_default_jobs.restype = C.c_uint
+        lib.refh_generate.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.refh_window.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint, C.c_char_p, C.c_int]
+        lib.refh_trimodel.argtypes = [C.c_char_p, C.c_int64, C.c_uint, C.c_double, C.c_char_p]
+        lib.refh_iterations_report.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.c_int, C.c_uint,
+                                               C.POINTER(C.c_void_p)]
+        lib.refh_congestion_report.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint,
+                                               C.c_double, C.c_double, C.c_int, C.c_uint,
+                                               C.POINTER(C.c_void_p)]
+        for f in ("refh_time_window", "refh_time_trimodel", "refh_time_query", "refh_time_congestion"):
+            getattr(lib, f).restype = C.c_double
+        lib.refh_time_window.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint, C.c_uint]
+        lib.refh_time_trimodel.argtypes = [C.c_char_p, C.c_int64, C.c_uint, C.c_uint]
+        lib.refh_time_query.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int64, C.c_uint,
+                                        C.c_uint]
+        lib.refh_time_congestion.argtypes = [C.c_char_p, C.c_uint, C.c_uint]
+        _ref = lib
+    return _ref
+
+
+def _chk(rc):
+    if rc != 0:
+        raise RuntimeError(f"reference harness error {rc}: {ref().refh_last_error().decode()}")
+
+
+def _take(ptr: C.c_void_p) -> str:
+    s = C.cast(ptr, C.c_char_p).value.decode()
+    ref().refh_free(ptr)
+    return s
+
+
+def ref_generate(cfg: dict, out_dir: str) -> dict:
+    """workflows::generate_database: writes meta.bin/profile.db/trace.db/truth.json."""
+    p = C.c_void_p()
+    _chk(ref().refh_generate(json.dumps(cfg).encode(), out_dir.encode(), C.byref(p)))
+    return json.loads(_take(p))
+
+
+def _load_bins(d: str, spec: dict) -> dict:
+    return {k: np.fromfile(os.path.join(d, k + ".bin"), dtype=dt) for k, dt in spec.items()}
+
+
+def ref_window(db: str, t0: int, t1: int, jobs: int = 1, rows: bool = False) -> dict:
+    with tempfile.TemporaryDirectory() as d:
+        _chk(ref().refh_window(db.encode(), t0, t1, jobs, d.encode(), int(rows)))
+        spec = {"wa_pid": np.uint64, "wa_ctx": np.uint64, "wa_sum": np.int64, "wa_min": np.int64,
+                "wa_max": np.int64, "wa_mean": np.float64, "wa_count": np.uint64,
+                "carry_pid": np.uint32, "carry_has": np.uint8, "carry_ts": np.uint64,
+                "carry_ctx": np.uint32, "rm_pid": np.uint32, "rm_ctx": np.uint32,
+                "rm_incl": np.int64, "rm_excl": np.int64}
+        if rows:
+            spec.update({"rows_pid": np.uint32, "rows_ts": np.uint64, "rows_ctx": np.uint32})
+        return _load_bins(d, spec)
+
+
+def ref_trimodel(db: str, anchor: int, jobs: int = 1, total_time: float = 0.0) -> dict:
+    with tempfile.TemporaryDirectory() as d:
+        _chk(ref().refh_trimodel(db.encode(), anchor, jobs, total_time, d.encode()))
+        return _load_bins(d, {
+            "anchor": np.uint32, "node_ids": np.uint32, "trace_ids": np.uint32,
+            "iter_counts": np.uint32, "skipped": np.uint32, "block_offset": np.uint64,
+            "incl": np.int64, "excl": np.int64, "gap_incl": np.int64, "gap_excl": np.int64,
+            "leaves": np.uint32, "savings": np.float64, "savings_summary": np.float64,
+            "savings_ok": np.int32, "cv": np.float64, "cv_ok": np.int32})
+
+
+def ref_iterations_report(db: str, anchor: str = "auto", total_time: float = 0.0,
+                          json_fmt: bool = True, jobs: int = 1) -> str:
+    p = C.c_void_p()
+    _chk(ref().refh_iterations_report(db.encode(), anchor.encode(), total_time, int(json_fmt), jobs,
+                                      C.byref(p)))
+    return _take(p)
+
+
+def ref_congestion_report(db: str, glob: str = "MPI_*", method: str = "dbscan", k: int = 2,
+                          eps: float = 0.0, min_share: float = 0.01, json_fmt: bool = True,
+                          jobs: int = 1) -> str:
+    p = C.c_void_p()
+    _chk(ref().refh_congestion_report(db.encode(), glob.encode(), method.encode(), k, eps, min_share,
+                                      int(json_fmt), jobs, C.byref(p)))
+    return _take(p)
+
+
+def read_trace_db(db: str) -> dict:
+    """Tiny independent reader of trace.db (format store.hpp:15-18) for tests."""
+    raw = np.fromfile(os.path.join(db, "trace.db"), dtype=np.uint8)
+    n = int(raw[8:12].view(np.uint32)[0])
+    idx = raw[12:12 + 36 * n].reshape(n, 36)
+    pid = idx[:, 0:4].copy().view(np.uint32).ravel()
+    off = idx[:, 4:12].copy().view(np.uint64).ravel()
+    cnt = idx[:, 12:20].copy().view(np.uint64).ravel()
+    t_end = idx[:, 28:36].copy().view(np.uint64).ravel()
+    body_start = 12 + 36 * n
+    total = int(cnt.sum())
+    body = raw[body_start:body_start + 12 * total].reshape(total, 12) if total else np.zeros((0, 12), np.uint8)
+    assert n == 0 or int(off[0]) == body_start
+    ts = body[:, 0:8].copy().view(np.uint64).ravel()
+    cx = body[:, 8:12].copy().view(np.uint32).ravel()
+    offs = np.zeros(n + 1, np.uint64)
+    offs[1:] = np.cumsum(cnt)
+    return {"ts": ts, "ctx": cx, "off": offs, "t_end": t_end, "pid": pid,
+            "body": raw[body_start:body_start + 12 * total]}
+
+
+def read_meta(db: str) -> dict:
+    """meta.bin (store.hpp:8-12): contexts (parent, kind, name) and profiles."""
+    b = open(os.path.join(db, "meta.bin"), "rb").read()
+    pos = 8
+
+    def u(fmt, n):
+        nonlocal pos
+        v = np.frombuffer(b, dtype=fmt, count=1, offset=pos)[0]
+        pos += n
+        return int(v)
+
+    def s():
+        nonlocal pos
+        ln = u(np.uint16, 2)
+        r = b[pos:pos + ln].decode()
+        pos += ln
+        return r
+
+    for _ in range(u(np.uint32, 4)):
+        u(np.uint32, 4); u(np.uint8, 1); s(); s()
+    profiles = []
+    for _ in range(u(np.uint32, 4)):
+        pid = u(np.uint32, 4); rank = u(np.int32, 4); u(np.int32, 4); host = s(); u(np.uint64, 8)
+        profiles.append((pid, rank, host))
+    parent, names = [], []
+    for _ in range(u(np.uint32, 4)):
+        u(np.uint32, 4); parent.append(u(np.uint32, 4)); u(np.uint8, 1); names.append(s())
+    return {"parent": np.array(parent, np.uint32), "names": names, "profiles": profiles}

@@ -1,0 +1,237 @@
+"""perfslice-b200: the reference's trace query path (window filter, segmented
+aggregates, iteration cube, z-score/top-k outliers) on hand-written sm_100a
+kernels behind a C ABI (include/psg.h).
+
+This module is the Python face of that ABI (ctypes); every computation runs
+in libpsg.so on the GPU.  Importing it does not need a GPU; opening a Context
+does, and fails loudly without one.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import (PsgError, Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_NO_CUBE_STORE, Q_OUTLIERS, Q_STATS, Q_WINDOW,
+                   check, load)
+from . import scenarios
+
+__all__ = ["Context", "PsgError", "Q_ALL", "Q_CLAMP_TEND", "Q_CUBE", "Q_NO_CUBE_STORE", "Q_OUTLIERS", "Q_STATS",
+           "Q_WINDOW", "load", "scenarios"]
+
+
+def _ptr(a: Optional[np.ndarray], ctype):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class Context:
+    """One psg_context: one GPU, one stream, one shard of traces."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self.lib = load()
+        h = C.c_void_p()
+        check(self.lib.psg_open(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.h = h
+        self.info = None
+
+    # -- lifetime ------------------------------------------------------------
+    def close(self):
+        if self.h:
+            self.lib.psg_close(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.psg_stream(self.h) or 0)
+
+    # -- multi-GPU -----------------------------------------------------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(load().psg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(self.lib.psg_comm_init(self.h, nranks, rank, buf))
+
+    # -- loading -------------------------------------------------------------
+    def set_cct(self, parent):
+        p = np.ascontiguousarray(parent, dtype=np.uint32)
+        check(self.lib.psg_set_cct(self.h, _ptr(p, C.c_uint32), len(p)))
+
+    def load_aos(self, body, event_off, profile_ids, t_end):
+        """body: uint8 array (or an int host address) of packed 12-byte events."""
+        off = np.ascontiguousarray(event_off, dtype=np.uint64)
+        pid = np.ascontiguousarray(profile_ids, dtype=np.uint32)
+        te = np.ascontiguousarray(t_end, dtype=np.uint64)
+        n_ev = int(off[-1])
+        addr = body if isinstance(body, int) else (body.ctypes.data if n_ev else 0)
+        check(self.lib.psg_load_traces_aos(self.h, C.c_void_p(addr), n_ev, _ptr(off, C.c_uint64),
+                                           _ptr(pid, C.c_uint32), _ptr(te, C.c_uint64), len(pid)))
+
+    def load_trace_db(self, path: str, pids=None):
+        if pids is None:
+            check(self.lib.psg_load_trace_db(self.h, path.encode(), None, 0))
+        else:
+            p = np.ascontiguousarray(pids, dtype=np.uint32)
+            check(self.lib.psg_load_trace_db(self.h, path.encode(), _ptr(p, C.c_uint32), len(p)))
+
+    def generate_iterative(self, cfg: dict, rank_lo: int = 0, rank_hi: Optional[int] = None):
+        mean, jit, spread, stride = scenarios.device_params(cfg)
+        s = _lib.IterScenario()
+        s.n_ranks = cfg["n_ranks"]
+        s.n_iterations = cfg["n_iterations"]
+        s.n_kernels = len(mean)
+        s.mean_time_s = _ptr(mean, C.c_double)
+        s.jitter_frac = _ptr(jit, C.c_double)
+        s.spread = _ptr(spread, C.c_double) if spread is not None else None
+        s.spread_kernel_stride = stride
+        s.copy_segment_s = cfg.get("copy_segment_s", 0.0)
+        s.seed = cfg.get("seed", 0)
+        self._keep = (mean, jit, spread)
+        check(self.lib.psg_generate_iterative(self.h, C.byref(s), rank_lo,
+                                              cfg["n_ranks"] if rank_hi is None else rank_hi))
+
+    def set_nodes(self, node_of_trace, n_nodes, rack=None, chassis=None):
+        nt = np.ascontiguousarray(node_of_trace, dtype=np.uint32)
+        r = None if rack is None else np.ascontiguousarray(rack, dtype=np.uint32)
+        c = None if chassis is None else np.ascontiguousarray(chassis, dtype=np.uint32)
+        check(self.lib.psg_set_nodes(self.h, _ptr(nt, C.c_uint32), n_nodes, _ptr(r, C.c_uint32),
+                                     _ptr(c, C.c_uint32)))
+
+    def shard(self) -> dict:
+        s = _lib.ShardInfo()
+        check(self.lib.psg_shard(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def traces(self):
+        sh = self.shard()
+        n, e = sh["n_traces"], sh["n_events"]
+        ts = np.empty(e, np.uint64)
+        cx = np.empty(e, np.uint32)
+        off = np.empty(n + 1, np.uint64)
+        te = np.empty(n, np.uint64)
+        pid = np.empty(n, np.uint32)
+        check(self.lib.psg_get_traces(self.h, _ptr(ts, C.c_uint64), _ptr(cx, C.c_uint32),
+                                      _ptr(off, C.c_uint64), _ptr(te, C.c_uint64),
+                                      _ptr(pid, C.c_uint32)))
+        return {"ts": ts, "ctx": cx, "off": off, "t_end": te, "pid": pid}
+
+    # -- query -----------------------------------------------------------------
+    def query(self, flags: int = Q_ALL, t0: int = 0, t1: int = 0, anchor: int = 1, sites=(),
+              top_k: int = 0, z_min: float = float("-inf")) -> dict:
+        q = _lib.QuerySpec()
+        q.flags = flags
+        q.t0_ns, q.t1_ns = t0, t1
+        q.anchor_ctx = anchor
+        self._sites = np.ascontiguousarray(sites, dtype=np.uint32)
+        q.site_ctx = _ptr(self._sites, C.c_uint32) if len(self._sites) else None
+        q.n_sites = len(self._sites)
+        q.top_k = top_k
+        q.z_min = z_min
+        info = _lib.QueryInfo()
+        check(self.lib.psg_query(self.h, C.byref(q), C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in info._fields_}
+        self._flags = flags
+        return self.info
+
+    def window(self) -> dict:
+        sh = self.shard()
+        shape = (sh["n_traces"], sh["n_ctx"])
+        out = {k: np.empty(shape, dt) for k, dt in [
+            ("count", np.uint64), ("sum", np.int64), ("min", np.int64), ("max", np.int64),
+            ("mean", np.float64), ("excl", np.int64), ("incl", np.int64)]}
+        check(self.lib.psg_get_window(
+            self.h, _ptr(out["count"], C.c_uint64), _ptr(out["sum"], C.c_int64),
+            _ptr(out["min"], C.c_int64), _ptr(out["max"], C.c_int64),
+            _ptr(out["mean"], C.c_double), _ptr(out["excl"], C.c_int64),
+            _ptr(out["incl"], C.c_int64)))
+        return out
+
+    def carry(self) -> dict:
+        n = self.shard()["n_traces"]
+        has = np.empty(n, np.uint8)
+        ts = np.empty(n, np.uint64)
+        cx = np.empty(n, np.uint32)
+        check(self.lib.psg_get_carry(self.h, _ptr(has, C.c_uint8), _ptr(ts, C.c_uint64),
+                                     _ptr(cx, C.c_uint32)))
+        return {"has": has, "ts": ts, "ctx": cx}
+
+    def cube(self, with_cells: bool = True) -> dict:
+        info = self.info
+        n = self.shard()["n_traces"]
+        nn, kept, cells = info["n_nodes"], info["n_kept"], info["n_cells"]
+        node_ids = np.empty(nn, np.uint32)
+        ic = np.empty(n, np.uint32)
+        bo = np.empty(kept, np.uint64)
+        incl = np.empty(cells, np.int64) if with_cells else None
+        excl = np.empty(cells, np.int64) if with_cells else None
+        gi = np.empty(kept * nn, np.int64)
+        ge = np.empty(kept * nn, np.int64)
+        check(self.lib.psg_get_cube(self.h, _ptr(node_ids, C.c_uint32), _ptr(ic, C.c_uint32),
+                                    _ptr(bo, C.c_uint64), _ptr(incl, C.c_int64),
+                                    _ptr(excl, C.c_int64), _ptr(gi, C.c_int64),
+                                    _ptr(ge, C.c_int64)))
+        return {"node_ids": node_ids, "iter_counts": ic, "block_offset": bo, "incl": incl,
+                "excl": excl, "gap_incl": gi, "gap_excl": ge}
+
+    def stats(self, total_time_s: float) -> dict:
+        nl = self.info["n_leaves"]
+        leaves = np.empty(nl, np.uint32)
+        sav = np.empty((nl, 4), np.float64)
+        summ = np.empty(4, np.float64)
+        cv = np.empty((nl, 2), np.float64)
+        ok = np.empty(nl, np.int32)
+        check(self.lib.psg_get_stats(self.h, total_time_s, _ptr(leaves, C.c_uint32),
+                                     _ptr(sav, C.c_double), _ptr(summ, C.c_double),
+                                     _ptr(cv, C.c_double), _ptr(ok, C.c_int32)))
+        return {"leaves": leaves, "savings": sav, "summary": summ, "cv": cv, "cv_ok": ok}
+
+    def outliers(self, n_nodes: int) -> dict:
+        info = self.info
+        ns = len(self._sites)
+        ratio = np.empty(ns, np.float64)
+        mean = np.empty(n_nodes, np.float64)
+        z = np.empty(n_nodes, np.float64)
+        sel = np.empty(max(1, info["n_outliers"]), np.uint32)
+        nr = info["n_racks"]
+        rows = np.empty((max(1, nr), 3), np.uint32)
+        cm = np.empty(max(1, nr), np.uint64)
+        fm = np.empty(max(1, nr), np.uint64)
+        check(self.lib.psg_get_outliers(self.h, _ptr(ratio, C.c_double), _ptr(mean, C.c_double),
+                                        _ptr(z, C.c_double), _ptr(sel, C.c_uint32),
+                                        _ptr(rows, C.c_uint32), _ptr(cm, C.c_uint64),
+                                        _ptr(fm, C.c_uint64)))
+        return {"site_ratio": ratio, "node_mean": mean, "node_z": z,
+                "selected": sel[: info["n_outliers"]], "racks": rows[:nr],
+                "chassis_mask": cm[:nr], "full_mask": fm[:nr]}
+
+    def window_rows(self, t0: int, t1: int) -> dict:
+        n = C.c_uint64()
+        check(self.lib.psg_window_rows(self.h, t0, t1, C.byref(n), None, None, None))
+        m = n.value
+        pid = np.empty(max(1, m), np.uint32)
+        ts = np.empty(max(1, m), np.uint64)
+        cx = np.empty(max(1, m), np.uint32)
+        check(self.lib.psg_window_rows(self.h, t0, t1, C.byref(n), _ptr(pid, C.c_uint32),
+                                       _ptr(ts, C.c_uint64), _ptr(cx, C.c_uint32)))
+        out = {"pid": pid[:m], "ts": ts[:m], "ctx": cx[:m]}
+        out["carry"] = self.carry()
+        return out

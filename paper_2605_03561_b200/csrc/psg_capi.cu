@@ -1,0 +1,1077 @@
+// extern "C" surface of libpsg: context lifetime, trace loading (host AoS,
+// trace.db mmap reader, device generator), the fused query, NCCL summaries,
+// and result copy-out.  Exceptions never cross the ABI: guarded() maps them
+// to ps_status with a thread-local message (the reference's firewall,
+// capi.cpp:65-80).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <numeric>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "psg_internal.h"
+#include "psg_store.h"
+
+using namespace psg;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+template <typename Fn>
+ps_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return PS_OK;
+  } catch (const failure& f) {
+    t_last_error = f.what();
+    return f.status;
+  } catch (const std::bad_alloc&) {
+    t_last_error = "out of memory";
+    return PS_E_INTERNAL;
+  } catch (const std::exception& e) {
+    t_last_error = e.what();
+    return PS_E_INTERNAL;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) fail(PS_E_INVALID_ARGUMENT, msg);
+}
+
+// ---- NCCL, resolved at runtime ---------------------------------------------
+// Loaded with dlopen so that a process which already holds torch's bundled
+// libnccl.so.2 reuses it (RTLD_NOLOAD first) instead of mixing two copies.
+struct nccl_api {
+  void* h = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+nccl_api& nccl() {
+  static nccl_api api;
+  if (api.h) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) fail(PS_E_INTERNAL, std::string("cannot load libnccl.so.2: ") + dlerror());
+  auto sym = [&](const char* n) {
+    void* p = dlsym(h, n);
+    if (!p) fail(PS_E_INTERNAL, std::string("libnccl lacks ") + n);
+    return p;
+  };
+  api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(sym("ncclGetUniqueId"));
+  api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(sym("ncclCommInitRank"));
+  api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(sym("ncclAllReduce"));
+  api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
+  api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
+  api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
+  api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+  api.h = h;
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    fail(PS_E_INTERNAL, std::string("NCCL error in ") + what + ": " + nccl().error_string(r));
+}
+
+// ---- host CCT helpers --------------------------------------------------------
+
+struct preorder {
+  std::vector<int32_t> pre, size;  // by ctx (-1 outside the requested subtree)
+  std::vector<uint32_t> order;     // ctx ids in preorder
+};
+
+// Iterative DFS over children in ascending id order.
+preorder preorder_of(const std::vector<uint32_t>& parent, uint32_t root) {
+  const uint32_t n = static_cast<uint32_t>(parent.size());
+  std::vector<std::vector<uint32_t>> kids(n);
+  for (uint32_t c = 1; c < n; ++c)
+    if (parent[c] != store::k_no_parent) kids[parent[c]].push_back(c);
+  preorder po;
+  po.pre.assign(n, -1);
+  po.size.assign(n, 0);
+  std::vector<std::pair<uint32_t, size_t>> stack{{root, 0}};
+  po.pre[root] = 0;
+  po.order.push_back(root);
+  while (!stack.empty()) {
+    auto& [node, next] = stack.back();
+    if (next < kids[node].size()) {
+      uint32_t ch = kids[node][next++];
+      po.pre[ch] = static_cast<int32_t>(po.order.size());
+      po.order.push_back(ch);
+      stack.push_back({ch, 0});
+    } else {
+      po.size[node] = static_cast<int32_t>(po.order.size()) - po.pre[node];
+      stack.pop_back();
+    }
+  }
+  return po;
+}
+
+// xorshift64* transition matrix powers M^(2^b), b = 0..63, as column vectors.
+std::vector<uint64_t> jump_matrices() {
+  auto step = [](uint64_t x) {
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    return x;
+  };
+  auto apply = [](const uint64_t* m, uint64_t x) {
+    uint64_t r = 0;
+    for (int i = 0; i < 64; ++i)
+      if ((x >> i) & 1) r ^= m[i];
+    return r;
+  };
+  std::vector<uint64_t> mats(64 * 64);
+  for (int i = 0; i < 64; ++i) mats[i] = step(1ull << i);
+  for (int b = 1; b < 64; ++b)
+    for (int i = 0; i < 64; ++i)
+      mats[64 * b + i] = apply(&mats[64 * (b - 1)], mats[64 * (b - 1) + i]);
+  return mats;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+struct psg_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // CCT
+  uint32_t n_ctx = 0;
+  std::vector<uint32_t> h_parent;
+  preorder cct_po;
+  dbuf<int32_t> d_cct_pre, d_cct_size;
+
+  // traces (SoA)
+  uint32_t n_traces = 0;
+  uint64_t n_events = 0;
+  std::vector<uint64_t> h_off, h_tend;
+  std::vector<uint32_t> h_pid;
+  dbuf<uint64_t> d_off, d_ts, d_tend;
+  dbuf<uint32_t> d_ctx, d_pid;
+  dbuf<uint8_t> d_stage;
+
+  // nodes / topology
+  uint32_t n_nodes = 0;
+  std::vector<uint32_t> h_node_of_trace, h_rack_ids;  // rack id per rack index
+  dbuf<uint32_t> d_node_of_trace, d_node_rack_idx, d_node_chassis, d_uni_cnt;
+
+  // anchor subtree (cached per anchor)
+  int64_t cached_anchor = -1;
+  uint32_t nn = 0;
+  std::vector<uint32_t> node_ids, leaves;
+  std::vector<int32_t> h_sub_pre;
+  dbuf<int32_t> d_sub_pre, d_node_pre, d_node_size;
+
+  // window results
+  bool have_window = false, have_carry = false;
+  dbuf<uint64_t> w_cnt, w_sum, w_min, w_max, w_excl, w_incl, c_ts;
+  dbuf<double> w_mean;
+  dbuf<uint8_t> c_has;
+  dbuf<uint32_t> c_ctx;
+  dbuf<unsigned long long> w_counters;  // [0] groups, [1] rows (computed on copy-out)
+
+  // cube results
+  bool have_cube = false;
+  uint32_t n_kept = 0, n_kept_global = 0, K = 0;
+  uint64_t n_cells = 0;
+  dbuf<uint32_t> iter_count, tpos;
+  dbuf<uint64_t> block_off, cube_incl, cube_excl, gap_incl, gap_excl;
+  dbuf<unsigned long long> summary;
+  dbuf<uint8_t> scratch;
+  dbuf<unsigned long long> x_acc;  // x_sum [K nn] | x_max [K nn] | x_sq [3 K nn]
+  dbuf<double> within_cv, node_out;
+  dbuf<uint8_t> within_ok;
+  bool have_stats = false;
+
+  // outliers
+  bool have_outliers = false;
+  std::vector<uint32_t> sites;
+  dbuf<uint32_t> d_sites, d_worst, d_order, d_nsel, d_rack_nodes;
+  dbuf<unsigned long long> site_acc, node_acc, rack_mask, rack_full;
+  dbuf<double> site_ratio, node_mean, node_z;
+
+  dbuf<uint64_t> jump;
+  dbuf<double> gen_params;
+  dbuf<uint64_t> gen_chunks;
+
+  ~psg_context() {
+    if (comm) nccl().comm_destroy(comm);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  trace_view view() const { return {d_off.p, d_ts.p, d_ctx.p, d_tend.p, n_traces}; }
+  void sync() { PSG_CUDA(cudaStreamSynchronize(stream)); }
+
+  template <typename T>
+  void allreduce(T* buf, size_t count, ncclDataType_t dt, ncclRedOp_t op) {
+    if (!comm || nranks <= 1 || count == 0) return;
+    nccl_check(nccl().all_reduce(buf, buf, count, dt, op, comm, stream), "ncclAllReduce");
+  }
+};
+
+namespace {
+
+void ensure_device(psg_context* c) { PSG_CUDA(cudaSetDevice(c->device)); }
+
+void invalidate_results(psg_context* c) {
+  c->have_window = c->have_carry = c->have_cube = c->have_stats = c->have_outliers = false;
+}
+
+void set_cct_impl(psg_context* c, const uint32_t* parent, uint32_t n_ctx) {
+  require(parent != nullptr && n_ctx > 0, "parent array and n_ctx > 0 are required");
+  if (parent[0] != store::k_no_parent) fail(PS_E_FORMAT, "ctx 0: root must have no parent");
+  for (uint32_t i = 1; i < n_ctx; ++i)
+    if (parent[i] >= i)
+      fail(PS_E_FORMAT, "ctx " + std::to_string(i) +
+                            ": parent id must be smaller than ctx id (topological order)");
+  c->n_ctx = n_ctx;
+  c->h_parent.assign(parent, parent + n_ctx);
+  c->cct_po = preorder_of(c->h_parent, 0);
+  PSG_CUDA(cudaMemcpyAsync(c->d_cct_pre.ensure(n_ctx), c->cct_po.pre.data(), 4ull * n_ctx,
+                           cudaMemcpyHostToDevice, c->stream));
+  PSG_CUDA(cudaMemcpyAsync(c->d_cct_size.ensure(n_ctx), c->cct_po.size.data(), 4ull * n_ctx,
+                           cudaMemcpyHostToDevice, c->stream));
+  c->cached_anchor = -1;
+  invalidate_results(c);
+  c->sync();
+}
+
+// Uploads the trace index and validates the SoA already in d_ts/d_ctx.
+void finish_load(psg_context* c) {
+  PSG_CUDA(cudaMemcpyAsync(c->d_off.ensure(c->n_traces + 1), c->h_off.data(),
+                           8ull * (c->n_traces + 1), cudaMemcpyHostToDevice, c->stream));
+  PSG_CUDA(cudaMemcpyAsync(c->d_tend.ensure(c->n_traces + 1), c->h_tend.data(), 8ull * c->n_traces,
+                           cudaMemcpyHostToDevice, c->stream));
+  PSG_CUDA(cudaMemcpyAsync(c->d_pid.ensure(c->n_traces + 1), c->h_pid.data(), 4ull * c->n_traces,
+                           cudaMemcpyHostToDevice, c->stream));
+  if (c->n_ctx == 0) fail(PS_E_INVALID_ARGUMENT, "set the calling-context tree before loading traces");
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(c->summary.ensure(4));
+  unsigned long long init[2] = {0ull, ~0ull};
+  PSG_CUDA(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  launch_validate(c->view(), c->n_ctx, flags, flags + 1, c->stream);
+  unsigned long long out[2];
+  PSG_CUDA(cudaMemcpyAsync(out, flags, sizeof(out), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (out[0] != 0)
+    fail(PS_E_FORMAT, std::to_string(out[0]) + " trace(s) violate the format (first: trace " +
+                          std::to_string(c->h_pid[out[1]]) +
+                          "): non-decreasing timestamps, ctx < n_ctx and t_end >= last event are required");
+  invalidate_results(c);
+}
+
+// Host AoS body -> HBM staging (chunked, double-buffered) -> SoA.
+void load_aos(psg_context* c, const uint8_t* body, uint64_t n_events) {
+  c->n_events = n_events;
+  c->d_ts.ensure(n_events + 1);
+  c->d_ctx.ensure(n_events + 4);
+  const uint64_t chunk_ev = 4ull << 24;  // 64 Mi events = 768 MB per chunk
+  const uint64_t chunk_bytes = chunk_ev * 12;
+  uint8_t* stage = c->d_stage.ensure(std::min<uint64_t>(2 * chunk_bytes, n_events * 12 + 64));
+  uint64_t done = 0;
+  int slot = 0;
+  while (done < n_events) {
+    uint64_t ev = std::min(chunk_ev, n_events - done);
+    uint8_t* dst = stage + (c->d_stage.n >= 2 * chunk_bytes ? slot * chunk_bytes : 0);
+    PSG_CUDA(cudaMemcpyAsync(dst, body + done * 12, ev * 12, cudaMemcpyHostToDevice, c->stream));
+    launch_aos_to_soa(dst, ev, c->d_ts.p + done, c->d_ctx.p + done, c->stream);
+    done += ev;
+    slot ^= 1;
+  }
+}
+
+void compute_subtree(psg_context* c, uint32_t anchor) {
+  if (c->cached_anchor == static_cast<int64_t>(anchor)) return;
+  if (anchor >= c->n_ctx)
+    fail(PS_E_NOT_FOUND, "anchor ctx " + std::to_string(anchor) + " not in tree");
+  preorder sub = preorder_of(c->h_parent, anchor);
+  c->node_ids.clear();
+  for (uint32_t id = 0; id < c->n_ctx; ++id)
+    if (sub.pre[id] >= 0) c->node_ids.push_back(id);
+  c->nn = static_cast<uint32_t>(c->node_ids.size());
+  std::vector<int32_t> npre(c->nn), nsize(c->nn);
+  std::vector<char> has_child(c->n_ctx, 0);
+  for (uint32_t id = 1; id < c->n_ctx; ++id) has_child[c->h_parent[id]] = 1;
+  c->leaves.clear();
+  for (uint32_t i = 0; i < c->nn; ++i) {
+    npre[i] = sub.pre[c->node_ids[i]];
+    nsize[i] = sub.size[c->node_ids[i]];
+    if (!has_child[c->node_ids[i]]) c->leaves.push_back(c->node_ids[i]);
+  }
+  if (c->leaves.empty()) c->leaves.push_back(anchor);  // itermodel.cpp:216
+  c->h_sub_pre = sub.pre;
+  PSG_CUDA(cudaMemcpyAsync(c->d_sub_pre.ensure(c->n_ctx), sub.pre.data(), 4ull * c->n_ctx,
+                           cudaMemcpyHostToDevice, c->stream));
+  PSG_CUDA(cudaMemcpyAsync(c->d_node_pre.ensure(c->nn), npre.data(), 4ull * c->nn,
+                           cudaMemcpyHostToDevice, c->stream));
+  PSG_CUDA(cudaMemcpyAsync(c->d_node_size.ensure(c->nn), nsize.data(), 4ull * c->nn,
+                           cudaMemcpyHostToDevice, c->stream));
+  c->sync();
+  c->cached_anchor = anchor;
+}
+
+uint32_t choose_warps(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table_bytes) {
+  // Aim for >= 2 CTAs per SM worth of traces; fit the carve-outs in 227 KB.
+  uint32_t w = 16;
+  while (w > 1 && static_cast<uint64_t>(n_traces) < 2ull * 148 * w) w /= 2;
+  while (w > 1 && table_bytes + w * per_warp_bytes > 227u * 1024) w /= 2;
+  if (table_bytes + w * per_warp_bytes > 227u * 1024)
+    fail(PS_E_INVALID_ARGUMENT,
+         "calling-context tree too large for the shared-memory tables of the fused kernel");
+  return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* psg_version(void) { return "0.1.0-sm100a"; }
+const char* psg_last_error(void) { return t_last_error.c_str(); }
+
+const char* psg_status_name(ps_status status) {
+  switch (status) {
+    case PS_OK: return "ok";
+    case PS_E_IO: return "io_error";
+    case PS_E_FORMAT: return "format_error";
+    case PS_E_INVALID_IMAGE: return "invalid_image";
+    case PS_E_NOT_FOUND: return "not_found";
+    case PS_E_INVALID_CONFIG: return "invalid_config";
+    case PS_E_NO_SUMMARY: return "no_summary";
+    case PS_E_DEGENERATE_SUMMARY: return "degenerate_summary";
+    case PS_E_PARSE: return "parse_error";
+    case PS_E_NO_SUCH_METRIC: return "no_such_metric";
+    case PS_E_NO_PERIODICITY: return "no_periodicity";
+    case PS_E_NO_OUTLIERS: return "no_outliers";
+    case PS_E_INSUFFICIENT_DATA: return "insufficient_data";
+    case PS_E_INVALID_ARGUMENT: return "invalid_argument";
+    case PS_E_INTERNAL: return "internal";
+  }
+  return "unknown";
+}
+
+ps_status psg_open(int device, void* stream, psg_context** out) {
+  if (!out) {
+    t_last_error = "out is required";
+    return PS_E_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    int n = 0;
+    PSG_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n)
+      fail(PS_E_INVALID_ARGUMENT, "no CUDA device " + std::to_string(device));
+    auto c = std::make_unique<psg_context>();
+    c->device = device;
+    PSG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    PSG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      fail(PS_E_INTERNAL, std::string("psg kernels are built for sm_100a; device is ") + prop.name);
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      PSG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    for (auto& e : c->ev) PSG_CUDA(cudaEventCreate(&e));
+    *out = c.release();
+  });
+}
+
+void psg_close(psg_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+void* psg_stream(psg_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+uint64_t psg_device_bytes(const psg_context* c) {
+  if (!c) return 0;
+  return c->d_off.bytes() + c->d_ts.bytes() + c->d_ctx.bytes() + c->d_tend.bytes() +
+         c->d_stage.bytes() + c->cube_incl.bytes() + c->cube_excl.bytes() + c->w_cnt.bytes() * 7;
+}
+
+ps_status psg_comm_unique_id(uint8_t out_id[128]) {
+  if (!out_id) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out_id, &id, 128);
+  });
+}
+
+ps_status psg_comm_init(psg_context* c, int nranks, int rank, const uint8_t id[128]) {
+  if (!c || !id) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad nranks/rank");
+    ensure_device(c);
+    if (c->comm) nccl().comm_destroy(c->comm);
+    c->comm = nullptr;
+    c->nranks = nranks;
+    c->rank = rank;
+    if (nranks == 1) return;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    nccl_check(nccl().comm_init_rank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
+  });
+}
+
+ps_status psg_set_cct(psg_context* c, const uint32_t* parent, uint32_t n_ctx) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    set_cct_impl(c, parent, n_ctx);
+  });
+}
+
+ps_status psg_load_traces_aos(psg_context* c, const void* body, uint64_t n_events,
+                              const uint64_t* event_off, const uint32_t* profile_ids,
+                              const uint64_t* t_end_ns, uint32_t n_traces) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    require(event_off && profile_ids && t_end_ns, "event_off, profile_ids and t_end_ns are required");
+    require(n_events == 0 || body, "body is required");
+    require(event_off[0] == 0 && event_off[n_traces] == n_events, "event_off must span [0, n_events]");
+    ensure_device(c);
+    c->n_traces = n_traces;
+    c->h_off.assign(event_off, event_off + n_traces + 1);
+    c->h_tend.assign(t_end_ns, t_end_ns + n_traces);
+    c->h_pid.assign(profile_ids, profile_ids + n_traces);
+    for (uint32_t i = 0; i < n_traces; ++i)
+      require(event_off[i] <= event_off[i + 1], "event_off must be non-decreasing");
+    load_aos(c, static_cast<const uint8_t*>(body), n_events);
+    finish_load(c);
+  });
+}
+
+ps_status psg_set_nodes(psg_context* c, const uint32_t* node_of_trace, uint32_t n_nodes,
+                        const uint32_t* node_rack, const uint32_t* node_chassis) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    require(node_of_trace && n_nodes > 0, "node_of_trace and n_nodes > 0 are required");
+    ensure_device(c);
+    for (uint32_t t = 0; t < c->n_traces; ++t)
+      require(node_of_trace[t] < n_nodes, "node_of_trace entry out of range");
+    c->n_nodes = n_nodes;
+    c->h_node_of_trace.assign(node_of_trace, node_of_trace + c->n_traces);
+    PSG_CUDA(cudaMemcpyAsync(c->d_node_of_trace.ensure(c->n_traces + 1), node_of_trace,
+                             4ull * c->n_traces, cudaMemcpyHostToDevice, c->stream));
+    c->h_rack_ids.clear();
+    if (node_rack && node_chassis) {
+      std::set<uint32_t> racks(node_rack, node_rack + n_nodes);
+      c->h_rack_ids.assign(racks.begin(), racks.end());
+      std::vector<uint32_t> ridx(n_nodes), uni(c->h_rack_ids.size() * 64, 0);
+      for (uint32_t i = 0; i < n_nodes; ++i) {
+        ridx[i] = static_cast<uint32_t>(
+            std::lower_bound(c->h_rack_ids.begin(), c->h_rack_ids.end(), node_rack[i]) -
+            c->h_rack_ids.begin());
+        require(node_chassis[i] < 64, "chassis ids >= 64 are not supported");
+        uni[ridx[i] * 64 + node_chassis[i]] += 1;
+      }
+      PSG_CUDA(cudaMemcpyAsync(c->d_node_rack_idx.ensure(n_nodes), ridx.data(), 4ull * n_nodes,
+                               cudaMemcpyHostToDevice, c->stream));
+      PSG_CUDA(cudaMemcpyAsync(c->d_node_chassis.ensure(n_nodes), node_chassis, 4ull * n_nodes,
+                               cudaMemcpyHostToDevice, c->stream));
+      PSG_CUDA(cudaMemcpyAsync(c->d_uni_cnt.ensure(uni.size()), uni.data(), 4ull * uni.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+    }
+    c->sync();
+  });
+}
+
+ps_status psg_load_trace_db(psg_context* c, const char* dir, const uint32_t* pids, uint32_t n_pids) {
+  if (!c || !dir) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    store::trace_db db;
+    store::open_trace_db(dir, db);
+    std::vector<const store::trace_index_entry*> sel;
+    if (pids) {
+      std::vector<uint32_t> ids(pids, pids + n_pids);
+      std::sort(ids.begin(), ids.end());
+      ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+      for (uint32_t id : ids) {
+        auto* e = db.find(id);
+        if (!e) fail(PS_E_NOT_FOUND, "trace " + std::to_string(id) + " not in database");
+        sel.push_back(e);
+      }
+    } else {
+      for (auto& e : db.index) sel.push_back(&e);
+    }
+    // CCT from meta.bin
+    std::vector<uint32_t> parent;
+    for (size_t i = 0; i < db.meta.contexts.size(); ++i) {
+      if (db.meta.contexts[i].id != i) fail(PS_E_FORMAT, "meta.bin: ctx ids must be dense");
+      parent.push_back(db.meta.contexts[i].parent);
+    }
+    set_cct_impl(c, parent.data(), static_cast<uint32_t>(parent.size()));
+    // index + body (contiguous fast path, gathered otherwise)
+    c->n_traces = static_cast<uint32_t>(sel.size());
+    c->h_off.assign(1, 0);
+    c->h_tend.clear();
+    c->h_pid.clear();
+    bool contiguous = true;
+    for (size_t i = 0; i < sel.size(); ++i) {
+      if (sel[i]->event_count > 0 && sel[i]->t_begin_ns != 0) {
+      }
+      c->h_off.push_back(c->h_off.back() + sel[i]->event_count);
+      c->h_tend.push_back(sel[i]->t_end_ns);
+      c->h_pid.push_back(sel[i]->profile_id);
+      if (i > 0 && sel[i]->offset != sel[i - 1]->offset + sel[i - 1]->event_count * 12)
+        contiguous = false;
+    }
+    const uint64_t n_ev = c->h_off.back();
+    // first event must equal the indexed t_begin (store.cpp:750-751)
+    for (auto* e : sel)
+      if (e->event_count > 0) {
+        uint64_t ts0;
+        std::memcpy(&ts0, db.map.data() + e->offset, 8);
+        if (ts0 != e->t_begin_ns)
+          fail(PS_E_FORMAT, "trace " + std::to_string(e->profile_id) +
+                                " event 0: first event does not match indexed t_begin");
+      }
+    if (contiguous || sel.empty()) {
+      load_aos(c, sel.empty() ? nullptr : db.map.data() + sel.front()->offset, n_ev);
+    } else {
+      std::vector<uint8_t> gathered(n_ev * 12);
+      uint64_t o = 0;
+      for (auto* e : sel) {
+        std::memcpy(gathered.data() + o, db.map.data() + e->offset, e->event_count * 12);
+        o += e->event_count * 12;
+      }
+      load_aos(c, gathered.data(), n_ev);
+      c->sync();
+    }
+    finish_load(c);
+    // rank -> hostname from the first profile with that rank (diagnostics.cpp:381-384);
+    // node index = position of the hostname in sorted order (std::map order).
+    std::map<int32_t, const std::string*> rank_host;
+    for (const auto& p : db.meta.profiles)
+      if (p.rank >= 0 && !rank_host.count(p.rank)) rank_host[p.rank] = &p.hostname;
+    std::vector<std::string> host_of_trace;
+    std::set<std::string> hosts;
+    for (auto* e : sel) {
+      const auto* pd = db.meta.find_profile(e->profile_id);
+      std::string h;
+      if (pd && pd->rank >= 0) h = *rank_host[pd->rank];
+      host_of_trace.push_back(h);
+      hosts.insert(h);
+    }
+    std::vector<std::string> host_list(hosts.begin(), hosts.end());
+    std::vector<uint32_t> node_of(sel.size()), rack(host_list.size()), chassis(host_list.size());
+    for (size_t i = 0; i < sel.size(); ++i)
+      node_of[i] = static_cast<uint32_t>(
+          std::lower_bound(host_list.begin(), host_list.end(), host_of_trace[i]) - host_list.begin());
+    bool topo = !host_list.empty();
+    for (size_t i = 0; i < host_list.size() && topo; ++i)
+      topo = store::parse_node_name(host_list[i], &rack[i], &chassis[i]) && chassis[i] < 64;
+    if (!sel.empty()) {
+      ps_status st = psg_set_nodes(c, node_of.data(), static_cast<uint32_t>(host_list.size()),
+                                   topo ? rack.data() : nullptr, topo ? chassis.data() : nullptr);
+      if (st != PS_OK) fail(st, t_last_error);
+    }
+  });
+}
+
+ps_status psg_generate_iterative(psg_context* c, const psg_iter_scenario* s, uint32_t rank_lo,
+                                 uint32_t rank_hi) {
+  if (!c || !s) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    require(s->n_ranks >= 1 && s->n_iterations >= 1 && s->n_kernels >= 1,
+            "n_ranks, n_iterations, n_kernels must be >= 1");
+    require(s->mean_time_s && s->jitter_frac, "mean_time_s and jitter_frac are required");
+    require(rank_lo <= rank_hi && rank_hi <= s->n_ranks, "bad rank range");
+    require(s->copy_segment_s >= 0.0, "copy_segment_s must be >= 0");
+    ensure_device(c);
+    const uint32_t nk = s->n_kernels;
+    const bool has_copy = s->copy_segment_s > 0.0;
+    std::vector<uint32_t> parent(2 + nk + (has_copy ? 1 : 0));
+    parent[0] = store::k_no_parent;
+    parent[1] = 0;
+    for (uint32_t k = 0; k < nk; ++k) parent[2 + k] = 1;
+    if (has_copy) parent[2 + nk] = 0;
+    set_cct_impl(c, parent.data(), static_cast<uint32_t>(parent.size()));
+
+    const uint32_t n_local = rank_hi - rank_lo;
+    const uint64_t epi = nk + 2 + (has_copy ? 1 : 0);
+    const uint64_t ept = epi * s->n_iterations;
+    c->n_traces = n_local;
+    c->n_events = ept * n_local;
+    c->h_off.resize(n_local + 1);
+    for (uint32_t r = 0; r <= n_local; ++r) c->h_off[r] = ept * r;
+    c->h_pid.resize(n_local);
+    for (uint32_t r = 0; r < n_local; ++r) c->h_pid[r] = rank_lo + r + 1;
+    c->h_tend.assign(n_local, 0);
+
+    if (!c->jump.p) {
+      auto mats = jump_matrices();
+      PSG_CUDA(cudaMemcpyAsync(c->jump.ensure(mats.size()), mats.data(), 8 * mats.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+    }
+    // parameters: mean[nk] | jitter[nk] | spread
+    uint64_t spread_n = 0;
+    if (s->spread) spread_n = s->spread_kernel_stride ? s->spread_kernel_stride * nk : s->n_ranks;
+    double* gp = c->gen_params.ensure(2 * nk + spread_n + 1);
+    PSG_CUDA(cudaMemcpyAsync(gp, s->mean_time_s, 8ull * nk, cudaMemcpyHostToDevice, c->stream));
+    PSG_CUDA(cudaMemcpyAsync(gp + nk, s->jitter_frac, 8ull * nk, cudaMemcpyHostToDevice, c->stream));
+    if (spread_n)
+      PSG_CUDA(cudaMemcpyAsync(gp + 2 * nk, s->spread, 8ull * spread_n, cudaMemcpyHostToDevice,
+                               c->stream));
+    const uint64_t copy_ns = static_cast<uint64_t>(std::llround(s->copy_segment_s * 1e9));
+    c->d_ts.ensure(c->n_events + 1);
+    c->d_ctx.ensure(c->n_events + 4);
+    c->d_tend.ensure(n_local + 1);
+    const uint32_t chunks = (s->n_iterations + 15) / 16;
+    uint64_t* scratch = c->gen_chunks.ensure(static_cast<uint64_t>(n_local) * chunks + 1);
+    launch_gen_iterative(c->jump.p, s->seed, s->n_ranks, s->n_iterations, nk, gp, gp + nk,
+                         spread_n ? gp + 2 * nk : nullptr, s->spread_kernel_stride, copy_ns, rank_lo,
+                         n_local, ept, scratch, c->d_ts.p, c->d_ctx.p, c->d_tend.p, c->stream);
+    PSG_CUDA(cudaMemcpyAsync(c->h_tend.data(), c->d_tend.p, 8ull * n_local, cudaMemcpyDeviceToHost,
+                             c->stream));
+    c->sync();
+    finish_load(c);
+  });
+}
+
+ps_status psg_shard(psg_context* c, psg_shard_info* out) {
+  if (!c || !out) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    out->n_traces = c->n_traces;
+    out->n_ctx = c->n_ctx;
+    out->n_events = c->n_events;
+    out->t_max = c->h_tend.empty() ? 0 : *std::max_element(c->h_tend.begin(), c->h_tend.end());
+    out->t_min = 0;
+    if (c->n_events) {
+      // min first timestamp over non-empty traces
+      uint64_t m = ~0ull;
+      for (uint32_t t = 0; t < c->n_traces; ++t) {
+        if (c->h_off[t + 1] == c->h_off[t]) continue;
+        uint64_t v;
+        PSG_CUDA(cudaMemcpy(&v, c->d_ts.p + c->h_off[t], 8, cudaMemcpyDeviceToHost));
+        m = std::min(m, v);
+        if (t > 64) break;  // synthetic traces start at 0; a sample is enough for a hint
+      }
+      out->t_min = m == ~0ull ? 0 : m;
+    }
+  });
+}
+
+ps_status psg_get_traces(psg_context* c, uint64_t* ts, uint32_t* ctx_ids, uint64_t* event_off,
+                         uint64_t* t_end, uint32_t* profile_ids) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    if (ts && c->n_events)
+      PSG_CUDA(cudaMemcpy(ts, c->d_ts.p, 8 * c->n_events, cudaMemcpyDeviceToHost));
+    if (ctx_ids && c->n_events)
+      PSG_CUDA(cudaMemcpy(ctx_ids, c->d_ctx.p, 4 * c->n_events, cudaMemcpyDeviceToHost));
+    if (event_off) std::copy(c->h_off.begin(), c->h_off.end(), event_off);
+    if (t_end) std::copy(c->h_tend.begin(), c->h_tend.end(), t_end);
+    if (profile_ids) std::copy(c->h_pid.begin(), c->h_pid.end(), profile_ids);
+  });
+}
+
+// ---------------------------------------------------------------------------
+ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* info) {
+  if (!c || !q || !info) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    const uint32_t f = q->flags;
+    const bool do_window = f & PSG_Q_WINDOW, do_cube = f & PSG_Q_CUBE;
+    const bool do_stats = f & PSG_Q_STATS, do_out = f & PSG_Q_OUTLIERS;
+    const bool store_cube = do_cube && !(f & PSG_Q_NO_CUBE_STORE);
+    require(do_window || do_cube, "query needs PSG_Q_WINDOW and/or PSG_Q_CUBE");
+    require(!do_stats || do_cube, "PSG_Q_STATS requires PSG_Q_CUBE");
+    require(!do_out || do_window, "PSG_Q_OUTLIERS requires PSG_Q_WINDOW");
+    if (do_window && q->t0_ns > q->t1_ns)
+      fail(PS_E_INVALID_ARGUMENT, "trace window start after end");
+    if (c->n_ctx == 0) fail(PS_E_INVALID_ARGUMENT, "no calling-context tree loaded");
+    invalidate_results(c);
+    std::memset(info, 0, sizeof(*info));
+    const uint32_t n = c->n_traces;
+    cudaStream_t s = c->stream;
+    PSG_CUDA(cudaEventRecord(c->ev[0], s));
+
+    query_params p{};
+    p.tr = c->view();
+    p.n_ctx = c->n_ctx;
+    p.G = 4;
+    if (do_window) {
+      const size_t cells = static_cast<size_t>(n) * c->n_ctx + 1;
+      p.do_window = 1;
+      p.clamp_tend = (f & PSG_Q_CLAMP_TEND) ? 1 : 0;
+      p.t0 = q->t0_ns;
+      p.t1 = q->t1_ns;
+      p.w_cnt = c->w_cnt.ensure(cells);
+      p.w_sum = c->w_sum.ensure(cells);
+      p.w_min = c->w_min.ensure(cells);
+      p.w_max = c->w_max.ensure(cells);
+      p.w_excl = c->w_excl.ensure(cells);
+      p.w_incl = c->w_incl.ensure(cells);
+      p.w_mean = c->w_mean.ensure(cells);
+      p.c_has = c->c_has.ensure(n + 1);
+      p.c_ts = c->c_ts.ensure(n + 1);
+      p.c_ctx = c->c_ctx.ensure(n + 1);
+      p.cct_pre = c->d_cct_pre.p;
+      p.cct_size = c->d_cct_size.p;
+    }
+    uint32_t nn = 0;
+    if (do_cube) {
+      compute_subtree(c, q->anchor_ctx);
+      nn = c->nn;
+      uint32_t* ic = c->iter_count.ensure(n + 1);
+      launch_iter_count(c->view(), c->d_sub_pre.p, c->n_ctx, ic, s);
+      const size_t sb = cube_layout_scratch_bytes(n);
+      unsigned long long* sum = c->summary.ensure(4);
+      launch_cube_layout(ic, n, nn, c->tpos.ensure(n + 1), c->block_off.ensure(n + 1), sum,
+                         c->scratch.ensure(sb), sb, s);
+      unsigned long long h[3];
+      PSG_CUDA(cudaMemcpyAsync(h, sum, sizeof(h), cudaMemcpyDeviceToHost, s));
+      c->sync();
+      c->n_kept = static_cast<uint32_t>(h[0]);
+      c->n_cells = h[2];
+      unsigned long long g[2] = {h[1], h[0]};  // min iterations, kept count
+      if (c->comm && c->nranks > 1) {
+        unsigned long long* d = c->summary.p;  // reuse as staging
+        PSG_CUDA(cudaMemcpyAsync(d, g, sizeof(g), cudaMemcpyHostToDevice, s));
+        nccl_check(nccl().group_start(), "ncclGroupStart");
+        c->allreduce(d, 1, ncclUint64, ncclMin);
+        c->allreduce(d + 1, 1, ncclUint64, ncclSum);
+        nccl_check(nccl().group_end(), "ncclGroupEnd");
+        PSG_CUDA(cudaMemcpyAsync(g, d, sizeof(g), cudaMemcpyDeviceToHost, s));
+        c->sync();
+      }
+      c->K = g[1] > 0 ? static_cast<uint32_t>(g[0]) : 0;
+      c->n_kept_global = static_cast<uint32_t>(g[1]);
+      p.do_cube = 1;
+      p.store_cube = store_cube ? 1 : 0;
+      p.sub_pre = c->d_sub_pre.p;
+      p.node_pre = c->d_node_pre.p;
+      p.node_size = c->d_node_size.p;
+      p.nn = nn;
+      p.iter_count = ic;
+      p.tpos = c->tpos.p;
+      p.block_off = c->block_off.p;
+      p.K = c->K;
+      if (store_cube) {
+        p.cube_incl = c->cube_incl.ensure(c->n_cells + 1);
+        p.cube_excl = c->cube_excl.ensure(c->n_cells + 1);
+      }
+      p.gap_incl = c->gap_incl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
+      p.gap_excl = c->gap_excl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
+      if (do_stats && c->K > 0) {
+        const size_t plane = static_cast<size_t>(c->K) * nn;
+        unsigned long long* x = c->x_acc.ensure(5 * plane);
+        PSG_CUDA(cudaMemsetAsync(x, 0, 5 * plane * sizeof(unsigned long long), s));
+        p.do_stats = 1;
+        p.x_sum = x;
+        p.x_max = x + plane;
+        p.x_sq = x + 2 * plane;
+        p.within_cv = c->within_cv.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
+        p.within_ok = c->within_ok.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
+      }
+    }
+    // launch geometry
+    warp_smem_layout L;
+    L.init(c->n_ctx, nn, p.G);
+    uint32_t W = choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16));
+    p.warps = W;
+    uint32_t smem = cta_table_bytes(c->n_ctx, nn, W) + W * L.bytes;
+    PSG_CUDA(cudaEventRecord(c->ev[1], s));
+    launch_trace_query(p, smem, s);
+    PSG_CUDA(cudaEventRecord(c->ev[2], s));
+
+    if (do_stats && c->K > 0) {
+      const size_t plane = static_cast<size_t>(c->K) * nn;
+      double* no = c->node_out.ensure(static_cast<size_t>(nn) * 10 + 1);
+      // within-rank partial sums per node, then cross-GPU sums of everything
+      launch_stats_finalize(nullptr, nullptr, nullptr, c->K, nn, c->n_kept_global, c->within_cv.p,
+                            c->within_ok.p, c->n_kept, no, s);
+      if (c->comm && c->nranks > 1) {
+        nccl_check(nccl().group_start(), "ncclGroupStart");
+        c->allreduce(c->x_acc.p, plane, ncclUint64, ncclSum);
+        c->allreduce(c->x_acc.p + plane, plane, ncclUint64, ncclMax);
+        c->allreduce(c->x_acc.p + 2 * plane, 3 * plane, ncclUint64, ncclSum);
+        c->allreduce(no + static_cast<size_t>(nn) * 8, 2 * nn, ncclFloat64, ncclSum);
+        nccl_check(nccl().group_end(), "ncclGroupEnd");
+      }
+      launch_stats_finalize(c->x_acc.p, c->x_acc.p + plane, c->x_acc.p + 2 * plane, c->K, nn,
+                            c->n_kept_global, nullptr, nullptr, c->n_kept, no, s);
+      c->have_stats = true;
+    }
+
+    if (do_out) {
+      require(q->site_ctx && q->n_sites > 0, "outliers need at least one candidate site ctx");
+      require(c->n_nodes > 0, "outliers need the rank -> node mapping (psg_set_nodes)");
+      for (uint32_t i = 0; i < q->n_sites; ++i)
+        require(q->site_ctx[i] < c->n_ctx, "site ctx out of range");
+      c->sites.assign(q->site_ctx, q->site_ctx + q->n_sites);
+      const uint32_t ns = q->n_sites;
+      PSG_CUDA(cudaMemcpyAsync(c->d_sites.ensure(ns), q->site_ctx, 4ull * ns, cudaMemcpyHostToDevice, s));
+      unsigned long long* sa = c->site_acc.ensure(2 * ns);
+      unsigned long long* na = c->node_acc.ensure(2 * c->n_nodes);
+      PSG_CUDA(cudaMemsetAsync(sa, 0, 16ull * ns, s));
+      PSG_CUDA(cudaMemsetAsync(na, 0, 16ull * c->n_nodes, s));
+      launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
+                      sa, na, c->d_worst.ensure(2), c->site_ratio.ensure(ns), 0, s);
+      uint64_t ranks_global = n;
+      if (c->comm && c->nranks > 1) {
+        nccl_check(nccl().group_start(), "ncclGroupStart");
+        c->allreduce(sa, ns, ncclUint64, ncclSum);
+        c->allreduce(sa + ns, ns, ncclUint64, ncclMax);
+        nccl_check(nccl().group_end(), "ncclGroupEnd");
+        unsigned long long* d = c->summary.p;
+        unsigned long long hn = n;
+        PSG_CUDA(cudaMemcpyAsync(d, &hn, 8, cudaMemcpyHostToDevice, s));
+        c->allreduce(d, 1, ncclUint64, ncclSum);
+        PSG_CUDA(cudaMemcpyAsync(&hn, d, 8, cudaMemcpyDeviceToHost, s));
+        c->sync();
+        ranks_global = hn;
+      }
+      launch_outliers(c->w_incl.p, static_cast<uint32_t>(ranks_global), c->n_ctx, c->d_sites.p, ns,
+                      c->d_node_of_trace.p, c->n_nodes, sa, na, c->d_worst.p, c->site_ratio.p, 1, s);
+      launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
+                      sa, na, c->d_worst.p, c->site_ratio.p, 2, s);
+      c->allreduce(na, 2ull * c->n_nodes, ncclUint64, ncclSum);
+      launch_node_select(na, c->n_nodes, q->top_k, q->z_min, c->node_mean.ensure(c->n_nodes),
+                         c->node_z.ensure(c->n_nodes), c->d_order.ensure(c->n_nodes),
+                         c->d_nsel.ensure(1), s);
+      const uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
+      if (nr) {
+        launch_topology(c->d_order.p, c->d_nsel.p, c->d_node_rack_idx.p, c->d_node_chassis.p,
+                        c->d_uni_cnt.p, nr, c->d_rack_nodes.ensure(nr), c->rack_mask.ensure(nr),
+                        c->rack_full.ensure(nr), s);
+      }
+      c->have_outliers = true;
+    }
+    PSG_CUDA(cudaEventRecord(c->ev[3], s));
+    c->sync();
+
+    // info
+    if (do_window) c->have_window = c->have_carry = true;
+    if (do_cube) c->have_cube = true;
+    info->n_nodes = nn;
+    info->n_kept = c->n_kept;
+    info->n_skipped = do_cube ? n - c->n_kept : 0;
+    info->min_iterations = c->K;
+    info->n_kept_global = c->n_kept_global;
+    info->n_cells = c->n_cells;
+    info->n_leaves = do_cube ? static_cast<uint32_t>(c->leaves.size()) : 0;
+    if (do_out) {
+      uint32_t w[2];
+      PSG_CUDA(cudaMemcpy(w, c->d_worst.p, 4, cudaMemcpyDeviceToHost));
+      PSG_CUDA(cudaMemcpy(&info->n_outliers, c->d_nsel.p, 4, cudaMemcpyDeviceToHost));
+      info->worst_site = c->sites[w[0]];
+      PSG_CUDA(cudaMemcpy(&info->worst_ratio, c->site_ratio.p + w[0], 8, cudaMemcpyDeviceToHost));
+      uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
+      if (nr) {
+        std::vector<uint32_t> rn(nr);
+        PSG_CUDA(cudaMemcpy(rn.data(), c->d_rack_nodes.p, 4ull * nr, cudaMemcpyDeviceToHost));
+        for (uint32_t x : rn) info->n_racks += x > 0;
+      }
+    }
+    PSG_CUDA(cudaEventElapsedTime(&info->ms_total, c->ev[0], c->ev[3]));
+    PSG_CUDA(cudaEventElapsedTime(&info->ms_main, c->ev[1], c->ev[2]));
+  });
+}
+
+ps_status psg_get_window(psg_context* c, uint64_t* count, int64_t* sum, int64_t* mn, int64_t* mx,
+                         double* mean, int64_t* excl, int64_t* incl) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_window) fail(PS_E_INVALID_ARGUMENT, "no window result (run psg_query with PSG_Q_WINDOW)");
+    ensure_device(c);
+    const size_t cells = static_cast<size_t>(c->n_traces) * c->n_ctx;
+    auto cp = [&](void* dst, const void* src, size_t b) {
+      if (dst && b) PSG_CUDA(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost));
+    };
+    cp(count, c->w_cnt.p, 8 * cells);
+    cp(sum, c->w_sum.p, 8 * cells);
+    cp(mn, c->w_min.p, 8 * cells);
+    cp(mx, c->w_max.p, 8 * cells);
+    cp(mean, c->w_mean.p, 8 * cells);
+    cp(excl, c->w_excl.p, 8 * cells);
+    cp(incl, c->w_incl.p, 8 * cells);
+  });
+}
+
+ps_status psg_get_carry(psg_context* c, uint8_t* has, uint64_t* ts, uint32_t* ctx_ids) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_carry) fail(PS_E_INVALID_ARGUMENT, "no window result");
+    ensure_device(c);
+    if (has) PSG_CUDA(cudaMemcpy(has, c->c_has.p, c->n_traces, cudaMemcpyDeviceToHost));
+    if (ts) PSG_CUDA(cudaMemcpy(ts, c->c_ts.p, 8ull * c->n_traces, cudaMemcpyDeviceToHost));
+    if (ctx_ids) PSG_CUDA(cudaMemcpy(ctx_ids, c->c_ctx.p, 4ull * c->n_traces, cudaMemcpyDeviceToHost));
+  });
+}
+
+ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts,
+                       uint64_t* block_offset, int64_t* incl, int64_t* excl, int64_t* gap_incl,
+                       int64_t* gap_excl) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_cube) fail(PS_E_INVALID_ARGUMENT, "no cube result (run psg_query with PSG_Q_CUBE)");
+    ensure_device(c);
+    if (node_ids) std::copy(c->node_ids.begin(), c->node_ids.end(), node_ids);
+    std::vector<uint32_t> ic(c->n_traces);
+    if (c->n_traces)
+      PSG_CUDA(cudaMemcpy(ic.data(), c->iter_count.p, 4ull * c->n_traces, cudaMemcpyDeviceToHost));
+    if (iter_counts) std::copy(ic.begin(), ic.end(), iter_counts);
+    if (block_offset) {
+      std::vector<uint64_t> bo(c->n_traces);
+      if (c->n_traces)
+        PSG_CUDA(cudaMemcpy(bo.data(), c->block_off.p, 8ull * c->n_traces, cudaMemcpyDeviceToHost));
+      size_t j = 0;
+      for (uint32_t t = 0; t < c->n_traces; ++t)
+        if (ic[t] > 0) block_offset[j++] = bo[t];
+    }
+    if ((incl || excl) && !c->cube_incl.p)
+      fail(PS_E_INVALID_ARGUMENT, "cube was streamed (PSG_Q_NO_CUBE_STORE); nothing to copy");
+    if (incl && c->n_cells)
+      PSG_CUDA(cudaMemcpy(incl, c->cube_incl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
+    if (excl && c->n_cells)
+      PSG_CUDA(cudaMemcpy(excl, c->cube_excl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
+    const size_t g = static_cast<size_t>(c->n_kept) * c->nn;
+    if (gap_incl && g) PSG_CUDA(cudaMemcpy(gap_incl, c->gap_incl.p, 8 * g, cudaMemcpyDeviceToHost));
+    if (gap_excl && g) PSG_CUDA(cudaMemcpy(gap_excl, c->gap_excl.p, 8 * g, cudaMemcpyDeviceToHost));
+  });
+}
+
+ps_status psg_get_stats(psg_context* c, double total_time_s, uint32_t* leaves, double* savings,
+                        double* summary, double* cv, int32_t* cv_ok) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_cube) fail(PS_E_INVALID_ARGUMENT, "no cube result");
+    if (total_time_s <= 0.0) fail(PS_E_INVALID_ARGUMENT, "total time must be positive");
+    if (c->K < 1) fail(PS_E_INSUFFICIENT_DATA, "model has no iterations");
+    if (!c->have_stats) fail(PS_E_INVALID_ARGUMENT, "no stats result (run psg_query with PSG_Q_STATS)");
+    ensure_device(c);
+    std::vector<double> no(static_cast<size_t>(c->nn) * 8);
+    PSG_CUDA(cudaMemcpy(no.data(), c->node_out.p, 8 * no.size(), cudaMemcpyDeviceToHost));
+    double total = 0.0;
+    for (size_t i = 0; i < c->leaves.size(); ++i) {
+      const uint32_t npos = static_cast<uint32_t>(
+          std::lower_bound(c->node_ids.begin(), c->node_ids.end(), c->leaves[i]) - c->node_ids.begin());
+      const double* r = &no[static_cast<size_t>(npos) * 8];
+      if (leaves) leaves[i] = c->leaves[i];
+      if (savings)
+        for (int j = 0; j < 4; ++j) savings[4 * i + j] = r[j];
+      total += r[3];  // savings_report: total_savings_s += total_reduction_s (diagnostics.cpp:153)
+      if (cv) {
+        cv[2 * i] = r[4];
+        cv[2 * i + 1] = r[5];
+      }
+      if (cv_ok) cv_ok[i] = (r[6] != 0.0 && r[7] != 0.0) ? 1 : 0;
+    }
+    if (summary) {
+      summary[0] = c->K;
+      summary[1] = total;
+      summary[2] = total_time_s;
+      summary[3] = total / total_time_s;
+    }
+  });
+}
+
+ps_status psg_get_outliers(psg_context* c, double* site_ratio, double* node_mean, double* node_z,
+                           uint32_t* selected, uint32_t* rack_rows, uint64_t* chassis_mask,
+                           uint64_t* full_mask) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_outliers) fail(PS_E_INVALID_ARGUMENT, "no outlier result (run psg_query with PSG_Q_OUTLIERS)");
+    ensure_device(c);
+    if (site_ratio)
+      PSG_CUDA(cudaMemcpy(site_ratio, c->site_ratio.p, 8 * c->sites.size(), cudaMemcpyDeviceToHost));
+    if (node_mean) PSG_CUDA(cudaMemcpy(node_mean, c->node_mean.p, 8ull * c->n_nodes, cudaMemcpyDeviceToHost));
+    if (node_z) PSG_CUDA(cudaMemcpy(node_z, c->node_z.p, 8ull * c->n_nodes, cudaMemcpyDeviceToHost));
+    uint32_t nsel = 0;
+    PSG_CUDA(cudaMemcpy(&nsel, c->d_nsel.p, 4, cudaMemcpyDeviceToHost));
+    if (selected && nsel) PSG_CUDA(cudaMemcpy(selected, c->d_order.p, 4ull * nsel, cudaMemcpyDeviceToHost));
+    const uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
+    if (nr && (rack_rows || chassis_mask || full_mask)) {
+      std::vector<uint32_t> rn(nr);
+      std::vector<uint64_t> m(nr), fm(nr);
+      PSG_CUDA(cudaMemcpy(rn.data(), c->d_rack_nodes.p, 4ull * nr, cudaMemcpyDeviceToHost));
+      PSG_CUDA(cudaMemcpy(m.data(), c->rack_mask.p, 8ull * nr, cudaMemcpyDeviceToHost));
+      PSG_CUDA(cudaMemcpy(fm.data(), c->rack_full.p, 8ull * nr, cudaMemcpyDeviceToHost));
+      size_t j = 0;
+      for (uint32_t r = 0; r < nr; ++r) {
+        if (!rn[r]) continue;
+        if (rack_rows) {
+          rack_rows[3 * j] = c->h_rack_ids[r];
+          rack_rows[3 * j + 1] = rn[r];
+          rack_rows[3 * j + 2] = static_cast<uint32_t>(__builtin_popcountll(m[r]));
+        }
+        if (chassis_mask) chassis_mask[j] = m[r];
+        if (full_mask) full_mask[j] = fm[r];
+        ++j;
+      }
+    }
+  });
+}
+
+ps_status psg_window_rows(psg_context* c, uint64_t t0, uint64_t t1, uint64_t* n_rows,
+                          uint32_t* row_pid, uint64_t* row_ts, uint32_t* row_ctx) {
+  if (!c || !n_rows) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (t0 > t1) fail(PS_E_INVALID_ARGUMENT, "trace window start after end");
+    ensure_device(c);
+    const uint32_t n = c->n_traces;
+    cudaStream_t s = c->stream;
+    uint64_t* cnt = c->gen_chunks.ensure(2ull * (n + 1));
+    uint64_t* roff = cnt + (n + 1);
+    launch_window_bounds(c->view(), t0, t1, cnt, c->c_has.ensure(n + 1), c->c_ts.ensure(n + 1),
+                         c->c_ctx.ensure(n + 1), s);
+    PSG_CUDA(cudaMemsetAsync(cnt + n, 0, 8, s));
+    size_t sb = exclusive_scan_u64_scratch(n + 1);
+    launch_exclusive_scan_u64(cnt, roff, n + 1, c->scratch.ensure(sb), sb, s);
+    uint64_t total = 0;
+    PSG_CUDA(cudaMemcpyAsync(&total, roff + n, 8, cudaMemcpyDeviceToHost, s));
+    c->sync();
+    *n_rows = total;
+    if (row_pid || row_ts || row_ctx) {
+      dbuf<uint32_t> op, oc;
+      dbuf<uint64_t> ot;
+      launch_window_copy(c->view(), c->d_pid.p, t0, roff, op.ensure(total + 1), ot.ensure(total + 1),
+                         oc.ensure(total + 1), s);
+      c->sync();
+      if (row_pid && total) PSG_CUDA(cudaMemcpy(row_pid, op.p, 4 * total, cudaMemcpyDeviceToHost));
+      if (row_ts && total) PSG_CUDA(cudaMemcpy(row_ts, ot.p, 8 * total, cudaMemcpyDeviceToHost));
+      if (row_ctx && total) PSG_CUDA(cudaMemcpy(row_ctx, oc.p, 4 * total, cudaMemcpyDeviceToHost));
+    }
+    c->have_window = false;  // carry buffers now hold window_rows carries only
+    c->have_carry = true;
+  });
+}
+
+}  // extern "C"

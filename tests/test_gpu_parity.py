@@ -1,0 +1,286 @@
+"""GPU parity: libpsg.so (through its C ABI) against the CPU oracle
+restatement and the reference itself (oracle/_ref), on identical inputs.
+
+Bar (north star): bit-exact for counts, sums, boundaries, cube cells, outlier
+ids; 1e-9 relative for the fp64 diagnostics (savings, CV)."""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2605_03561_b200 import Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_OUTLIERS, Q_STATS, Q_WINDOW, PsgError, scenarios
+from tests.helpers import assert_rel, random_cct, random_traces, ref_db, to_aos
+
+pytestmark = pytest.mark.gpu
+
+WINDOW_KEYS = ["count", "sum", "min", "max", "mean", "excl", "incl"]
+
+
+def check_window(ctx, tr, parent, t0, t1):
+    ctx.query(Q_WINDOW, t0=t0, t1=t1)
+    g = ctx.window()
+    o = oracle.window(tr, parent, t0, t1)
+    for k in WINDOW_KEYS:
+        assert np.array_equal(g[k], o[k]), f"window {k} differs for [{t0},{t1})"
+    gc = ctx.carry()
+    for k in ("has", "ts", "ctx"):
+        assert np.array_equal(gc[k], o["carry"][k]), f"carry {k}"
+
+
+def check_cube(ctx, tr, parent, anchor, stats=True):
+    info = ctx.query(Q_CUBE | (Q_STATS if stats else 0), anchor=anchor)
+    g = ctx.cube()
+    o = oracle.cube(tr, parent, anchor)
+    for k in ("node_ids", "iter_counts", "block_offset", "incl", "excl", "gap_incl", "gap_excl"):
+        assert np.array_equal(g[k], o[k]), f"cube {k} differs (anchor {anchor})"
+    kept = int((o["iter_counts"] > 0).sum())
+    assert info["n_kept"] == kept
+    if stats and kept > 0:
+        s = ctx.stats(1.0)
+        for j, leaf in enumerate(s["leaves"]):
+            npos = int(np.searchsorted(o["node_ids"], leaf))
+            want, ok = oracle.node_stats(o, npos)
+            assert_rel(s["savings"][j], want[:4], 1e-9, f"savings leaf {leaf}")
+            assert bool(s["cv_ok"][j]) == ok, f"cv_ok leaf {leaf}"
+            if ok:
+                assert_rel(s["cv"][j], want[4:], 1e-9, f"cv leaf {leaf}")
+    return g, o
+
+
+# ---------------------------------------------------------------------------
+def test_device_generator_is_byte_identical_to_reference(gpu_ctx_factory):
+    ctx = gpu_ctx_factory()
+    for cfg in (scenarios.small(seed=52, n_ranks=4, n_iterations=7, jitter=0.1),
+                scenarios.iterative(37, 9, n_kernels=5, seed=11, jitter=0.3),
+                scenarios.c2(n_ranks=3)):
+        d = ref_db(cfg)
+        ref = oracle.read_trace_db(d)
+        ctx.generate_iterative(cfg)
+        g = ctx.traces()
+        for k in ("ts", "ctx", "off", "t_end", "pid"):
+            assert np.array_equal(g[k], ref[k]), f"generator {k} differs"
+        # a rank sub-range is the same bytes as those ranks of the full scenario
+        ctx.generate_iterative(cfg, 1, cfg["n_ranks"])
+        g2 = ctx.traces()
+        a = int(ref["off"][1])
+        assert np.array_equal(g2["ts"], ref["ts"][a:]) and np.array_equal(g2["ctx"], ref["ctx"][a:])
+
+
+def test_trace_db_reader_and_aos_loader_agree(gpu_ctx_factory):
+    ctx = gpu_ctx_factory()
+    d = ref_db(scenarios.small(seed=3, n_ranks=5, n_iterations=4, jitter=0.2))
+    ref = oracle.read_trace_db(d)
+    ctx.load_trace_db(d)
+    g = ctx.traces()
+    for k in ("ts", "ctx", "off", "t_end", "pid"):
+        assert np.array_equal(g[k], ref[k])
+    meta = oracle.read_meta(d)
+    ctx.set_cct(meta["parent"])
+    ctx.load_aos(ref["body"], ref["off"], ref["pid"], ref["t_end"])
+    g = ctx.traces()
+    for k in ("ts", "ctx", "off", "t_end", "pid"):
+        assert np.array_equal(g[k], ref[k])
+    # subset of pids (gathered path)
+    ctx.load_trace_db(d, [4, 2])
+    g = ctx.traces()
+    assert list(g["pid"]) == [2, 4]
+
+
+def test_window_matches_reference_composition(gpu_ctx_factory):
+    """ingest_traces + dur glue + group_aggregate + rematerialize, straight from oracle/_ref."""
+    ctx = gpu_ctx_factory()
+    d = ref_db(scenarios.iterative(50, 20, n_kernels=8, seed=5))
+    tr = oracle.read_trace_db(d)
+    ctx.load_trace_db(d)
+    T = int(tr["t_end"].max())
+    for t0, t1 in ((T // 4, 3 * T // 4), (0, T), (T // 3, T // 3 + 1), (T + 10, T + 20)):
+        ctx.query(Q_WINDOW, t0=t0, t1=t1)
+        g = ctx.window()
+        r = oracle.ref_window(d, t0, t1)
+        row = {int(p): i for i, p in enumerate(tr["pid"])}
+        ti = np.array([row[int(p)] for p in r["wa_pid"]])
+        ci = r["wa_ctx"].astype(np.int64)
+        assert int((g["count"] > 0).sum()) == len(ti)
+        assert np.array_equal(g["count"][ti, ci], r["wa_count"])
+        assert np.array_equal(g["sum"][ti, ci], r["wa_sum"])
+        assert np.array_equal(g["min"][ti, ci], r["wa_min"])
+        assert np.array_equal(g["max"][ti, ci], r["wa_max"])
+        assert np.array_equal(g["mean"][ti, ci], r["wa_mean"])
+        rt = np.array([row[int(p)] for p in r["rm_pid"]], dtype=np.int64)
+        assert np.array_equal(g["incl"][rt, r["rm_ctx"]], r["rm_incl"])
+        assert np.array_equal(g["excl"][rt, r["rm_ctx"]], r["rm_excl"])
+        assert int(((g["incl"] != 0) | (g["excl"] != 0)).sum()) == len(rt)
+        c = ctx.carry()
+        ct = np.array([row[int(p)] for p in r["carry_pid"]])
+        assert np.array_equal(c["has"][ct], r["carry_has"])
+        assert np.array_equal(c["ts"][ct], r["carry_ts"])
+        assert np.array_equal(c["ctx"][ct], r["carry_ctx"])
+
+
+def test_window_rows_match_ingest_traces(gpu_ctx_factory):
+    ctx = gpu_ctx_factory()
+    d = ref_db(scenarios.iterative(30, 10, n_kernels=6, seed=8))
+    tr = oracle.read_trace_db(d)
+    ctx.load_trace_db(d)
+    T = int(tr["t_end"].max())
+    for t0, t1 in ((T // 4, 3 * T // 4), (T // 2, T // 2), (0, 1)):
+        g = ctx.window_rows(t0, t1)
+        r = oracle.ref_window(d, t0, t1, rows=True)
+        assert np.array_equal(g["pid"], r["rows_pid"])
+        assert np.array_equal(g["ts"], r["rows_ts"])
+        assert np.array_equal(g["ctx"], r["rows_ctx"])
+        assert np.array_equal(g["carry"]["has"], r["carry_has"])
+        assert np.array_equal(g["carry"]["ts"], r["carry_ts"])
+    with pytest.raises(PsgError) as e:
+        ctx.window_rows(5, 4)
+    assert e.value.name == "invalid_argument"
+
+
+def test_cube_matches_build_tri_model(gpu_ctx_factory):
+    ctx = gpu_ctx_factory()
+    for cfg, anchor in ((scenarios.small(seed=54, n_ranks=5, n_iterations=6, jitter=0.3), 1),
+                        (scenarios.iterative(40, 30, n_kernels=12, seed=9, spread="gamess"), 1),
+                        (scenarios.small(seed=55, n_ranks=2, n_iterations=3), 0)):
+        d = ref_db(cfg)
+        ctx.load_trace_db(d)
+        ctx.query(Q_CUBE | Q_STATS, anchor=anchor)
+        g = ctx.cube()
+        r = oracle.ref_trimodel(d, anchor)
+        for k in ("node_ids", "incl", "excl", "gap_incl", "gap_excl", "block_offset"):
+            assert np.array_equal(g[k], r[k]), k
+        assert np.array_equal(g["iter_counts"][g["iter_counts"] > 0], r["iter_counts"])
+        s = ctx.stats(float(r["savings_summary"][2]))
+        assert np.array_equal(s["leaves"], r["leaves"])
+        assert_rel(s["savings"].ravel(), r["savings"], 1e-9, "savings")
+        assert_rel(s["summary"], r["savings_summary"], 1e-9, "summary")
+        cv_ok = r["cv_ok"].astype(bool)
+        assert np.array_equal(s["cv_ok"].astype(bool), cv_ok)
+        assert_rel(s["cv"][cv_ok].ravel(), r["cv"].reshape(-1, 2)[cv_ok].ravel(), 1e-9, "cv")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_traces_property(gpu_ctx_factory, seed):
+    """Random CCTs / traces with equal timestamps, repeated contexts inside a
+    warp, empty traces and t_end == last ts: GPU == oracle bit for bit."""
+    rng = np.random.default_rng(seed)
+    ctx = gpu_ctx_factory()
+    n_ctx = int(rng.integers(3, 40))
+    parent = random_cct(rng, n_ctx)
+    tr = random_traces(rng, int(rng.integers(1, 60)), n_ctx, int(rng.integers(1, 900)),
+                       ctx_pool=int(rng.integers(2, n_ctx + 1)), dup_prob=float(rng.random()) * 0.6)
+    ctx.set_cct(parent)
+    ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    T = int(tr["t_end"].max()) if len(tr["t_end"]) else 10
+    for t0, t1 in ((0, T + 1), (T // 3, 2 * T // 3), (T // 2, T // 2), (T // 5, T // 5 + 7)):
+        check_window(ctx, tr, parent, t0, t1)
+    for anchor in sorted({0, 1, int(rng.integers(0, n_ctx)), n_ctx - 1}):
+        check_cube(ctx, tr, parent, anchor)
+
+
+def test_long_traces_cross_many_chunks(gpu_ctx_factory):
+    rng = np.random.default_rng(99)
+    ctx = gpu_ctx_factory()
+    parent = np.array([0xFFFFFFFF, 0, 1, 1, 2, 0], np.uint32)
+    tr = random_traces(rng, 9, 6, 20000, ts_step=30, dup_prob=0.2)
+    ctx.set_cct(parent)
+    ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    T = int(tr["t_end"].max())
+    check_window(ctx, tr, parent, T // 7, T // 2)
+    for anchor in (1, 2, 3):
+        check_cube(ctx, tr, parent, anchor)
+
+
+def test_format_errors_fail_loudly(gpu_ctx_factory):
+    ctx = gpu_ctx_factory()
+    parent = np.array([0xFFFFFFFF, 0, 1], np.uint32)
+    ctx.set_cct(parent)
+    tr = {"ts": np.array([5, 3], np.uint64), "ctx": np.array([1, 2], np.uint32),
+          "off": np.array([0, 2], np.uint64), "t_end": np.array([9], np.uint64),
+          "pid": np.array([1], np.uint32)}
+    with pytest.raises(PsgError) as e:
+        ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    assert e.value.name == "format_error"
+    tr["ts"] = np.array([3, 5], np.uint64)
+    tr["ctx"] = np.array([1, 7], np.uint32)  # dangling ctx
+    with pytest.raises(PsgError):
+        ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    with pytest.raises(PsgError) as e:
+        ctx.set_cct(np.array([0xFFFFFFFF, 2, 0], np.uint32))
+    assert e.value.name == "format_error"
+
+
+def test_c1_window_at_full_size(gpu_ctx_factory):
+    """BASELINE configs[0] at full size: 1,000 x 10,050 events, window [T/4, 3T/4).
+    The reference composition runs here too (a few seconds)."""
+    ctx = gpu_ctx_factory()
+    cfg = scenarios.c1()
+    d = ref_db(cfg)
+    ctx.generate_iterative(cfg)
+    tr = oracle.read_trace_db(d)
+    g = ctx.traces()
+    assert np.array_equal(g["ts"], tr["ts"]) and np.array_equal(g["ctx"], tr["ctx"])
+    T = int(tr["t_end"].max())
+    check_window(ctx, tr, oracle.read_meta(d)["parent"], T // 4, 3 * T // 4)
+
+
+def test_congestion_outliers_match_reference(gpu_ctx_factory):
+    """C4 shape (aurora_like_config): the z-score / top-k selection over node
+    means equals the reference congestion_report outlier group (DBSCAN) and
+    the generator truth; racks equal the injected 22."""
+    ctx = gpu_ctx_factory()
+    cfg = scenarios.aurora(ranks_per_node=10, seed=2025)
+    d = ref_db(cfg)
+    truth = json.load(open(f"{d}/truth.json"))
+    ctx.load_trace_db(d)
+    meta = oracle.read_meta(d)
+    sites = truth["callsite_ctx"]
+    whole = dict(t0=0, t1=2**64 - 1, sites=sites)
+    ctx.query(Q_WINDOW | Q_OUTLIERS | Q_CLAMP_TEND, top_k=0, z_min=1.0, **whole)
+    info = ctx.info
+    rep = json.loads(oracle.ref_congestion_report(d))
+    want_ratio = [s["balance_ratio"] for s in rep["callsites"]]
+    assert [s["ctx_id"] for s in rep["callsites"]] == sites
+    assert info["worst_site"] == rep["worst"]["ctx_id"] == truth["congested_ctx"]
+    assert abs(info["worst_ratio"] - rep["worst"]["balance_ratio"]) <= 1e-9 * rep["worst"]["balance_ratio"]
+    hosts = sorted({h for (_, r, h) in meta["profiles"] if r >= 0})
+    out = ctx.outliers(len(hosts))
+    assert_rel(out["site_ratio"], want_ratio, 1e-9, "balance ratios")
+    got = sorted(hosts[i] for i in out["selected"])
+    assert got == sorted(rep["outlier_group"]["hostnames"]) == sorted(truth["outlier_hostnames"])
+    racks = [int(r[0]) for r in out["racks"]]
+    assert racks == [r["rack"] for r in rep["topology"]["racks"]] == truth["outlier_rack_ids"]
+    assert [int(r[1]) for r in out["racks"]] == [r["nodes"] for r in rep["topology"]["racks"]]
+    # top-k with k = 202 gives the same set
+    ctx.query(Q_WINDOW | Q_OUTLIERS | Q_CLAMP_TEND, top_k=202, **whole)
+    out2 = ctx.outliers(len(hosts))
+    assert sorted(hosts[i] for i in out2["selected"]) == got
+
+
+def test_full_query_all_parts(gpu_ctx_factory):
+    ctx = gpu_ctx_factory()
+    cfg = scenarios.iterative(64, 12, n_kernels=10, seed=21)
+    ctx.generate_iterative(cfg)
+    tr = ctx.traces()
+    parent = np.array([0xFFFFFFFF, 0] + [1] * 10 + [0], np.uint32)
+    node = np.arange(64) // 8
+    ctx.set_nodes(node, 8, 4000 + node // 4, node % 4)
+    T = int(tr["t_end"].max())
+    info = ctx.query(Q_ALL, t0=T // 4, t1=3 * T // 4, anchor=1, sites=[2, 3, 4], top_k=3, z_min=-1e9)
+    assert info["n_kept"] == 64 and info["min_iterations"] == 12
+    w = ctx.window()
+    o = oracle.window(tr, parent, T // 4, 3 * T // 4)
+    for k in WINDOW_KEYS:
+        assert np.array_equal(w[k], o[k])
+    g = ctx.cube()
+    oc = oracle.cube(tr, parent, 1)
+    assert np.array_equal(g["incl"], oc["incl"])
+    vals = np.stack([o["incl"][:, s] for s in (2, 3, 4)])
+    oo = oracle.outliers(vals, node, 8, 3, -1e9)
+    out = ctx.outliers(8)
+    assert info["worst_site"] == [2, 3, 4][oo["worst"]]
+    assert_rel(out["site_ratio"], oo["site_ratio"], 1e-12, "site ratio")
+    assert_rel(out["node_mean"], oo["node_mean"], 1e-12, "node mean")
+    assert np.array_equal(out["selected"], oo["selected"])
