@@ -101,7 +101,7 @@ def test_window_matches_reference_composition(gpu_ctx_factory):
         g = ctx.window()
         r = oracle.ref_window(d, t0, t1)
         row = {int(p): i for i, p in enumerate(tr["pid"])}
-        ti = np.array([row[int(p)] for p in r["wa_pid"]])
+        ti = np.array([row[int(p)] for p in r["wa_pid"]], dtype=np.int64)
         ci = r["wa_ctx"].astype(np.int64)
         assert int((g["count"] > 0).sum()) == len(ti)
         assert np.array_equal(g["count"][ti, ci], r["wa_count"])
@@ -114,7 +114,7 @@ def test_window_matches_reference_composition(gpu_ctx_factory):
         assert np.array_equal(g["excl"][rt, r["rm_ctx"]], r["rm_excl"])
         assert int(((g["incl"] != 0) | (g["excl"] != 0)).sum()) == len(rt)
         c = ctx.carry()
-        ct = np.array([row[int(p)] for p in r["carry_pid"]])
+        ct = np.array([row[int(p)] for p in r["carry_pid"]], dtype=np.int64)
         assert np.array_equal(c["has"][ct], r["carry_has"])
         assert np.array_equal(c["ts"][ct], r["carry_ts"])
         assert np.array_equal(c["ctx"][ct], r["carry_ctx"])
