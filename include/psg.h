@@ -113,6 +113,13 @@ ps_status psg_shard(psg_context* ctx, psg_shard_info* out);
 ps_status psg_get_traces(psg_context* ctx, uint64_t* ts, uint32_t* ctx_ids, uint64_t* event_off,
                          uint64_t* t_end, uint32_t* profile_ids);
 
+/* Writes the loaded traces back as a packed trace.db body (12-byte AoS,
+ * n_events * 12 bytes) into host memory (the inverse of K1). */
+ps_status psg_export_aos(psg_context* ctx, void* body);
+/* Process-wide number of psg kernel launches so far (CUB library kernels
+ * are not counted). */
+uint64_t psg_kernel_launches(void);
+
 /* ---- query ------------------------------------------------------------- */
 enum {
   PSG_Q_WINDOW = 1u << 0,      /* (1)+(2): window filter + per-(trace,ctx) aggregates */

@@ -134,6 +134,16 @@ class Context:
                                       _ptr(pid, C.c_uint32)))
         return {"ts": ts, "ctx": cx, "off": off, "t_end": te, "pid": pid}
 
+    def index(self) -> dict:
+        """The trace index only (event offsets, t_end, profile ids)."""
+        n = self.shard()["n_traces"]
+        off = np.empty(n + 1, np.uint64)
+        te = np.empty(n, np.uint64)
+        pid = np.empty(n, np.uint32)
+        check(self.lib.psg_get_traces(self.h, None, None, _ptr(off, C.c_uint64),
+                                      _ptr(te, C.c_uint64), _ptr(pid, C.c_uint32)))
+        return {"off": off, "t_end": te, "pid": pid}
+
     # -- query -----------------------------------------------------------------
     def query(self, flags: int = Q_ALL, t0: int = 0, t1: int = 0, anchor: int = 1, sites=(),
               top_k: int = 0, z_min: float = float("-inf")) -> dict:
@@ -222,6 +232,14 @@ class Context:
         return {"site_ratio": ratio, "node_mean": mean, "node_z": z,
                 "selected": sel[: info["n_outliers"]], "racks": rows[:nr],
                 "chassis_mask": cm[:nr], "full_mask": fm[:nr]}
+
+    def export_aos(self, body_addr: int):
+        """Writes the loaded traces as packed trace.db bytes to host address body_addr."""
+        check(self.lib.psg_export_aos(self.h, C.c_void_p(body_addr)))
+
+    @staticmethod
+    def kernel_launches() -> int:
+        return int(load().psg_kernel_launches())
 
     def window_rows(self, t0: int, t1: int) -> dict:
         n = C.c_uint64()

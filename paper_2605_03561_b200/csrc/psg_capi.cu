@@ -1040,6 +1040,24 @@ ps_status psg_get_outliers(psg_context* c, double* site_ratio, double* node_mean
   });
 }
 
+uint64_t psg_kernel_launches(void) { return kernel_launches(); }
+
+ps_status psg_export_aos(psg_context* c, void* body) {
+  if (!c || (!body && c->n_events)) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    const uint64_t chunk_ev = 4ull << 24;
+    uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, chunk_ev * 12));
+    for (uint64_t done = 0; done < c->n_events; done += chunk_ev) {
+      uint64_t ev = std::min(chunk_ev, c->n_events - done);
+      launch_soa_to_aos(c->d_ts.p + done, c->d_ctx.p + done, ev, stage, c->stream);
+      PSG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(body) + done * 12, stage, ev * 12,
+                               cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+    }
+  });
+}
+
 ps_status psg_window_rows(psg_context* c, uint64_t t0, uint64_t t1, uint64_t* n_rows,
                           uint32_t* row_pid, uint64_t* row_ts, uint32_t* row_ctx) {
   if (!c || !n_rows) return PS_E_INVALID_ARGUMENT;

@@ -136,6 +136,13 @@ __host__ __device__ inline uint32_t cta_table_bytes(uint32_t n_ctx, uint32_t nn,
 
 // ---- launchers (psg_kernels.cu) ------------------------------------------
 
+// Process-wide count of psg kernel launches (library kernels such as CUB's
+// scans/sorts are not counted).
+void count_launch(unsigned n = 1);
+unsigned long long kernel_launches();
+void launch_soa_to_aos(const uint64_t* ts, const uint32_t* ctx, uint64_t n_events, uint8_t* body,
+                       cudaStream_t s);
+
 void launch_aos_to_soa(const uint8_t* body, uint64_t n_events, uint64_t* ts, uint32_t* ctx,
                        cudaStream_t s);
 void launch_validate(const trace_view& tr, uint32_t n_ctx, unsigned long long* bad,

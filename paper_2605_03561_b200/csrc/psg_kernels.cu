@@ -21,12 +21,20 @@
 // derived from exact integer sufficient statistics at the end.
 #include <cub/cub.cuh>
 
+#include <atomic>
 #include <climits>
 #include <cstdint>
 
 #include "psg_internal.h"
 
 namespace psg {
+
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}  // namespace
+
+void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+unsigned long long kernel_launches() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
 
@@ -200,6 +208,43 @@ void launch_aos_to_soa(const uint8_t* body, uint64_t n_events, uint64_t* ts, uin
   uint64_t groups = (n_events + 3) / 4;
   unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((groups + 255) / 256, 148ull * 16));
   k_aos_to_soa<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(body), n_events, ts, ctx);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
+// K1 inverse (trace.db body export): SoA -> packed 12-byte AoS.
+__global__ void k_soa_to_aos(const uint64_t* __restrict__ ts, const uint32_t* __restrict__ ctx,
+                             uint64_t n_events, uint4* __restrict__ body) {
+  uint64_t groups = n_events / 4;
+  uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t g = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; g < groups;
+       g += stride) {
+    ulonglong2 t01 = reinterpret_cast<const ulonglong2*>(ts)[2 * g];
+    ulonglong2 t23 = reinterpret_cast<const ulonglong2*>(ts)[2 * g + 1];
+    uint4 cx = reinterpret_cast<const uint4*>(ctx)[g];
+    body[3 * g] = make_uint4(static_cast<uint32_t>(t01.x), static_cast<uint32_t>(t01.x >> 32), cx.x,
+                             static_cast<uint32_t>(t01.y));
+    body[3 * g + 1] = make_uint4(static_cast<uint32_t>(t01.y >> 32), cx.y,
+                                 static_cast<uint32_t>(t23.x), static_cast<uint32_t>(t23.x >> 32));
+    body[3 * g + 2] = make_uint4(cx.z, static_cast<uint32_t>(t23.y),
+                                 static_cast<uint32_t>(t23.y >> 32), cx.w);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n_events - groups * 4) {
+    uint64_t e = groups * 4 + threadIdx.x;
+    uint32_t* w = reinterpret_cast<uint32_t*>(body) + 3 * e;
+    w[0] = static_cast<uint32_t>(ts[e]);
+    w[1] = static_cast<uint32_t>(ts[e] >> 32);
+    w[2] = ctx[e];
+  }
+}
+
+void launch_soa_to_aos(const uint64_t* ts, const uint32_t* ctx, uint64_t n_events, uint8_t* body,
+                       cudaStream_t s) {
+  if (n_events == 0) return;
+  uint64_t groups = (n_events + 3) / 4;
+  unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((groups + 255) / 256, 148ull * 16));
+  k_soa_to_aos<<<blocks, 256, 0, s>>>(ts, ctx, n_events, reinterpret_cast<uint4*>(body));
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -227,6 +272,7 @@ void launch_validate(const trace_view& tr, uint32_t n_ctx, unsigned long long* b
                      unsigned long long* first_bad, cudaStream_t s) {
   if (tr.n == 0) return;
   k_validate<<<(tr.n + 7) / 8, 256, 0, s>>>(tr, n_ctx, bad, first_bad);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -366,8 +412,10 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
   if (threads == 0) return;
   unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
   k_gen_chunks<<<blocks, 128, 0, s>>>(a);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
   k_gen_write<<<blocks, 128, 0, s>>>(a);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -424,6 +472,7 @@ void launch_iter_count(const trace_view& tr, const int32_t* sub_pre, uint32_t n_
   (void)n_ctx;
   if (tr.n == 0) return;
   k_iter_count<<<(tr.n + 7) / 8, 256, 0, s>>>(tr, sub_pre, iter_count);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -477,10 +526,12 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
   unsigned long long init[3] = {0ull, 0xFFFFFFFFull, 0ull};
   PSG_CUDA(cudaMemcpyAsync(summary, init, sizeof(init), cudaMemcpyHostToDevice, s));
   k_layout_prep<<<(n + 255) / 256, 256, 0, s>>>(iter_count, n, nn, kept, cells, summary);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
   launch_exclusive_scan_u64(kept, tpos64, n, temp, temp_bytes, s);
   launch_exclusive_scan_u64(cells, block_off, n, temp, temp_bytes, s);
   k_u64_to_u32<<<(n + 255) / 256, 256, 0, s>>>(tpos64, tpos, n);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -767,6 +818,7 @@ void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t
     configured_bytes = static_cast<int>(smem_bytes);
   }
   k_trace_query<<<blocks, p.warps * 32, smem_bytes, s>>>(p);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -838,11 +890,13 @@ void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long 
   double* wbad = wsum + nn;
   if (within_cv) {
     k_within_reduce<<<nn, 256, 0, s>>>(within_cv, within_ok, n_kept_local, nn, wsum, wbad);
+    count_launch();
     PSG_CUDA(cudaGetLastError());
   }
   if (x_sum) {
     k_stats_finalize<<<(nn + 127) / 128, 128, 0, s>>>(x_sum, x_max, x_sq, K, nn, n_kept, wsum, wbad,
                                                       node_out);
+    count_launch();
     PSG_CUDA(cudaGetLastError());
   }
 }
@@ -878,6 +932,7 @@ void launch_window_bounds(const trace_view& tr, uint64_t t0, uint64_t t1, uint64
                           uint8_t* c_has, uint64_t* c_ts, uint32_t* c_ctx, cudaStream_t s) {
   if (tr.n == 0) return;
   k_window_bounds<<<(tr.n + 255) / 256, 256, 0, s>>>(tr, t0, t1, cnt, c_has, c_ts, c_ctx);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -902,6 +957,7 @@ void launch_window_copy(const trace_view& tr, const uint32_t* pid, uint64_t t0,
                         uint32_t* out_ctx, cudaStream_t s) {
   if (tr.n == 0) return;
   k_window_copy<<<(tr.n + 7) / 8, 256, 0, s>>>(tr, pid, t0, row_off, out_pid, out_ts, out_ctx);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -962,6 +1018,7 @@ void launch_outliers(const uint64_t* w_incl, uint32_t n_traces, uint32_t n_ctx,
       k_node_acc<<<(n_traces + 255) / 256, 256, 0, s>>>(w_incl, n_traces, n_ctx, site_ctx, worst,
                                                         node_of_trace, node_acc);
   }
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 
@@ -1028,10 +1085,12 @@ void launch_node_select(const unsigned long long* node_acc, uint32_t n_nodes, ui
   ids_in = reinterpret_cast<uint32_t*>(k_out + n_nodes);
   temp = reinterpret_cast<uint8_t*>(ids_in + n_nodes + 8);
   k_node_stats<<<1, 1024, 0, s>>>(node_acc, n_nodes, node_mean, node_z, k_in, ids_in);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
   PSG_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, k_in, k_out, ids_in, order,
                                                      static_cast<int>(n_nodes), 0, 64, s));
   k_node_cut<<<1, 1024, 0, s>>>(order, node_z, n_nodes, top_k, z_min, n_sel);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
   PSG_CUDA(cudaFreeAsync(k_in, s));
 }
@@ -1080,6 +1139,7 @@ void launch_topology(const uint32_t* selected, const uint32_t* n_sel, const uint
                                   static_cast<int>(sm)));
   k_topology<<<1, 512, sm, s>>>(selected, n_sel, node_rack_idx, node_chassis, uni_cnt, n_racks,
                                 rack_nodes, rack_mask, rack_full);
+  count_launch();
   PSG_CUDA(cudaGetLastError());
 }
 

@@ -120,8 +120,26 @@ def events_per_trace(cfg: dict) -> int:
     return cfg["n_iterations"] * (len(cfg["kernels"]) + 2 + (1 if cfg.get("copy_segment_s", 0) > 0 else 0))
 
 
+def device_scenario(n_ranks: int, n_iterations: int, *, n_kernels: int = N_KERNELS,
+                    spread: str = "ladder", jitter: float = 0.1, copy_segment_s: float = 1e-4,
+                    seed: int = 1) -> dict:
+    """Compact form of iterative() for the device generator (no per-kernel
+    JSON lists; the ladder is shared by every kernel, spread_kernel_stride 0)."""
+    f = (ladder_spread if spread == "ladder" else gamess_spread)(n_ranks)
+    return {"n_ranks": n_ranks, "n_iterations": n_iterations, "copy_segment_s": copy_segment_s,
+            "seed": seed, "device": (np.array(kernel_means(n_kernels), np.float64),
+                                     np.full(n_kernels, jitter, np.float64),
+                                     np.ascontiguousarray(f, np.float64), 0)}
+
+
+def c2_device(n_ranks: int = 100_000) -> dict:
+    return device_scenario(n_ranks, 746, seed=1)
+
+
 def device_params(cfg: dict):
     """(mean[k], jitter[k], spread[k][r] or None, stride) for psg_generate_iterative."""
+    if "device" in cfg:
+        return cfg["device"]
     ks = cfg["kernels"]
     n = cfg["n_ranks"]
     mean = np.array([k["mean_time_s"] for k in ks], dtype=np.float64)
