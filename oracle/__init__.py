@@ -46,7 +46,7 @@ def orc():
         lib = C.CDLL(build_oracle())
         lib.orc_window.restype = None
         lib.orc_window.argtypes = [U64P, U64P, U32P, C.c_uint32, U32P, C.c_uint32, C.c_uint64,
-                                   C.c_uint64, U64P, I64P, I64P, I64P, F64P, I64P, I64P, U8P, U64P,
+                                   C.c_uint64, U64P, U64P, I64P, I64P, I64P, F64P, I64P, I64P, U8P, U64P,
                                    U32P]
         lib.orc_iter_counts.restype = None
         lib.orc_iter_counts.argtypes = [U64P, U64P, U32P, U64P, C.c_uint32, U32P, C.c_uint32,
@@ -68,7 +68,7 @@ def orc():
 
 # ---- oracle restatement wrappers -------------------------------------------
 
-def window(tr: dict, parent, t0: int, t1: int) -> dict:
+def window(tr: dict, parent, t0: int, t1: int, clamp_tend: bool = False) -> dict:
     n = len(tr["off"]) - 1
     parent = np.ascontiguousarray(parent, np.uint32)
     nc = len(parent)
@@ -77,7 +77,9 @@ def window(tr: dict, parent, t0: int, t1: int) -> dict:
         ("mean", np.float64), ("excl", np.int64), ("incl", np.int64)]}
     has, cts, cctx = np.zeros(n, np.uint8), np.zeros(n, np.uint64), np.zeros(n, np.uint32)
     orc().orc_window(_p(tr["off"], C.c_uint64), _p(tr["ts"], C.c_uint64), _p(tr["ctx"], C.c_uint32),
-                     n, _p(parent, C.c_uint32), nc, t0, t1, _p(out["count"], C.c_uint64),
+                     n, _p(parent, C.c_uint32), nc, t0, t1,
+                     _p(np.ascontiguousarray(tr["t_end"], np.uint64), C.c_uint64) if clamp_tend else None,
+                     _p(out["count"], C.c_uint64),
                      _p(out["sum"], C.c_int64), _p(out["min"], C.c_int64), _p(out["max"], C.c_int64),
                      _p(out["mean"], C.c_double), _p(out["excl"], C.c_int64),
                      _p(out["incl"], C.c_int64), _p(has, C.c_uint8), _p(cts, C.c_uint64),
@@ -155,6 +157,8 @@ def ref():
         lib.refh_free.argtypes = [C.c_void_p]
         lib.refh_default_jobs.restype = C.c_uint
         lib.refh_generate.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.refh_write_traces.argtypes = [C.c_char_p, U32P, C.c_uint32, U32P, U64P, U64P, U32P,
+                                          U64P, C.c_uint32]
         lib.refh_window.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint, C.c_char_p, C.c_int]
         lib.refh_trimodel.argtypes = [C.c_char_p, C.c_int64, C.c_uint, C.c_double, C.c_char_p]
         lib.refh_iterations_report.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.c_int, C.c_uint,
@@ -189,6 +193,18 @@ def ref_generate(cfg: dict, out_dir: str) -> dict:
     p = C.c_void_p()
     _chk(ref().refh_generate(json.dumps(cfg).encode(), out_dir.encode(), C.byref(p)))
     return json.loads(_take(p))
+
+
+def ref_write_traces(tr: dict, parent, out_dir: str) -> None:
+    """store::write_database of raw SoA traces (one profile per trace)."""
+    parent = np.ascontiguousarray(parent, np.uint32)
+    a = {k: np.ascontiguousarray(tr[k], dt) for k, dt in
+         (("pid", np.uint32), ("off", np.uint64), ("ts", np.uint64), ("ctx", np.uint32),
+          ("t_end", np.uint64))}
+    _chk(ref().refh_write_traces(out_dir.encode(), _p(parent, C.c_uint32), len(parent),
+                                 _p(a["pid"], C.c_uint32), _p(a["off"], C.c_uint64),
+                                 _p(a["ts"], C.c_uint64), _p(a["ctx"], C.c_uint32),
+                                 _p(a["t_end"], C.c_uint64), len(a["pid"])))
 
 
 def _load_bins(d: str, spec: dict) -> dict:

@@ -76,14 +76,20 @@ static uint64_t lower_bound(const uint64_t* ts, uint64_t lo, uint64_t hi, uint64
  * same trace or t1, group_aggregate by (trace, ctx) with sum/min/max/mean/
  * count (frame.cpp:290-408; mean = (0.0 + sum)/count in row order), and the
  * time-integrated excl/incl of rematerialize(window, carry, [t0,t1)).
- * Outputs are dense [n][n_ctx]; count == 0 marks an absent group. */
+ * Outputs are dense [n][n_ctx]; count == 0 marks an absent group.
+ * clamp_tend (may be NULL): per-trace t_end; the window end becomes
+ * min(t1, t_end[t]). */
 void orc_window(const uint64_t* off, const uint64_t* ts, const uint32_t* ctx, uint32_t n,
-                const uint32_t* parent, uint32_t n_ctx, uint64_t t0, uint64_t t1, uint64_t* count,
+                const uint32_t* parent, uint32_t n_ctx, uint64_t t0, uint64_t t1_all,
+                const uint64_t* clamp_tend, uint64_t* count,
                 int64_t* sum, int64_t* mn, int64_t* mx, double* mean, int64_t* excl, int64_t* incl,
                 uint8_t* c_has, uint64_t* c_ts, uint32_t* c_ctx) {
   for (uint32_t t = 0; t < n; ++t) {
     const uint64_t b = off[t], e = off[t + 1];
     const size_t base = (size_t)t * n_ctx;
+    /* clamp_tend (psg PSG_Q_CLAMP_TEND): the window ends at min(t1, t_end) per
+     * trace, so [0, t_end) integrates the whole trace like its profile record */
+    const uint64_t t1 = clamp_tend && clamp_tend[t] < t1_all ? clamp_tend[t] : t1_all;
     uint64_t i0 = lower_bound(ts, b, e, t0), i1 = lower_bound(ts, i0, e, t1);
     double* acc = (double*)calloc(n_ctx, sizeof(double));
     for (uint32_t c = 0; c < n_ctx; ++c) {

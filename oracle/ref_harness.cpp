@@ -144,6 +144,33 @@ int refh_generate(const char* config_json, const char* dir, char** truth_out) {
   });
 }
 
+// Writes raw SoA traces as a reference database through the reference's own
+// writer (store::write_database, store.cpp:313-392): contexts from parent[]
+// (kind function), one profile per trace (rank = position, hostname given per
+// trace or "x1000c0s0b0n0"), no profile records.  Lets the golden-vector
+// script pin arbitrary (random, edge-case) trace sets on the reference.
+int refh_write_traces(const char* dir, const uint32_t* parent, uint32_t n_ctx,
+                      const uint32_t* pid, const uint64_t* off, const uint64_t* ts,
+                      const uint32_t* ctx, const uint64_t* t_end, uint32_t n) {
+  return guarded([&] {
+    store::database_image img;
+    img.meta.metrics.push_back({0, store::metric_scope::inclusive, "cputime", "s"});
+    for (uint32_t c = 0; c < n_ctx; ++c)
+      img.meta.contexts.push_back(
+          {c, parent[c], store::ctx_kind::function, "c" + std::to_string(c)});
+    for (uint32_t t = 0; t < n; ++t) {
+      img.meta.profiles.push_back({pid[t], static_cast<int32_t>(t), 0, "x1000c0s0b0n0", 0});
+      img.records.emplace_back();
+      store::trace_data td;
+      td.profile_id = pid[t];
+      td.t_end_ns = t_end[t];
+      for (uint64_t i = off[t]; i < off[t + 1]; ++i) td.events.push_back({ts[i], ctx[i]});
+      img.traces.push_back(std::move(td));
+    }
+    store::write_database(img, dir);
+  });
+}
+
 // Window composition goldens (see file header).
 int refh_window(const char* dir, uint64_t t0, uint64_t t1, unsigned jobs,
                 const char* outdir, int write_rows) {
