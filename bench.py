@@ -208,7 +208,7 @@ def main():
     info = ctx.info
     launches0 = Context.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    main_ms = []
+    main_ms, bounds_ms = [], []
     with ClockSampler(local) as clocks:
         barrier()
         torch.cuda.synchronize()
@@ -216,6 +216,7 @@ def main():
         for _ in range(args.steps):
             info = ctx.query(**q)
             main_ms.append(info["ms_main"])
+            bounds_ms.append(info["ms_bounds"])
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -240,7 +241,8 @@ def main():
                 "frac": achieved / peak, "peak_kind": peak_kind,
                 "traffic": per_ev * events_local if per_ev else None,
                 "kernel": "k_trace_query", "alg_bytes_per_launch": alg_bytes,
-                "kernel_ms": main_s * 1000.0, "kernel_share_of_step": main_s * 1000.0 / (ms / args.steps)}
+                "kernel_ms": main_s * 1000.0, "kernel_share_of_step": main_s * 1000.0 / (ms / args.steps),
+                "pass1_k_bounds_ms": statistics.mean(bounds_ms)}
 
     # end to end through the public API: pinned host trace.db bytes -> HBM ->
     # query -> results back to host, every step.

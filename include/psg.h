@@ -165,7 +165,8 @@ typedef struct psg_query_info {
   uint32_t n_racks;
   /* timing of the last query on the device (CUDA events on psg_stream) */
   float ms_total;
-  float ms_main;                 /* the fused window+cube kernel */
+  float ms_main;                 /* pass 2: the fused window+cube kernel (k_trace_query) */
+  float ms_bounds;               /* pass 1: iteration boundaries (k_bounds), 0 without CUBE */
 } psg_query_info;
 
 ps_status psg_query(psg_context* ctx, const psg_query_spec* spec, psg_query_info* info);

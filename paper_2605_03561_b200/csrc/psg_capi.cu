@@ -155,7 +155,7 @@ struct psg_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 
   // NCCL
   ncclComm_t comm = nullptr;
@@ -186,7 +186,17 @@ struct psg_context {
   uint32_t nn = 0;
   std::vector<uint32_t> node_ids, leaves;
   std::vector<int32_t> h_sub_pre;
-  dbuf<int32_t> d_sub_pre, d_node_pre, d_node_size;
+  uint32_t root_only = 0;  // the anchor is the only internal node of its subtree
+  dbuf<int32_t> d_sub_pre;
+  dbuf<int4> d_node_tab;  // [nn] {preorder position, subtree size, internal?, 0}
+  dbuf<uint32_t> d_contains;  // subtree membership bitset [ceil(n_ctx/32)]
+  uint32_t contains_words = 0;
+
+  // pass-1 boundary regions: trace t owns bidx[cap_off[t], cap_off[t+1])
+  uint32_t cap_div = 16;  // capacity = n_t / cap_div + 16 (2 after an overflow)
+  bool caps_valid = false;
+  dbuf<uint64_t> d_cap_off;
+  dbuf<uint32_t> d_bidx, d_nbounds;
 
   // window results
   bool have_window = false, have_carry = false;
@@ -239,7 +249,28 @@ struct psg_context {
 
 namespace {
 
+// The query kernels read whole 128-bit-aligned block steps and prefetch ahead:
+// event arrays carry this many events of slack past the last event.
+constexpr uint64_t kEventPad = 2048;
+
 void ensure_device(psg_context* c) { PSG_CUDA(cudaSetDevice(c->device)); }
+
+// Per-trace boundary regions for pass 1 (k_bounds).  A trace of n events has
+// at most ceil(n/2) boundaries (two adjacent events cannot both enter the
+// subtree); the default region n/16 + 16 covers iterations of >= 16 events
+// on average and an overflow re-runs pass 1 with the exact bound.
+void build_caps(psg_context* c) {
+  std::vector<uint64_t> cap(c->n_traces + 1, 0);
+  for (uint32_t t = 0; t < c->n_traces; ++t) {
+    const uint64_t n = c->h_off[t + 1] - c->h_off[t];
+    cap[t + 1] = cap[t] + (c->cap_div <= 2 ? (n + 1) / 2 + 1 : n / c->cap_div + 16);
+  }
+  PSG_CUDA(cudaMemcpyAsync(c->d_cap_off.ensure(c->n_traces + 1), cap.data(), 8ull * cap.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+  c->d_bidx.ensure(cap.back() + 1);
+  c->sync();
+  c->caps_valid = true;
+}
 
 void invalidate_results(psg_context* c) {
   c->have_window = c->have_carry = c->have_cube = c->have_stats = c->have_outliers = false;
@@ -273,6 +304,12 @@ void finish_load(psg_context* c) {
   PSG_CUDA(cudaMemcpyAsync(c->d_pid.ensure(c->n_traces + 1), c->h_pid.data(), 4ull * c->n_traces,
                            cudaMemcpyHostToDevice, c->stream));
   if (c->n_ctx == 0) fail(PS_E_INVALID_ARGUMENT, "set the calling-context tree before loading traces");
+  for (uint32_t t = 0; t < c->n_traces; ++t)
+    if (c->h_off[t + 1] - c->h_off[t] >= (1ull << 32))
+      fail(PS_E_INVALID_ARGUMENT, "trace " + std::to_string(c->h_pid[t]) +
+                                      " has 2^32 or more events (boundary indices are 32-bit)");
+  c->caps_valid = false;
+  c->cap_div = 16;
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(c->summary.ensure(4));
   unsigned long long init[2] = {0ull, ~0ull};
   PSG_CUDA(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
@@ -290,8 +327,8 @@ void finish_load(psg_context* c) {
 // Host AoS body -> HBM staging (chunked, double-buffered) -> SoA.
 void load_aos(psg_context* c, const uint8_t* body, uint64_t n_events) {
   c->n_events = n_events;
-  c->d_ts.ensure(n_events + 1);
-  c->d_ctx.ensure(n_events + 4);
+  c->d_ts.ensure(n_events + kEventPad);
+  c->d_ctx.ensure(n_events + kEventPad);
   const uint64_t chunk_ev = 4ull << 24;  // 64 Mi events = 768 MB per chunk
   const uint64_t chunk_bytes = chunk_ev * 12;
   uint8_t* stage = c->d_stage.ensure(std::min<uint64_t>(2 * chunk_bytes, n_events * 12 + 64));
@@ -316,23 +353,31 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
   for (uint32_t id = 0; id < c->n_ctx; ++id)
     if (sub.pre[id] >= 0) c->node_ids.push_back(id);
   c->nn = static_cast<uint32_t>(c->node_ids.size());
-  std::vector<int32_t> npre(c->nn), nsize(c->nn);
+  std::vector<int4> tab(c->nn);
   std::vector<char> has_child(c->n_ctx, 0);
   for (uint32_t id = 1; id < c->n_ctx; ++id) has_child[c->h_parent[id]] = 1;
   c->leaves.clear();
+  uint32_t n_internal = 0;
   for (uint32_t i = 0; i < c->nn; ++i) {
-    npre[i] = sub.pre[c->node_ids[i]];
-    nsize[i] = sub.size[c->node_ids[i]];
-    if (!has_child[c->node_ids[i]]) c->leaves.push_back(c->node_ids[i]);
+    const uint32_t id = c->node_ids[i];
+    tab[i] = make_int4(sub.pre[id], sub.size[id], has_child[id] ? 1 : 0, 0);
+    if (has_child[id])
+      ++n_internal;  // internal: inclusive time = sum over its preorder range
+    else
+      c->leaves.push_back(id);
   }
+  c->root_only = (n_internal == 1 && has_child[anchor]) ? 1u : 0u;
+  c->contains_words = (c->n_ctx + 31) / 32;
+  std::vector<uint32_t> bits(c->contains_words, 0);
+  for (uint32_t id : c->node_ids) bits[id >> 5] |= 1u << (id & 31);
   if (c->leaves.empty()) c->leaves.push_back(anchor);  // itermodel.cpp:216
   c->h_sub_pre = sub.pre;
   PSG_CUDA(cudaMemcpyAsync(c->d_sub_pre.ensure(c->n_ctx), sub.pre.data(), 4ull * c->n_ctx,
                            cudaMemcpyHostToDevice, c->stream));
-  PSG_CUDA(cudaMemcpyAsync(c->d_node_pre.ensure(c->nn), npre.data(), 4ull * c->nn,
+  PSG_CUDA(cudaMemcpyAsync(c->d_node_tab.ensure(c->nn), tab.data(), sizeof(int4) * c->nn,
                            cudaMemcpyHostToDevice, c->stream));
-  PSG_CUDA(cudaMemcpyAsync(c->d_node_size.ensure(c->nn), nsize.data(), 4ull * c->nn,
-                           cudaMemcpyHostToDevice, c->stream));
+  PSG_CUDA(cudaMemcpyAsync(c->d_contains.ensure(c->contains_words), bits.data(),
+                           4ull * c->contains_words, cudaMemcpyHostToDevice, c->stream));
   c->sync();
   c->cached_anchor = anchor;
 }
@@ -648,8 +693,8 @@ ps_status psg_generate_iterative(psg_context* c, const psg_iter_scenario* s, uin
       PSG_CUDA(cudaMemcpyAsync(gp + 2 * nk, s->spread, 8ull * spread_n, cudaMemcpyHostToDevice,
                                c->stream));
     const uint64_t copy_ns = static_cast<uint64_t>(std::llround(s->copy_segment_s * 1e9));
-    c->d_ts.ensure(c->n_events + 1);
-    c->d_ctx.ensure(c->n_events + 4);
+    c->d_ts.ensure(c->n_events + kEventPad);
+    c->d_ctx.ensure(c->n_events + kEventPad);
     c->d_tend.ensure(n_local + 1);
     const uint32_t chunks = (s->n_iterations + 15) / 16;
     uint64_t* scratch = c->gen_chunks.ensure(static_cast<uint64_t>(n_local) * chunks + 1);
@@ -750,13 +795,34 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       compute_subtree(c, q->anchor_ctx);
       nn = c->nn;
       uint32_t* ic = c->iter_count.ensure(n + 1);
-      launch_iter_count(c->view(), c->d_sub_pre.p, c->n_ctx, ic, s);
-      const size_t sb = cube_layout_scratch_bytes(n);
+      // pass 1: iteration boundaries (re-run with exact region bounds on overflow)
       unsigned long long* sum = c->summary.ensure(4);
+      unsigned long long h[4];
+      PSG_CUDA(cudaEventRecord(c->ev[4], s));
+      for (;;) {
+        if (!c->caps_valid) build_caps(c);
+        bound_params bp{};
+        bp.tr = c->view();
+        bp.contains = c->d_contains.p;
+        bp.words = c->contains_words;
+        bp.cap_off = c->d_cap_off.p;
+        bp.bidx = c->d_bidx.p;
+        bp.n_bounds = c->d_nbounds.ensure(n + 1);
+        bp.iter_count = ic;
+        bp.overflow = sum + 3;
+        PSG_CUDA(cudaMemsetAsync(sum + 3, 0, 8, s));
+        launch_bounds(bp, s);
+        PSG_CUDA(cudaMemcpyAsync(&h[3], sum + 3, 8, cudaMemcpyDeviceToHost, s));
+        c->sync();
+        if (h[3] == 0 || c->cap_div <= 2) break;
+        c->cap_div = 2;
+        c->caps_valid = false;
+      }
+      PSG_CUDA(cudaEventRecord(c->ev[5], s));
+      const size_t sb = cube_layout_scratch_bytes(n);
       launch_cube_layout(ic, n, nn, c->tpos.ensure(n + 1), c->block_off.ensure(n + 1), sum,
                          c->scratch.ensure(sb), sb, s);
-      unsigned long long h[3];
-      PSG_CUDA(cudaMemcpyAsync(h, sum, sizeof(h), cudaMemcpyDeviceToHost, s));
+      PSG_CUDA(cudaMemcpyAsync(h, sum, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       c->sync();
       c->n_kept = static_cast<uint32_t>(h[0]);
       c->n_cells = h[2];
@@ -776,9 +842,12 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       p.do_cube = 1;
       p.store_cube = store_cube ? 1 : 0;
       p.sub_pre = c->d_sub_pre.p;
-      p.node_pre = c->d_node_pre.p;
-      p.node_size = c->d_node_size.p;
+      p.node_tab = c->d_node_tab.p;
       p.nn = nn;
+      p.root_only = c->root_only;
+      p.cap_off = c->d_cap_off.p;
+      p.bidx = c->d_bidx.p;
+      p.n_bounds = c->d_nbounds.p;
       p.iter_count = ic;
       p.tpos = c->tpos.p;
       p.block_off = c->block_off.p;
@@ -902,6 +971,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     }
     PSG_CUDA(cudaEventElapsedTime(&info->ms_total, c->ev[0], c->ev[3]));
     PSG_CUDA(cudaEventElapsedTime(&info->ms_main, c->ev[1], c->ev[2]));
+    if (do_cube) PSG_CUDA(cudaEventElapsedTime(&info->ms_bounds, c->ev[4], c->ev[5]));
   });
 }
 

@@ -63,6 +63,19 @@ struct trace_view {
   uint32_t n;
 };
 
+// Pass 1 (k_bounds): iteration boundaries per trace (itermodel.cpp:111-143).
+struct bound_params {
+  trace_view tr;
+  const uint32_t* contains;  // [ceil(n_ctx/32)] bit c set iff ctx c is in the anchor subtree
+  uint32_t words;
+  const uint64_t* cap_off;   // [n+1] offsets of the per-trace boundary regions in bidx
+  uint32_t* bidx;            // boundary event index, relative to the trace's first event
+  uint32_t* n_bounds;        // [n] boundaries found (may exceed the region capacity)
+  uint32_t* iter_count;      // [n] iterations (n_bounds minus a zero-length last interval)
+  unsigned long long* overflow;  // traces whose boundaries did not fit their region
+};
+
+// Pass 2 (k_trace_query): window + cube + stats in one read of the events.
 struct query_params {
   trace_view tr;
   uint32_t n_ctx;
@@ -79,9 +92,12 @@ struct query_params {
   // cube part
   uint32_t do_cube, store_cube, do_stats;
   const int32_t* sub_pre;    // [n_ctx] preorder position inside the anchor subtree or -1
-  const int32_t* node_pre;   // [nn] per node position (ascending ctx id)
-  const int32_t* node_size;  // [nn]
-  uint32_t nn;               // anchor subtree size (cube nodes)
+  const int4* node_tab;      // [nn] {preorder position, subtree size, internal?, 0}, ascending ctx id
+  uint32_t nn;
+  uint32_t root_only;        // the only internal node is the anchor: incl(anchor) = row total
+  const uint64_t* cap_off;     // pass-1 boundary regions
+  const uint32_t* bidx;
+  const uint32_t* n_bounds;
   const uint32_t* iter_count;  // [n] 0 = skipped
   const uint32_t* tpos;        // [n] position among kept traces
   const uint64_t* block_off;   // [n] cell offset of the trace's first row (kept traces)
@@ -91,46 +107,57 @@ struct query_params {
   unsigned long long *x_sum, *x_max, *x_sq;  // [K][nn], x_sq = 3 limbs [3][K][nn]
   double* within_cv;   // [n_kept][nn]
   uint8_t* within_ok;  // [n_kept][nn]
-  uint32_t G;          // iterations per CTA chunk
+  uint32_t G;          // iterations per chunk (power of two); the row ring holds 2G + gap
   uint32_t warps;      // traces per CTA
 };
 
-// Per-warp shared-memory carve-out sizes (bytes), shared by host and device.
+// Per-warp shared-memory carve-out (bytes), shared by host and device.
 struct warp_smem_layout {
-  uint32_t n_ctx, nn, G;
-  uint32_t off_wcnt, off_wsum, off_wmin, off_wmax, off_wtag;
-  uint32_t off_rows, off_rtag, off_scan, off_tmp, off_wsx, off_wsqlo, off_wsqhi;
+  uint32_t off_rows;   // (2G+1) x nn  u64 cube rows (ring of 2G iterations + the gap row)
+  uint32_t off_rtot;   // 2G+1 u64     row totals (= incl of the anchor when root_only)
+  uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
+  uint32_t off_inrow;  // nn u64       inclusive values of the row being flushed (stats)
+  uint32_t off_bwin;   // 2G+2 u32     boundary window (event indices relative to the trace)
+  uint32_t off_wcnt, off_wslo, off_wshi, off_wmin, off_wmax, off_wnbig;  // n_ctx u32 each
+  uint32_t off_wminb, off_wmaxb;        // n_ctx u64: values >= 2^32
+  uint32_t off_wsx, off_wsqlo, off_wsqhi;  // nn u64: within-trace sums over k < K
+  uint32_t off_carry;  // {u64 ts, u64 dur, u64 (has << 32 | ctx)}
+  uint32_t off_scan;   // 2 x (n_ctx + 1) u64 at finalize (aliases the rows)
   uint32_t bytes;
-  __host__ __device__ void init(uint32_t nctx, uint32_t nnodes, uint32_t g) {
-    n_ctx = nctx;
-    nn = nnodes;
-    G = g;
+  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G) {
     uint32_t o = 0;
     auto take = [&](uint32_t b) {
       uint32_t r = o;
       o += (b + 15u) & ~15u;
       return r;
     };
-    off_wcnt = take(8u * nctx);
-    off_wsum = take(8u * nctx);
-    off_wmin = take(8u * nctx);
-    off_wmax = take(8u * nctx);
-    off_wtag = take(nctx);
-    off_rows = take(8u * (g + 1) * nnodes);
-    off_rtag = take((g + 1) * nnodes);
-    uint32_t m = nctx > nnodes ? nctx : nnodes;
-    off_scan = take(8u * (m + 1));
-    off_tmp = take(8u * m);
-    off_wsx = take(8u * nnodes);
-    off_wsqlo = take(8u * nnodes);
-    off_wsqhi = take(8u * nnodes);
+    const uint32_t rows = 8u * (2 * G + 1) * nn, scan = 16u * (n_ctx + 1);
+    off_rows = take(rows > scan ? rows : scan);
+    off_scan = off_rows;
+    off_rtot = take(8u * (2 * G + 1));
+    off_pref = take(8u * (nn + 1));
+    off_inrow = take(8u * nn);
+    off_bwin = take(4u * (2 * G + 2));
+    off_wcnt = take(4u * n_ctx);
+    off_wslo = take(4u * n_ctx);
+    off_wshi = take(4u * n_ctx);
+    off_wmin = take(4u * n_ctx);
+    off_wmax = take(4u * n_ctx);
+    off_wnbig = take(4u * n_ctx);
+    off_wminb = take(8u * n_ctx);
+    off_wmaxb = take(8u * n_ctx);
+    off_wsx = take(8u * nn);
+    off_wsqlo = take(8u * nn);
+    off_wsqhi = take(8u * nn);
+    off_carry = take(24);
     bytes = o;
   }
 };
 
-// CTA-shared tables placed before the per-warp carve-outs.
+// CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]
+// (int4), then sub_pre, cct_pre, cct_size [n_ctx], then per-warp kept flags.
 __host__ __device__ inline uint32_t cta_table_bytes(uint32_t n_ctx, uint32_t nn, uint32_t warps) {
-  uint32_t b = 4u * n_ctx * 3 + 4u * nn * 2 + 4u * warps * 2;
+  uint32_t b = 16u * nn + 4u * n_ctx * 3 + 4u * warps;
   return (b + 15u) & ~15u;
 }
 
@@ -153,8 +180,7 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
                           uint32_t rank_lo, uint32_t n_local, uint64_t events_per_trace,
                           uint64_t* chunk_scratch, uint64_t* ts, uint32_t* ctx, uint64_t* t_end,
                           cudaStream_t s);
-void launch_iter_count(const trace_view& tr, const int32_t* sub_pre, uint32_t n_ctx,
-                       uint32_t* iter_count, cudaStream_t s);
+void launch_bounds(const bound_params& p, cudaStream_t s);
 void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t* tpos,
                         uint64_t* block_off,
                         unsigned long long* summary /*[0]=kept [1]=min_it [2]=cells*/,

@@ -3,12 +3,7 @@
 //   K1 k_aos_to_soa      trace.db 12-byte AoS -> SoA ts/ctx      (store.cpp:573-580, 678-692)
 //   K1v k_validate       format invariants of the loaded events   (store.cpp:743-761)
 //   K0 k_gen_*           device replay of synthgen's iterative scenario (synthgen.cpp:146-246)
-//   K4a k_iter_count     boundary detection -> iterations per trace (itermodel.cpp:111-143)
-//   K3+K4+K5+K6a k_trace_query  ONE pass over every event: window filter + per-(trace,ctx)
-//                        count/sum/min/max/mean + time integration (ingest.cpp:178-208,
-//                        frame.cpp:290-408, itermodel.cpp:145-183), iteration boundaries and
-//                        the trace x iteration x node cube (itermodel.cpp:242-360), and the
-//                        cross-rank / within-rank sufficient statistics (diagnostics.cpp:83-158)
+//   (the two passes of the fused query, k_bounds and k_trace_query, are in psg_query.cu)
 //   K6b k_within_reduce / k_stats_finalize   savings + CV rows
 //   K2 k_window_bounds / k_window_copy       ingest_traces rows + carry-ins
 //   K7 k_site_acc / k_pick_worst / k_node_acc / k_node_stats   balance ratio, node means,
@@ -42,132 +37,12 @@ constexpr unsigned FULL = 0xffffffffu;
 typedef unsigned long long u64;
 typedef unsigned __int128 u128;
 
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-__device__ __forceinline__ unsigned lanemask_le() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
-  return m;
-}
 __device__ __forceinline__ u64 ldg_u64(const uint64_t* p) {
   return static_cast<u64>(__ldg(reinterpret_cast<const unsigned long long*>(p)));
 }
 __device__ __forceinline__ double u128_to_double(u128 v) {
   return static_cast<double>(static_cast<u64>(v >> 64)) * 18446744073709551616.0 +
          static_cast<double>(static_cast<u64>(v));
-}
-
-// ---------------------------------------------------------------------------
-// Iteration-boundary scan state (itermodel.cpp:111-143).  `inside` is the
-// containment of the previous event; a boundary is a candidate (entering the
-// anchor subtree) whose timestamp is strictly greater than the last accepted
-// boundary, which for sorted timestamps is the same as "no earlier candidate
-// at the same timestamp".
-struct bstate {
-  int k;         // iteration index of the last processed event (-1: gap)
-  int inside;    // containment of the last processed event
-  int has_lct;   // a candidate has been seen
-  u64 lct;       // timestamp of the last candidate
-};
-
-__device__ __forceinline__ int boundary_step(const bstate& st, bool valid, bool in_sub, u64 ts,
-                                             int lane, unsigned& cmask, unsigned& bmask) {
-  int prev_in = __shfl_up_sync(FULL, (int)in_sub, 1);
-  if (lane == 0) prev_in = st.inside;
-  bool cand = valid && in_sub && !prev_in;
-  cmask = __ballot_sync(FULL, cand);
-  unsigned lower = cmask & lanemask_lt();
-  int src = lower ? 31 - __clz(lower) : lane;
-  u64 pts = __shfl_sync(FULL, ts, src);
-  bool have = lower != 0 || st.has_lct;
-  if (lower == 0) pts = st.lct;
-  bool bnd = cand && (!have || pts < ts);
-  bmask = __ballot_sync(FULL, bnd);
-  return st.k + __popc(bmask & lanemask_le());
-}
-
-__device__ __forceinline__ void boundary_advance(bstate& st, int nproc, bool in_sub, unsigned cmask,
-                                                 u64 ts, int ki) {
-  if (nproc <= 0) return;
-  int last = nproc - 1;
-  st.inside = __shfl_sync(FULL, (int)in_sub, last);
-  st.k = __shfl_sync(FULL, ki, last);
-  unsigned pc = cmask & (nproc >= 32 ? FULL : ((1u << nproc) - 1u));
-  if (pc) {
-    st.lct = __shfl_sync(FULL, ts, 31 - __clz(pc));
-    st.has_lct = 1;
-  }
-}
-
-// Warp-private non-atomic accumulation keyed by a small integer.  The fast
-// path is conflict-free (one lane per key, detected with a byte tag table);
-// duplicates fall back to __match_any_sync plus a shuffle fold so that one
-// leader lane writes each key.  All lanes of the warp must call it.
-template <int NV>
-__device__ __forceinline__ void warp_keyed_update(uint8_t* tag, unsigned key, bool flag, int lane,
-                                                 u64 v, u64* sum, u64* cnt, u64* mn, u64* mx) {
-  if (!__any_sync(FULL, flag)) return;
-  if (flag) tag[key] = static_cast<uint8_t>(lane);
-  __syncwarp();
-  bool conf = flag && tag[key] != static_cast<uint8_t>(lane);
-  if (!__any_sync(FULL, conf)) {
-    if (flag) {
-      sum[key] += v;
-      if (NV > 1) {
-        cnt[key] += 1;
-        mn[key] = min(mn[key], v);
-        mx[key] = max(mx[key], v);
-      }
-    }
-  } else {
-    unsigned k2 = flag ? key : (0x80000000u | static_cast<unsigned>(lane));
-    unsigned peers = __match_any_sync(FULL, k2);
-    unsigned others = peers & ~(1u << lane);
-    unsigned rounds = __reduce_max_sync(FULL, static_cast<unsigned>(__popc(others)));
-    u64 s = v, lo = v, hi = v, c = 1;
-    for (unsigned r = 0; r < rounds; ++r) {
-      int src = others ? __ffs(others) - 1 : lane;
-      u64 x = __shfl_sync(FULL, v, src);
-      if (others) {
-        s += x;
-        lo = min(lo, x);
-        hi = max(hi, x);
-        c += 1;
-        others &= others - 1;
-      }
-    }
-    if (flag && lane == __ffs(peers) - 1) {
-      sum[key] += s;
-      if (NV > 1) {
-        cnt[key] += c;
-        mn[key] = min(mn[key], lo);
-        mx[key] = max(mx[key], hi);
-      }
-    }
-  }
-  __syncwarp();
-}
-
-// Warp inclusive scan of u64 over `n` values at src (any order), written as an
-// exclusive-prefix array dst[0..n] (dst[0] = 0).
-__device__ __forceinline__ void warp_prefix(const u64* src, u64* dst, uint32_t n, int lane) {
-  u64 carry = 0;
-  for (uint32_t b = 0; b < n; b += 32) {
-    uint32_t j = b + lane;
-    u64 v = j < n ? src[j] : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      u64 y = __shfl_up_sync(FULL, v, d);
-      if (lane >= d) v += y;
-    }
-    if (j < n) dst[j + 1] = carry + v;
-    carry += __shfl_sync(FULL, v, 31);
-  }
-  if (lane == 0) dst[0] = 0;
-  __syncwarp();
 }
 
 }  // namespace
@@ -419,63 +294,6 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
   PSG_CUDA(cudaGetLastError());
 }
 
-// ===========================================================================
-// K4a: iterations per trace.  One warp per trace streams ctx only; ts is read
-// just for candidate lanes (one per iteration), so the pass costs ~4 B/event.
-__global__ void __launch_bounds__(256) k_iter_count(trace_view tr, const int32_t* __restrict__ sub_pre,
-                                                    uint32_t* __restrict__ iter_count) {
-  uint32_t t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  int lane = threadIdx.x & 31;
-  if (t >= tr.n) return;
-  const u64 b = tr.off[t], e = tr.off[t + 1];
-  bstate st{-1, 0, 0, 0};
-  int nb = 0;
-  u64 b_last = 0;
-  for (u64 base = b; base < e; base += 128) {
-    uint32_t cx[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      u64 i = base + j * 32 + lane;
-      cx[j] = i < e ? __ldg(tr.ctx + i) : 0;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      u64 i0 = base + j * 32;
-      if (i0 >= e) break;
-      u64 i = i0 + lane;
-      bool valid = i < e;
-      bool in_sub = valid && __ldg(sub_pre + cx[j]) >= 0;
-      int prev_in = __shfl_up_sync(FULL, (int)in_sub, 1);
-      if (lane == 0) prev_in = st.inside;
-      bool cand = valid && in_sub && !prev_in;
-      u64 ts = cand ? ldg_u64(tr.ts + i) : 0;
-      unsigned cmask, bmask;
-      int ki = boundary_step(st, valid, in_sub, ts, lane, cmask, bmask);
-      if (bmask) {
-        int lb = 31 - __clz(bmask);
-        b_last = __shfl_sync(FULL, ts, lb);
-        nb += __popc(bmask);
-      }
-      int nvalid = static_cast<int>((e - i0) < 32ull ? (e - i0) : 32ull);
-      boundary_advance(st, nvalid, in_sub, cmask, ts, ki);
-    }
-  }
-  if (lane == 0) {
-    uint32_t it = static_cast<uint32_t>(nb);
-    if (nb > 0 && b_last >= tr.t_end[t]) it -= 1;  // empty last interval dropped
-    iter_count[t] = it;
-  }
-}
-
-void launch_iter_count(const trace_view& tr, const int32_t* sub_pre, uint32_t n_ctx,
-                       uint32_t* iter_count, cudaStream_t s) {
-  (void)n_ctx;
-  if (tr.n == 0) return;
-  k_iter_count<<<(tr.n + 7) / 8, 256, 0, s>>>(tr, sub_pre, iter_count);
-  count_launch();
-  PSG_CUDA(cudaGetLastError());
-}
-
 // Cube layout: kept flags, cell counts, then exclusive scans (CUB).
 __global__ void k_layout_prep(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint64_t* kept,
                               uint64_t* cells, unsigned long long* summary) {
@@ -531,293 +349,6 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
   launch_exclusive_scan_u64(kept, tpos64, n, temp, temp_bytes, s);
   launch_exclusive_scan_u64(cells, block_off, n, temp, temp_bytes, s);
   k_u64_to_u32<<<(n + 255) / 256, 256, 0, s>>>(tpos64, tpos, n);
-  count_launch();
-  PSG_CUDA(cudaGetLastError());
-}
-
-// ===========================================================================
-// K3+K4+K5+K6a: the fused trace pass.
-//
-// A CTA owns `warps` consecutive traces, one warp per trace.  Each warp walks
-// its trace in 32-event steps (lane l <-> event pos+l, 4 steps of ts/ctx in
-// registers per batch) and keeps, in its private shared-memory carve-out:
-//   * the window table cnt/sum/min/max per ctx (non-atomic; conflict-free
-//     fast path, __match_any_sync fold on duplicate keys);
-//   * G+1 cube rows of exclusive ns in anchor-subtree preorder (G iterations
-//     of the current chunk plus the gap row);
-//   * within-trace sums over the first K iterations.
-// The CTA advances in chunks of G iterations: every warp stops at its trace's
-// boundary G*(c+1); rows are then rolled up to inclusive time with one warp
-// prefix scan (preorder makes every subtree a contiguous range), stored to
-// the dense cube, and reduced across the CTA's traces into the cross-rank
-// (iteration, node) statistics with 64-bit global reductions.
-__global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t W = p.warps, n_ctx = p.n_ctx, nn = p.nn, G = p.G;
-
-  int32_t* s_sub_pre = reinterpret_cast<int32_t*>(smem);
-  int32_t* s_cct_pre = s_sub_pre + n_ctx;
-  int32_t* s_cct_size = s_cct_pre + n_ctx;
-  int32_t* s_node_pre = s_cct_size + n_ctx;
-  int32_t* s_node_size = s_node_pre + nn;
-  uint32_t* s_wkept = reinterpret_cast<uint32_t*>(s_node_size + nn);
-
-  warp_smem_layout L;
-  L.init(n_ctx, nn, G);
-  uint8_t* wb = smem + cta_table_bytes(n_ctx, nn, W) + static_cast<size_t>(warp) * L.bytes;
-  u64* wcnt = reinterpret_cast<u64*>(wb + L.off_wcnt);
-  u64* wsum = reinterpret_cast<u64*>(wb + L.off_wsum);
-  u64* wmin = reinterpret_cast<u64*>(wb + L.off_wmin);
-  u64* wmax = reinterpret_cast<u64*>(wb + L.off_wmax);
-  uint8_t* wtag = wb + L.off_wtag;
-  u64* rows = reinterpret_cast<u64*>(wb + L.off_rows);
-  uint8_t* rtag = wb + L.off_rtag;
-  u64* scan = reinterpret_cast<u64*>(wb + L.off_scan);
-  u64* wsx = reinterpret_cast<u64*>(wb + L.off_wsx);
-  u64* wsqlo = reinterpret_cast<u64*>(wb + L.off_wsqlo);
-  u64* wsqhi = reinterpret_cast<u64*>(wb + L.off_wsqhi);
-
-  for (uint32_t i = threadIdx.x; i < n_ctx; i += blockDim.x) {
-    s_sub_pre[i] = p.do_cube ? p.sub_pre[i] : -1;
-    s_cct_pre[i] = p.do_window ? p.cct_pre[i] : 0;
-    s_cct_size[i] = p.do_window ? p.cct_size[i] : 0;
-  }
-  for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
-    s_node_pre[i] = p.node_pre[i];
-    s_node_size[i] = p.node_size[i];
-  }
-  for (uint32_t c = lane; c < n_ctx; c += 32) {
-    wcnt[c] = 0;
-    wsum[c] = 0;
-    wmin[c] = ~0ull;
-    wmax[c] = 0;
-  }
-  for (uint32_t j = lane; j < (G + 1) * nn; j += 32) rows[j] = 0;
-  for (uint32_t j = lane; j < nn; j += 32) {
-    wsx[j] = 0;
-    wsqlo[j] = 0;
-    wsqhi[j] = 0;
-  }
-
-  const uint32_t t = blockIdx.x * W + warp;
-  const bool active = t < p.tr.n;
-  u64 pos = active ? p.tr.off[t] : 0, end = active ? p.tr.off[t + 1] : 0;
-  const u64 tend = active ? p.tr.t_end[t] : 0;
-  const uint32_t iters = (active && p.do_cube) ? p.iter_count[t] : 0;
-  const bool kept = iters > 0;
-  const uint32_t tp = kept ? p.tpos[t] : 0;
-  const u64 bo = kept ? p.block_off[t] : 0;
-  if (lane == 0) s_wkept[warp] = (active && kept) ? 1u : 0u;
-  const u64 t0 = p.t0, t1 = (p.clamp_tend && tend < p.t1) ? tend : p.t1;
-
-  bstate st{-1, 0, 0, 0};
-  bool c_has = false;
-  u64 c_ts = 0, c_d = 0;
-  uint32_t c_ctx = 0;
-  bool wdone = !active || pos >= end;
-  __syncthreads();
-
-  for (uint32_t chunk = 0;; ++chunk) {
-    const int kbase = static_cast<int>(chunk * G);
-    const int k_stop = p.do_cube ? static_cast<int>((chunk + 1) * G) : INT_MAX;
-    if (!wdone) {
-      bool stopped = false;
-      while (!stopped && pos < end) {
-        u64 bts[4];
-        uint32_t bcx[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          u64 i = pos + j * 32 + lane;
-          bool v = i < end;
-          bts[j] = v ? ldg_u64(p.tr.ts + i) : ~0ull;
-          bcx[j] = v ? __ldg(p.tr.ctx + i) : 0u;
-        }
-        u64 tail = (lane == 0 && pos + 128 < end) ? ldg_u64(p.tr.ts + pos + 128) : ~0ull;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const u64 base = pos + j * 32;
-          if (base >= end) break;
-          const u64 i = base + lane;
-          const bool valid = i < end;
-          const u64 tsi = bts[j];
-          const uint32_t ci = bcx[j];
-          u64 nfirst = __shfl_sync(FULL, j + 1 < 4 ? bts[(j + 1) & 3] : tail, 0);
-          u64 nxt = __shfl_down_sync(FULL, tsi, 1);
-          if (lane == 31) nxt = nfirst;
-          const bool is_last = valid && (i + 1 == end);
-          const int nvalid = static_cast<int>((end - base) < 32ull ? (end - base) : 32ull);
-          int nproc = nvalid;
-          int ki = st.k;
-          unsigned cmask = 0, bmask = 0;
-          bool in_sub = false;
-          int pp = -1;
-          if (p.do_cube) {
-            pp = valid ? s_sub_pre[ci] : -1;
-            in_sub = pp >= 0;
-            ki = boundary_step(st, valid, in_sub, tsi, lane, cmask, bmask);
-            unsigned stopm = __ballot_sync(FULL, valid && ki >= k_stop);
-            if (stopm) nproc = __ffs(stopm) - 1;
-            const bool cu = lane < nproc && in_sub && ki < static_cast<int>(iters);
-            const u64 cd = (is_last ? tend : nxt) - tsi;
-            const int slot = ki < 0 ? static_cast<int>(G) : ki - kbase;
-            const unsigned key = cu ? static_cast<unsigned>(slot) * nn + static_cast<unsigned>(pp) : 0u;
-            warp_keyed_update<1>(rtag, key, cu, lane, cd, rows, nullptr, nullptr, nullptr);
-          }
-          const bool act = lane < nproc;
-          if (p.do_window) {
-            const bool carry_here = act && tsi < t0 && (is_last || nxt >= t0);
-            unsigned cm = __ballot_sync(FULL, carry_here);
-            if (cm) {
-              int src = __ffs(cm) - 1;
-              c_has = true;
-              c_ts = __shfl_sync(FULL, tsi, src);
-              c_ctx = __shfl_sync(FULL, ci, src);
-              u64 e2 = __shfl_sync(FULL, is_last ? t1 : min(nxt, t1), src);
-              c_d = e2 > t0 ? e2 - t0 : 0;
-            }
-            const bool in_w = act && tsi >= t0 && tsi < t1;
-            const u64 wd = (is_last ? t1 : min(nxt, t1)) - tsi;
-            warp_keyed_update<4>(wtag, in_w ? ci : 0u, in_w, lane, wd, wsum, wcnt, wmin, wmax);
-          }
-          if (p.do_cube) boundary_advance(st, nproc, in_sub, cmask, tsi, ki);
-          if (nproc < nvalid) {
-            pos = base + nproc;
-            stopped = true;
-            break;
-          }
-        }
-        if (!stopped) pos = min(pos + 128, end);
-      }
-      if (pos >= end) wdone = true;
-    }
-
-    if (p.do_cube) {
-      __syncwarp();
-      if (active && kept) {
-        const int k_hi = min(kbase + static_cast<int>(G), static_cast<int>(iters));
-        for (int k = (chunk == 0 ? -1 : kbase); k < k_hi; ++k) {
-          const int slot = k < 0 ? static_cast<int>(G) : k - kbase;
-          u64* row = rows + static_cast<size_t>(slot) * nn;
-          warp_prefix(row, scan, nn, lane);
-          for (uint32_t n = lane; n < nn; n += 32) {
-            const int pr = s_node_pre[n], sz = s_node_size[n];
-            const u64 ex = scan[pr + 1] - scan[pr], in = scan[pr + sz] - scan[pr];
-            if (k < 0) {
-              p.gap_excl[static_cast<size_t>(tp) * nn + n] = ex;
-              p.gap_incl[static_cast<size_t>(tp) * nn + n] = in;
-            } else {
-              if (p.store_cube) {
-                p.cube_excl[bo + static_cast<u64>(k) * nn + n] = ex;
-                p.cube_incl[bo + static_cast<u64>(k) * nn + n] = in;
-              }
-              if (p.do_stats && static_cast<uint32_t>(k) < p.K) {
-                wsx[n] += in;
-                u128 sq = static_cast<u128>(in) * in;
-                u64 lo = wsqlo[n] + static_cast<u64>(sq);
-                wsqhi[n] += static_cast<u64>(sq >> 64) + (lo < wsqlo[n] ? 1ull : 0ull);
-                wsqlo[n] = lo;
-              }
-            }
-          }
-          __syncwarp();
-          // keep inclusive values in node order for the CTA cross-rank reduction
-          for (uint32_t n = lane; n < nn; n += 32) {
-            const int pr = s_node_pre[n], sz = s_node_size[n];
-            row[n] = scan[pr + sz] - scan[pr];
-          }
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-      if (p.do_stats) {
-        for (uint32_t idx = threadIdx.x; idx < G * nn; idx += blockDim.x) {
-          const uint32_t s = idx / nn, n = idx - s * nn;
-          const uint32_t k = static_cast<uint32_t>(kbase) + s;
-          if (k >= p.K) continue;
-          u64 sum = 0, mx = 0;
-          u128 sq = 0;
-          bool any = false;
-          for (uint32_t w = 0; w < W; ++w) {
-            if (!s_wkept[w]) continue;
-            const u64 v = reinterpret_cast<const u64*>(smem + cta_table_bytes(n_ctx, nn, W) +
-                                                       static_cast<size_t>(w) * L.bytes +
-                                                       L.off_rows)[idx];
-            sum += v;
-            mx = max(mx, v);
-            sq += static_cast<u128>(v) * v;
-            any = true;
-          }
-          if (any) {
-            const size_t cell = static_cast<size_t>(k) * nn + n;
-            const size_t plane = static_cast<size_t>(p.K) * nn;
-            atomicAdd(p.x_sum + cell, sum);
-            atomicMax(p.x_max + cell, mx);
-            const u64 mask43 = (1ull << 43) - 1;
-            atomicAdd(p.x_sq + cell, static_cast<u64>(sq) & mask43);
-            atomicAdd(p.x_sq + plane + cell, static_cast<u64>(sq >> 43) & mask43);
-            atomicAdd(p.x_sq + 2 * plane + cell, static_cast<u64>(sq >> 86));
-          }
-        }
-      }
-      __syncthreads();
-      for (uint32_t j = lane; j < (G + 1) * nn; j += 32) rows[j] = 0;
-      __syncwarp();
-    }
-    if (__syncthreads_and(wdone ? 1 : 0)) break;
-  }
-
-  if (!active) return;
-  if (p.do_window) {
-    // excl incl. the carry-in segment, in CCT preorder, then inclusive roll-up
-    u64* tmp = reinterpret_cast<u64*>(wb + L.off_tmp);
-    for (uint32_t c = lane; c < n_ctx; c += 32) {
-      u64 ex = wsum[c] + ((c_has && c == c_ctx) ? c_d : 0ull);
-      tmp[s_cct_pre[c]] = ex;
-    }
-    __syncwarp();
-    warp_prefix(tmp, scan, n_ctx, lane);
-    const size_t base = static_cast<size_t>(t) * n_ctx;
-    for (uint32_t c = lane; c < n_ctx; c += 32) {
-      const int pr = s_cct_pre[c], sz = s_cct_size[c];
-      const u64 cnt = wcnt[c], sum = wsum[c];
-      p.w_cnt[base + c] = cnt;
-      p.w_sum[base + c] = sum;
-      p.w_min[base + c] = cnt ? wmin[c] : 0ull;
-      p.w_max[base + c] = wmax[c];
-      p.w_mean[base + c] = cnt ? static_cast<double>(sum) / static_cast<double>(cnt) : 0.0;
-      p.w_excl[base + c] = scan[pr + 1] - scan[pr];
-      p.w_incl[base + c] = scan[pr + sz] - scan[pr];
-    }
-    if (lane == 0) {
-      p.c_has[t] = c_has ? 1 : 0;
-      p.c_ts[t] = c_has ? c_ts : 0;
-      p.c_ctx[t] = c_has ? c_ctx : 0;
-    }
-  }
-  if (p.do_stats && kept && p.K > 0) {
-    for (uint32_t n = lane; n < nn; n += 32) {
-      const u64 sx = wsx[n];
-      const u128 sq = (static_cast<u128>(wsqhi[n]) << 64) | wsqlo[n];
-      const u128 num = static_cast<u128>(p.K) * sq - static_cast<u128>(sx) * sx;
-      const bool ok = sx > 0;
-      p.within_cv[static_cast<size_t>(tp) * nn + n] =
-          ok ? 100.0 * sqrt(u128_to_double(num)) / static_cast<double>(sx) : 0.0;
-      p.within_ok[static_cast<size_t>(tp) * nn + n] = ok ? 1 : 0;
-    }
-  }
-}
-
-void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
-  if (p.tr.n == 0) return;
-  unsigned blocks = (p.tr.n + p.warps - 1) / p.warps;
-  static int configured_bytes = 0;
-  if (static_cast<int>(smem_bytes) > configured_bytes) {
-    PSG_CUDA(cudaFuncSetAttribute(k_trace_query, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_bytes)));
-    configured_bytes = static_cast<int>(smem_bytes);
-  }
-  k_trace_query<<<blocks, p.warps * 32, smem_bytes, s>>>(p);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
