@@ -126,7 +126,7 @@ enum {
   PSG_Q_CUBE = 1u << 1,        /* (3): iteration detection + trace x iteration x node cube */
   PSG_Q_STATS = 1u << 2,       /* cross-rank savings / CV over the cube (needs CUBE) */
   PSG_Q_OUTLIERS = 1u << 3,    /* (4): balance ratios, node means, z-score / top-k, topology (needs WINDOW) */
-  PSG_Q_NO_CUBE_STORE = 1u << 8, /* stream cube rows into STATS without materialising them */
+  PSG_Q_NO_CUBE_STORE = 1u << 8, /* store only the incl half of the cube (excl is dropped) */
   PSG_Q_CLAMP_TEND = 1u << 9,    /* window end = min(t1, trace t_end) per trace: whole-trace
                                     integration equals the trace's profile record exactly */
   PSG_Q_ALL = PSG_Q_WINDOW | PSG_Q_CUBE | PSG_Q_STATS | PSG_Q_OUTLIERS

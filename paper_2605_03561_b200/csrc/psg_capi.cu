@@ -218,6 +218,7 @@ struct psg_context {
   dbuf<double> within_cv, node_out;
   dbuf<uint8_t> within_ok;
   bool have_stats = false;
+  bool have_excl = false;  // PSG_Q_NO_CUBE_STORE keeps only the incl half
 
   // outliers
   bool have_outliers = false;
@@ -852,10 +853,11 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       p.tpos = c->tpos.p;
       p.block_off = c->block_off.p;
       p.K = c->K;
-      if (store_cube) {
-        p.cube_incl = c->cube_incl.ensure(c->n_cells + 1);
-        p.cube_excl = c->cube_excl.ensure(c->n_cells + 1);
-      }
+      // incl is always materialised (the cross-rank statistics stream it);
+      // PSG_Q_NO_CUBE_STORE drops the excl half
+      p.cube_incl = c->cube_incl.ensure(c->n_cells + 1);
+      if (store_cube) p.cube_excl = c->cube_excl.ensure(c->n_cells + 1);
+      c->have_excl = store_cube;
       p.gap_incl = c->gap_incl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
       p.gap_excl = c->gap_excl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
       if (do_stats && c->K > 0) {
@@ -872,7 +874,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     }
     // launch geometry
     warp_smem_layout L;
-    L.init(c->n_ctx, nn, p.G);
+    L.init(c->n_ctx, nn, p.G, c->root_only != 0 || !do_cube);
     uint32_t W = choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16));
     p.warps = W;
     uint32_t smem = cta_table_bytes(c->n_ctx, nn, W) + W * L.bytes;
@@ -882,6 +884,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
 
     if (do_stats && c->K > 0) {
       const size_t plane = static_cast<size_t>(c->K) * nn;
+      launch_cross_stats(c->cube_incl.p, c->block_off.p, c->iter_count.p, n, nn, c->K, c->x_acc.p,
+                         c->x_acc.p + plane, c->x_acc.p + 2 * plane, s);
       double* no = c->node_out.ensure(static_cast<size_t>(nn) * 10 + 1);
       // within-rank partial sums per node, then cross-GPU sums of everything
       launch_stats_finalize(nullptr, nullptr, nullptr, c->K, nn, c->n_kept_global, c->within_cv.p,
@@ -1026,8 +1030,8 @@ ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts
       for (uint32_t t = 0; t < c->n_traces; ++t)
         if (ic[t] > 0) block_offset[j++] = bo[t];
     }
-    if ((incl || excl) && !c->cube_incl.p)
-      fail(PS_E_INVALID_ARGUMENT, "cube was streamed (PSG_Q_NO_CUBE_STORE); nothing to copy");
+    if (excl && !c->have_excl)
+      fail(PS_E_INVALID_ARGUMENT, "the excl cube was not stored (PSG_Q_NO_CUBE_STORE)");
     if (incl && c->n_cells)
       PSG_CUDA(cudaMemcpy(incl, c->cube_incl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
     if (excl && c->n_cells)

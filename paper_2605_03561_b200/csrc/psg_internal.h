@@ -112,38 +112,45 @@ struct query_params {
 };
 
 // Per-warp shared-memory carve-out (bytes), shared by host and device.
+// Cube cells and window sums are split into 32-bit words so that the hot
+// loop can use native 32-bit shared reductions (RED) without return values;
+// the overflow guards are the time spans of iterations and block steps (see
+// psg_query.cu).
 struct warp_smem_layout {
-  uint32_t off_rows;   // (2G+1) x nn  u64 cube rows (ring of 2G iterations + the gap row)
+  uint32_t off_rlo, off_rhi;  // (2G+1) x nn u32: cube rows by subtree preorder (ring of 2G + gap)
   uint32_t off_rtot;   // 2G+1 u64     row totals (= incl of the anchor when root_only)
   uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
-  uint32_t off_inrow;  // nn u64       inclusive values of the row being flushed (stats)
+  uint32_t off_inrows; // G x nn u64   inclusive rows kept for the statistics (generic trees)
   uint32_t off_bwin;   // 2G+2 u32     boundary window (event indices relative to the trace)
-  uint32_t off_wcnt, off_wslo, off_wshi, off_wmin, off_wmax, off_wnbig;  // n_ctx u32 each
-  uint32_t off_wminb, off_wmaxb;        // n_ctx u64: values >= 2^32
+  uint32_t off_bts;    // 2G+2 u64     timestamps of those boundaries
+  uint32_t off_wcnt, off_wlo, off_wmin, off_wmax, off_wnbig;  // n_ctx u32 each
+  uint32_t off_wacc, off_wminb, off_wmaxb;                    // n_ctx u64 each
   uint32_t off_wsx, off_wsqlo, off_wsqhi;  // nn u64: within-trace sums over k < K
   uint32_t off_carry;  // {u64 ts, u64 dur, u64 (has << 32 | ctx)}
   uint32_t off_scan;   // 2 x (n_ctx + 1) u64 at finalize (aliases the rows)
   uint32_t bytes;
-  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G) {
+  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G, bool root_only) {
     uint32_t o = 0;
     auto take = [&](uint32_t b) {
       uint32_t r = o;
       o += (b + 15u) & ~15u;
       return r;
     };
-    const uint32_t rows = 8u * (2 * G + 1) * nn, scan = 16u * (n_ctx + 1);
-    off_rows = take(rows > scan ? rows : scan);
-    off_scan = off_rows;
+    const uint32_t rows = 4u * (2 * G + 1) * nn, scan = 16u * (n_ctx + 1);
+    off_rlo = take(rows > scan ? rows : scan);
+    off_scan = off_rlo;
+    off_rhi = take(rows);
     off_rtot = take(8u * (2 * G + 1));
-    off_pref = take(8u * (nn + 1));
-    off_inrow = take(8u * nn);
+    off_pref = take(root_only ? 0u : 8u * (nn + 1));
+    off_inrows = take(root_only ? 0u : 8u * G * nn);
     off_bwin = take(4u * (2 * G + 2));
+    off_bts = take(8u * (2 * G + 2));
     off_wcnt = take(4u * n_ctx);
-    off_wslo = take(4u * n_ctx);
-    off_wshi = take(4u * n_ctx);
+    off_wlo = take(4u * n_ctx);
     off_wmin = take(4u * n_ctx);
     off_wmax = take(4u * n_ctx);
     off_wnbig = take(4u * n_ctx);
+    off_wacc = take(8u * n_ctx);
     off_wminb = take(8u * n_ctx);
     off_wmaxb = take(8u * n_ctx);
     off_wsx = take(8u * nn);
@@ -187,6 +194,9 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
                         void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t cube_layout_scratch_bytes(uint32_t n);
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s);
+void launch_cross_stats(const uint64_t* incl, const uint64_t* block_off, const uint32_t* iter_count,
+                        uint32_t n, uint32_t nn, uint32_t K, unsigned long long* x_sum,
+                        unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s);
 void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,
                            const unsigned long long* x_sq, uint32_t K, uint32_t nn,
                            uint32_t n_kept, const double* within_cv, const uint8_t* within_ok,

@@ -27,6 +27,7 @@
 // Everything on the event stream is integer arithmetic in nanoseconds, which
 // is exact and order-free, so the results are bit-identical to the reference
 // regardless of thread order.
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -203,26 +204,45 @@ void launch_bounds(const bound_params& p, cudaStream_t s) {
 // each, and advances in chunks of G iterations.  Phase 1: every warp consumes
 // events until its trace has passed the end of chunk c (it may run ahead into
 // chunk c+1: the cube rows form a ring of 2G iterations plus the gap row).
-// Phase 2: each warp rolls the chunk's rows up to inclusive time, stores them
-// (coalesced along the node axis) and folds them into its within-rank sums;
-// with statistics on, the CTA then folds its traces into the cross-rank
-// (iteration, node) accumulators.  Without statistics the warps never
-// synchronise with each other.
+// Phase 2: each warp rolls the chunk's rows up to inclusive time and stores
+// them (coalesced along the node axis); with statistics on, the CTA then
+// folds its traces into the within-rank sums and the cross-rank (iteration,
+// node) accumulators.  Without statistics the warps never synchronise.
+//
+// Overflow guards for the 32-bit reductions.  A cube cell sums disjoint
+// segments of one iteration, so it cannot exceed the iteration's time span;
+// a chunk whose iterations all span < 2^32 ns (4.29 s) accumulates with
+// 32-bit REDs into the low words, otherwise with carried 64-bit adds.  The
+// window sums of a block step cannot exceed the block's time span, so the
+// 32-bit pending sums are folded into 64-bit accumulators before the spans
+// added since the last fold can reach 2^32; a block spanning >= 2^32 ns (or
+// holding the trace's last event, whose segment runs to t1) takes the 64-bit
+// path.
 namespace {
 
-enum : int { WIN_NONE = 0, WIN_FULL = 1, WIN_PART = 2 };
+constexpr u64 kSpan32 = 1ull << 32;
+
+enum : int { WIN_NONE = 0, WIN_FULL = 1, WIN_PART = 2, WIN_WIDE = 3 };
 
 struct warp_tables {
-  uint32_t *wcnt, *wslo, *wshi, *wmin, *wmax, *wnbig;
-  u64 *wminb, *wmaxb;
+  uint32_t *wcnt, *wlo, *wmin, *wmax, *wnbig;
+  u64 *wacc, *wminb, *wmaxb;
   u64* carry;
 };
 
 // One window row of duration d for ctx c (frame::group_aggregate's
 // count/sum/min/max fold, order-free in integers).
-__device__ __forceinline__ void win_row(const warp_tables& T, uint32_t c, u64 d) {
+__device__ __forceinline__ void win_row32(const warp_tables& T, uint32_t c, uint32_t d) {
   atomicAdd(T.wcnt + c, 1u);
-  sadd64(T.wslo + c, T.wshi + c, d);
+  atomicAdd(T.wlo + c, d);
+  atomicMin(T.wmin + c, d);
+  atomicMax(T.wmax + c, d);
+}
+
+__device__ __forceinline__ void win_row64(const warp_tables& T, uint32_t c, u64 d) {
+  atomicAdd(T.wcnt + c, 1u);
+  uint32_t* acc = reinterpret_cast<uint32_t*>(T.wacc + c);
+  sadd64(acc, acc + 1, d);
   if (d >> 32) {
     atomicAdd(T.wnbig + c, 1u);
     atomicMin(reinterpret_cast<unsigned long long*>(T.wminb + c), d);
@@ -233,15 +253,25 @@ __device__ __forceinline__ void win_row(const warp_tables& T, uint32_t c, u64 d)
   }
 }
 
-struct run_state {
-  int k;            // iteration of the current event (-1: before the first boundary)
-  uint32_t cnt;     // boundaries of the window at or before the current event
-  int nxt;          // local index of the next boundary
-  bool cube_ok;     // k is a stored iteration (or the gap of a kept trace)
-  uint32_t* rb;     // cube row of k (32-bit words)
-  u64* rt;          // row total of k
-  u64 racc;         // this lane's pending contribution to *rt
-};
+__device__ __forceinline__ void carry_in(const warp_tables& T, uint32_t c, u64 ts, u64 end, u64 t0) {
+  T.carry[0] = ts;
+  T.carry[1] = end > t0 ? end - t0 : 0;
+  T.carry[2] = (1ull << 32) | c;
+}
+
+// x^2 accumulated into a 128-bit (hi, lo) pair; one IMAD.WIDE when x < 2^32.
+__device__ __forceinline__ void acc_sq(u64& lo, u64& hi, u64 x) {
+  if ((x >> 32) == 0) {
+    const u64 q = static_cast<u64>(static_cast<uint32_t>(x)) * static_cast<uint32_t>(x);
+    lo += q;
+    hi += lo < q ? 1ull : 0ull;
+  } else {
+    const u128 q = static_cast<u128>(x) * x;
+    const u64 ql = static_cast<u64>(q);
+    lo += ql;
+    hi += static_cast<u64>(q >> 64) + (lo < ql ? 1ull : 0ull);
+  }
+}
 
 // Boundary event index (relative to the trace) as a local index of the block
 // step starting at `base` (clamped past the step).
@@ -250,57 +280,128 @@ __device__ __forceinline__ int local_of(uint32_t bw, int64_t base) {
   return v > STEP_M ? STEP_M + 1 : static_cast<int>(v);
 }
 
-template <bool WIN, bool CUBE, int WM>
+struct run_state {
+  int k;          // iteration of the current event (-1: before the first boundary)
+  uint32_t cnt;   // boundaries of the window at or before the current event
+  int nxt;        // local index of the next boundary
+  bool cube_ok;   // k is a stored iteration (or the gap of a kept trace)
+  uint32_t slot;  // ring slot of k
+  u64 racc;       // this lane's pending contribution to the row total of k
+};
+
+struct run_ctx {
+  const int32_t* s_sub_pre;
+  const uint32_t* bwin;
+  uint32_t *rlo, *rhi;
+  uint32_t* rtot;  // (lo, hi) word pairs
+  int64_t base;
+  u64 tend, t0, t1w;
+  uint32_t R2, nn;
+  int iters;  // iterations stored for this trace; -1 for a skipped trace (no gap row either)
+  int lb, lo, hi, last_li;
+  bool root_only;
+};
+
+template <bool CWIDE>
+__device__ __forceinline__ void flush_racc(const run_ctx& R, run_state& st) {
+  if (st.racc) {
+    uint32_t* t = R.rtot + 2 * st.slot;
+    if (CWIDE)
+      sadd64(t, t + 1, st.racc);
+    else
+      atomicAdd(t, static_cast<uint32_t>(st.racc));
+    st.racc = 0;
+  }
+}
+
+template <bool WIN, bool CUBE, int WM, bool CWIDE>
 __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
-                                           int lb, int lo, int hi, int last_li, u64 tend, u64 t0,
-                                           u64 t1w, const int32_t* s_sub_pre,
-                                           const uint32_t* bwin, int64_t base, uint32_t R2,
-                                           uint32_t iters, u64* rows, u64* rtot, uint32_t nn,
-                                           bool root_only, run_state& st, const warp_tables& T) {
+                                           const run_ctx& R, run_state& st, const warp_tables& T) {
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
-    const int li = lb + j;
-    const bool valid = static_cast<unsigned>(li - lo) < static_cast<unsigned>(hi - lo);
+    const int li = R.lb + j;
+    const bool valid = static_cast<unsigned>(li - R.lo) < static_cast<unsigned>(R.hi - R.lo);
     const u64 tsj = tv[j], nts = tv[j + 1];
     const uint32_t cj = valid ? cv[j] : 0u;
-    const bool last = li == last_li;
     if (CUBE) {
       if (li >= st.nxt) {  // boundaries are distinct events: at most one per event
-        if (root_only && st.racc) {
-          sadd64(reinterpret_cast<uint32_t*>(st.rt), reinterpret_cast<uint32_t*>(st.rt) + 1,
-                 st.racc);
-          st.racc = 0;
-        }
+        if (R.root_only) flush_racc<CWIDE>(R, st);
         ++st.k;
         ++st.cnt;
-        st.nxt = st.cnt <= R2 ? local_of(bwin[st.cnt], base) : INT_MAX;
-        const uint32_t slot = st.k < 0 ? R2 : (static_cast<uint32_t>(st.k) & (R2 - 1));
-        st.cube_ok = st.k < static_cast<int>(iters);
-        st.rb = reinterpret_cast<uint32_t*>(rows + slot * nn);
-        st.rt = rtot + slot;
+        st.nxt = st.cnt <= R.R2 ? local_of(R.bwin[st.cnt], R.base) : INT_MAX;
+        st.slot = st.k < 0 ? R.R2 : (static_cast<uint32_t>(st.k) & (R.R2 - 1));
+        st.cube_ok = st.k < R.iters;
       }
-      const int pp = s_sub_pre[cj];
+      const int pp = R.s_sub_pre[cj];
       if (valid && pp >= 0 && st.cube_ok) {
-        const u64 dc = (last ? tend : nts) - tsj;
-        sadd64(st.rb + 2 * pp, st.rb + 2 * pp + 1, dc);
-        if (root_only) st.racc += dc;
+        const u64 dc = (li == R.last_li ? R.tend : nts) - tsj;
+        const uint32_t idx = st.slot * R.nn + pp;
+        if (CWIDE)
+          sadd64(R.rlo + idx, R.rhi + idx, dc);
+        else
+          atomicAdd(R.rlo + idx, static_cast<uint32_t>(dc));
+        if (R.root_only) st.racc += dc;
       }
     }
     if (WIN && WM == WIN_FULL) {
-      if (valid) win_row(T, cj, nts - tsj);
-    } else if (WIN && WM == WIN_PART) {
+      if (valid) win_row32(T, cj, static_cast<uint32_t>(nts - tsj));
+    } else if (WIN && WM == WIN_PART) {  // no trace end in this block step
       if (valid) {
-        if (tsj >= t0) {
-          if (tsj < t1w) win_row(T, cj, (last ? t1w : min(nts, t1w)) - tsj);
-        } else if (last || nts >= t0) {  // the carry-in event (store.cpp:667-670): unique
-          const u64 e2 = last ? t1w : min(nts, t1w);
-          T.carry[0] = tsj;
-          T.carry[1] = e2 > t0 ? e2 - t0 : 0;
-          T.carry[2] = (1ull << 32) | cj;
+        if (tsj >= R.t0) {
+          if (tsj < R.t1w) win_row32(T, cj, static_cast<uint32_t>(min(nts, R.t1w) - tsj));
+        } else if (nts >= R.t0) {  // the carry-in event (store.cpp:667-670): unique
+          carry_in(T, cj, tsj, min(nts, R.t1w), R.t0);
+        }
+      }
+    } else if (WIN && WM == WIN_WIDE) {
+      if (valid) {
+        const bool last = li == R.last_li;
+        const u64 e2 = last ? R.t1w : min(nts, R.t1w);
+        if (tsj >= R.t0) {
+          if (tsj < R.t1w) win_row64(T, cj, e2 - tsj);
+        } else if (last || nts >= R.t0) {
+          carry_in(T, cj, tsj, e2, R.t0);
         }
       }
     }
   }
+}
+
+template <bool WIN, bool CUBE, bool CWIDE>
+__device__ __forceinline__ void run_block(int wm, const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
+                                          const run_ctx& R, run_state& st, const warp_tables& T) {
+  if (wm == WIN_FULL)
+    run_events<WIN, CUBE, WIN_FULL, CWIDE>(tv, cv, R, st, T);
+  else if (wm == WIN_PART)
+    run_events<WIN, CUBE, WIN_PART, CWIDE>(tv, cv, R, st, T);
+  else if (wm == WIN_WIDE)
+    run_events<WIN, CUBE, WIN_WIDE, CWIDE>(tv, cv, R, st, T);
+  else
+    run_events<WIN, CUBE, WIN_NONE, CWIDE>(tv, cv, R, st, T);
+  if (CUBE && R.root_only) flush_racc<CWIDE>(R, st);
+}
+
+__device__ __forceinline__ u64 cell64(const uint32_t* lo, const uint32_t* hi, uint32_t i) {
+  return static_cast<u64>(lo[i]) | (static_cast<u64>(hi[i]) << 32);
+}
+
+// Exclusive prefix over a (lo, hi) word row into dst[0..n] (generic roll-up).
+__device__ __forceinline__ void warp_prefix_row(const uint32_t* lo, const uint32_t* hi, u64* dst,
+                                                uint32_t n, int lane) {
+  u64 carry = 0;
+  for (uint32_t b = 0; b < n; b += 32) {
+    const uint32_t j = b + lane;
+    u64 v = j < n ? cell64(lo, hi, j) : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u64 y = __shfl_up_sync(FULL, v, d);
+      if (lane >= d) v += y;
+    }
+    if (j < n) dst[j + 1] = carry + v;
+    carry += __shfl_sync(FULL, v, 31);
+  }
+  if (lane == 0) dst[0] = 0;
+  __syncwarp();
 }
 
 template <bool WIN, bool CUBE>
@@ -314,28 +415,27 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
   int32_t* s_sub_pre = reinterpret_cast<int32_t*>(s_node + nn);
   int32_t* s_cct_pre = s_sub_pre + n_ctx;
   int32_t* s_cct_size = s_cct_pre + n_ctx;
-  uint32_t* s_kept = reinterpret_cast<uint32_t*>(s_cct_size + n_ctx);
 
   warp_smem_layout L;
-  L.init(n_ctx, nn, G);
+  L.init(n_ctx, nn, G, root_only || !CUBE);
   const uint32_t tbl = cta_table_bytes(n_ctx, nn, W);
-  auto wbase = [&](uint32_t w) { return smem + tbl + static_cast<size_t>(w) * L.bytes; };
-  uint8_t* wb = wbase(warp);
-  u64* rows = reinterpret_cast<u64*>(wb + L.off_rows);
+  uint8_t* wb = smem + tbl + static_cast<size_t>(warp) * L.bytes;
+  uint32_t* rlo = reinterpret_cast<uint32_t*>(wb + L.off_rlo);
+  uint32_t* rhi = reinterpret_cast<uint32_t*>(wb + L.off_rhi);
   u64* rtot = reinterpret_cast<u64*>(wb + L.off_rtot);
   u64* pref = reinterpret_cast<u64*>(wb + L.off_pref);
-  u64* inrow = reinterpret_cast<u64*>(wb + L.off_inrow);
   uint32_t* bwin = reinterpret_cast<uint32_t*>(wb + L.off_bwin);
+  u64* bts = reinterpret_cast<u64*>(wb + L.off_bts);
   u64* wsx = reinterpret_cast<u64*>(wb + L.off_wsx);
   u64* wsqlo = reinterpret_cast<u64*>(wb + L.off_wsqlo);
   u64* wsqhi = reinterpret_cast<u64*>(wb + L.off_wsqhi);
   warp_tables T;
   T.wcnt = reinterpret_cast<uint32_t*>(wb + L.off_wcnt);
-  T.wslo = reinterpret_cast<uint32_t*>(wb + L.off_wslo);
-  T.wshi = reinterpret_cast<uint32_t*>(wb + L.off_wshi);
+  T.wlo = reinterpret_cast<uint32_t*>(wb + L.off_wlo);
   T.wmin = reinterpret_cast<uint32_t*>(wb + L.off_wmin);
   T.wmax = reinterpret_cast<uint32_t*>(wb + L.off_wmax);
   T.wnbig = reinterpret_cast<uint32_t*>(wb + L.off_wnbig);
+  T.wacc = reinterpret_cast<u64*>(wb + L.off_wacc);
   T.wminb = reinterpret_cast<u64*>(wb + L.off_wminb);
   T.wmaxb = reinterpret_cast<u64*>(wb + L.off_wmaxb);
   T.carry = reinterpret_cast<u64*>(wb + L.off_carry);
@@ -345,17 +445,17 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
     s_cct_pre[i] = WIN ? p.cct_pre[i] : 0;
     s_cct_size[i] = WIN ? p.cct_size[i] : 0;
   }
-  if (CUBE)
-    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) s_node[i] = p.node_tab[i];
   if (CUBE) {
-    for (uint32_t j = lane; j < (R2 + 1) * nn; j += 32) rows[j] = 0;
+    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) s_node[i] = p.node_tab[i];
+    for (uint32_t j = lane; j < (R2 + 1) * nn; j += 32) rlo[j] = rhi[j] = 0;
     for (uint32_t j = lane; j <= R2; j += 32) rtot[j] = 0;
     for (uint32_t j = lane; j < nn; j += 32) wsx[j] = wsqlo[j] = wsqhi[j] = 0;
   }
   if (WIN) {
     for (uint32_t c = lane; c < n_ctx; c += 32) {
-      T.wcnt[c] = T.wslo[c] = T.wshi[c] = T.wmax[c] = T.wnbig[c] = 0u;
+      T.wcnt[c] = T.wlo[c] = T.wmax[c] = T.wnbig[c] = 0u;
       T.wmin[c] = 0xFFFFFFFFu;
+      T.wacc[c] = 0ull;
       T.wminb[c] = ~0ull;
       T.wmaxb[c] = 0ull;
     }
@@ -374,21 +474,47 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
   const u64 bo = kept ? p.block_off[t] : 0;
   const uint32_t* bt = p.bidx + ((CUBE && active) ? p.cap_off[t] : 0);
   const u64 t0 = p.t0, t1w = (p.clamp_tend && tend < p.t1) ? tend : p.t1;
-  if (lane == 0) s_kept[warp] = kept ? 1u : 0u;
-  u64 pos = 0;  // next unprocessed event, relative to b
+  u64 pos = 0;    // next unprocessed event, relative to b
+  u64 wspan = 0;  // time span added to the 32-bit pending window sums since the last fold
+
+  run_ctx R;
+  R.s_sub_pre = s_sub_pre;
+  R.bwin = bwin;
+  R.rlo = rlo;
+  R.rhi = rhi;
+  R.rtot = reinterpret_cast<uint32_t*>(rtot);
+  R.tend = tend;
+  R.t0 = t0;
+  R.t1w = t1w;
+  R.R2 = R2;
+  R.iters = kept ? static_cast<int>(iters) : -1;
+  R.nn = nn;
+  R.root_only = root_only;
+  R.lb = lane * RM;
   __syncthreads();
 
   for (uint32_t c = 0;; ++c) {
     const uint32_t kb = c * G;
     u64 E1 = n_t, E2 = n_t;
-    if (CUBE) {
+    bool cwide = false;
+    if (CUBE && kept) {
       if (lane <= static_cast<int>(R2)) {
         const u64 k = static_cast<u64>(kb) + lane;
-        bwin[lane] = k < nbd ? __ldg(bt + k) : static_cast<uint32_t>(n_t);
+        const uint32_t bi = k < nbd ? __ldg(bt + k) : static_cast<uint32_t>(n_t);
+        bwin[lane] = bi;
+        bts[lane] = bi < n_t ? ldg64(p.tr.ts + b + bi) : tend;
       }
       __syncwarp();
       E1 = bwin[G];
       E2 = bwin[R2];
+      // iteration spans of the ring (and the gap in chunk 0) decide 32- vs 64-bit cells
+      bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan32;
+      if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan32;
+      cwide = __any_sync(FULL, w);
+    } else if (CUBE && active) {
+      // skipped trace: only the window runs; iterations are not stored
+      if (lane <= static_cast<int>(R2)) bwin[lane] = static_cast<uint32_t>(n_t);
+      __syncwarp();
     }
 
     // ---- phase 1: consume events [pos, E1), possibly running ahead to E2 ----
@@ -396,12 +522,12 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
       const u64 s_abs = (b + pos) & ~3ull;
       const int64_t base = static_cast<int64_t>(s_abs) - static_cast<int64_t>(b);  // >= -3
       const u64 lim = min(static_cast<u64>(base + STEP_M), E2);
-      const int lo = static_cast<int>(static_cast<int64_t>(pos) - base);
-      const int hi = static_cast<int>(static_cast<int64_t>(lim) - base);
+      R.base = base;
+      R.lo = static_cast<int>(static_cast<int64_t>(pos) - base);
+      R.hi = static_cast<int>(static_cast<int64_t>(lim) - base);
       const int64_t lr = static_cast<int64_t>(n_t) - 1 - base;
-      const int last_li = lr < STEP_M ? static_cast<int>(lr) : -1;
-      const int lb = lane * RM;
-      const u64 r0 = s_abs + static_cast<u64>(lb);
+      R.last_li = lr < STEP_M ? static_cast<int>(lr) : -1;
+      const u64 r0 = s_abs + static_cast<u64>(R.lb);
       if (lane == 0 && s_abs + 3 * STEP_M <= e) {
         prefetch_l2(p.tr.ts + s_abs + 2 * STEP_M, 8 * STEP_M);
         prefetch_l2(p.tr.ctx + s_abs + 2 * STEP_M, 4 * STEP_M);
@@ -430,23 +556,47 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
       if (lane == 31) nf = ldg64(p.tr.ts + s_abs + STEP_M);
       tv[RM] = nf;
 
-      // window mode of this block step (warp-uniform)
+      // window class of this block step (warp-uniform)
       int wm = WIN_NONE;
       if (WIN) {
         u64 f = tv[0];
-        if (lo >= 1) f = tv[1];
-        if (lo >= 2) f = tv[2];
-        if (lo >= 3) f = tv[3];
-        const u64 first = __shfl_sync(FULL, f, 0);                // first valid event
-        const u64 after = __shfl_sync(FULL, tv[RM], (hi - 1) >> 3);  // ts after the last valid one
-        const bool has_end = last_li >= 0 && last_li < hi;
-        // "after" bounds the successor timestamp of every valid event
-        if ((first >= t1w && first >= t0) || (!has_end && after < t0))
+        if (R.lo >= 1) f = tv[1];
+        if (R.lo >= 2) f = tv[2];
+        if (R.lo >= 3) f = tv[3];
+        // first valid event and the successor of the last valid one (index hi)
+        u64 a;
+        switch (R.hi & 7) {  // warp-uniform
+          case 0: a = tv[0]; break;
+          case 1: a = tv[1]; break;
+          case 2: a = tv[2]; break;
+          case 3: a = tv[3]; break;
+          case 4: a = tv[4]; break;
+          case 5: a = tv[5]; break;
+          case 6: a = tv[6]; break;
+          default: a = tv[7]; break;
+        }
+        const u64 first = __shfl_sync(FULL, f, 0);
+        const u64 after = R.hi >= STEP_M ? __shfl_sync(FULL, tv[RM], 31)
+                                         : __shfl_sync(FULL, a, R.hi >> 3);
+        const bool has_end = R.last_li >= 0 && R.last_li < R.hi;
+        if ((first >= t1w && first >= t0) || (!has_end && after < t0)) {
           wm = WIN_NONE;
-        else if (!has_end && first >= t0 && after < t1w)
-          wm = WIN_FULL;
-        else
-          wm = WIN_PART;
+        } else if (has_end || after - first >= kSpan32) {
+          wm = WIN_WIDE;
+        } else {
+          const u64 span = after - first;
+          if (wspan + span >= kSpan32) {  // fold the pending 32-bit sums
+            __syncwarp();
+            for (uint32_t x = lane; x < n_ctx; x += 32) {
+              T.wacc[x] += T.wlo[x];
+              T.wlo[x] = 0;
+            }
+            __syncwarp();
+            wspan = 0;
+          }
+          wspan += span;
+          wm = (first >= t0 && after < t1w) ? WIN_FULL : WIN_PART;
+        }
       }
 
       run_state st;
@@ -455,146 +605,126 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
       st.cnt = 0;
       st.nxt = INT_MAX;
       st.cube_ok = false;
-      st.rb = nullptr;
-      st.rt = nullptr;
+      st.slot = R2;
       if (CUBE) {
         // iteration of this lane's first event: boundaries of the window at or before it
         uint32_t cnt = 0;
-        for (uint32_t j = 0; j <= R2; ++j) cnt += lb >= local_of(bwin[j], base) ? 1u : 0u;
+        for (uint32_t j = 0; j <= R2; ++j) cnt += R.lb >= local_of(bwin[j], base) ? 1u : 0u;
         st.cnt = cnt;
         st.k = static_cast<int>(kb) - 1 + static_cast<int>(cnt);
         st.nxt = cnt <= R2 ? local_of(bwin[cnt], base) : INT_MAX;
-        const uint32_t slot = st.k < 0 ? R2 : (static_cast<uint32_t>(st.k) & (R2 - 1));
-        st.cube_ok = st.k < static_cast<int>(iters);
-        st.rb = reinterpret_cast<uint32_t*>(rows + slot * nn);
-        st.rt = rtot + slot;
+        st.slot = st.k < 0 ? R2 : (static_cast<uint32_t>(st.k) & (R2 - 1));
+        st.cube_ok = st.k < R.iters;
       }
-      if (wm == WIN_FULL)
-        run_events<WIN, CUBE, WIN_FULL>(tv, cv, lb, lo, hi, last_li, tend, t0, t1w, s_sub_pre, bwin,
-                                        base, R2, iters, rows, rtot, nn, root_only, st, T);
-      else if (wm == WIN_PART)
-        run_events<WIN, CUBE, WIN_PART>(tv, cv, lb, lo, hi, last_li, tend, t0, t1w, s_sub_pre, bwin,
-                                        base, R2, iters, rows, rtot, nn, root_only, st, T);
+      if (cwide)
+        run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
       else
-        run_events<WIN, CUBE, WIN_NONE>(tv, cv, lb, lo, hi, last_li, tend, t0, t1w, s_sub_pre, bwin,
-                                        base, R2, iters, rows, rtot, nn, root_only, st, T);
-      if (CUBE && root_only && st.racc)
-        sadd64(reinterpret_cast<uint32_t*>(st.rt), reinterpret_cast<uint32_t*>(st.rt) + 1, st.racc);
+        run_block<WIN, CUBE, false>(wm, tv, cv, R, st, T);
       pos = lim;
     }
     __syncwarp();
 
-    // ---- phase 2a: inclusive roll-up, cube stores, within-rank sums ----
+    // ---- phase 2: inclusive roll-up, cube stores (node-contiguous), within-rank sums ----
     const uint32_t k_lo = kb;
     const uint32_t k_hi = min(kb + G, iters);
     const uint32_t n_iter_rows = k_hi > k_lo ? k_hi - k_lo : 0;
+    const uint32_t kcap = (CUBE && p.do_stats && kb < p.K) ? min(n_iter_rows, p.K - kb) : 0;
     if (CUBE && kept) {
-      const uint32_t s0 = k_lo & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
-      const bool stats = p.do_stats && k_lo < p.K;
-      const uint32_t kcap = stats ? min(n_iter_rows, p.K - k_lo) : 0;
-      const u64 ob = bo + static_cast<u64>(k_lo) * nn;
-      const uint32_t n_rows = n_iter_rows + (c == 0 ? 1u : 0u);  // + the gap row
-      for (uint32_t r = 0; r < n_rows; ++r) {
-        const bool gap = r >= n_iter_rows;
-        const uint32_t slot = gap ? R2 : s0 + r;
-        u64* row = rows + slot * nn;
-        if (!root_only) warp_prefix(row, pref, nn, lane);  // generic roll-up over preorder ranges
-        const u64 tot = rtot[slot];
-        for (uint32_t n = lane; n < nn; n += 32) {
+      const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
+      const u64 ob = bo + static_cast<u64>(kb) * nn;
+      if (root_only) {
+        uint32_t r = lane / nn, n = lane - (lane / nn) * nn;
+        for (uint32_t x = lane; x < n_iter_rows * nn; x += 32) {
           const int4 nd = s_node[n];
-          const u64 ex = row[nd.x];
-          const u64 in = !nd.z ? ex : (root_only ? tot : pref[nd.x + nd.y] - pref[nd.x]);
-          if (gap) {
-            p.gap_excl[static_cast<size_t>(tp) * nn + n] = ex;
-            p.gap_incl[static_cast<size_t>(tp) * nn + n] = in;
-          } else {
-            if (p.store_cube) {
-              p.cube_excl[ob + static_cast<u64>(r) * nn + n] = ex;
-              p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
+          const uint32_t slot = s0 + r, idx = slot * nn + nd.x;
+          const u64 ex = cell64(rlo, rhi, idx);
+          const u64 in = nd.z ? rtot[slot] : ex;
+          if (p.store_cube) p.cube_excl[ob + x] = ex;
+          p.cube_incl[ob + x] = in;  // always stored: the cross-rank statistics read it
+          if (r >= kcap) rlo[idx] = rhi[idx] = 0;
+          n += 32;
+          while (n >= nn) {
+            n -= nn;
+            ++r;
+          }
+        }
+        if (kcap) {  // within-rank sums over k < K (iteration_cv_report), one lane per node
+          __syncwarp();
+          for (uint32_t n = lane; n < nn; n += 32) {
+            const int4 nd = s_node[n];
+            u64 sx = 0, ql = 0, qh = 0;
+            for (uint32_t r2 = 0; r2 < kcap; ++r2) {
+              const uint32_t slot = s0 + r2, idx = slot * nn + nd.x;
+              const u64 v = nd.z ? rtot[slot] : cell64(rlo, rhi, idx);
+              rlo[idx] = rhi[idx] = 0;
+              sx += v;
+              acc_sq(ql, qh, v);
+            }
+            wsx[n] += sx;
+            const u64 l2 = wsqlo[n] + ql;
+            wsqhi[n] += qh + (l2 < ql ? 1ull : 0ull);
+            wsqlo[n] = l2;
+          }
+        }
+      } else {
+        for (uint32_t r = 0; r < n_iter_rows; ++r) {
+          const uint32_t slot = s0 + r;
+          warp_prefix_row(rlo + slot * nn, rhi + slot * nn, pref, nn, lane);
+          for (uint32_t n = lane; n < nn; n += 32) {
+            const int4 nd = s_node[n];
+            const u64 ex = cell64(rlo, rhi, slot * nn + nd.x);
+            const u64 in = nd.z ? pref[nd.x + nd.y] - pref[nd.x] : ex;
+            if (p.store_cube) p.cube_excl[ob + static_cast<u64>(r) * nn + n] = ex;
+            p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
+            if (r < kcap) {
+              wsx[n] += in;
+              u64 ql = 0, qh = 0;
+              acc_sq(ql, qh, in);
+              const u64 l2 = wsqlo[n] + ql;
+              wsqhi[n] += qh + (l2 < ql ? 1ull : 0ull);
+              wsqlo[n] = l2;
             }
           }
-          if (!gap && r < kcap) {
-            // within-rank sums (iteration_cv_report) and the value for the
-            // CTA's cross-rank fold, kept (node-indexed) until phase 2b reads it
-            inrow[n] = in;
-            wsx[n] += in;
-            const u128 sq = static_cast<u128>(in) * in;
-            const u64 lo2 = wsqlo[n] + static_cast<u64>(sq);
-            wsqhi[n] += static_cast<u64>(sq >> 64) + (lo2 < wsqlo[n] ? 1ull : 0ull);
-            wsqlo[n] = lo2;
-          }
-        }
-        __syncwarp();
-        // slots [0, kcap) keep their inclusive values for phase 2b (indexed by
-        // node); everything else is released for chunk c + 2 right away
-        if (!gap && r < kcap) {
-          for (uint32_t n = lane; n < nn; n += 32) row[n] = inrow[n];
-        } else {
-          for (uint32_t n = lane; n < nn; n += 32) row[n] = 0;
-        }
-        __syncwarp();
-        if (lane == 0) rtot[slot] = 0;
-      }
-    }
-
-    // ---- phase 2b: cross-rank statistics over k < K (diagnostics.cpp:83-158) ----
-    if (CUBE && p.do_stats) {
-      __syncthreads();
-      if (kb < p.K) {
-        const uint32_t kcap = min(G, p.K - kb);
-        const uint32_t s0 = kb & (R2 - 1);
-        for (uint32_t cell = threadIdx.x; cell < kcap * nn; cell += blockDim.x) {
-          const uint32_t off = (s0 * nn + cell) * 8u + L.off_rows;  // rows are node-indexed now
-          u64 sum = 0, mx = 0, sqlo = 0, sqhi = 0;
-          bool any = false;
-          for (uint32_t w = 0; w < W; ++w) {
-            if (!s_kept[w]) continue;
-            u64* vp = reinterpret_cast<u64*>(wbase(w) + off);
-            const u64 v = *vp;
-            *vp = 0;
-            sum += v;
-            mx = max(mx, v);
-            const u128 sq = static_cast<u128>(v) * v;
-            const u64 l2 = sqlo + static_cast<u64>(sq);
-            sqhi += static_cast<u64>(sq >> 64) + (l2 < sqlo ? 1ull : 0ull);
-            sqlo = l2;
-            any = true;
-          }
-          if (any) {
-            const uint32_t s = cell / nn, n = cell - s * nn;
-            const size_t ci = static_cast<size_t>(kb + s) * nn + n;
-            const size_t plane = static_cast<size_t>(p.K) * nn;
-            const u64 mask43 = (1ull << 43) - 1;
-            atomicAdd(p.x_sum + ci, sum);
-            atomicMax(p.x_max + ci, mx);
-            atomicAdd(p.x_sq + ci, sqlo & mask43);
-            atomicAdd(p.x_sq + plane + ci, ((sqlo >> 43) | (sqhi << 21)) & mask43);
-            const u64 top = sqhi >> 22;
-            if (top) atomicAdd(p.x_sq + 2 * plane + ci, top);
-          }
+          __syncwarp();
+          for (uint32_t n = lane; n < nn; n += 32) rlo[slot * nn + n] = rhi[slot * nn + n] = 0;
+          __syncwarp();
         }
       }
+      if (c == 0) {  // the gap row [first_ts, b_0) (itermodel.cpp:331-338)
+        __syncwarp();
+        if (!root_only) warp_prefix_row(rlo + R2 * nn, rhi + R2 * nn, pref, nn, lane);
+        for (uint32_t n = lane; n < nn; n += 32) {
+          const int4 nd = s_node[n];
+          const u64 ex = cell64(rlo, rhi, R2 * nn + nd.x);
+          const u64 in = !nd.z ? ex : (root_only ? rtot[R2] : pref[nd.x + nd.y] - pref[nd.x]);
+          p.gap_excl[static_cast<size_t>(tp) * nn + n] = ex;
+          p.gap_incl[static_cast<size_t>(tp) * nn + n] = in;
+        }
+        __syncwarp();
+        for (uint32_t n = lane; n < nn; n += 32) rlo[R2 * nn + n] = rhi[R2 * nn + n] = 0;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (c == 0) rtot[R2] = 0;
+        for (uint32_t r = 0; r < n_iter_rows; ++r) rtot[s0 + r] = 0;
+      }
+      __syncwarp();
     }
-    const bool done = pos >= n_t && static_cast<u64>(kb) + G >= iters;
-    if (CUBE && p.do_stats) {
-      if (__syncthreads_and(done ? 1 : 0)) break;
-    } else if (done) {
-      break;
-    }
+    if (pos >= n_t && static_cast<u64>(kb) + G >= iters) break;
   }
 
   if (!active) return;
   if (WIN) {
     // exclusive ns incl. the carry-in segment, in CCT preorder, then the
     // inclusive roll-up: every subtree is a contiguous preorder range
+    __syncwarp();
     u64* tmp = reinterpret_cast<u64*>(wb + L.off_scan);
     u64* scan = tmp + (n_ctx + 1);
     const bool c_has = (T.carry[2] >> 32) != 0;
     const uint32_t c_ctx = static_cast<uint32_t>(T.carry[2]);
     const u64 c_d = T.carry[1];
-    __syncwarp();
     for (uint32_t c = lane; c < n_ctx; c += 32) {
-      const u64 sum = (static_cast<u64>(T.wshi[c]) << 32) | T.wslo[c];
+      const u64 sum = T.wacc[c] + T.wlo[c];
       tmp[s_cct_pre[c]] = sum + ((c_has && c == c_ctx) ? c_d : 0ull);
     }
     __syncwarp();
@@ -603,7 +733,7 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
     for (uint32_t c = lane; c < n_ctx; c += 32) {
       const int pr = s_cct_pre[c], sz = s_cct_size[c];
       const u64 cnt = T.wcnt[c], nbig = T.wnbig[c];
-      const u64 sum = (static_cast<u64>(T.wshi[c]) << 32) | T.wslo[c];
+      const u64 sum = T.wacc[c] + T.wlo[c];
       p.w_cnt[base + c] = cnt;
       p.w_sum[base + c] = sum;
       p.w_min[base + c] = cnt == 0 ? 0ull : (cnt > nbig ? static_cast<u64>(T.wmin[c]) : T.wminb[c]);
@@ -654,6 +784,84 @@ void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t
     launch_variant<true, false>(p, smem_bytes, s);
   else
     launch_variant<false, true>(p, smem_bytes, s);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
+// ===========================================================================
+// Cross-rank (iteration, node) statistics over the stored inclusive cube: the
+// sufficient statistics of node_matrix / savings_report / iteration_cv_report
+// (diagnostics.cpp:83-158) — per cell Σx, max x and Σx² over the kept traces,
+// for k < K (the ordinal intersection).  Grid = (k tiles) x (trace tiles): a
+// thread owns one (k, node) cell of its tile and streams it over the tile's
+// traces (a trace's tile is kt*nn contiguous values, so the loads coalesce);
+// the global atomics happen once per cell per trace tile.
+__global__ void __launch_bounds__(512) k_cross_stats(const uint64_t* __restrict__ incl,
+                                                     const uint64_t* __restrict__ block_off,
+                                                     const uint32_t* __restrict__ iter_count,
+                                                     uint32_t n, uint32_t nn, uint32_t K, uint32_t kt,
+                                                     uint32_t per_tile, unsigned long long* x_sum,
+                                                     unsigned long long* x_max,
+                                                     unsigned long long* x_sq) {
+  const uint32_t k0 = blockIdx.x * kt;
+  const uint32_t kc = min(kt, K - k0);
+  const uint32_t t_lo = blockIdx.y * per_tile, t_hi = min(n, t_lo + per_tile);
+  const size_t plane = static_cast<size_t>(K) * nn;
+  for (uint32_t cell = threadIdx.x; cell < kc * nn; cell += blockDim.x) {
+    const u64 off = static_cast<u64>(k0) * nn + cell;
+    u64 sum = 0, mx = 0, ql = 0, qh = 0;
+    bool any = false;
+    uint32_t t = t_lo;
+    for (; t + 8 <= t_hi; t += 8) {
+      u64 v[8];
+      bool k[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        k[u] = __ldg(iter_count + t + u) > 0;
+        v[u] = k[u] ? ldg64(incl + ldg64(block_off + t + u) + off) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (!k[u]) continue;
+        sum += v[u];
+        mx = max(mx, v[u]);
+        acc_sq(ql, qh, v[u]);
+        any = true;
+      }
+    }
+    for (; t < t_hi; ++t) {
+      if (__ldg(iter_count + t) == 0) continue;
+      const u64 v = ldg64(incl + ldg64(block_off + t) + off);
+      sum += v;
+      mx = max(mx, v);
+      acc_sq(ql, qh, v);
+      any = true;
+    }
+    if (any) {
+      const size_t ci = static_cast<size_t>(off);
+      const u64 mask43 = (1ull << 43) - 1;
+      atomicAdd(x_sum + ci, sum);
+      atomicMax(x_max + ci, mx);
+      atomicAdd(x_sq + ci, ql & mask43);
+      atomicAdd(x_sq + plane + ci, ((ql >> 43) | (qh << 21)) & mask43);
+      const u64 top = qh >> 22;
+      if (top) atomicAdd(x_sq + 2 * plane + ci, top);
+    }
+  }
+}
+
+void launch_cross_stats(const uint64_t* incl, const uint64_t* block_off, const uint32_t* iter_count,
+                        uint32_t n, uint32_t nn, uint32_t K, unsigned long long* x_sum,
+                        unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s) {
+  if (n == 0 || K == 0 || nn == 0) return;
+  const uint32_t kt = nn >= 512 ? 1u : 512u / nn;
+  const uint32_t gx = (K + kt - 1) / kt;
+  uint32_t gy = (4u * 148u + gx - 1) / gx;  // ~4 CTAs per SM in total
+  gy = std::max(1u, std::min(gy, (n + 63) / 64));
+  const uint32_t per_tile = (n + gy - 1) / gy;
+  gy = (n + per_tile - 1) / per_tile;
+  k_cross_stats<<<dim3(gx, gy), 512, 0, s>>>(incl, block_off, iter_count, n, nn, K, kt, per_tile,
+                                            x_sum, x_max, x_sq);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
