@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpsg.so")
+# PSG_LIB overrides the library path (A/B runs of tools/variants.sh builds)
+LIB_PATH = os.environ.get("PSG_LIB") or os.path.join(HERE, "libpsg.so")
 
 # ps_status (reference proj/include/perfslice.h:24-40)
 PS_OK = 0

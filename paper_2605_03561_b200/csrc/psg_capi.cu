@@ -193,10 +193,11 @@ struct psg_context {
   uint32_t contains_words = 0;
 
   // pass-1 boundary regions: trace t owns bidx[cap_off[t], cap_off[t+1])
-  uint32_t cap_div = 16;  // capacity = n_t / cap_div + 16 (2 after an overflow)
+  uint32_t cap_div = 32;  // capacity = n_t / cap_div + 32 (exact bound after an overflow)
   bool caps_valid = false;
   dbuf<uint64_t> d_cap_off;
   dbuf<uint32_t> d_bidx, d_nbounds;
+  dbuf<uint64_t> d_bts;
 
   // window results
   bool have_window = false, have_carry = false;
@@ -258,17 +259,18 @@ void ensure_device(psg_context* c) { PSG_CUDA(cudaSetDevice(c->device)); }
 
 // Per-trace boundary regions for pass 1 (k_bounds).  A trace of n events has
 // at most ceil(n/2) boundaries (two adjacent events cannot both enter the
-// subtree); the default region n/16 + 16 covers iterations of >= 16 events
+// subtree); the default region n/32 + 32 covers iterations of >= 32 events
 // on average and an overflow re-runs pass 1 with the exact bound.
 void build_caps(psg_context* c) {
   std::vector<uint64_t> cap(c->n_traces + 1, 0);
   for (uint32_t t = 0; t < c->n_traces; ++t) {
     const uint64_t n = c->h_off[t + 1] - c->h_off[t];
-    cap[t + 1] = cap[t] + (c->cap_div <= 2 ? (n + 1) / 2 + 1 : n / c->cap_div + 16);
+    cap[t + 1] = cap[t] + (c->cap_div <= 2 ? (n + 1) / 2 + 1 : n / c->cap_div + 32);
   }
   PSG_CUDA(cudaMemcpyAsync(c->d_cap_off.ensure(c->n_traces + 1), cap.data(), 8ull * cap.size(),
                            cudaMemcpyHostToDevice, c->stream));
   c->d_bidx.ensure(cap.back() + 1);
+  c->d_bts.ensure(cap.back() + 1);
   c->sync();
   c->caps_valid = true;
 }
@@ -306,11 +308,11 @@ void finish_load(psg_context* c) {
                            cudaMemcpyHostToDevice, c->stream));
   if (c->n_ctx == 0) fail(PS_E_INVALID_ARGUMENT, "set the calling-context tree before loading traces");
   for (uint32_t t = 0; t < c->n_traces; ++t)
-    if (c->h_off[t + 1] - c->h_off[t] >= (1ull << 32))
+    if (c->h_off[t + 1] - c->h_off[t] >= (1ull << 32) - 4096)
       fail(PS_E_INVALID_ARGUMENT, "trace " + std::to_string(c->h_pid[t]) +
-                                      " has 2^32 or more events (boundary indices are 32-bit)");
+                                      " has 2^32 - 4096 or more events (event indices are 32-bit)");
   c->caps_valid = false;
-  c->cap_div = 16;
+  c->cap_div = 32;
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(c->summary.ensure(4));
   unsigned long long init[2] = {0ull, ~0ull};
   PSG_CUDA(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
@@ -372,8 +374,15 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
   std::vector<uint32_t> bits(c->contains_words, 0);
   for (uint32_t id : c->node_ids) bits[id >> 5] |= 1u << (id & 31);
   if (c->leaves.empty()) c->leaves.push_back(anchor);  // itermodel.cpp:216
-  c->h_sub_pre = sub.pre;
-  PSG_CUDA(cudaMemcpyAsync(c->d_sub_pre.ensure(c->n_ctx), sub.pre.data(), 4ull * c->n_ctx,
+  // cube rows are indexed by node position (ascending ctx id, the output
+  // order); .w of the node table is the inverse map preorder -> node position
+  std::vector<int32_t> npos(c->n_ctx, -1);
+  for (uint32_t i = 0; i < c->nn; ++i) {
+    npos[c->node_ids[i]] = static_cast<int32_t>(i);
+    tab[sub.pre[c->node_ids[i]]].w = static_cast<int32_t>(i);
+  }
+  c->h_sub_pre = npos;
+  PSG_CUDA(cudaMemcpyAsync(c->d_sub_pre.ensure(c->n_ctx), npos.data(), 4ull * c->n_ctx,
                            cudaMemcpyHostToDevice, c->stream));
   PSG_CUDA(cudaMemcpyAsync(c->d_node_tab.ensure(c->nn), tab.data(), sizeof(int4) * c->nn,
                            cudaMemcpyHostToDevice, c->stream));
@@ -383,9 +392,16 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
   c->cached_anchor = anchor;
 }
 
+#ifndef PSG_WMAX
+#define PSG_WMAX 16  // warps (traces) per CTA of k_trace_query (<= its launch bound / 32)
+#endif
+#ifndef PSG_G
+#define PSG_G 4  // iterations per chunk of k_trace_query (power of two)
+#endif
+
 uint32_t choose_warps(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table_bytes) {
   // Aim for >= 2 CTAs per SM worth of traces; fit the carve-outs in 227 KB.
-  uint32_t w = 16;
+  uint32_t w = PSG_WMAX;
   while (w > 1 && static_cast<uint64_t>(n_traces) < 2ull * 148 * w) w /= 2;
   while (w > 1 && table_bytes + w * per_warp_bytes > 227u * 1024) w /= 2;
   if (table_bytes + w * per_warp_bytes > 227u * 1024)
@@ -771,7 +787,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     query_params p{};
     p.tr = c->view();
     p.n_ctx = c->n_ctx;
-    p.G = 4;
+    p.G = PSG_G;
     if (do_window) {
       const size_t cells = static_cast<size_t>(n) * c->n_ctx + 1;
       p.do_window = 1;
@@ -808,6 +824,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
         bp.words = c->contains_words;
         bp.cap_off = c->d_cap_off.p;
         bp.bidx = c->d_bidx.p;
+        bp.bts = c->d_bts.p;
         bp.n_bounds = c->d_nbounds.ensure(n + 1);
         bp.iter_count = ic;
         bp.overflow = sum + 3;
@@ -848,6 +865,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       p.root_only = c->root_only;
       p.cap_off = c->d_cap_off.p;
       p.bidx = c->d_bidx.p;
+      p.bts = c->d_bts.p;
       p.n_bounds = c->d_nbounds.p;
       p.iter_count = ic;
       p.tpos = c->tpos.p;

@@ -70,6 +70,7 @@ struct bound_params {
   uint32_t words;
   const uint64_t* cap_off;   // [n+1] offsets of the per-trace boundary regions in bidx
   uint32_t* bidx;            // boundary event index, relative to the trace's first event
+  uint64_t* bts;             // boundary timestamp (same layout as bidx)
   uint32_t* n_bounds;        // [n] boundaries found (may exceed the region capacity)
   uint32_t* iter_count;      // [n] iterations (n_bounds minus a zero-length last interval)
   unsigned long long* overflow;  // traces whose boundaries did not fit their region
@@ -91,12 +92,14 @@ struct query_params {
   const int32_t* cct_size;  // [n_ctx] subtree size
   // cube part
   uint32_t do_cube, store_cube, do_stats;
-  const int32_t* sub_pre;    // [n_ctx] preorder position inside the anchor subtree or -1
-  const int4* node_tab;      // [nn] {preorder position, subtree size, internal?, 0}, ascending ctx id
+  const int32_t* sub_pre;    // [n_ctx] node position (ascending ctx id) in the anchor subtree or -1
+  const int4* node_tab;      // [nn] {preorder position, subtree size, internal?, node at preorder
+                             //       position n}, indexed by node position
   uint32_t nn;
   uint32_t root_only;        // the only internal node is the anchor: incl(anchor) = row total
   const uint64_t* cap_off;     // pass-1 boundary regions
   const uint32_t* bidx;
+  const uint64_t* bts;
   const uint32_t* n_bounds;
   const uint32_t* iter_count;  // [n] 0 = skipped
   const uint32_t* tpos;        // [n] position among kept traces
@@ -117,7 +120,7 @@ struct query_params {
 // the overflow guards are the time spans of iterations and block steps (see
 // psg_query.cu).
 struct warp_smem_layout {
-  uint32_t off_rlo, off_rhi;  // (2G+1) x nn u32: cube rows by subtree preorder (ring of 2G + gap)
+  uint32_t off_rlo, off_rhi;  // (2G+1) x nn u32: cube rows by node position (ring of 2G + gap)
   uint32_t off_rtot;   // 2G+1 u64     row totals (= incl of the anchor when root_only)
   uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
   uint32_t off_inrows; // G x nn u64   inclusive rows kept for the statistics (generic trees)

@@ -41,8 +41,19 @@ constexpr unsigned FULL = 0xffffffffu;
 typedef unsigned long long u64;
 typedef unsigned __int128 u128;
 
-constexpr int RB = 16;  // events per lane per block step, pass 1 (ctx: 4 x 128-bit loads)
-constexpr int RM = 8;   // events per lane per block step, pass 2 (ts: 4, ctx: 2 x 128-bit loads)
+// Tuning knobs (compile-time; tools/variants.sh builds alternatives for A/B runs).
+#ifndef PSG_RM
+#define PSG_RM 8
+#endif
+#ifndef PSG_LB_THREADS
+#define PSG_LB_THREADS 512
+#endif
+#ifndef PSG_LB_MINB
+#define PSG_LB_MINB 1
+#endif
+
+constexpr int RB = 16;      // events per lane per block step, pass 1 (ctx: 4 x 128-bit loads)
+constexpr int RM = PSG_RM;  // events per lane per block step, pass 2 (ts: RM/2, ctx: RM/4 x 128-bit)
 constexpr int STEP_B = 32 * RB;
 constexpr int STEP_M = 32 * RM;
 
@@ -113,6 +124,7 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   const u64 b = p.tr.off[t], e = p.tr.off[t + 1];
   const u64 cap = p.cap_off[t + 1] - p.cap_off[t];
   uint32_t* out = p.bidx + p.cap_off[t];
+  uint64_t* out_ts = p.bts + p.cap_off[t];
   uint32_t prev_in = 0;  // containment of the event before the block step
   bool have_c = false;   // a candidate has been seen ...
   u64 last_c = 0;        // ... with this timestamp
@@ -176,7 +188,11 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
     const uint32_t tot = __shfl_sync(FULL, inc, 31);
     u64 kk = nb + inc - nbl;
     for (uint32_t m = bm; m; m &= m - 1, ++kk)
-      if (kk < cap) out[kk] = static_cast<uint32_t>(r0 + (__ffs(m) - 1) - b);
+      if (kk < cap) {
+        const int j = __ffs(m) - 1;
+        out[kk] = static_cast<uint32_t>(r0 + j - b);
+        out_ts[kk] = ldg64(p.tr.ts + r0 + j);
+      }
     nb += tot;
     last_c = __shfl_sync(FULL, my_last, 31 - __clz(any));
     have_c = true;
@@ -273,11 +289,13 @@ __device__ __forceinline__ void acc_sq(u64& lo, u64& hi, u64 x) {
   }
 }
 
-// Boundary event index (relative to the trace) as a local index of the block
-// step starting at `base` (clamped past the step).
-__device__ __forceinline__ int local_of(uint32_t bw, int64_t base) {
-  const int64_t v = static_cast<int64_t>(bw) - base;
-  return v > STEP_M ? STEP_M + 1 : static_cast<int>(v);
+// Boundary windows hold event indices relative to the trace plus 3 (the block
+// step start is aligned down by at most 3 events), so all index arithmetic is
+// unsigned 32-bit (traces have < 2^32 - 4096 events).  Local index of a
+// boundary in the block step starting at base3 (clamped past the step).
+__device__ __forceinline__ int local_of(uint32_t bw3, uint32_t base3) {
+  const uint32_t v = bw3 - base3;
+  return v > static_cast<uint32_t>(STEP_M) ? STEP_M + 1 : static_cast<int>(v);
 }
 
 struct run_state {
@@ -286,7 +304,9 @@ struct run_state {
   int nxt;        // local index of the next boundary
   bool cube_ok;   // k is a stored iteration (or the gap of a kept trace)
   uint32_t slot;  // ring slot of k
-  u64 racc;       // this lane's pending contribution to the row total of k
+  uint32_t rowb;  // slot * nn
+  u64 racc;       // this lane's pending contribution to the row total of k (wide chunks)
+  uint32_t racc32;  // the same for 32-bit chunks
 };
 
 struct run_ctx {
@@ -294,7 +314,7 @@ struct run_ctx {
   const uint32_t* bwin;
   uint32_t *rlo, *rhi;
   uint32_t* rtot;  // (lo, hi) word pairs
-  int64_t base;
+  uint32_t base3;  // block step start relative to the trace, + 3
   u64 tend, t0, t1w;
   uint32_t R2, nn;
   int iters;  // iterations stored for this trace; -1 for a skipped trace (no gap row either)
@@ -304,13 +324,13 @@ struct run_ctx {
 
 template <bool CWIDE>
 __device__ __forceinline__ void flush_racc(const run_ctx& R, run_state& st) {
-  if (st.racc) {
-    uint32_t* t = R.rtot + 2 * st.slot;
-    if (CWIDE)
-      sadd64(t, t + 1, st.racc);
-    else
-      atomicAdd(t, static_cast<uint32_t>(st.racc));
+  uint32_t* t = R.rtot + 2 * st.slot;
+  if (CWIDE) {
+    if (st.racc) sadd64(t, t + 1, st.racc);
     st.racc = 0;
+  } else {
+    if (st.racc32) atomicAdd(t, st.racc32);
+    st.racc32 = 0;
   }
 }
 
@@ -328,27 +348,33 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
         if (R.root_only) flush_racc<CWIDE>(R, st);
         ++st.k;
         ++st.cnt;
-        st.nxt = st.cnt <= R.R2 ? local_of(R.bwin[st.cnt], R.base) : INT_MAX;
+        st.nxt = st.cnt <= R.R2 ? local_of(R.bwin[st.cnt], R.base3) : INT_MAX;
         st.slot = st.k < 0 ? R.R2 : (static_cast<uint32_t>(st.k) & (R.R2 - 1));
+        st.rowb = st.slot * R.nn;
         st.cube_ok = st.k < R.iters;
       }
       const int pp = R.s_sub_pre[cj];
       if (valid && pp >= 0 && st.cube_ok) {
-        const u64 dc = (li == R.last_li ? R.tend : nts) - tsj;
-        const uint32_t idx = st.slot * R.nn + pp;
-        if (CWIDE)
+        const uint32_t idx = st.rowb + pp;
+        if (CWIDE) {
+          const u64 dc = (li == R.last_li ? R.tend : nts) - tsj;
           sadd64(R.rlo + idx, R.rhi + idx, dc);
-        else
-          atomicAdd(R.rlo + idx, static_cast<uint32_t>(dc));
-        if (R.root_only) st.racc += dc;
+          if (R.root_only) st.racc += dc;
+        } else {  // the iteration spans < 2^32 ns: 32-bit differences are exact
+          const uint32_t dc = static_cast<uint32_t>(li == R.last_li ? R.tend : nts) -
+                              static_cast<uint32_t>(tsj);
+          atomicAdd(R.rlo + idx, dc);
+          if (R.root_only) st.racc32 += dc;
+        }
       }
     }
-    if (WIN && WM == WIN_FULL) {
-      if (valid) win_row32(T, cj, static_cast<uint32_t>(nts - tsj));
+    if (WIN && WM == WIN_FULL) {  // the block spans < 2^32 ns
+      if (valid) win_row32(T, cj, static_cast<uint32_t>(nts) - static_cast<uint32_t>(tsj));
     } else if (WIN && WM == WIN_PART) {  // no trace end in this block step
       if (valid) {
         if (tsj >= R.t0) {
-          if (tsj < R.t1w) win_row32(T, cj, static_cast<uint32_t>(min(nts, R.t1w) - tsj));
+          if (tsj < R.t1w)
+            win_row32(T, cj, static_cast<uint32_t>(min(nts, R.t1w)) - static_cast<uint32_t>(tsj));
         } else if (nts >= R.t0) {  // the carry-in event (store.cpp:667-670): unique
           carry_in(T, cj, tsj, min(nts, R.t1w), R.t0);
         }
@@ -385,13 +411,14 @@ __device__ __forceinline__ u64 cell64(const uint32_t* lo, const uint32_t* hi, ui
   return static_cast<u64>(lo[i]) | (static_cast<u64>(hi[i]) << 32);
 }
 
-// Exclusive prefix over a (lo, hi) word row into dst[0..n] (generic roll-up).
-__device__ __forceinline__ void warp_prefix_row(const uint32_t* lo, const uint32_t* hi, u64* dst,
-                                                uint32_t n, int lane) {
+// Exclusive prefix, in subtree preorder, over a node-indexed (lo, hi) word row
+// into dst[0..n] (generic roll-up: incl(node) = dst[pre + size] - dst[pre]).
+__device__ __forceinline__ void warp_prefix_row(const uint32_t* lo, const uint32_t* hi,
+                                                const int4* node, u64* dst, uint32_t n, int lane) {
   u64 carry = 0;
   for (uint32_t b = 0; b < n; b += 32) {
     const uint32_t j = b + lane;
-    u64 v = j < n ? cell64(lo, hi, j) : 0;
+    u64 v = j < n ? cell64(lo, hi, static_cast<uint32_t>(node[j].w)) : 0;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const u64 y = __shfl_up_sync(FULL, v, d);
@@ -405,7 +432,7 @@ __device__ __forceinline__ void warp_prefix_row(const uint32_t* lo, const uint32
 }
 
 template <bool WIN, bool CUBE>
-__global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
+__global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(query_params p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t W = p.warps, n_ctx = p.n_ctx, nn = p.nn, G = p.G, R2 = 2 * G;
@@ -472,7 +499,16 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
   const bool kept = iters > 0;
   const uint32_t tp = kept ? p.tpos[t] : 0;
   const u64 bo = kept ? p.block_off[t] : 0;
-  const uint32_t* bt = p.bidx + ((CUBE && active) ? p.cap_off[t] : 0);
+  const u64 region = (CUBE && active) ? p.cap_off[t] : 0;
+  const uint32_t* bt = p.bidx + region;
+  const uint64_t* btt = p.bts + region;
+  uint32_t nx_idx = static_cast<uint32_t>(n_t);  // this lane's entry of the next boundary window
+  u64 nx_ts = tend;
+  if (CUBE && kept && lane <= static_cast<int>(2 * G)) {
+    const bool have = static_cast<uint32_t>(lane) < nbd;
+    nx_idx = have ? __ldg(bt + lane) : static_cast<uint32_t>(n_t);
+    nx_ts = have ? ldg64(btt + lane) : tend;
+  }
   const u64 t0 = p.t0, t1w = (p.clamp_tend && tend < p.t1) ? tend : p.t1;
   u64 pos = 0;    // next unprocessed event, relative to b
   u64 wspan = 0;  // time span added to the 32-bit pending window sums since the last fold
@@ -498,22 +534,26 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
     u64 E1 = n_t, E2 = n_t;
     bool cwide = false;
     if (CUBE && kept) {
+      // boundary window of this chunk (prefetched during the previous one)
       if (lane <= static_cast<int>(R2)) {
-        const u64 k = static_cast<u64>(kb) + lane;
-        const uint32_t bi = k < nbd ? __ldg(bt + k) : static_cast<uint32_t>(n_t);
-        bwin[lane] = bi;
-        bts[lane] = bi < n_t ? ldg64(p.tr.ts + b + bi) : tend;
+        bwin[lane] = nx_idx + 3;  // stored + 3, see local_of
+        bts[lane] = nx_ts;
       }
+      // prefetch the next chunk's window: its loads overlap this chunk's events
+      const u64 k = static_cast<u64>(kb + G) + lane;
+      const bool have = lane <= static_cast<int>(R2) && k < nbd;
+      nx_idx = have ? __ldg(bt + k) : static_cast<uint32_t>(n_t);
+      nx_ts = have ? ldg64(btt + k) : tend;
       __syncwarp();
-      E1 = bwin[G];
-      E2 = bwin[R2];
+      E1 = bwin[G] - 3;
+      E2 = bwin[R2] - 3;
       // iteration spans of the ring (and the gap in chunk 0) decide 32- vs 64-bit cells
       bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan32;
       if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan32;
       cwide = __any_sync(FULL, w);
     } else if (CUBE && active) {
       // skipped trace: only the window runs; iterations are not stored
-      if (lane <= static_cast<int>(R2)) bwin[lane] = static_cast<uint32_t>(n_t);
+      if (lane <= static_cast<int>(R2)) bwin[lane] = static_cast<uint32_t>(n_t) + 3;
       __syncwarp();
     }
 
@@ -522,7 +562,7 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
       const u64 s_abs = (b + pos) & ~3ull;
       const int64_t base = static_cast<int64_t>(s_abs) - static_cast<int64_t>(b);  // >= -3
       const u64 lim = min(static_cast<u64>(base + STEP_M), E2);
-      R.base = base;
+      R.base3 = static_cast<uint32_t>(base + 3);
       R.lo = static_cast<int>(static_cast<int64_t>(pos) - base);
       R.hi = static_cast<int>(static_cast<int64_t>(lim) - base);
       const int64_t lr = static_cast<int64_t>(n_t) - 1 - base;
@@ -559,25 +599,27 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
       // window class of this block step (warp-uniform)
       int wm = WIN_NONE;
       if (WIN) {
-        u64 f = tv[0];
+        u64 f = tv[0];  // lo <= 3 < RM: lane 0 owns the first valid event
         if (R.lo >= 1) f = tv[1];
         if (R.lo >= 2) f = tv[2];
         if (R.lo >= 3) f = tv[3];
         // first valid event and the successor of the last valid one (index hi)
         u64 a;
-        switch (R.hi & 7) {  // warp-uniform
-          case 0: a = tv[0]; break;
+        switch (R.hi & (RM - 1)) {  // warp-uniform; constant register indices
           case 1: a = tv[1]; break;
           case 2: a = tv[2]; break;
           case 3: a = tv[3]; break;
+#if PSG_RM > 4
           case 4: a = tv[4]; break;
           case 5: a = tv[5]; break;
           case 6: a = tv[6]; break;
-          default: a = tv[7]; break;
+          case 7: a = tv[7]; break;
+#endif
+          default: a = tv[0]; break;
         }
         const u64 first = __shfl_sync(FULL, f, 0);
         const u64 after = R.hi >= STEP_M ? __shfl_sync(FULL, tv[RM], 31)
-                                         : __shfl_sync(FULL, a, R.hi >> 3);
+                                         : __shfl_sync(FULL, a, R.hi / RM);
         const bool has_end = R.last_li >= 0 && R.last_li < R.hi;
         if ((first >= t1w && first >= t0) || (!has_end && after < t0)) {
           wm = WIN_NONE;
@@ -601,19 +643,23 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
 
       run_state st;
       st.racc = 0;
+      st.racc32 = 0;
       st.k = -1;
       st.cnt = 0;
       st.nxt = INT_MAX;
       st.cube_ok = false;
       st.slot = R2;
+      st.rowb = R2 * nn;
       if (CUBE) {
         // iteration of this lane's first event: boundaries of the window at or before it
         uint32_t cnt = 0;
-        for (uint32_t j = 0; j <= R2; ++j) cnt += R.lb >= local_of(bwin[j], base) ? 1u : 0u;
+        const uint32_t lp3 = R.base3 + static_cast<uint32_t>(R.lb);
+        for (uint32_t j = 0; j <= R2; ++j) cnt += bwin[j] <= lp3 ? 1u : 0u;
         st.cnt = cnt;
         st.k = static_cast<int>(kb) - 1 + static_cast<int>(cnt);
-        st.nxt = cnt <= R2 ? local_of(bwin[cnt], base) : INT_MAX;
+        st.nxt = cnt <= R2 ? local_of(bwin[cnt], R.base3) : INT_MAX;
         st.slot = st.k < 0 ? R2 : (static_cast<uint32_t>(st.k) & (R2 - 1));
+        st.rowb = st.slot * nn;
         st.cube_ok = st.k < R.iters;
       }
       if (cwide)
@@ -633,15 +679,20 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
       const u64 ob = bo + static_cast<u64>(kb) * nn;
       if (root_only) {
-        uint32_t r = lane / nn, n = lane - (lane / nn) * nn;
+        // rows are node-indexed: the chunk's rows [s0, s0 + n) are one contiguous
+        // block, copied straight to the cube; node 0 (the anchor, the only
+        // internal node) takes the row total as its inclusive time
+        const uint32_t cb = s0 * nn, nkeep = kcap * nn;
+        uint32_t n = lane, r = 0;
+        while (n >= nn) {
+          n -= nn;
+          ++r;
+        }
         for (uint32_t x = lane; x < n_iter_rows * nn; x += 32) {
-          const int4 nd = s_node[n];
-          const uint32_t slot = s0 + r, idx = slot * nn + nd.x;
-          const u64 ex = cell64(rlo, rhi, idx);
-          const u64 in = nd.z ? rtot[slot] : ex;
+          const u64 ex = cell64(rlo, rhi, cb + x);
           if (p.store_cube) p.cube_excl[ob + x] = ex;
-          p.cube_incl[ob + x] = in;  // always stored: the cross-rank statistics read it
-          if (r >= kcap) rlo[idx] = rhi[idx] = 0;
+          p.cube_incl[ob + x] = n == 0 ? rtot[s0 + r] : ex;  // always stored: the stats read it
+          if (x >= nkeep) rlo[cb + x] = rhi[cb + x] = 0;
           n += 32;
           while (n >= nn) {
             n -= nn;
@@ -650,29 +701,28 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
         }
         if (kcap) {  // within-rank sums over k < K (iteration_cv_report), one lane per node
           __syncwarp();
-          for (uint32_t n = lane; n < nn; n += 32) {
-            const int4 nd = s_node[n];
+          for (uint32_t n2 = lane; n2 < nn; n2 += 32) {
             u64 sx = 0, ql = 0, qh = 0;
             for (uint32_t r2 = 0; r2 < kcap; ++r2) {
-              const uint32_t slot = s0 + r2, idx = slot * nn + nd.x;
-              const u64 v = nd.z ? rtot[slot] : cell64(rlo, rhi, idx);
+              const uint32_t idx = cb + r2 * nn + n2;
+              const u64 v = n2 == 0 ? rtot[s0 + r2] : cell64(rlo, rhi, idx);
               rlo[idx] = rhi[idx] = 0;
               sx += v;
               acc_sq(ql, qh, v);
             }
-            wsx[n] += sx;
-            const u64 l2 = wsqlo[n] + ql;
-            wsqhi[n] += qh + (l2 < ql ? 1ull : 0ull);
-            wsqlo[n] = l2;
+            wsx[n2] += sx;
+            const u64 l2 = wsqlo[n2] + ql;
+            wsqhi[n2] += qh + (l2 < ql ? 1ull : 0ull);
+            wsqlo[n2] = l2;
           }
         }
       } else {
         for (uint32_t r = 0; r < n_iter_rows; ++r) {
           const uint32_t slot = s0 + r;
-          warp_prefix_row(rlo + slot * nn, rhi + slot * nn, pref, nn, lane);
+          warp_prefix_row(rlo + slot * nn, rhi + slot * nn, s_node, pref, nn, lane);
           for (uint32_t n = lane; n < nn; n += 32) {
             const int4 nd = s_node[n];
-            const u64 ex = cell64(rlo, rhi, slot * nn + nd.x);
+            const u64 ex = cell64(rlo, rhi, slot * nn + n);
             const u64 in = nd.z ? pref[nd.x + nd.y] - pref[nd.x] : ex;
             if (p.store_cube) p.cube_excl[ob + static_cast<u64>(r) * nn + n] = ex;
             p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
@@ -692,10 +742,10 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
       }
       if (c == 0) {  // the gap row [first_ts, b_0) (itermodel.cpp:331-338)
         __syncwarp();
-        if (!root_only) warp_prefix_row(rlo + R2 * nn, rhi + R2 * nn, pref, nn, lane);
+        if (!root_only) warp_prefix_row(rlo + R2 * nn, rhi + R2 * nn, s_node, pref, nn, lane);
         for (uint32_t n = lane; n < nn; n += 32) {
           const int4 nd = s_node[n];
-          const u64 ex = cell64(rlo, rhi, R2 * nn + nd.x);
+          const u64 ex = cell64(rlo, rhi, R2 * nn + n);
           const u64 in = !nd.z ? ex : (root_only ? rtot[R2] : pref[nd.x + nd.y] - pref[nd.x]);
           p.gap_excl[static_cast<size_t>(tp) * nn + n] = ex;
           p.gap_incl[static_cast<size_t>(tp) * nn + n] = in;
@@ -704,10 +754,8 @@ __global__ void __launch_bounds__(512, 1) k_trace_query(query_params p) {
         for (uint32_t n = lane; n < nn; n += 32) rlo[R2 * nn + n] = rhi[R2 * nn + n] = 0;
       }
       __syncwarp();
-      if (lane == 0) {
-        if (c == 0) rtot[R2] = 0;
-        for (uint32_t r = 0; r < n_iter_rows; ++r) rtot[s0 + r] = 0;
-      }
+      if (static_cast<uint32_t>(lane) < n_iter_rows) rtot[s0 + lane] = 0;
+      if (c == 0 && lane == 0) rtot[R2] = 0;
       __syncwarp();
     }
     if (pos >= n_t && static_cast<u64>(kb) + G >= iters) break;

@@ -11,6 +11,7 @@ import numpy as np  # noqa: E402
 from paper_2605_03561_b200 import Q_CUBE, Q_NO_CUBE_STORE, Q_STATS, Q_WINDOW, Context, scenarios  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
+only = sys.argv[2] if len(sys.argv) > 2 else None  # run one flavour (for ncu)
 ctx = Context(0)
 ctx.generate_iterative(scenarios.device_scenario(n, 746, seed=1))
 T = ctx.shard()["t_max"]
@@ -19,6 +20,8 @@ res = {}
 for name, fl in [("window", Q_WINDOW), ("cube", Q_CUBE), ("cube_nostore", Q_CUBE | Q_NO_CUBE_STORE),
                  ("cube_stats", Q_CUBE | Q_STATS), ("window_cube", Q_WINDOW | Q_CUBE),
                  ("full", Q_WINDOW | Q_CUBE | Q_STATS)]:
+    if only and name != only:
+        continue
     ms = []
     for i in range(6):
         info = ctx.query(fl, t0=T // 4, t1=3 * T // 4, anchor=1)
