@@ -688,18 +688,32 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           n -= nn;
           ++r;
         }
-        for (uint32_t x = lane; x < n_iter_rows * nn; x += 32) {
-          const u64 ex = cell64(rlo, rhi, cb + x);
-          if (p.store_cube) p.cube_excl[ob + x] = ex;
-          p.cube_incl[ob + x] = n == 0 ? rtot[s0 + r] : ex;  // always stored: the stats read it
-          if (x >= nkeep) rlo[cb + x] = rhi[cb + x] = 0;
+        const uint32_t total = n_iter_rows * nn;
+        const bool fold = kcap && nn >= 32;  // lanes of one step hit distinct nodes: fold inline
+        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+          const uint32_t x = x0 + lane;
+          if (x < total) {
+            const u64 ex = cell64(rlo, rhi, cb + x);
+            const u64 in = n == 0 ? rtot[s0 + r] : ex;
+            if (p.store_cube) p.cube_excl[ob + x] = ex;
+            p.cube_incl[ob + x] = in;  // always stored: the cross-rank statistics read it
+            if (fold || x >= nkeep) rlo[cb + x] = rhi[cb + x] = 0;
+            if (fold && x < nkeep) {  // within-rank sums over k < K (iteration_cv_report)
+              wsx[n] += in;
+              u64 ql = wsqlo[n], qh = wsqhi[n];
+              acc_sq(ql, qh, in);
+              wsqlo[n] = ql;
+              wsqhi[n] = qh;
+            }
+          }
+          if (fold) __syncwarp();  // the same node recurs in later steps on other lanes
           n += 32;
           while (n >= nn) {
             n -= nn;
             ++r;
           }
         }
-        if (kcap) {  // within-rank sums over k < K (iteration_cv_report), one lane per node
+        if (kcap && !fold) {  // small subtrees: one lane per node
           __syncwarp();
           for (uint32_t n2 = lane; n2 < nn; n2 += 32) {
             u64 sx = 0, ql = 0, qh = 0;
