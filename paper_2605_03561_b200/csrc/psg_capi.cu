@@ -212,7 +212,7 @@ struct psg_context {
   uint32_t n_kept = 0, n_kept_global = 0, K = 0;
   uint64_t n_cells = 0;
   dbuf<uint32_t> iter_count, tpos;
-  dbuf<uint64_t> block_off, cube_incl, cube_excl, gap_incl, gap_excl;
+  dbuf<uint64_t> block_off, kept_bo, cube_incl, cube_excl, gap_incl, gap_excl;
   dbuf<unsigned long long> summary;
   dbuf<uint8_t> scratch;
   dbuf<unsigned long long> x_acc;  // x_sum [K nn] | x_max [K nn] | x_sq [3 K nn]
@@ -838,7 +838,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       }
       PSG_CUDA(cudaEventRecord(c->ev[5], s));
       const size_t sb = cube_layout_scratch_bytes(n);
-      launch_cube_layout(ic, n, nn, c->tpos.ensure(n + 1), c->block_off.ensure(n + 1), sum,
+      launch_cube_layout(ic, n, nn, c->tpos.ensure(n + 1), c->block_off.ensure(n + 1),
+                         c->kept_bo.ensure(n + 1), sum,
                          c->scratch.ensure(sb), sb, s);
       PSG_CUDA(cudaMemcpyAsync(h, sum, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       c->sync();
@@ -902,7 +903,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
 
     if (do_stats && c->K > 0) {
       const size_t plane = static_cast<size_t>(c->K) * nn;
-      launch_cross_stats(c->cube_incl.p, c->block_off.p, c->iter_count.p, n, nn, c->K, c->x_acc.p,
+      launch_cross_stats(c->cube_incl.p, c->kept_bo.p, c->n_kept, nn, c->K, c->x_acc.p,
                          c->x_acc.p + plane, c->x_acc.p + 2 * plane, s);
       double* no = c->node_out.ensure(static_cast<size_t>(nn) * 10 + 1);
       // within-rank partial sums per node, then cross-GPU sums of everything

@@ -192,13 +192,13 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
                           cudaStream_t s);
 void launch_bounds(const bound_params& p, cudaStream_t s);
 void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t* tpos,
-                        uint64_t* block_off,
+                        uint64_t* block_off, uint64_t* kept_bo,
                         unsigned long long* summary /*[0]=kept [1]=min_it [2]=cells*/,
                         void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t cube_layout_scratch_bytes(uint32_t n);
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s);
-void launch_cross_stats(const uint64_t* incl, const uint64_t* block_off, const uint32_t* iter_count,
-                        uint32_t n, uint32_t nn, uint32_t K, unsigned long long* x_sum,
+void launch_cross_stats(const uint64_t* incl, const uint64_t* kept_bo, uint32_t n_kept,
+                        uint32_t nn, uint32_t K, unsigned long long* x_sum,
                         unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s);
 void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,
                            const unsigned long long* x_sq, uint32_t K, uint32_t nn,

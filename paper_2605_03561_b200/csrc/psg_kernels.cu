@@ -16,6 +16,7 @@
 // derived from exact integer sufficient statistics at the end.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <cstdint>
@@ -309,9 +310,15 @@ __global__ void k_layout_prep(const uint32_t* iter_count, uint32_t n, uint32_t n
   }
 }
 
-__global__ void k_u64_to_u32(const uint64_t* in, uint32_t* out, uint32_t n) {
+// Kept-trace positions (u32) and the compact list of kept block offsets.
+__global__ void k_finish_layout(const uint64_t* tpos64, const uint32_t* iter_count,
+                                const uint64_t* block_off, uint32_t n, uint32_t* tpos,
+                                uint64_t* kept_bo) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < n) out[t] = static_cast<uint32_t>(in[t]);
+  if (t >= n) return;
+  const uint32_t tp = static_cast<uint32_t>(tpos64[t]);
+  tpos[t] = tp;
+  if (iter_count[t] > 0) kept_bo[tp] = block_off[t];
 }
 
 size_t exclusive_scan_u64_scratch(uint32_t n) {
@@ -333,8 +340,8 @@ size_t cube_layout_scratch_bytes(uint32_t n) {
 }
 
 void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t* tpos,
-                        uint64_t* block_off, unsigned long long* summary, void* scratch,
-                        size_t scratch_bytes, cudaStream_t s) {
+                        uint64_t* block_off, uint64_t* kept_bo, unsigned long long* summary,
+                        void* scratch, size_t scratch_bytes, cudaStream_t s) {
   if (n == 0) return;
   uint64_t* kept = static_cast<uint64_t*>(scratch);
   uint64_t* cells = kept + (n + 1);
@@ -348,7 +355,7 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
   PSG_CUDA(cudaGetLastError());
   launch_exclusive_scan_u64(kept, tpos64, n, temp, temp_bytes, s);
   launch_exclusive_scan_u64(cells, block_off, n, temp, temp_bytes, s);
-  k_u64_to_u32<<<(n + 255) / 256, 256, 0, s>>>(tpos64, tpos, n);
+  k_finish_layout<<<(n + 255) / 256, 256, 0, s>>>(tpos64, iter_count, block_off, n, tpos, kept_bo);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
@@ -375,40 +382,50 @@ __global__ void k_within_reduce(const double* within_cv, const uint8_t* within_o
   }
 }
 
-__global__ void k_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,
-                                 const unsigned long long* x_sq, uint32_t K, uint32_t nn,
-                                 uint32_t n_kept, const double* within_sum, const double* within_bad,
-                                 double* out) {
-  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= nn) return;
+// One CTA per node: the per-iteration terms are summed with a fixed-order
+// block reduction (deterministic; the fp64 association differs from the
+// reference's sequential fold by ~1e-16 relative).
+__global__ void __launch_bounds__(256) k_stats_finalize(const unsigned long long* x_sum,
+                                                        const unsigned long long* x_max,
+                                                        const unsigned long long* x_sq, uint32_t K,
+                                                        uint32_t nn, uint32_t n_kept,
+                                                        const double* within_sum,
+                                                        const double* within_bad, double* out) {
+  const uint32_t n = blockIdx.x;
   const size_t plane = static_cast<size_t>(K) * nn;
-  double avg_mean = 0.0, avg_max = 0.0, across = 0.0;
-  bool across_ok = true;
-  for (uint32_t k = 0; k < K; ++k) {
+  double m = 0.0, mx_s = 0.0, across = 0.0, bad = 0.0;
+  for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) {
     const size_t cell = static_cast<size_t>(k) * nn + n;
     const u64 s = x_sum[cell], mx = x_max[cell];
     const u128 sq = static_cast<u128>(x_sq[cell]) + (static_cast<u128>(x_sq[plane + cell]) << 43) +
                     (static_cast<u128>(x_sq[2 * plane + cell]) << 86);
-    avg_mean += (static_cast<double>(s) / 1e9) / static_cast<double>(n_kept);
-    avg_max += static_cast<double>(mx) / 1e9;
+    m += (static_cast<double>(s) / 1e9) / static_cast<double>(n_kept);
+    mx_s += static_cast<double>(mx) / 1e9;
     if (s == 0) {
-      across_ok = false;
+      bad += 1.0;
     } else {
       const u128 num = static_cast<u128>(n_kept) * sq - static_cast<u128>(s) * s;
       across += 100.0 * sqrt(u128_to_double(num)) / static_cast<double>(s);
     }
   }
-  avg_mean /= static_cast<double>(K);
-  avg_max /= static_cast<double>(K);
-  across /= static_cast<double>(K);
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const double avg_mean = BR(tmp).Sum(m) / static_cast<double>(K);
+  __syncthreads();
+  const double avg_max = BR(tmp).Sum(mx_s) / static_cast<double>(K);
+  __syncthreads();
+  const double acr = BR(tmp).Sum(across) / static_cast<double>(K);
+  __syncthreads();
+  const double nbad = BR(tmp).Sum(bad);
+  if (threadIdx.x != 0) return;
   double* o = out + static_cast<size_t>(n) * 8;
   o[0] = avg_mean;
   o[1] = avg_max;
   o[2] = avg_max - avg_mean;
   o[3] = (avg_max - avg_mean) * K;
-  o[4] = across;
+  o[4] = acr;
   o[5] = within_sum[n] / static_cast<double>(n_kept);
-  o[6] = (across_ok && n_kept >= 2 && K >= 2) ? 1.0 : 0.0;
+  o[6] = (nbad == 0.0 && n_kept >= 2 && K >= 2) ? 1.0 : 0.0;
   o[7] = (within_bad[n] == 0.0 && n_kept >= 2 && K >= 2) ? 1.0 : 0.0;
 }
 
@@ -425,8 +442,7 @@ void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long 
     PSG_CUDA(cudaGetLastError());
   }
   if (x_sum) {
-    k_stats_finalize<<<(nn + 127) / 128, 128, 0, s>>>(x_sum, x_max, x_sq, K, nn, n_kept, wsum, wbad,
-                                                      node_out);
+    k_stats_finalize<<<nn, 256, 0, s>>>(x_sum, x_max, x_sq, K, nn, n_kept, wsum, wbad, node_out);
     count_launch();
     PSG_CUDA(cudaGetLastError());
   }
@@ -497,14 +513,26 @@ void launch_window_copy(const trace_view& tr, const uint32_t* pid, uint64_t t0,
 // ns (rank_vector + balance_ratio, workflows.cpp:442-453); phase 1: pick the
 // worst site (strict <, first wins, workflows.cpp:455-457); phase 2: per-node
 // sums/counts of the worst site's values (node_correlate, diagnostics.cpp:378-403).
-__global__ void k_site_acc(const uint64_t* w_incl, uint32_t n, uint32_t n_ctx, const uint32_t* site,
-                           uint32_t n_sites, unsigned long long* acc) {
-  u64 g = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-  if (g >= static_cast<u64>(n) * n_sites) return;
-  uint32_t t = static_cast<uint32_t>(g / n_sites), s = static_cast<uint32_t>(g % n_sites);
-  u64 v = w_incl[static_cast<size_t>(t) * n_ctx + site[s]];
-  atomicAdd(acc + s, v);
-  atomicMax(acc + n_sites + s, v);
+__global__ void __launch_bounds__(256) k_site_acc(const uint64_t* w_incl, uint32_t n, uint32_t n_ctx,
+                                                  const uint32_t* site, uint32_t n_sites,
+                                                  unsigned long long* acc) {
+  const uint32_t s = blockIdx.y;
+  const uint32_t c = site[s];
+  u64 sum = 0, mx = 0;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const u64 v = w_incl[static_cast<size_t>(t) * n_ctx + c];
+    sum += v;
+    mx = max(mx, v);
+  }
+  typedef cub::BlockReduce<u64, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  sum = BR(tmp).Sum(sum);
+  __syncthreads();
+  mx = BR(tmp).Reduce(mx, cub::Max());
+  if (threadIdx.x == 0) {
+    atomicAdd(acc + s, sum);
+    atomicMax(acc + n_sites + s, mx);
+  }
 }
 
 __global__ void k_pick_worst(const unsigned long long* acc, uint32_t n_sites, uint32_t n_ranks,
@@ -538,9 +566,10 @@ void launch_outliers(const uint64_t* w_incl, uint32_t n_traces, uint32_t n_ctx,
                      uint32_t phase, cudaStream_t s) {
   (void)n_nodes;
   if (phase == 0) {
-    u64 th = static_cast<u64>(n_traces) * n_sites;
-    if (th) k_site_acc<<<static_cast<unsigned>((th + 255) / 256), 256, 0, s>>>(w_incl, n_traces, n_ctx,
-                                                                              site_ctx, n_sites, site_acc);
+    if (n_traces && n_sites) {
+      const unsigned gx = std::max(1u, std::min(64u, (n_traces + 1023) / 1024));
+      k_site_acc<<<dim3(gx, n_sites), 256, 0, s>>>(w_incl, n_traces, n_ctx, site_ctx, n_sites, site_acc);
+    }
   } else if (phase == 1) {
     k_pick_worst<<<1, 32, 0, s>>>(site_acc, n_sites, n_traces /* global rank count */, worst,
                                   site_ratio);

@@ -52,7 +52,10 @@ typedef unsigned __int128 u128;
 #define PSG_LB_MINB 1
 #endif
 
-constexpr int RB = 16;      // events per lane per block step, pass 1 (ctx: 4 x 128-bit loads)
+#ifndef PSG_RB
+#define PSG_RB 16
+#endif
+constexpr int RB = PSG_RB;  // events per lane per block step, pass 1 (ctx: RB/4 x 128-bit loads)
 constexpr int RM = PSG_RM;  // events per lane per block step, pass 2 (ts: RM/2, ctx: RM/4 x 128-bit)
 constexpr int STEP_B = 32 * RB;
 constexpr int STEP_M = 32 * RM;
@@ -859,47 +862,39 @@ void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t
 // traces (a trace's tile is kt*nn contiguous values, so the loads coalesce);
 // the global atomics happen once per cell per trace tile.
 __global__ void __launch_bounds__(512) k_cross_stats(const uint64_t* __restrict__ incl,
-                                                     const uint64_t* __restrict__ block_off,
-                                                     const uint32_t* __restrict__ iter_count,
-                                                     uint32_t n, uint32_t nn, uint32_t K, uint32_t kt,
-                                                     uint32_t per_tile, unsigned long long* x_sum,
+                                                     const uint64_t* __restrict__ kept_bo,
+                                                     uint32_t n_kept, uint32_t nn, uint32_t K,
+                                                     uint32_t kt, uint32_t per_tile,
+                                                     unsigned long long* x_sum,
                                                      unsigned long long* x_max,
                                                      unsigned long long* x_sq) {
+  constexpr int U = 16;  // independent loads in flight per thread
   const uint32_t k0 = blockIdx.x * kt;
   const uint32_t kc = min(kt, K - k0);
-  const uint32_t t_lo = blockIdx.y * per_tile, t_hi = min(n, t_lo + per_tile);
+  const uint32_t t_lo = blockIdx.y * per_tile, t_hi = min(n_kept, t_lo + per_tile);
   const size_t plane = static_cast<size_t>(K) * nn;
   for (uint32_t cell = threadIdx.x; cell < kc * nn; cell += blockDim.x) {
     const u64 off = static_cast<u64>(k0) * nn + cell;
     u64 sum = 0, mx = 0, ql = 0, qh = 0;
-    bool any = false;
     uint32_t t = t_lo;
-    for (; t + 8 <= t_hi; t += 8) {
-      u64 v[8];
-      bool k[8];
+    for (; t + U <= t_hi; t += U) {
+      u64 v[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        k[u] = __ldg(iter_count + t + u) > 0;
-        v[u] = k[u] ? ldg64(incl + ldg64(block_off + t + u) + off) : 0;
-      }
+      for (int u = 0; u < U; ++u) v[u] = ldg64(incl + ldg64(kept_bo + t + u) + off);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (!k[u]) continue;
+      for (int u = 0; u < U; ++u) {
         sum += v[u];
         mx = max(mx, v[u]);
         acc_sq(ql, qh, v[u]);
-        any = true;
       }
     }
     for (; t < t_hi; ++t) {
-      if (__ldg(iter_count + t) == 0) continue;
-      const u64 v = ldg64(incl + ldg64(block_off + t) + off);
+      const u64 v = ldg64(incl + ldg64(kept_bo + t) + off);
       sum += v;
       mx = max(mx, v);
       acc_sq(ql, qh, v);
-      any = true;
     }
-    if (any) {
+    if (t_hi > t_lo) {
       const size_t ci = static_cast<size_t>(off);
       const u64 mask43 = (1ull << 43) - 1;
       atomicAdd(x_sum + ci, sum);
@@ -912,18 +907,18 @@ __global__ void __launch_bounds__(512) k_cross_stats(const uint64_t* __restrict_
   }
 }
 
-void launch_cross_stats(const uint64_t* incl, const uint64_t* block_off, const uint32_t* iter_count,
-                        uint32_t n, uint32_t nn, uint32_t K, unsigned long long* x_sum,
+void launch_cross_stats(const uint64_t* incl, const uint64_t* kept_bo, uint32_t n_kept,
+                        uint32_t nn, uint32_t K, unsigned long long* x_sum,
                         unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s) {
-  if (n == 0 || K == 0 || nn == 0) return;
+  if (n_kept == 0 || K == 0 || nn == 0) return;
   const uint32_t kt = nn >= 512 ? 1u : 512u / nn;
   const uint32_t gx = (K + kt - 1) / kt;
   uint32_t gy = (4u * 148u + gx - 1) / gx;  // ~4 CTAs per SM in total
-  gy = std::max(1u, std::min(gy, (n + 63) / 64));
-  const uint32_t per_tile = (n + gy - 1) / gy;
-  gy = (n + per_tile - 1) / per_tile;
-  k_cross_stats<<<dim3(gx, gy), 512, 0, s>>>(incl, block_off, iter_count, n, nn, K, kt, per_tile,
-                                            x_sum, x_max, x_sq);
+  gy = std::max(1u, std::min(gy, (n_kept + 63) / 64));
+  const uint32_t per_tile = (n_kept + gy - 1) / gy;
+  gy = (n_kept + per_tile - 1) / per_tile;
+  k_cross_stats<<<dim3(gx, gy), 512, 0, s>>>(incl, kept_bo, n_kept, nn, K, kt, per_tile, x_sum,
+                                            x_max, x_sq);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }

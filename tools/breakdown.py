@@ -22,10 +22,13 @@ for name, fl in [("window", Q_WINDOW), ("cube", Q_CUBE), ("cube_nostore", Q_CUBE
                  ("full", Q_WINDOW | Q_CUBE | Q_STATS)]:
     if only and name != only:
         continue
-    ms = []
+    ms, mb, mt = [], [], []
     for i in range(6):
         info = ctx.query(fl, t0=T // 4, t1=3 * T // 4, anchor=1)
         if i >= 2:
             ms.append(info["ms_main"])
-    res[name] = {"ms": statistics.mean(ms), "Gev_s": ev / statistics.mean(ms) / 1e6}
+            mb.append(info["ms_bounds"])
+            mt.append(info["ms_total"])
+    res[name] = {"ms": statistics.mean(ms), "bounds_ms": statistics.mean(mb),
+                 "total_ms": statistics.mean(mt), "Gev_s": ev / statistics.mean(ms) / 1e6}
 print(json.dumps({"traces": n, "events": ev, "k_trace_query": res}))
