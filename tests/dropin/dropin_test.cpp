@@ -1,0 +1,281 @@
+// TEST INFRASTRUCTURE — drop-in parity of integration/perfslice_gpu.* against
+// the UNMODIFIED reference, through the reference's own types.
+//
+// Linked with the reference core built by oracle/build_ref.sh (the checker)
+// and with libpsg.so (the product under test).  Each case calls a reference
+// function and its perfslice::gpu counterpart on the same database and
+// compares the results with the reference's own operator== (bit-exact) or
+// within 1e-9 relative for fp64 diagnostics — the style of the reference's
+// acceptance suite (proj/tests/acceptance.cpp): PASS/FAIL lines, exit code =
+// number of failures.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "core/diagnostics.hpp"
+#include "core/frame.hpp"
+#include "core/ingest.hpp"
+#include "core/itermodel.hpp"
+#include "core/store.hpp"
+#include "core/synthgen.hpp"
+#include "core/util.hpp"
+#include "helpers.hpp"
+#include "perfslice_gpu.hpp"
+
+using namespace perfslice;
+using testutil::scratch_dir;
+
+namespace {
+
+int g_failures = 0;
+
+struct check_failure {
+  std::string message;
+};
+
+void expect(bool ok, const std::string& what) {
+  if (!ok) throw check_failure{what};
+}
+
+// 1e-9 relative; `abs` is the floor for values that are zero up to rounding
+// (a CV over identical values is exactly 0 in exact integers but may come out
+// as ~1e-14 % from the reference's two-pass fp64 fold).
+void expect_rel(double got, double want, const std::string& what, double rel = 1e-9,
+                double abs = 0.0) {
+  const double d = std::abs(got - want);
+  if (!(got == want || d <= rel * std::abs(want) || d <= abs))
+    throw check_failure{what + ": got " + std::to_string(got) + ", want " + std::to_string(want)};
+}
+
+void run(const std::string& name, const std::function<void()>& body) {
+  std::string failure;
+  try {
+    body();
+  } catch (const check_failure& f) {
+    failure = f.message;
+  } catch (const std::exception& e) {
+    failure = std::string("exception: ") + e.what();
+  }
+  if (failure.empty()) {
+    std::printf("PASS  %s\n", name.c_str());
+  } else {
+    std::printf("FAIL  %s: %s\n", name.c_str(), failure.c_str());
+    ++g_failures;
+  }
+  std::fflush(stdout);
+}
+
+template <typename Fn>
+errc raised(Fn&& fn) {
+  try {
+    fn();
+  } catch (const error& e) {
+    return e.code();
+  }
+  return errc::ok;
+}
+
+struct db {
+  scratch_dir dir{"dropin"};
+  std::unique_ptr<store::db_handle> h;
+  explicit db(const store::database_image& image) {
+    store::write_database(image, dir.path());
+    h = std::make_unique<store::db_handle>(store::db_handle::open(dir.path()));
+  }
+  std::vector<uint32_t> ids() const {
+    std::vector<uint32_t> v;
+    for (const auto& e : h->trace_index()) v.push_back(e.profile_id);
+    return v;
+  }
+  uint64_t t_max() const {
+    uint64_t m = 0;
+    for (const auto& e : h->trace_index()) m = std::max(m, e.t_end_ns);
+    return m;
+  }
+};
+
+// ingest_traces -> dur glue -> group_aggregate
+frame::table ref_window_aggregate(const store::db_handle& h, const std::vector<uint32_t>& ids,
+                                  uint64_t t0, uint64_t t1) {
+  auto ing = ingest::ingest_traces(h, ids, t0, t1, 1);
+  const auto& ev = ing.events;
+  const size_t n = ev.size();
+  std::vector<uint64_t> pid(n), ctx(n);
+  std::vector<int64_t> dur(n);
+  for (size_t i = 0; i < n; ++i) {
+    pid[i] = ev.profile_id[i];
+    ctx[i] = ev.ctx_id[i];
+    const uint64_t next =
+        (i + 1 < n && ev.profile_id[i + 1] == ev.profile_id[i]) ? ev.timestamp_ns[i + 1] : t1;
+    dur[i] = static_cast<int64_t>(next - ev.timestamp_ns[i]);
+  }
+  frame::table t;
+  t.add(frame::column::of_u64("profile_id", std::move(pid)));
+  t.add(frame::column::of_u64("ctx_id", std::move(ctx)));
+  t.add(frame::column::of_i64("dur_ns", std::move(dur)));
+  return frame::group_aggregate(t, {"profile_id", "ctx_id"},
+                                {{"dur_ns", frame::agg_fn::sum},
+                                 {"dur_ns", frame::agg_fn::min},
+                                 {"dur_ns", frame::agg_fn::max},
+                                 {"dur_ns", frame::agg_fn::mean},
+                                 {"dur_ns", frame::agg_fn::count}},
+                                frame::backend::seq());
+}
+
+void same_model(const itermodel::tri_model& a, const itermodel::tri_model& b) {
+  expect(a.anchor_ctx == b.anchor_ctx, "anchor");
+  expect(a.node_ids == b.node_ids, "node_ids");
+  expect(a.trace_ids == b.trace_ids, "trace_ids");
+  expect(a.iter_counts == b.iter_counts, "iter_counts");
+  expect(a.skipped_traces == b.skipped_traces, "skipped_traces");
+  expect(a.block_offset == b.block_offset, "block_offset");
+  expect(a.incl_ns == b.incl_ns, "incl_ns");
+  expect(a.excl_ns == b.excl_ns, "excl_ns");
+  expect(a.gap_incl_ns == b.gap_incl_ns, "gap_incl_ns");
+  expect(a.gap_excl_ns == b.gap_excl_ns, "gap_excl_ns");
+  expect(a.to_csv() == b.to_csv(), "to_csv");
+}
+
+// Random CCT + traces with repeated timestamps, empty traces and t_end == last ts.
+store::database_image random_image(uint64_t seed) {
+  util::xorshift64s rng(seed);
+  store::database_image img;
+  img.meta.metrics.push_back({0, store::metric_scope::inclusive, "cputime", "s"});
+  const uint32_t n_ctx = 3 + static_cast<uint32_t>(rng.next_below(20));
+  for (uint32_t c = 0; c < n_ctx; ++c)
+    img.meta.contexts.push_back({c, c == 0 ? store::k_no_parent
+                                           : static_cast<uint32_t>(rng.next_below(c)),
+                                 store::ctx_kind::function, "c" + std::to_string(c)});
+  const uint32_t n_tr = 1 + static_cast<uint32_t>(rng.next_below(12));
+  for (uint32_t t = 0; t < n_tr; ++t) {
+    const uint32_t pid = 1 + t * 2;
+    img.meta.profiles.push_back({pid, static_cast<int32_t>(t), 0, "x1000c0s0b0n0", 0});
+    img.records.emplace_back();
+    store::trace_data td;
+    td.profile_id = pid;
+    const uint32_t n = t % 5 == 4 ? 0 : static_cast<uint32_t>(rng.next_below(600));
+    uint64_t ts = rng.next_below(1000);
+    for (uint32_t i = 0; i < n; ++i) {
+      if (rng.next_below(3)) ts += rng.next_below(40);
+      td.events.push_back({ts, static_cast<uint32_t>(rng.next_below(n_ctx))});
+    }
+    td.t_end_ns = ts + (rng.next_below(3) ? rng.next_below(300) : 0);
+    img.traces.push_back(std::move(td));
+  }
+  return img;
+}
+
+void check_everything(const db& d, const std::string& tag, std::vector<uint32_t> anchors) {
+  const auto ids = d.ids();
+  const uint64_t T = d.t_max();
+  const std::vector<std::pair<uint64_t, uint64_t>> windows = {
+      {T / 4, 3 * T / 4}, {0, T + 1}, {T / 3, T / 3}, {T / 5, T / 5 + 7}, {T + 5, T + 9}};
+  run(tag + ": ingest_traces == reference (5 windows)", [&] {
+    for (auto [t0, t1] : windows) {
+      auto a = ingest::ingest_traces(*d.h, ids, t0, t1, 2);
+      auto b = gpu::ingest_traces(*d.h, ids, t0, t1, 2);
+      expect(a.events == b.events, "events for window " + std::to_string(t0));
+      expect(a.carry_in == b.carry_in, "carry_in for window " + std::to_string(t0));
+    }
+    // a subset, unsorted with duplicates (ingest.cpp:184-186)
+    if (ids.size() >= 2) {
+      std::vector<uint32_t> sub = {ids.back(), ids.front(), ids.back()};
+      auto a = ingest::ingest_traces(*d.h, sub, T / 4, T / 2, 1);
+      auto b = gpu::ingest_traces(*d.h, sub, T / 4, T / 2, 1);
+      expect(a.events == b.events && a.carry_in == b.carry_in, "subset");
+    }
+  });
+  run(tag + ": window aggregate == ingest_traces + group_aggregate", [&] {
+    for (auto [t0, t1] : windows)
+      expect(ref_window_aggregate(*d.h, ids, t0, t1) == gpu::window_aggregate(*d.h, ids, t0, t1),
+             "table for window " + std::to_string(t0));
+  });
+  for (uint32_t a : anchors)
+    run(tag + ": build_tri_model == reference (anchor " + std::to_string(a) + ")", [&] {
+      auto pol = itermodel::anchor_policy::explicit_ctx(a);
+      same_model(itermodel::build_tri_model(*d.h, ids, pol, 2),
+                 gpu::build_tri_model(*d.h, ids, pol, 2));
+    });
+}
+
+void check_diagnostics(const db& d, const std::string& tag, uint32_t anchor, double total) {
+  run(tag + ": savings_report + iteration_cv_report == reference (1e-9)", [&] {
+    const auto ids = d.ids();
+    auto model = itermodel::build_tri_model(*d.h, ids, itermodel::anchor_policy::explicit_ctx(anchor), 1);
+    auto leaves = model.subtree_leaves(d.h->meta());
+    auto want = diagnostics::savings_report(model, leaves, total);
+    auto got = gpu::iteration_report(*d.h, ids, anchor, total);
+    expect(got.leaves == leaves, "leaves");
+    expect(got.savings.n_iterations == want.n_iterations, "n_iterations");
+    expect(got.savings.rows.size() == want.rows.size(), "rows");
+    for (size_t i = 0; i < want.rows.size(); ++i) {
+      const auto &g = got.savings.rows[i], &w = want.rows[i];
+      expect(g.ctx_id == w.ctx_id, "row ctx");
+      expect_rel(g.avg_mean_s, w.avg_mean_s, "avg_mean");
+      expect_rel(g.avg_max_s, w.avg_max_s, "avg_max");
+      expect_rel(g.savings_per_iter_s, w.savings_per_iter_s, "savings");
+      expect_rel(g.total_reduction_s, w.total_reduction_s, "total_reduction");
+      std::optional<diagnostics::cv_report> cv;
+      try {
+        cv = diagnostics::iteration_cv_report(model, w.ctx_id);
+      } catch (const error&) {
+      }
+      expect(cv.has_value() == got.cv[i].has_value(), "cv availability");
+      if (cv) {
+        expect_rel(got.cv[i]->across_rank_cv_pct, cv->across_rank_cv_pct, "across cv", 1e-9, 1e-9);
+        expect_rel(got.cv[i]->within_rank_cv_pct, cv->within_rank_cv_pct, "within cv", 1e-9, 1e-9);
+      }
+    }
+    expect_rel(got.savings.total_savings_s, want.total_savings_s, "total savings");
+    expect_rel(got.savings.speedup_frac, want.speedup_frac, "speedup");
+  });
+}
+
+}  // namespace
+
+int main() {
+  {
+    auto [image, truth] = synthgen::generate_iterative_scenario(testutil::small_iter_config(52, 5, 7, 0.1));
+    db d(image);
+    check_everything(d, "small_iter", {0, 1, 2});
+    check_diagnostics(d, "small_iter", 1, 10.0);
+    run("small_iter: auto anchor == reference (itermodel.cpp:253-255)", [&] {
+      auto pol = itermodel::anchor_policy::auto_detect();
+      same_model(itermodel::build_tri_model(*d.h, d.ids(), pol, 1),
+                 gpu::build_tri_model(*d.h, d.ids(), pol, 1));
+    });
+    run("small_iter: boundaries == generator truth", [&] {
+      auto m = gpu::build_tri_model(*d.h, d.ids(), itermodel::anchor_policy::explicit_ctx(truth.anchor_ctx), 1);
+      for (size_t t = 0; t < m.trace_ids.size(); ++t)
+        expect(m.iter_counts[t] == truth.boundaries_ns[t].size(), "iteration count");
+    });
+    run("errors map to the reference's errc", [&] {
+      expect(raised([&] { gpu::ingest_traces(*d.h, d.ids(), 5, 4, 1); }) == errc::invalid_argument,
+             "t0 > t1");
+      expect(raised([&] { gpu::ingest_traces(*d.h, {999}, 0, 1, 1); }) == errc::not_found,
+             "missing trace");
+      expect(raised([&] { gpu::build_tri_model(*d.h, {}, itermodel::anchor_policy::explicit_ctx(1), 1); }) ==
+                 errc::invalid_argument,
+             "no traces");
+      expect(raised([&] { gpu::build_tri_model(*d.h, d.ids(), itermodel::anchor_policy::explicit_ctx(10000), 1); }) ==
+                 errc::not_found,
+             "anchor out of range");
+      expect(raised([&] { gpu::iteration_report(*d.h, d.ids(), 1, 0.0); }) == errc::invalid_total,
+             "total time");
+    });
+  }
+  {
+    auto [image, truth] = synthgen::generate_iterative_scenario(testutil::gamess_like_config());
+    db d(image);
+    check_everything(d, "gamess_like", {1});
+    check_diagnostics(d, "gamess_like", truth.anchor_ctx, 87.0);
+  }
+  for (uint64_t seed = 1; seed <= 6; ++seed) {
+    db d(random_image(seed));
+    check_everything(d, "random_" + std::to_string(seed), {0, 1, static_cast<uint32_t>(d.h->meta().contexts.size() - 1)});
+  }
+  std::printf("%s: %d failure(s)\n", g_failures ? "FAILED" : "OK", g_failures);
+  return g_failures;
+}
