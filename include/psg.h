@@ -50,6 +50,15 @@ uint64_t psg_device_bytes(const psg_context* ctx);
 /* ---- multi-GPU (NCCL over NVLink; loaded at runtime) ------ */
 ps_status psg_comm_unique_id(uint8_t out_id[128]);
 ps_status psg_comm_init(psg_context* ctx, int nranks, int rank, const uint8_t id[128]);
+/* Host-side summary exchange instead of NCCL (an MPI or torch.distributed
+ * process group, or several ranks sharing one GPU): the library calls
+ * fn(buf, count, dtype, op, user) with a HOST buffer of `count` elements
+ * (dtype 0 = uint64, 1 = float64; op 0 = sum, 1 = max, 2 = min), expects the
+ * element-wise reduction over all ranks in place, and treats a nonzero return
+ * as an error.  Every rank must issue the same queries in the same order. */
+typedef int (*psg_allreduce_fn)(void* buf, uint64_t count, int dtype, int op, void* user);
+ps_status psg_comm_init_host(psg_context* ctx, int nranks, int rank, psg_allreduce_fn fn,
+                             void* user);
 
 /* ---- calling-context tree (meta.bin contexts, store.hpp:70-75) ----------- */
 /* parent[0] must be 0xFFFFFFFF; parent[c] < c for c > 0 (topological ids). */

@@ -71,6 +71,23 @@ class Context:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         check(self.lib.psg_comm_init(self.h, nranks, rank, buf))
 
+    def comm_init_host(self, nranks: int, rank: int, reduce):
+        """Summary exchange through a host reducer instead of NCCL:
+        reduce(array, op) must reduce the numpy array (uint64 or float64) in
+        place across ranks, op in {"sum", "max", "min"} (see dist.py)."""
+        ops = ("sum", "max", "min")
+
+        def cb(buf, count, dtype, op, _user):
+            try:
+                ctype = C.c_double if dtype == 1 else C.c_uint64
+                arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(ctype)), shape=(count,))
+                reduce(arr, ops[op])
+                return 0
+            except Exception:  # reported as PS_E_INTERNAL by the library
+                return 1
+        self._host_cb = _lib.ALLREDUCE_FN(cb)
+        check(self.lib.psg_comm_init_host(self.h, nranks, rank, self._host_cb, None))
+
     # -- loading -------------------------------------------------------------
     def set_cct(self, parent):
         p = np.ascontiguousarray(parent, dtype=np.uint32)

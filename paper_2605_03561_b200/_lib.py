@@ -70,6 +70,9 @@ class QueryInfo(C.Structure):
 
 _lib = None
 
+# int (*)(void* buf, uint64_t count, int dtype, int op, void* user)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p)
+
 P = C.c_void_p
 U8P, U32P, U64P = C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
 I32P, I64P, F64P = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_double)
@@ -84,6 +87,7 @@ _SIGS = {
     "psg_device_bytes": (C.c_uint64, [P]),
     "psg_comm_unique_id": (C.c_int, [U8P]),
     "psg_comm_init": (C.c_int, [P, C.c_int, C.c_int, U8P]),
+    "psg_comm_init_host": (C.c_int, [P, C.c_int, C.c_int, ALLREDUCE_FN, P]),
     "psg_set_cct": (C.c_int, [P, U32P, C.c_uint32]),
     "psg_load_traces_aos": (C.c_int, [P, P, C.c_uint64, U64P, U32P, U64P, C.c_uint32]),
     "psg_load_trace_db": (C.c_int, [P, C.c_char_p, U32P, C.c_uint32]),

@@ -242,10 +242,34 @@ struct psg_context {
   trace_view view() const { return {d_off.p, d_ts.p, d_ctx.p, d_tend.p, n_traces}; }
   void sync() { PSG_CUDA(cudaStreamSynchronize(stream)); }
 
+  // Summary exchange between ranks: NCCL on device buffers, or a host
+  // callback (psg_comm_init_host) on a staged host copy.
+  psg_allreduce_fn host_fn = nullptr;
+  void* host_user = nullptr;
+  bool multi() const { return nranks > 1 && (comm || host_fn); }
+  void group_begin() {
+    if (comm && nranks > 1) nccl_check(nccl().group_start(), "ncclGroupStart");
+  }
+  void group_end() {
+    if (comm && nranks > 1) nccl_check(nccl().group_end(), "ncclGroupEnd");
+  }
   template <typename T>
   void allreduce(T* buf, size_t count, ncclDataType_t dt, ncclRedOp_t op) {
-    if (!comm || nranks <= 1 || count == 0) return;
-    nccl_check(nccl().all_reduce(buf, buf, count, dt, op, comm, stream), "ncclAllReduce");
+    if (nranks <= 1 || count == 0) return;
+    if (comm) {
+      nccl_check(nccl().all_reduce(buf, buf, count, dt, op, comm, stream), "ncclAllReduce");
+      return;
+    }
+    if (!host_fn) return;
+    std::vector<T> h(count);
+    PSG_CUDA(cudaMemcpyAsync(h.data(), buf, sizeof(T) * count, cudaMemcpyDeviceToHost, stream));
+    sync();
+    const int dtype = dt == ncclFloat64 ? 1 : 0;
+    const int o = op == ncclSum ? 0 : (op == ncclMax ? 1 : 2);
+    if (host_fn(h.data(), count, dtype, o, host_user) != 0)
+      fail(PS_E_INTERNAL, "host all-reduce callback failed");
+    PSG_CUDA(cudaMemcpyAsync(buf, h.data(), sizeof(T) * count, cudaMemcpyHostToDevice, stream));
+    sync();
   }
 };
 
@@ -499,12 +523,27 @@ ps_status psg_comm_init(psg_context* c, int nranks, int rank, const uint8_t id[1
     ensure_device(c);
     if (c->comm) nccl().comm_destroy(c->comm);
     c->comm = nullptr;
+    c->host_fn = nullptr;
     c->nranks = nranks;
     c->rank = rank;
     if (nranks == 1) return;
     ncclUniqueId uid;
     std::memcpy(&uid, id, 128);
     nccl_check(nccl().comm_init_rank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
+  });
+}
+
+ps_status psg_comm_init_host(psg_context* c, int nranks, int rank, psg_allreduce_fn fn,
+                             void* user) {
+  if (!c || (nranks > 1 && !fn)) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad nranks/rank");
+    if (c->comm) nccl().comm_destroy(c->comm);
+    c->comm = nullptr;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->host_fn = fn;
+    c->host_user = user;
   });
 }
 
@@ -846,13 +885,13 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       c->n_kept = static_cast<uint32_t>(h[0]);
       c->n_cells = h[2];
       unsigned long long g[2] = {h[1], h[0]};  // min iterations, kept count
-      if (c->comm && c->nranks > 1) {
+      if (c->multi()) {
         unsigned long long* d = c->summary.p;  // reuse as staging
         PSG_CUDA(cudaMemcpyAsync(d, g, sizeof(g), cudaMemcpyHostToDevice, s));
-        nccl_check(nccl().group_start(), "ncclGroupStart");
+        c->group_begin();
         c->allreduce(d, 1, ncclUint64, ncclMin);
         c->allreduce(d + 1, 1, ncclUint64, ncclSum);
-        nccl_check(nccl().group_end(), "ncclGroupEnd");
+        c->group_end();
         PSG_CUDA(cudaMemcpyAsync(g, d, sizeof(g), cudaMemcpyDeviceToHost, s));
         c->sync();
       }
@@ -909,13 +948,13 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       // within-rank partial sums per node, then cross-GPU sums of everything
       launch_stats_finalize(nullptr, nullptr, nullptr, c->K, nn, c->n_kept_global, c->within_cv.p,
                             c->within_ok.p, c->n_kept, no, s);
-      if (c->comm && c->nranks > 1) {
-        nccl_check(nccl().group_start(), "ncclGroupStart");
+      if (c->multi()) {
+        c->group_begin();
         c->allreduce(c->x_acc.p, plane, ncclUint64, ncclSum);
         c->allreduce(c->x_acc.p + plane, plane, ncclUint64, ncclMax);
         c->allreduce(c->x_acc.p + 2 * plane, 3 * plane, ncclUint64, ncclSum);
         c->allreduce(no + static_cast<size_t>(nn) * 8, 2 * nn, ncclFloat64, ncclSum);
-        nccl_check(nccl().group_end(), "ncclGroupEnd");
+        c->group_end();
       }
       launch_stats_finalize(c->x_acc.p, c->x_acc.p + plane, c->x_acc.p + 2 * plane, c->K, nn,
                             c->n_kept_global, nullptr, nullptr, c->n_kept, no, s);
@@ -937,11 +976,11 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
                       sa, na, c->d_worst.ensure(2), c->site_ratio.ensure(ns), 0, s);
       uint64_t ranks_global = n;
-      if (c->comm && c->nranks > 1) {
-        nccl_check(nccl().group_start(), "ncclGroupStart");
+      if (c->multi()) {
+        c->group_begin();
         c->allreduce(sa, ns, ncclUint64, ncclSum);
         c->allreduce(sa + ns, ns, ncclUint64, ncclMax);
-        nccl_check(nccl().group_end(), "ncclGroupEnd");
+        c->group_end();
         unsigned long long* d = c->summary.p;
         unsigned long long hn = n;
         PSG_CUDA(cudaMemcpyAsync(d, &hn, 8, cudaMemcpyHostToDevice, s));

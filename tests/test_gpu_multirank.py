@@ -1,0 +1,48 @@
+"""GPU, N>1: the rank-sharded query.  Two ranks on the one
+GPU of the test box exchange the query summaries over gloo
+(psg_comm_init_host); the merged results must equal one context over all
+traces: bit-exact for every integer output (per-shard window rows, cube
+cells, iteration counts, global min iterations, outlier ids, racks) and 1e-9
+relative for the fp64 diagnostics."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests.helpers import ROOT, assert_rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_query_equals_single_context(tmp_path, world):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
+           f"--nproc-per-node={world}", os.path.join(ROOT, "tests", "mp_shard_worker.py"),
+           str(tmp_path)]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    one = dict(np.load(tmp_path / "single.npz"))
+    ranks = [dict(np.load(tmp_path / f"rank{i}.npz")) for i in range(world)]
+    # per-trace outputs: the concatenation of the shards
+    for k in ("w_count", "w_sum", "w_min", "w_max", "w_mean", "w_excl", "w_incl", "c_iter_counts"):
+        assert np.array_equal(np.concatenate([x[k] for x in ranks]), one[k]), k
+    for k in ("c_incl", "c_excl", "c_gap_incl", "c_gap_excl"):
+        assert np.array_equal(np.concatenate([x[k] for x in ranks]), one[k]), k
+    # global summaries: identical on every rank
+    for x in ranks:
+        assert x["info"][1] == one["info"][1] and x["info"][2] == one["info"][2]  # kept, K
+        assert x["info"][3] == one["info"][3] and x["info"][4] == one["info"][4]  # worst site, n out
+        assert np.array_equal(x["s_leaves"], one["s_leaves"])
+        assert_rel(x["s_savings"], one["s_savings"], 1e-9, "savings")
+        assert_rel(x["s_summary"], one["s_summary"], 1e-9, "summary")
+        assert_rel(x["s_cv"], one["s_cv"], 1e-9, "cv")
+        assert np.array_equal(x["s_cv_ok"], one["s_cv_ok"])
+        assert_rel(x["o_site_ratio"], one["o_site_ratio"], 1e-12, "balance ratios")
+        assert_rel(x["o_node_mean"], one["o_node_mean"], 1e-12, "node means")
+        assert np.array_equal(x["o_selected"], one["o_selected"])
+        assert np.array_equal(x["o_racks"], one["o_racks"])
