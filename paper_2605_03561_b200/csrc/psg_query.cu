@@ -51,6 +51,9 @@ typedef unsigned __int128 u128;
 #ifndef PSG_LB_MINB
 #define PSG_LB_MINB 1
 #endif
+#ifndef PSG_G
+#define PSG_G 4
+#endif
 
 #ifndef PSG_RB
 #define PSG_RB 16
@@ -58,6 +61,7 @@ typedef unsigned __int128 u128;
 constexpr int RB = PSG_RB;  // events per lane per block step, pass 1 (ctx: RB/4 x 128-bit loads)
 constexpr int RM = PSG_RM;  // events per lane per block step, pass 2 (ts: RM/2, ctx: RM/4 x 128-bit)
 constexpr int STEP_B = 32 * RB;
+constexpr uint32_t GC = PSG_G;  // iterations per chunk of pass 2 (the host passes the same G)
 constexpr int STEP_M = 32 * RM;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -438,7 +442,8 @@ template <bool WIN, bool CUBE>
 __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(query_params p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t W = p.warps, n_ctx = p.n_ctx, nn = p.nn, G = p.G, R2 = 2 * G;
+  const uint32_t W = p.warps, n_ctx = p.n_ctx, nn = p.nn;
+  constexpr uint32_t G = GC, R2 = 2 * GC;  // p.G == GC (same PSG_G on both sides)
   const bool root_only = p.root_only != 0;
 
   int4* s_node = reinterpret_cast<int4*>(smem);
@@ -682,55 +687,33 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
       const u64 ob = bo + static_cast<u64>(kb) * nn;
       if (root_only) {
-        // rows are node-indexed: the chunk's rows [s0, s0 + n) are one contiguous
-        // block, copied straight to the cube; node 0 (the anchor, the only
-        // internal node) takes the row total as its inclusive time
-        const uint32_t cb = s0 * nn, nkeep = kcap * nn;
-        uint32_t n = lane, r = 0;
-        while (n >= nn) {
-          n -= nn;
-          ++r;
-        }
-        const uint32_t total = n_iter_rows * nn;
-        const bool fold = kcap && nn >= 32;  // lanes of one step hit distinct nodes: fold inline
-        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
-          const uint32_t x = x0 + lane;
-          if (x < total) {
-            const u64 ex = cell64(rlo, rhi, cb + x);
-            const u64 in = n == 0 ? rtot[s0 + r] : ex;
-            if (p.store_cube) p.cube_excl[ob + x] = ex;
-            p.cube_incl[ob + x] = in;  // always stored: the cross-rank statistics read it
-            if (fold || x >= nkeep) rlo[cb + x] = rhi[cb + x] = 0;
-            if (fold && x < nkeep) {  // within-rank sums over k < K (iteration_cv_report)
-              wsx[n] += in;
-              u64 ql = wsqlo[n], qh = wsqhi[n];
-              acc_sq(ql, qh, in);
-              wsqlo[n] = ql;
-              wsqhi[n] = qh;
-            }
-          }
-          if (fold) __syncwarp();  // the same node recurs in later steps on other lanes
-          n += 32;
-          while (n >= nn) {
-            n -= nn;
-            ++r;
-          }
-        }
-        if (kcap && !fold) {  // small subtrees: one lane per node
-          __syncwarp();
-          for (uint32_t n2 = lane; n2 < nn; n2 += 32) {
-            u64 sx = 0, ql = 0, qh = 0;
-            for (uint32_t r2 = 0; r2 < kcap; ++r2) {
-              const uint32_t idx = cb + r2 * nn + n2;
-              const u64 v = n2 == 0 ? rtot[s0 + r2] : cell64(rlo, rhi, idx);
+        // rows are node-indexed, so a lane owns one node across the chunk's
+        // rows: straight copies to the cube (coalesced along the node axis),
+        // node 0 (the anchor, the only internal node) takes the row total as
+        // its inclusive time, and the within-rank sums stay in registers
+        for (uint32_t n = lane; n < nn; n += 32) {
+          u64 sx = 0, ql = 0, qh = 0;
+#pragma unroll
+          for (uint32_t r = 0; r < GC; ++r) {
+            if (r < n_iter_rows) {
+              const uint32_t idx = (s0 + r) * nn + n;
+              const u64 ex = cell64(rlo, rhi, idx);
+              const u64 in = n == 0 ? rtot[s0 + r] : ex;
+              const u64 o = ob + static_cast<u64>(r) * nn + n;
+              if (p.store_cube) p.cube_excl[o] = ex;
+              p.cube_incl[o] = in;  // always stored: the cross-rank statistics read it
               rlo[idx] = rhi[idx] = 0;
-              sx += v;
-              acc_sq(ql, qh, v);
+              if (r < kcap) {  // within-rank sums over k < K (iteration_cv_report)
+                sx += in;
+                acc_sq(ql, qh, in);
+              }
             }
-            wsx[n2] += sx;
-            const u64 l2 = wsqlo[n2] + ql;
-            wsqhi[n2] += qh + (l2 < ql ? 1ull : 0ull);
-            wsqlo[n2] = l2;
+          }
+          if (kcap) {
+            wsx[n] += sx;
+            const u64 l2 = wsqlo[n] + ql;
+            wsqhi[n] += qh + (l2 < ql ? 1ull : 0ull);
+            wsqlo[n] = l2;
           }
         }
       } else {
