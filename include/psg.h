@@ -167,6 +167,7 @@ typedef struct psg_query_info {
   uint32_t n_kept_global;
   uint64_t n_cells;              /* local cube cells (sum iter_counts * n_nodes) */
   uint32_t n_leaves;
+  uint32_t n_internal;           /* internal nodes of the subtree (the cube stores excl only for these) */
   /* outliers */
   uint32_t worst_site;           /* ctx id */
   double worst_ratio;

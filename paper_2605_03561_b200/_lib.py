@@ -62,7 +62,7 @@ class QueryInfo(C.Structure):
         ("n_window_groups", C.c_uint64), ("n_window_rows", C.c_uint64),
         ("n_nodes", C.c_uint32), ("n_kept", C.c_uint32), ("n_skipped", C.c_uint32),
         ("min_iterations", C.c_uint32), ("n_kept_global", C.c_uint32), ("n_cells", C.c_uint64),
-        ("n_leaves", C.c_uint32), ("worst_site", C.c_uint32), ("worst_ratio", C.c_double),
+        ("n_leaves", C.c_uint32), ("n_internal", C.c_uint32), ("worst_site", C.c_uint32), ("worst_ratio", C.c_double),
         ("n_outliers", C.c_uint32), ("n_racks", C.c_uint32),
         ("ms_total", C.c_float), ("ms_main", C.c_float), ("ms_bounds", C.c_float),
     ]

@@ -187,6 +187,7 @@ struct psg_context {
   std::vector<uint32_t> node_ids, leaves;
   std::vector<int32_t> h_sub_pre;
   uint32_t root_only = 0;  // the anchor is the only internal node of its subtree
+  std::vector<uint32_t> internal_pos;  // node positions of the internal nodes
   dbuf<int32_t> d_sub_pre;
   dbuf<int4> d_node_tab;  // [nn] {preorder position, subtree size, internal?, 0}
   dbuf<uint32_t> d_contains;  // subtree membership bitset [ceil(n_ctx/32)]
@@ -212,7 +213,7 @@ struct psg_context {
   uint32_t n_kept = 0, n_kept_global = 0, K = 0;
   uint64_t n_cells = 0;
   dbuf<uint32_t> iter_count, tpos;
-  dbuf<uint64_t> block_off, kept_bo, cube_incl, cube_excl, gap_incl, gap_excl;
+  dbuf<uint64_t> block_off, kept_bo, cube_incl, cube_xint, gap_incl, gap_excl;
   dbuf<unsigned long long> summary;
   dbuf<uint8_t> scratch;
   dbuf<unsigned long long> x_acc;  // x_sum [K nn] | x_max [K nn] | x_sq [3 K nn]
@@ -384,14 +385,17 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
   std::vector<char> has_child(c->n_ctx, 0);
   for (uint32_t id = 1; id < c->n_ctx; ++id) has_child[c->h_parent[id]] = 1;
   c->leaves.clear();
+  c->internal_pos.clear();
   uint32_t n_internal = 0;
   for (uint32_t i = 0; i < c->nn; ++i) {
     const uint32_t id = c->node_ids[i];
-    tab[i] = make_int4(sub.pre[id], sub.size[id], has_child[id] ? 1 : 0, 0);
-    if (has_child[id])
-      ++n_internal;  // internal: inclusive time = sum over its preorder range
-    else
+    tab[i] = make_int4(sub.pre[id], sub.size[id], has_child[id] ? static_cast<int>(n_internal) + 1 : 0, 0);
+    if (has_child[id]) {  // internal: inclusive time = sum over its preorder range
+      c->internal_pos.push_back(i);
+      ++n_internal;
+    } else {
       c->leaves.push_back(id);
+    }
   }
   c->root_only = (n_internal == 1 && has_child[anchor]) ? 1u : 0u;
   c->contains_words = (c->n_ctx + 31) / 32;
@@ -503,7 +507,7 @@ void* psg_stream(psg_context* ctx) { return ctx ? ctx->stream : nullptr; }
 uint64_t psg_device_bytes(const psg_context* c) {
   if (!c) return 0;
   return c->d_off.bytes() + c->d_ts.bytes() + c->d_ctx.bytes() + c->d_tend.bytes() +
-         c->d_stage.bytes() + c->cube_incl.bytes() + c->cube_excl.bytes() + c->w_cnt.bytes() * 7;
+         c->d_stage.bytes() + c->cube_incl.bytes() + c->cube_xint.bytes() + c->w_cnt.bytes() * 7;
 }
 
 ps_status psg_comm_unique_id(uint8_t out_id[128]) {
@@ -914,7 +918,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       // incl is always materialised (the cross-rank statistics stream it);
       // PSG_Q_NO_CUBE_STORE drops the excl half
       p.cube_incl = c->cube_incl.ensure(c->n_cells + 1);
-      if (store_cube) p.cube_excl = c->cube_excl.ensure(c->n_cells + 1);
+      p.m = static_cast<uint32_t>(c->internal_pos.size());
+      if (store_cube) p.cube_xint = c->cube_xint.ensure((nn ? c->n_cells / nn : 0) * p.m + 1);
       c->have_excl = store_cube;
       p.gap_incl = c->gap_incl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
       p.gap_excl = c->gap_excl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
@@ -1018,6 +1023,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     info->n_kept_global = c->n_kept_global;
     info->n_cells = c->n_cells;
     info->n_leaves = do_cube ? static_cast<uint32_t>(c->leaves.size()) : 0;
+    info->n_internal = do_cube ? static_cast<uint32_t>(c->internal_pos.size()) : 0;
     if (do_out) {
       uint32_t w[2];
       PSG_CUDA(cudaMemcpy(w, c->d_worst.p, 4, cudaMemcpyDeviceToHost));
@@ -1092,8 +1098,21 @@ ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts
       fail(PS_E_INVALID_ARGUMENT, "the excl cube was not stored (PSG_Q_NO_CUBE_STORE)");
     if (incl && c->n_cells)
       PSG_CUDA(cudaMemcpy(incl, c->cube_incl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
-    if (excl && c->n_cells)
-      PSG_CUDA(cudaMemcpy(excl, c->cube_excl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
+    if (excl && c->n_cells) {
+      // expand the compact cube: a leaf's excl equals its incl; internal nodes
+      // come from the [iteration][internal node] table
+      if (incl)
+        std::memcpy(excl, incl, 8 * c->n_cells);
+      else
+        PSG_CUDA(cudaMemcpy(excl, c->cube_incl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
+      const size_t rows = c->n_cells / c->nn, m = c->internal_pos.size();
+      if (m) {
+        std::vector<int64_t> xi(rows * m);
+        PSG_CUDA(cudaMemcpy(xi.data(), c->cube_xint.p, 8 * rows * m, cudaMemcpyDeviceToHost));
+        for (size_t r = 0; r < rows; ++r)
+          for (size_t q = 0; q < m; ++q) excl[r * c->nn + c->internal_pos[q]] = xi[r * m + q];
+      }
+    }
     const size_t g = static_cast<size_t>(c->n_kept) * c->nn;
     if (gap_incl && g) PSG_CUDA(cudaMemcpy(gap_incl, c->gap_incl.p, 8 * g, cudaMemcpyDeviceToHost));
     if (gap_excl && g) PSG_CUDA(cudaMemcpy(gap_excl, c->gap_excl.p, 8 * g, cudaMemcpyDeviceToHost));

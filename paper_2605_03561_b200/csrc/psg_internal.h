@@ -93,8 +93,8 @@ struct query_params {
   // cube part
   uint32_t do_cube, store_cube, do_stats;
   const int32_t* sub_pre;    // [n_ctx] node position (ascending ctx id) in the anchor subtree or -1
-  const int4* node_tab;      // [nn] {preorder position, subtree size, internal?, node at preorder
-                             //       position n}, indexed by node position
+  const int4* node_tab;      // [nn] {preorder position, subtree size, internal index + 1 (0: leaf),
+                             //       node at preorder position n}, indexed by node position
   uint32_t nn;
   uint32_t root_only;        // the only internal node is the anchor: incl(anchor) = row total
   const uint64_t* cap_off;     // pass-1 boundary regions
@@ -105,7 +105,11 @@ struct query_params {
   const uint32_t* tpos;        // [n] position among kept traces
   const uint64_t* block_off;   // [n] cell offset of the trace's first row (kept traces)
   uint32_t K;                  // global min iterations over kept traces (0: none)
-  uint64_t *cube_incl, *cube_excl, *gap_incl, *gap_excl;
+  // The cube is stored compactly: incl dense [cells]; excl only for the m
+  // internal nodes [Σ iters][m] (a leaf's exclusive time IS its inclusive
+  // time), expanded to the reference's dense layout on copy-out.
+  uint64_t *cube_incl, *cube_xint, *gap_incl, *gap_excl;
+  uint32_t m;  // internal nodes of the anchor subtree
   // cross-rank stats accumulators (k < K) and within-trace CVs
   unsigned long long *x_sum, *x_max, *x_sq;  // [K][nn], x_sq = 3 limbs [3][K][nn]
   double* within_cv;   // [n_kept][nn]

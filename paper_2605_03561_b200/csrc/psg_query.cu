@@ -686,6 +686,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     if (CUBE && kept) {
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
       const u64 ob = bo + static_cast<u64>(kb) * nn;
+      const u64 ib = bo / nn;  // iterations stored before this trace
       if (root_only) {
         // rows are node-indexed, so a lane owns one node across the chunk's
         // rows: straight copies to the cube (coalesced along the node axis),
@@ -699,9 +700,8 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
               const uint32_t idx = (s0 + r) * nn + n;
               const u64 ex = cell64(rlo, rhi, idx);
               const u64 in = n == 0 ? rtot[s0 + r] : ex;
-              const u64 o = ob + static_cast<u64>(r) * nn + n;
-              if (p.store_cube) p.cube_excl[o] = ex;
-              p.cube_incl[o] = in;  // always stored: the cross-rank statistics read it
+              p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
+              if (n == 0 && p.store_cube) p.cube_xint[ib + kb + r] = ex;  // m == 1
               rlo[idx] = rhi[idx] = 0;
               if (r < kcap) {  // within-rank sums over k < K (iteration_cv_report)
                 sx += in;
@@ -724,8 +724,8 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
             const int4 nd = s_node[n];
             const u64 ex = cell64(rlo, rhi, slot * nn + n);
             const u64 in = nd.z ? pref[nd.x + nd.y] - pref[nd.x] : ex;
-            if (p.store_cube) p.cube_excl[ob + static_cast<u64>(r) * nn + n] = ex;
             p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
+            if (nd.z && p.store_cube) p.cube_xint[(ib + kb + r) * p.m + (nd.z - 1)] = ex;
             if (r < kcap) {
               wsx[n] += in;
               u64 ql = 0, qh = 0;
