@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   const bool kept = iters > 0;
   const uint32_t tp = kept ? p.tpos[t] : 0;
   const u64 bo = kept ? p.block_off[t] : 0;
+  const u64 ib = kept ? bo / nn : 0;  // iterations stored before this trace
   const u64 region = (CUBE && active) ? p.cap_off[t] : 0;
   const uint32_t* bt = p.bidx + region;
   const uint64_t* btt = p.bts + region;
@@ -686,8 +687,38 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     if (CUBE && kept) {
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
       const u64 ob = bo + static_cast<u64>(kb) * nn;
-      const u64 ib = bo / nn;  // iterations stored before this trace
-      if (root_only) {
+      if (root_only && !cwide) {
+        // narrow chunk (every iteration spans < 2^32 ns): cells and row totals
+        // fit their low words, squares fit 64 bits
+        const uint32_t* rt32 = reinterpret_cast<const uint32_t*>(rtot);
+        for (uint32_t n = lane; n < nn; n += 32) {
+          u64 sx = 0, ql = 0, qh = 0;
+          uint64_t* dst = p.cube_incl + ob + n;
+#pragma unroll
+          for (uint32_t r = 0; r < GC; ++r) {
+            if (r < n_iter_rows) {
+              const uint32_t idx = (s0 + r) * nn + n;
+              const uint32_t ex = rlo[idx];
+              const uint32_t in = n == 0 ? rt32[2 * (s0 + r)] : ex;
+              dst[r * nn] = in;
+              if (n == 0 && p.store_cube) p.cube_xint[ib + kb + r] = ex;  // m == 1
+              rlo[idx] = 0;
+              if (r < kcap) {
+                sx += in;
+                const u64 q = static_cast<u64>(in) * in;
+                ql += q;
+                qh += ql < q ? 1ull : 0ull;
+              }
+            }
+          }
+          if (kcap) {
+            wsx[n] += sx;
+            const u64 l2 = wsqlo[n] + ql;
+            wsqhi[n] += qh + (l2 < ql ? 1ull : 0ull);
+            wsqlo[n] = l2;
+          }
+        }
+      } else if (root_only) {
         // rows are node-indexed, so a lane owns one node across the chunk's
         // rows: straight copies to the cube (coalesced along the node axis),
         // node 0 (the anchor, the only internal node) takes the row total as
