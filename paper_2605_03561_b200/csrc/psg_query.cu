@@ -890,6 +890,8 @@ __global__ void __launch_bounds__(512) k_cross_stats(const uint64_t* __restrict_
   for (uint32_t cell = threadIdx.x; cell < kc * nn; cell += blockDim.x) {
     const u64 off = static_cast<u64>(k0) * nn + cell;
     u64 sum = 0, mx = 0, ql = 0, qh = 0;
+    // squares on the 32-bit fast path (one IMAD.WIDE each); the maximum says
+    // whether any value reached 2^32, in which case the cell is redone exactly
     uint32_t t = t_lo;
     for (; t + U <= t_hi; t += U) {
       u64 v[U];
@@ -899,14 +901,22 @@ __global__ void __launch_bounds__(512) k_cross_stats(const uint64_t* __restrict_
       for (int u = 0; u < U; ++u) {
         sum += v[u];
         mx = max(mx, v[u]);
-        acc_sq(ql, qh, v[u]);
+        const u64 q = static_cast<u64>(static_cast<uint32_t>(v[u])) * static_cast<uint32_t>(v[u]);
+        ql += q;
+        qh += ql < q ? 1ull : 0ull;
       }
     }
     for (; t < t_hi; ++t) {
       const u64 v = ldg64(incl + ldg64(kept_bo + t) + off);
       sum += v;
       mx = max(mx, v);
-      acc_sq(ql, qh, v);
+      const u64 q = static_cast<u64>(static_cast<uint32_t>(v)) * static_cast<uint32_t>(v);
+      ql += q;
+      qh += ql < q ? 1ull : 0ull;
+    }
+    if (mx >> 32) {  // a value >= 2^32: exact 128-bit squares
+      ql = qh = 0;
+      for (t = t_lo; t < t_hi; ++t) acc_sq(ql, qh, ldg64(incl + ldg64(kept_bo + t) + off));
     }
     if (t_hi > t_lo) {
       const size_t ci = static_cast<size_t>(off);
