@@ -121,9 +121,13 @@ __device__ __forceinline__ void warp_prefix(const u64* src, u64* dst, uint32_t n
 // kept).  The number of iterations drops a zero-length last interval
 // (boundary at t_end).  Boundary event indices are relative to the trace's
 // first event.
+template <bool SMALL>  // SMALL: the CCT has <= 64 contexts, membership bits live in a register
 __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   extern __shared__ uint32_t s_bits[];
   for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) s_bits[i] = p.contains[i];
+  const u64 bits64 = SMALL ? (static_cast<u64>(p.contains[0]) |
+                              (p.words > 1 ? static_cast<u64>(p.contains[1]) << 32 : 0ull))
+                           : 0ull;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -150,15 +154,24 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
       cx[4 * q + 2] = v.z;
       cx[4 * q + 3] = v.w;
     }
+    // events of this trace in the lane's run: local indices [lo, hi) of [0, RB)
+    const int64_t lo64 = static_cast<int64_t>(b) - static_cast<int64_t>(r0);
+    const int64_t hi64 = static_cast<int64_t>(e) - static_cast<int64_t>(r0);
+    const int lo = lo64 < 0 ? 0 : static_cast<int>(lo64 > RB ? RB : lo64);
+    const int hi = hi64 < 0 ? 0 : static_cast<int>(hi64 > RB ? RB : hi64);
+    const uint32_t real = (hi >= 32 ? FULL : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
     uint32_t inm = 0;
 #pragma unroll
     for (int j = 0; j < RB; ++j) {
-      const u64 i = r0 + j;
-      const bool real = i >= b && i < e;
-      const uint32_t c = real ? cx[j] : 0u;
-      const uint32_t in = real ? ((s_bits[c >> 5] >> (c & 31)) & 1u) : 0u;
+      const uint32_t c = cx[j];
+      uint32_t in;
+      if (SMALL)
+        in = static_cast<uint32_t>(bits64 >> (c & 63)) & 1u;  // ctx < 64 on real events
+      else
+        in = (s_bits[min(c, p.words * 32 - 1) >> 5] >> (c & 31)) & 1u;
       inm |= in << j;
     }
+    inm &= real;
     uint32_t up = __shfl_up_sync(FULL, inm >> (RB - 1), 1);
     if (lane == 0) up = prev_in;
     const uint32_t candm = inm & ~((inm << 1) | (up & 1u));
@@ -217,7 +230,10 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
 
 void launch_bounds(const bound_params& p, cudaStream_t s) {
   if (p.tr.n == 0) return;
-  k_bounds<<<(p.tr.n + 7) / 8, 256, 4u * p.words, s>>>(p);
+  if (p.words <= 2)
+    k_bounds<true><<<(p.tr.n + 7) / 8, 256, 4u * p.words, s>>>(p);
+  else
+    k_bounds<false><<<(p.tr.n + 7) / 8, 256, 4u * p.words, s>>>(p);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
