@@ -125,7 +125,6 @@ struct query_params {
 // psg_query.cu).
 struct warp_smem_layout {
   uint32_t off_rlo, off_rhi;  // (2G+1) x nn u32: cube rows by node position (ring of 2G + gap)
-  uint32_t off_rtot;   // 2G+1 u64     row totals (= incl of the anchor when root_only)
   uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
   uint32_t off_inrows; // G x nn u64   inclusive rows kept for the statistics (generic trees)
   uint32_t off_bwin;   // 2G+2 u32     boundary window (event indices relative to the trace)
@@ -147,8 +146,7 @@ struct warp_smem_layout {
     off_rlo = take(rows > scan ? rows : scan);
     off_scan = off_rlo;
     off_rhi = take(rows);
-    off_rtot = take(8u * (2 * G + 1));
-    off_pref = take(root_only ? 0u : 8u * (nn + 1));
+    off_pref = take(8u * (nn + 1));  // generic rows and the gap row
     off_inrows = take(root_only ? 0u : 8u * G * nn);
     off_bwin = take(4u * (2 * G + 2));
     off_bts = take(8u * (2 * G + 2));

@@ -260,6 +260,7 @@ void launch_bounds(const bound_params& p, cudaStream_t s) {
 namespace {
 
 constexpr u64 kSpan32 = 1ull << 32;
+constexpr u64 kSpan31 = 1ull << 31;  // narrow chunks: 4 squares of cells < 2^31 fit 64 bits
 
 enum : int { WIN_NONE = 0, WIN_FULL = 1, WIN_PART = 2, WIN_WIDE = 3 };
 
@@ -328,15 +329,12 @@ struct run_state {
   bool cube_ok;   // k is a stored iteration (or the gap of a kept trace)
   uint32_t slot;  // ring slot of k
   uint32_t rowb;  // slot * nn
-  u64 racc;       // this lane's pending contribution to the row total of k (wide chunks)
-  uint32_t racc32;  // the same for 32-bit chunks
 };
 
 struct run_ctx {
   const int32_t* s_sub_pre;
   const uint32_t* bwin;
   uint32_t *rlo, *rhi;
-  uint32_t* rtot;  // (lo, hi) word pairs
   uint32_t base3;  // block step start relative to the trace, + 3
   u64 tend, t0, t1w;
   uint32_t R2, nn;
@@ -344,18 +342,6 @@ struct run_ctx {
   int lb, lo, hi, last_li;
   bool root_only;
 };
-
-template <bool CWIDE>
-__device__ __forceinline__ void flush_racc(const run_ctx& R, run_state& st) {
-  uint32_t* t = R.rtot + 2 * st.slot;
-  if (CWIDE) {
-    if (st.racc) sadd64(t, t + 1, st.racc);
-    st.racc = 0;
-  } else {
-    if (st.racc32) atomicAdd(t, st.racc32);
-    st.racc32 = 0;
-  }
-}
 
 template <bool WIN, bool CUBE, int WM, bool CWIDE>
 __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
@@ -368,7 +354,6 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
     const uint32_t cj = valid ? cv[j] : 0u;
     if (CUBE) {
       if (li >= st.nxt) {  // boundaries are distinct events: at most one per event
-        if (R.root_only) flush_racc<CWIDE>(R, st);
         ++st.k;
         ++st.cnt;
         st.nxt = st.cnt <= R.R2 ? local_of(R.bwin[st.cnt], R.base3) : INT_MAX;
@@ -382,12 +367,10 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
         if (CWIDE) {
           const u64 dc = (li == R.last_li ? R.tend : nts) - tsj;
           sadd64(R.rlo + idx, R.rhi + idx, dc);
-          if (R.root_only) st.racc += dc;
         } else {  // the iteration spans < 2^32 ns: 32-bit differences are exact
           const uint32_t dc = static_cast<uint32_t>(li == R.last_li ? R.tend : nts) -
                               static_cast<uint32_t>(tsj);
           atomicAdd(R.rlo + idx, dc);
-          if (R.root_only) st.racc32 += dc;
         }
       }
     }
@@ -427,7 +410,6 @@ __device__ __forceinline__ void run_block(int wm, const u64 (&tv)[RM + 1], const
     run_events<WIN, CUBE, WIN_WIDE, CWIDE>(tv, cv, R, st, T);
   else
     run_events<WIN, CUBE, WIN_NONE, CWIDE>(tv, cv, R, st, T);
-  if (CUBE && R.root_only) flush_racc<CWIDE>(R, st);
 }
 
 __device__ __forceinline__ u64 cell64(const uint32_t* lo, const uint32_t* hi, uint32_t i) {
@@ -473,7 +455,6 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   uint8_t* wb = smem + tbl + static_cast<size_t>(warp) * L.bytes;
   uint32_t* rlo = reinterpret_cast<uint32_t*>(wb + L.off_rlo);
   uint32_t* rhi = reinterpret_cast<uint32_t*>(wb + L.off_rhi);
-  u64* rtot = reinterpret_cast<u64*>(wb + L.off_rtot);
   u64* pref = reinterpret_cast<u64*>(wb + L.off_pref);
   uint32_t* bwin = reinterpret_cast<uint32_t*>(wb + L.off_bwin);
   u64* bts = reinterpret_cast<u64*>(wb + L.off_bts);
@@ -499,7 +480,6 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   if (CUBE) {
     for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) s_node[i] = p.node_tab[i];
     for (uint32_t j = lane; j < (R2 + 1) * nn; j += 32) rlo[j] = rhi[j] = 0;
-    for (uint32_t j = lane; j <= R2; j += 32) rtot[j] = 0;
     for (uint32_t j = lane; j < nn; j += 32) wsx[j] = wsqlo[j] = wsqhi[j] = 0;
   }
   if (WIN) {
@@ -543,7 +523,6 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   R.bwin = bwin;
   R.rlo = rlo;
   R.rhi = rhi;
-  R.rtot = reinterpret_cast<uint32_t*>(rtot);
   R.tend = tend;
   R.t0 = t0;
   R.t1w = t1w;
@@ -573,8 +552,8 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       E1 = bwin[G] - 3;
       E2 = bwin[R2] - 3;
       // iteration spans of the ring (and the gap in chunk 0) decide 32- vs 64-bit cells
-      bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan32;
-      if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan32;
+      bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan31;
+      if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan31;
       cwide = __any_sync(FULL, w);
     } else if (CUBE && active) {
       // skipped trace: only the window runs; iterations are not stored
@@ -667,8 +646,6 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       }
 
       run_state st;
-      st.racc = 0;
-      st.racc32 = 0;
       st.k = -1;
       st.cnt = 0;
       st.nxt = INT_MAX;
@@ -704,63 +681,63 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
       const u64 ob = bo + static_cast<u64>(kb) * nn;
       if (root_only && !cwide) {
-        // narrow chunk (every iteration spans < 2^32 ns): cells and row totals
-        // fit their low words, squares fit 64 bits
-        const uint32_t* rt32 = reinterpret_cast<const uint32_t*>(rtot);
-        for (uint32_t n = lane; n < nn; n += 32) {
-          u64 sx = 0, ql = 0, qh = 0;
+        // Narrow chunk (every iteration spans < 2^31 ns) and the anchor is the
+        // only internal node: rows are node-indexed, so a lane owns one leaf
+        // across the chunk's rows (a leaf's incl IS its excl: straight copies,
+        // coalesced along the node axis, within-rank sums in registers); the
+        // anchor's inclusive time is the row total, reduced across the warp.
+        uint32_t rs[GC];
+#pragma unroll
+        for (uint32_t r = 0; r < GC; ++r)
+          rs[r] = (lane == 0 && r < n_iter_rows) ? rlo[(s0 + r) * nn] : 0u;  // anchor's own excl
+        for (uint32_t n = 1 + lane; n < nn; n += 32) {
+          u64 sx = 0, sq = 0;
           uint64_t* dst = p.cube_incl + ob + n;
 #pragma unroll
           for (uint32_t r = 0; r < GC; ++r) {
             if (r < n_iter_rows) {
               const uint32_t idx = (s0 + r) * nn + n;
               const uint32_t ex = rlo[idx];
-              const uint32_t in = n == 0 ? rt32[2 * (s0 + r)] : ex;
-              dst[r * nn] = in;
-              if (n == 0 && p.store_cube) p.cube_xint[ib + kb + r] = ex;  // m == 1
+              rs[r] += ex;
+              dst[r * nn] = ex;
               rlo[idx] = 0;
               if (r < kcap) {
-                sx += in;
-                const u64 q = static_cast<u64>(in) * in;
-                ql += q;
-                qh += ql < q ? 1ull : 0ull;
+                sx += ex;
+                sq += static_cast<u64>(ex) * ex;  // < 4 * 2^62
               }
             }
           }
           if (kcap) {
             wsx[n] += sx;
-            const u64 l2 = wsqlo[n] + ql;
-            wsqhi[n] += qh + (l2 < ql ? 1ull : 0ull);
+            const u64 l2 = wsqlo[n] + sq;
+            wsqhi[n] += l2 < sq ? 1ull : 0ull;
             wsqlo[n] = l2;
           }
         }
-      } else if (root_only) {
-        // rows are node-indexed, so a lane owns one node across the chunk's
-        // rows: straight copies to the cube (coalesced along the node axis),
-        // node 0 (the anchor, the only internal node) takes the row total as
-        // its inclusive time, and the within-rank sums stay in registers
-        for (uint32_t n = lane; n < nn; n += 32) {
-          u64 sx = 0, ql = 0, qh = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < GC; ++r)
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) rs[r] += __shfl_xor_sync(FULL, rs[r], d);
+        if (lane == 0) {
+          u64 sx = 0, sq = 0;
 #pragma unroll
           for (uint32_t r = 0; r < GC; ++r) {
             if (r < n_iter_rows) {
-              const uint32_t idx = (s0 + r) * nn + n;
-              const u64 ex = cell64(rlo, rhi, idx);
-              const u64 in = n == 0 ? rtot[s0 + r] : ex;
-              p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
-              if (n == 0 && p.store_cube) p.cube_xint[ib + kb + r] = ex;  // m == 1
-              rlo[idx] = rhi[idx] = 0;
-              if (r < kcap) {  // within-rank sums over k < K (iteration_cv_report)
-                sx += in;
-                acc_sq(ql, qh, in);
+              const uint32_t idx = (s0 + r) * nn;
+              p.cube_incl[ob + static_cast<u64>(r) * nn] = rs[r];
+              if (p.store_cube) p.cube_xint[ib + kb + r] = rlo[idx];  // m == 1
+              rlo[idx] = 0;
+              if (r < kcap) {
+                sx += rs[r];
+                sq += static_cast<u64>(rs[r]) * rs[r];
               }
             }
           }
           if (kcap) {
-            wsx[n] += sx;
-            const u64 l2 = wsqlo[n] + ql;
-            wsqhi[n] += qh + (l2 < ql ? 1ull : 0ull);
-            wsqlo[n] = l2;
+            wsx[0] += sx;
+            const u64 l2 = wsqlo[0] + sq;
+            wsqhi[0] += l2 < sq ? 1ull : 0ull;
+            wsqlo[0] = l2;
           }
         }
       } else {
@@ -789,11 +766,11 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       }
       if (c == 0) {  // the gap row [first_ts, b_0) (itermodel.cpp:331-338)
         __syncwarp();
-        if (!root_only) warp_prefix_row(rlo + R2 * nn, rhi + R2 * nn, s_node, pref, nn, lane);
+        warp_prefix_row(rlo + R2 * nn, rhi + R2 * nn, s_node, pref, nn, lane);
         for (uint32_t n = lane; n < nn; n += 32) {
           const int4 nd = s_node[n];
           const u64 ex = cell64(rlo, rhi, R2 * nn + n);
-          const u64 in = !nd.z ? ex : (root_only ? rtot[R2] : pref[nd.x + nd.y] - pref[nd.x]);
+          const u64 in = !nd.z ? ex : pref[nd.x + nd.y] - pref[nd.x];
           p.gap_excl[static_cast<size_t>(tp) * nn + n] = ex;
           p.gap_incl[static_cast<size_t>(tp) * nn + n] = in;
         }
@@ -801,8 +778,6 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         for (uint32_t n = lane; n < nn; n += 32) rlo[R2 * nn + n] = rhi[R2 * nn + n] = 0;
       }
       __syncwarp();
-      if (static_cast<uint32_t>(lane) < n_iter_rows) rtot[s0 + lane] = 0;
-      if (c == 0 && lane == 0) rtot[R2] = 0;
       __syncwarp();
     }
     if (pos >= n_t && static_cast<u64>(kb) + G >= iters) break;
