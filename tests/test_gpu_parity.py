@@ -284,3 +284,51 @@ def test_full_query_all_parts(gpu_ctx_factory):
     assert_rel(out["site_ratio"], oo["site_ratio"], 1e-12, "site ratio")
     assert_rel(out["node_mean"], oo["node_mean"], 1e-12, "node mean")
     assert np.array_equal(out["selected"], oo["selected"])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_wide_durations(gpu_ctx_factory, seed):
+    """Segments, iterations and block steps spanning >= 2^31 / 2^32 ns take the
+    64-bit paths (carried shared adds, big min/max, 128-bit squares): still
+    bit-exact against the oracle."""
+    rng = np.random.default_rng(500 + seed)
+    ctx = gpu_ctx_factory()
+    n_ctx = int(rng.integers(3, 12))
+    parent = random_cct(rng, n_ctx)
+    tr = random_traces(rng, int(rng.integers(2, 20)), n_ctx, int(rng.integers(50, 700)),
+                       ts_step=2**34, dup_prob=0.3)
+    ctx.set_cct(parent)
+    ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    T = int(tr["t_end"].max())
+    for t0, t1 in ((0, T + 1), (T // 3, 2 * T // 3), (T // 5, T // 5 + 2**33)):
+        check_window(ctx, tr, parent, t0, t1)
+    for anchor in sorted({0, 1, int(rng.integers(0, n_ctx))}):
+        check_cube(ctx, tr, parent, anchor)
+
+
+def test_narrow_and_wide_iterations_mixed(gpu_ctx_factory):
+    """One trace whose iterations alternate between short (< 2^31 ns) and
+    long (> 2^32 ns) spans: chunks switch between the 32-bit and the 64-bit
+    cube paths inside one trace."""
+    parent = np.array([0xFFFFFFFF, 0, 1, 1, 0], np.uint32)
+    ts, cx = [], []
+    t = 1000
+    for it in range(40):
+        long_it = (it // 3) % 2 == 1
+        ts.append(t); cx.append(1)
+        for k in (2, 3):
+            ts.append(t); cx.append(k)
+            t += (3 * 2**31 if long_it else 10_000 + 37 * it) + k
+        ts.append(t); cx.append(4)
+        t += 5
+        ts.append(t); cx.append(0)
+        t += 3
+    tr = {"ts": np.array(ts, np.uint64), "ctx": np.array(cx, np.uint32),
+          "off": np.array([0, len(ts)], np.uint64), "t_end": np.array([t + 7], np.uint64),
+          "pid": np.array([1], np.uint32)}
+    ctx = gpu_ctx_factory()
+    ctx.set_cct(parent)
+    ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    for anchor in (1, 0):
+        check_cube(ctx, tr, parent, anchor, stats=False)
+    check_window(ctx, tr, parent, 0, t + 8)
