@@ -52,7 +52,7 @@ typedef unsigned __int128 u128;
 #define PSG_LB_MINB 1
 #endif
 #ifndef PSG_G
-#define PSG_G 4
+#define PSG_G 8
 #endif
 
 #ifndef PSG_RB
@@ -718,27 +718,29 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         for (uint32_t r = 0; r < GC; ++r)
 #pragma unroll
           for (int d = 16; d > 0; d >>= 1) rs[r] += __shfl_xor_sync(FULL, rs[r], d);
-        if (lane == 0) {
+        // the anchor's cells: lane r writes row r; lane 0 folds the within sums
+        uint32_t mine = rs[0];
+#pragma unroll
+        for (uint32_t r = 1; r < GC; ++r)
+          if (static_cast<uint32_t>(lane) == r) mine = rs[r];
+        if (static_cast<uint32_t>(lane) < n_iter_rows) {
+          const uint32_t idx = (s0 + lane) * nn;
+          p.cube_incl[ob + static_cast<u64>(lane) * nn] = mine;
+          if (p.store_cube) p.cube_xint[ib + kb + lane] = rlo[idx];  // m == 1
+          rlo[idx] = 0;
+        }
+        if (kcap && lane == 0) {
           u64 sx = 0, sq = 0;
 #pragma unroll
-          for (uint32_t r = 0; r < GC; ++r) {
-            if (r < n_iter_rows) {
-              const uint32_t idx = (s0 + r) * nn;
-              p.cube_incl[ob + static_cast<u64>(r) * nn] = rs[r];
-              if (p.store_cube) p.cube_xint[ib + kb + r] = rlo[idx];  // m == 1
-              rlo[idx] = 0;
-              if (r < kcap) {
-                sx += rs[r];
-                sq += static_cast<u64>(rs[r]) * rs[r];
-              }
+          for (uint32_t r = 0; r < GC; ++r)
+            if (r < kcap) {
+              sx += rs[r];
+              sq += static_cast<u64>(rs[r]) * rs[r];
             }
-          }
-          if (kcap) {
-            wsx[0] += sx;
-            const u64 l2 = wsqlo[0] + sq;
-            wsqhi[0] += l2 < sq ? 1ull : 0ull;
-            wsqlo[0] = l2;
-          }
+          wsx[0] += sx;
+          const u64 l2 = wsqlo[0] + sq;
+          wsqhi[0] += l2 < sq ? 1ull : 0ull;
+          wsqlo[0] = l2;
         }
       } else {
         for (uint32_t r = 0; r < n_iter_rows; ++r) {
