@@ -424,7 +424,7 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
 #define PSG_WMAX 16  // warps (traces) per CTA of k_trace_query (<= its launch bound / 32)
 #endif
 #ifndef PSG_G
-#define PSG_G 4  // iterations per chunk of k_trace_query (power of two)
+#define PSG_G 8  // iterations per chunk of k_trace_query (power of two, <= 15)
 #endif
 
 uint32_t choose_warps(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table_bytes) {
