@@ -850,6 +850,7 @@ void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) 
 
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
   if (p.tr.n == 0) return;
+  if (p.G != GC) fail(PS_E_INTERNAL, "chunk size mismatch between host and kernel (PSG_G)");
   if (p.do_window && p.do_cube)
     launch_variant<true, true>(p, smem_bytes, s);
   else if (p.do_window)
