@@ -343,13 +343,16 @@ struct run_ctx {
   bool root_only;
 };
 
-template <bool WIN, bool CUBE, int WM, bool CWIDE>
+// ALL: every event of the block step is valid and none is the trace's last
+// (the common interior step): no per-event range or end checks.
+template <bool WIN, bool CUBE, int WM, bool CWIDE, bool ALL>
 __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
                                            const run_ctx& R, run_state& st, const warp_tables& T) {
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
     const int li = R.lb + j;
-    const bool valid = static_cast<unsigned>(li - R.lo) < static_cast<unsigned>(R.hi - R.lo);
+    const bool valid =
+        ALL || static_cast<unsigned>(li - R.lo) < static_cast<unsigned>(R.hi - R.lo);
     const u64 tsj = tv[j], nts = tv[j + 1];
     const uint32_t cj = valid ? cv[j] : 0u;
     if (CUBE) {
@@ -365,10 +368,10 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
       if (valid && pp >= 0 && st.cube_ok) {
         const uint32_t idx = st.rowb + pp;
         if (CWIDE) {
-          const u64 dc = (li == R.last_li ? R.tend : nts) - tsj;
+          const u64 dc = ((!ALL && li == R.last_li) ? R.tend : nts) - tsj;
           sadd64(R.rlo + idx, R.rhi + idx, dc);
         } else {  // the iteration spans < 2^32 ns: 32-bit differences are exact
-          const uint32_t dc = static_cast<uint32_t>(li == R.last_li ? R.tend : nts) -
+          const uint32_t dc = static_cast<uint32_t>((!ALL && li == R.last_li) ? R.tend : nts) -
                               static_cast<uint32_t>(tsj);
           atomicAdd(R.rlo + idx, dc);
         }
@@ -402,14 +405,19 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
 template <bool WIN, bool CUBE, bool CWIDE>
 __device__ __forceinline__ void run_block(int wm, const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
                                           const run_ctx& R, run_state& st, const warp_tables& T) {
-  if (wm == WIN_FULL)
-    run_events<WIN, CUBE, WIN_FULL, CWIDE>(tv, cv, R, st, T);
+  const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
+  if (!CWIDE && all && wm == WIN_FULL)
+    run_events<WIN, CUBE, WIN_FULL, false, true>(tv, cv, R, st, T);
+  else if (!CWIDE && all && wm == WIN_NONE)
+    run_events<WIN, CUBE, WIN_NONE, false, true>(tv, cv, R, st, T);
+  else if (wm == WIN_FULL)
+    run_events<WIN, CUBE, WIN_FULL, CWIDE, false>(tv, cv, R, st, T);
   else if (wm == WIN_PART)
-    run_events<WIN, CUBE, WIN_PART, CWIDE>(tv, cv, R, st, T);
+    run_events<WIN, CUBE, WIN_PART, CWIDE, false>(tv, cv, R, st, T);
   else if (wm == WIN_WIDE)
-    run_events<WIN, CUBE, WIN_WIDE, CWIDE>(tv, cv, R, st, T);
+    run_events<WIN, CUBE, WIN_WIDE, CWIDE, false>(tv, cv, R, st, T);
   else
-    run_events<WIN, CUBE, WIN_NONE, CWIDE>(tv, cv, R, st, T);
+    run_events<WIN, CUBE, WIN_NONE, CWIDE, false>(tv, cv, R, st, T);
 }
 
 __device__ __forceinline__ u64 cell64(const uint32_t* lo, const uint32_t* hi, uint32_t i) {
