@@ -141,10 +141,15 @@ enum {
   PSG_Q_ALL = PSG_Q_WINDOW | PSG_Q_CUBE | PSG_Q_STATS | PSG_Q_OUTLIERS
 };
 
+#define PSG_ANCHOR_AUTO 0xFFFFFFFFu
+
 typedef struct psg_query_spec {
   uint32_t flags;
   uint64_t t0_ns, t1_ns;         /* window [t0, t1); t0 > t1 is PS_E_INVALID_ARGUMENT */
-  uint32_t anchor_ctx;           /* explicit anchor (itermodel anchor_policy::explicit_ctx) */
+  uint32_t anchor_ctx;           /* explicit anchor (itermodel anchor_policy::explicit_ctx), or
+                                    PSG_ANCHOR_AUTO: suggest_anchor on the trace with the
+                                    smallest profile id, on the device (itermodel.cpp:45-109,
+                                    253-255) */
   /* outliers: candidate call-site contexts (the worst balance ratio wins,
    * workflows.cpp:442-459), then node means of its per-rank window-inclusive
    * time, z-scores, and the top-k (value desc, node id asc) among z >= z_min
@@ -168,6 +173,7 @@ typedef struct psg_query_info {
   uint64_t n_cells;              /* local cube cells (sum iter_counts * n_nodes) */
   uint32_t n_leaves;
   uint32_t n_internal;           /* internal nodes of the subtree (the cube stores excl only for these) */
+  uint32_t anchor;               /* the anchor used (the suggested one for PSG_ANCHOR_AUTO) */
   /* outliers */
   uint32_t worst_site;           /* ctx id */
   double worst_ratio;

@@ -62,6 +62,9 @@ def orc():
         lib.orc_outliers.restype = C.c_uint32
         lib.orc_outliers.argtypes = [I64P, C.c_uint32, C.c_uint32, U32P, C.c_uint32, C.c_uint32,
                                      C.c_double, F64P, U32P, F64P, F64P, U32P]
+        lib.orc_suggest_anchor.restype = C.c_uint32
+        lib.orc_suggest_anchor.argtypes = [U64P, U32P, C.c_uint64, C.c_uint64, U32P, C.c_uint32,
+                                           C.c_uint32, C.c_double]
         _orc = lib
     return _orc
 
@@ -110,6 +113,17 @@ def cube(tr: dict, parent, anchor: int) -> dict:
         bo[1:] = np.cumsum(kept.astype(np.uint64) * nn)[:-1]
     return {"node_ids": node_ids, "iter_counts": ic, "block_offset": bo, "incl": incl,
             "excl": excl, "gap_incl": gi, "gap_excl": ge}
+
+
+def suggest_anchor(tr: dict, parent, t: int = 0, min_iters: int = 3, cv_max: float = 0.2) -> int:
+    """suggest_anchor on trace t (0xFFFFFFFF: no periodic context)."""
+    parent = np.ascontiguousarray(parent, np.uint32)
+    b, e = int(tr["off"][t]), int(tr["off"][t + 1])
+    ts = np.ascontiguousarray(tr["ts"][b:e], np.uint64)
+    cx = np.ascontiguousarray(tr["ctx"][b:e], np.uint32)
+    return int(orc().orc_suggest_anchor(_p(ts, C.c_uint64), _p(cx, C.c_uint32), e - b,
+                                        int(tr["t_end"][t]), _p(parent, C.c_uint32), len(parent),
+                                        min_iters, cv_max))
 
 
 def node_stats(cb: dict, npos: int) -> tuple[np.ndarray, bool]:

@@ -367,3 +367,88 @@ uint32_t orc_outliers(const int64_t* values, uint32_t n_sites, uint32_t n_ranks,
   free(cnt);
   return ns;
 }
+
+/* itermodel.cpp:27-41 gap_cv(): population CV (fraction) of inter-entry gaps. */
+static double gap_cv(const uint64_t* e, uint64_t n) {
+  double mean = 0.0;
+  for (uint64_t i = 1; i < n; ++i) mean += (double)(e[i] - e[i - 1]);
+  mean /= (double)(n - 1);
+  if (mean <= 0.0) return INFINITY;
+  double var = 0.0;
+  for (uint64_t i = 1; i < n; ++i) {
+    double g = (double)(e[i] - e[i - 1]);
+    var += (g - mean) * (g - mean);
+  }
+  var /= (double)(n - 1);
+  return sqrt(var) / mean;
+}
+
+/* itermodel.cpp:45-109 suggest_anchor(): walk the step function once; a
+ * context is ENTERED at event i when it is on the ancestor chain of ctx[i]
+ * but not on the previous event's chain; covered time = inclusive time of the
+ * segments (the last one ends at max(t_end, ts)).  Candidates have >=
+ * min_iters entries and gap CV <= cv_max; the winner covers the most time
+ * (ties: smallest id).  Returns 0xFFFFFFFF when there is no candidate (the
+ * reference raises no_periodicity). */
+uint32_t orc_suggest_anchor(const uint64_t* ts, const uint32_t* ctx, uint64_t n, uint64_t t_end,
+                            const uint32_t* parent, uint32_t n_ctx, uint32_t min_iters,
+                            double cv_max) {
+  uint64_t* cnt = (uint64_t*)calloc(n_ctx, sizeof(uint64_t));
+  uint64_t* covered = (uint64_t*)calloc(n_ctx, sizeof(uint64_t));
+  char* on_prev = (char*)calloc(n_ctx, 1);
+  char* on_cur = (char*)calloc(n_ctx, 1);
+  /* pass 1: entry counts and covered time */
+  for (uint64_t i = 0; i < n; ++i) {
+    memset(on_cur, 0, n_ctx);
+    for (uint32_t c = ctx[i];; c = parent[c]) {
+      on_cur[c] = 1;
+      if (!on_prev[c]) cnt[c] += 1;
+      if (parent[c] == NO_PARENT) break;
+    }
+    uint64_t end = i + 1 < n ? ts[i + 1] : (t_end > ts[i] ? t_end : ts[i]);
+    uint64_t dur = end - ts[i];
+    if (dur)
+      for (uint32_t c = ctx[i];; c = parent[c]) {
+        covered[c] += dur;
+        if (parent[c] == NO_PARENT) break;
+      }
+    char* tmp = on_prev;
+    on_prev = on_cur;
+    on_cur = tmp;
+  }
+  /* pass 2: entry timestamps per context, in order */
+  uint64_t* off = (uint64_t*)calloc(n_ctx + 1, sizeof(uint64_t));
+  for (uint32_t c = 0; c < n_ctx; ++c) off[c + 1] = off[c] + cnt[c];
+  uint64_t* ent = (uint64_t*)malloc(sizeof(uint64_t) * (off[n_ctx] + 1));
+  uint64_t* fill = (uint64_t*)calloc(n_ctx, sizeof(uint64_t));
+  memset(on_prev, 0, n_ctx);
+  for (uint64_t i = 0; i < n; ++i) {
+    memset(on_cur, 0, n_ctx);
+    for (uint32_t c = ctx[i];; c = parent[c]) {
+      on_cur[c] = 1;
+      if (!on_prev[c]) ent[off[c] + fill[c]++] = ts[i];
+      if (parent[c] == NO_PARENT) break;
+    }
+    char* tmp = on_prev;
+    on_prev = on_cur;
+    on_cur = tmp;
+  }
+  uint32_t best = NO_PARENT;
+  uint64_t best_cov = 0;
+  for (uint32_t c = 0; c < n_ctx; ++c) {
+    if (cnt[c] < min_iters) continue;
+    if (gap_cv(ent + off[c], cnt[c]) > cv_max) continue;
+    if (best == NO_PARENT || covered[c] > best_cov) {
+      best = c;
+      best_cov = covered[c];
+    }
+  }
+  free(cnt);
+  free(covered);
+  free(on_prev);
+  free(on_cur);
+  free(off);
+  free(ent);
+  free(fill);
+  return best;
+}

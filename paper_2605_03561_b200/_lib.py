@@ -25,6 +25,7 @@ Q_WINDOW, Q_CUBE, Q_STATS, Q_OUTLIERS = 1, 2, 4, 8
 Q_NO_CUBE_STORE = 1 << 8
 Q_CLAMP_TEND = 1 << 9
 Q_ALL = Q_WINDOW | Q_CUBE | Q_STATS | Q_OUTLIERS
+ANCHOR_AUTO = 0xFFFFFFFF
 
 
 class PsgError(RuntimeError):
@@ -62,7 +63,8 @@ class QueryInfo(C.Structure):
         ("n_window_groups", C.c_uint64), ("n_window_rows", C.c_uint64),
         ("n_nodes", C.c_uint32), ("n_kept", C.c_uint32), ("n_skipped", C.c_uint32),
         ("min_iterations", C.c_uint32), ("n_kept_global", C.c_uint32), ("n_cells", C.c_uint64),
-        ("n_leaves", C.c_uint32), ("n_internal", C.c_uint32), ("worst_site", C.c_uint32), ("worst_ratio", C.c_double),
+        ("n_leaves", C.c_uint32), ("n_internal", C.c_uint32), ("anchor", C.c_uint32),
+        ("worst_site", C.c_uint32), ("worst_ratio", C.c_double),
         ("n_outliers", C.c_uint32), ("n_racks", C.c_uint32),
         ("ms_total", C.c_float), ("ms_main", C.c_float), ("ms_bounds", C.c_float),
     ]

@@ -16,6 +16,7 @@
 #include <numeric>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "psg_internal.h"
@@ -166,6 +167,7 @@ struct psg_context {
   std::vector<uint32_t> h_parent;
   preorder cct_po;
   dbuf<int32_t> d_cct_pre, d_cct_size;
+  dbuf<uint32_t> d_parent;
 
   // traces (SoA)
   uint32_t n_traces = 0;
@@ -175,6 +177,8 @@ struct psg_context {
   dbuf<uint64_t> d_off, d_ts, d_tend;
   dbuf<uint32_t> d_ctx, d_pid;
   dbuf<uint8_t> d_stage;
+  uint8_t* pinned[3] = {nullptr, nullptr, nullptr};  // pageable-source staging ring
+  cudaEvent_t pinned_ev[3] = {nullptr, nullptr, nullptr};
 
   // nodes / topology
   uint32_t n_nodes = 0;
@@ -234,6 +238,10 @@ struct psg_context {
   dbuf<uint64_t> gen_chunks;
 
   ~psg_context() {
+    for (int i = 0; i < 3; ++i) {
+      if (pinned_ev[i]) cudaEventDestroy(pinned_ev[i]);
+      if (pinned[i]) cudaFreeHost(pinned[i]);
+    }
     if (comm) nccl().comm_destroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -318,6 +326,8 @@ void set_cct_impl(psg_context* c, const uint32_t* parent, uint32_t n_ctx) {
                            cudaMemcpyHostToDevice, c->stream));
   PSG_CUDA(cudaMemcpyAsync(c->d_cct_size.ensure(n_ctx), c->cct_po.size.data(), 4ull * n_ctx,
                            cudaMemcpyHostToDevice, c->stream));
+  PSG_CUDA(cudaMemcpyAsync(c->d_parent.ensure(n_ctx), parent, 4ull * n_ctx,
+                           cudaMemcpyHostToDevice, c->stream));
   c->cached_anchor = -1;
   invalidate_results(c);
   c->sync();
@@ -353,10 +363,60 @@ void finish_load(psg_context* c) {
 }
 
 // Host AoS body -> HBM staging (chunked, double-buffered) -> SoA.
+// Pageable sources (an mmap'd trace.db, a std::vector) go through a ring of
+// pinned staging buffers: host threads fill buffer i+1 (page faults and
+// copies in parallel) while the DMA engine moves buffer i, then K1 transposes
+// on the stream.  Pinned sources are DMA'd directly (load_aos_pinned).
+void load_aos_pageable(psg_context* c, const uint8_t* body, uint64_t n_events) {
+  constexpr uint64_t kBufEv = 1ull << 22;             // 4 Mi events = 48 MB per buffer
+  constexpr uint64_t kBufBytes = kBufEv * 12;
+  constexpr int kBufs = 3;
+  if (!c->pinned[0]) {
+    for (int i = 0; i < kBufs; ++i) {
+      PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned[i]), kBufBytes,
+                             cudaHostAllocDefault));
+      PSG_CUDA(cudaEventCreateWithFlags(&c->pinned_ev[i], cudaEventDisableTiming));
+    }
+  }
+  uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, 2 * kBufBytes));
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nthreads = std::min(8u, hw);
+  uint64_t done = 0;
+  for (int i = 0; done < n_events; ++i) {
+    const uint64_t ev = std::min(kBufEv, n_events - done);
+    const int slot = i % kBufs;
+    PSG_CUDA(cudaEventSynchronize(c->pinned_ev[slot]));  // the buffer's previous DMA finished
+    const uint8_t* src = body + done * 12;
+    uint8_t* dst = c->pinned[slot];
+    const uint64_t bytes = ev * 12, part = (bytes + nthreads - 1) / nthreads;
+    std::vector<std::thread> th;
+    for (unsigned k = 1; k < nthreads; ++k) {
+      const uint64_t a = std::min(bytes, k * part), e = std::min(bytes, a + part);
+      if (a < e) th.emplace_back([=] { std::memcpy(dst + a, src + a, e - a); });
+    }
+    std::memcpy(dst, src, std::min(bytes, part));
+    for (auto& t : th) t.join();
+    uint8_t* dev = stage + static_cast<uint64_t>(i % 2) * kBufBytes;
+    PSG_CUDA(cudaMemcpyAsync(dev, dst, bytes, cudaMemcpyHostToDevice, c->stream));
+    PSG_CUDA(cudaEventRecord(c->pinned_ev[slot], c->stream));
+    launch_aos_to_soa(dev, ev, c->d_ts.p + done, c->d_ctx.p + done, c->stream);
+    done += ev;
+  }
+}
+
 void load_aos(psg_context* c, const uint8_t* body, uint64_t n_events) {
   c->n_events = n_events;
   c->d_ts.ensure(n_events + kEventPad);
   c->d_ctx.ensure(n_events + kEventPad);
+  if (n_events == 0) return;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, body) != cudaSuccess) {
+    cudaGetLastError();  // clear: unregistered host memory
+    attr.type = cudaMemoryTypeUnregistered;
+  }
+  if (attr.type != cudaMemoryTypeHost && attr.type != cudaMemoryTypeDevice &&
+      attr.type != cudaMemoryTypeManaged)
+    return load_aos_pageable(c, body, n_events);
   const uint64_t chunk_ev = 4ull << 24;  // 64 Mi events = 768 MB per chunk
   const uint64_t chunk_bytes = chunk_ev * 12;
   uint8_t* stage = c->d_stage.ensure(std::min<uint64_t>(2 * chunk_bytes, n_events * 12 + 64));
@@ -426,6 +486,46 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
 #ifndef PSG_G
 #define PSG_G 8  // iterations per chunk of k_trace_query (power of two, <= 15)
 #endif
+
+// itermodel::suggest_anchor on the trace with the smallest profile id over all
+// ranks (build_tri_model uses pids.front(), itermodel.cpp:253-255): its owner
+// runs the device pass, every rank receives the result.
+uint32_t auto_anchor(psg_context* c) {
+  uint64_t mine = ~0ull;
+  uint32_t t_min = 0;
+  for (uint32_t t = 0; t < c->n_traces; ++t)
+    if (c->h_pid[t] < mine) {
+      mine = c->h_pid[t];
+      t_min = t;
+    }
+  unsigned long long* d = c->summary.ensure(4);
+  uint64_t g = mine;
+  if (c->multi()) {
+    PSG_CUDA(cudaMemcpyAsync(d, &g, 8, cudaMemcpyHostToDevice, c->stream));
+    c->allreduce(reinterpret_cast<unsigned long long*>(d), 1, ncclUint64, ncclMin);
+    PSG_CUDA(cudaMemcpyAsync(&g, d, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  }
+  if (g == ~0ull) fail(PS_E_INVALID_ARGUMENT, "no traces loaded");
+  uint64_t anchor = ~0ull;
+  if (g == mine) {
+    const uint64_t b = c->h_off[t_min], n = c->h_off[t_min + 1] - b;
+    const uint32_t a = launch_suggest_anchor(c->d_ts.p + b, c->d_ctx.p + b, n, c->h_tend[t_min],
+                                             c->d_parent.p, c->d_cct_pre.p, c->d_cct_size.p,
+                                             c->n_ctx, 3, 0.2, c->stream);
+    // kNone (no periodic context) travels as a valid "minimum" too
+    anchor = a;
+  }
+  if (c->multi()) {
+    PSG_CUDA(cudaMemcpyAsync(d, &anchor, 8, cudaMemcpyHostToDevice, c->stream));
+    c->allreduce(reinterpret_cast<unsigned long long*>(d), 1, ncclUint64, ncclMin);
+    PSG_CUDA(cudaMemcpyAsync(&anchor, d, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  }
+  if (anchor >= 0xFFFFFFFFull)  // itermodel.cpp:106-107
+    fail(PS_E_NO_PERIODICITY, "no context shows periodic entries");
+  return static_cast<uint32_t>(anchor);
+}
 
 uint32_t choose_warps(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table_bytes) {
   // Aim for >= 2 CTAs per SM worth of traces; fit the carve-outs in 227 KB.
@@ -851,8 +951,11 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       p.cct_size = c->d_cct_size.p;
     }
     uint32_t nn = 0;
+    uint32_t anchor = q->anchor_ctx;
+    if (do_cube && anchor == PSG_ANCHOR_AUTO) anchor = auto_anchor(c);
+    info->anchor = do_cube ? anchor : 0;
     if (do_cube) {
-      compute_subtree(c, q->anchor_ctx);
+      compute_subtree(c, anchor);
       nn = c->nn;
       uint32_t* ic = c->iter_count.ensure(n + 1);
       // pass 1: iteration boundaries (re-run with exact region bounds on overflow)

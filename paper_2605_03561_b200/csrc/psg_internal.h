@@ -193,6 +193,11 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
                           uint64_t* chunk_scratch, uint64_t* ts, uint32_t* ctx, uint64_t* t_end,
                           cudaStream_t s);
 void launch_bounds(const bound_params& p, cudaStream_t s);
+// itermodel::suggest_anchor on one trace (psg_anchor.cu); returns the anchor
+// ctx or 0xFFFFFFFF when no context shows periodic entries.
+uint32_t launch_suggest_anchor(const uint64_t* ts, const uint32_t* ctx, uint64_t n, uint64_t t_end,
+                               const uint32_t* parent, const int32_t* pre, const int32_t* size,
+                               uint32_t n_ctx, uint32_t min_iters, double cv_max, cudaStream_t s);
 void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t* tpos,
                         uint64_t* block_off, uint64_t* kept_bo,
                         unsigned long long* summary /*[0]=kept [1]=min_it [2]=cells*/,

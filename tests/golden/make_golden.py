@@ -64,6 +64,15 @@ def add_cubes(out: dict, db: str, anchors) -> None:
             out[f"c{i}_{k}"] = r[k]
 
 
+def auto_anchor(db: str) -> np.ndarray:
+    """suggest_anchor on the first trace (itermodel.cpp:253-255); 0xFFFFFFFF
+    where the reference raises no_periodicity (or empty_input)."""
+    try:
+        return oracle.ref_trimodel(db, -1)["anchor"]
+    except RuntimeError:
+        return np.array([0xFFFFFFFF], np.uint32)
+
+
 def iterative_fixture(name: str, cfg: dict, anchors=(1,)) -> None:
     with tempfile.TemporaryDirectory() as d:
         oracle.ref_generate(cfg, d)
@@ -71,6 +80,7 @@ def iterative_fixture(name: str, cfg: dict, anchors=(1,)) -> None:
         T = int(out["t_end"].max())
         add_windows(out, d, [(T // 4, 3 * T // 4), (0, T + 1), (T // 3, T // 3)])
         add_cubes(out, d, anchors)
+        out["auto_anchor"] = auto_anchor(d)
         out["config"] = np.frombuffer(json.dumps(cfg).encode(), np.uint8)
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
 
@@ -88,6 +98,7 @@ def random_fixture(name: str, seed: int) -> None:
         T = int(tr["t_end"].max()) if len(tr["t_end"]) else 10
         add_windows(out, d, [(0, T + 1), (T // 3, 2 * T // 3), (T // 2, T // 2), (T // 5, T // 5 + 7)])
         add_cubes(out, d, sorted({0, 1, int(rng.integers(0, n_ctx)), n_ctx - 1}))
+        out["auto_anchor"] = auto_anchor(d)
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
 
 
@@ -104,6 +115,49 @@ def kat_single_segment() -> None:
         out["parent"] = parent
         add_windows(out, d, [(100, 105)])
         np.savez_compressed(os.path.join(HERE, "kat_single_segment.npz"), **out)
+
+
+def anchor_cases() -> None:
+    """suggest_anchor on hand-shaped traces: nested periodic loops (the most
+    covered periodic context wins), exact ties in covered time (smallest id),
+    jittered gaps around the 0.2 CV cut, repeated timestamps."""
+    rng = np.random.default_rng(77)
+    out = {}
+    cases = []
+    # ctx: 0 root, 1 outer, 2 inner, 3 leafA (under inner), 4 leafB (under outer), 5 other (root)
+    parent = np.array([0xFFFFFFFF, 0, 1, 2, 1, 0, 2, 4], np.uint32)
+    for case in range(8):
+        ts, cx = [], []
+        t = int(rng.integers(0, 50))
+        jit = [0.0, 0.05, 0.15, 0.3, 0.5, 0.0, 0.1, 0.25][case]
+        for it in range(int(rng.integers(4, 12))):
+            ts.append(t); cx.append(1)
+            for j in range(int(rng.integers(1, 4))):
+                ts.append(t); cx.append(2)
+                d = max(1, int(100 * (1 + jit * rng.standard_normal())))
+                ts.append(t); cx.append(3 if case % 2 else 6)
+                t += d
+                ts.append(t); cx.append(7 if case == 5 else 4)
+                t += max(1, int(40 * (1 + jit * rng.standard_normal())))
+            ts.append(t); cx.append(0)
+            t += int(rng.integers(0, 3)) * (0 if case == 5 else 1)
+            if case in (6, 7):
+                ts.append(t); cx.append(5)
+                t += 30
+        t_end = t + int(rng.integers(0, 20))
+        tr = {"ts": np.array(ts, np.uint64), "ctx": np.array(cx, np.uint32),
+              "off": np.array([0, len(ts)], np.uint64), "t_end": np.array([t_end], np.uint64),
+              "pid": np.array([1], np.uint32)}
+        with tempfile.TemporaryDirectory() as d:
+            oracle.ref_write_traces(tr, parent, d)
+            a = auto_anchor(d)
+        for k, v in tr.items():
+            out[f"case{case}_{k}"] = v
+        out[f"case{case}_anchor"] = a
+        cases.append(int(a[0]))
+    out["parent"] = parent
+    out["n_cases"] = np.array([len(cases)])
+    np.savez_compressed(os.path.join(HERE, "anchor_cases.npz"), **out)
 
 
 def congestion_fixture(name: str, ranks_per_node: int, seed: int) -> None:
@@ -149,6 +203,7 @@ def main() -> None:
                       anchors=(1,))
     for s in range(4):
         random_fixture(f"random_{s}", s)
+    anchor_cases()
     congestion_fixture("congestion_rpn2", ranks_per_node=2, seed=2025)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):

@@ -332,3 +332,32 @@ def test_narrow_and_wide_iterations_mixed(gpu_ctx_factory):
     for anchor in (1, 0):
         check_cube(ctx, tr, parent, anchor, stats=False)
     check_window(ctx, tr, parent, 0, t + 8)
+
+
+def test_auto_anchor_on_device_matches_reference(gpu_ctx_factory):
+    """PSG_ANCHOR_AUTO runs suggest_anchor on the device over the trace with the
+    smallest profile id; the reference's choice (golden), then the same cube."""
+    from paper_2605_03561_b200 import ANCHOR_AUTO
+    from tests.test_oracle import load
+    ctx = gpu_ctx_factory()
+    z = load("anchor_cases")
+    for i in range(int(z["n_cases"][0])):
+        tr = {k: z[f"case{i}_{k}"] for k in ("ts", "ctx", "off", "t_end", "pid")}
+        want = int(z[f"case{i}_anchor"][0])
+        ctx.set_cct(z["parent"])
+        ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+        if want == 0xFFFFFFFF:
+            with pytest.raises(PsgError) as e:
+                ctx.query(Q_CUBE, anchor=ANCHOR_AUTO)
+            assert e.value.name == "no_periodicity"
+            continue
+        info = ctx.query(Q_CUBE, anchor=ANCHOR_AUTO)
+        assert info["anchor"] == want, i
+        assert np.array_equal(ctx.cube()["incl"], oracle.cube(tr, z["parent"], want)["incl"])
+    for name in ("small_iter", "gamess_like"):
+        g = load(name)
+        tr = {k: g[k] for k in ("ts", "ctx", "off", "t_end", "pid")}
+        ctx.set_cct(g["parent"])
+        ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+        info = ctx.query(Q_CUBE | Q_STATS, anchor=ANCHOR_AUTO)
+        assert info["anchor"] == int(g["auto_anchor"][0])

@@ -223,3 +223,15 @@ def test_libpsg_is_sm100a_only():
                          capture_output=True, text=True).stdout
     archs = set(re.findall(r"sm_(\d+a?)", out))
     assert archs == {"100a"}, archs
+
+
+def test_suggest_anchor_oracle_matches_reference():
+    """itermodel.cpp:45-109 on the first trace: the oracle's restatement picks
+    the reference's anchor (or none, where the reference raises no_periodicity)."""
+    for name in FIXTURES:
+        g = load(name)
+        assert oracle.suggest_anchor(traces(g), g["parent"], 0) == int(g["auto_anchor"][0]), name
+    z = load("anchor_cases")
+    for i in range(int(z["n_cases"][0])):
+        tr = {k: z[f"case{i}_{k}"] for k in ("ts", "ctx", "off", "t_end", "pid")}
+        assert oracle.suggest_anchor(tr, z["parent"], 0) == int(z[f"case{i}_anchor"][0]), i
