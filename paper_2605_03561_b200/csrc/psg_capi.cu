@@ -5,6 +5,8 @@
 // capi.cpp:65-80).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -173,6 +175,8 @@ struct psg_context {
   uint32_t n_traces = 0;
   uint64_t n_events = 0;
   std::vector<uint64_t> h_off, h_tend;
+  std::vector<uint64_t> h_tbegin;  // trace.db index t_begin (validated on load; empty otherwise)
+  dbuf<uint64_t> d_tbegin;
   std::vector<uint32_t> h_pid;
   dbuf<uint64_t> d_off, d_ts, d_tend;
   dbuf<uint32_t> d_ctx, d_pid;
@@ -351,7 +355,13 @@ void finish_load(psg_context* c) {
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(c->summary.ensure(4));
   unsigned long long init[2] = {0ull, ~0ull};
   PSG_CUDA(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-  launch_validate(c->view(), c->n_ctx, flags, flags + 1, c->stream);
+  const uint64_t* tb = nullptr;
+  if (!c->h_tbegin.empty()) {
+    PSG_CUDA(cudaMemcpyAsync(c->d_tbegin.ensure(c->n_traces + 1), c->h_tbegin.data(),
+                             8ull * c->n_traces, cudaMemcpyHostToDevice, c->stream));
+    tb = c->d_tbegin.p;
+  }
+  launch_validate(c->view(), c->n_ctx, tb, flags, flags + 1, c->stream);
   unsigned long long out[2];
   PSG_CUDA(cudaMemcpyAsync(out, flags, sizeof(out), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
@@ -367,17 +377,23 @@ void finish_load(psg_context* c) {
 // pinned staging buffers: host threads fill buffer i+1 (page faults and
 // copies in parallel) while the DMA engine moves buffer i, then K1 transposes
 // on the stream.  Pinned sources are DMA'd directly (load_aos_pinned).
-void load_aos_pageable(psg_context* c, const uint8_t* body, uint64_t n_events) {
-  constexpr uint64_t kBufEv = 1ull << 22;             // 4 Mi events = 48 MB per buffer
-  constexpr uint64_t kBufBytes = kBufEv * 12;
-  constexpr int kBufs = 3;
-  if (!c->pinned[0]) {
-    for (int i = 0; i < kBufs; ++i) {
-      PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned[i]), kBufBytes,
-                             cudaHostAllocDefault));
-      PSG_CUDA(cudaEventCreateWithFlags(&c->pinned_ev[i], cudaEventDisableTiming));
-    }
+constexpr uint64_t kRingEvents = 1ull << 22;  // 4 Mi events = 48 MB per pinned buffer
+constexpr uint64_t kRingBytes = kRingEvents * 12;
+constexpr int kRingBufs = 3;
+
+void ensure_pinned_ring(psg_context* c) {
+  if (c->pinned[0]) return;
+  for (int i = 0; i < kRingBufs; ++i) {
+    PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned[i]), kRingBytes,
+                           cudaHostAllocDefault));
+    PSG_CUDA(cudaEventCreateWithFlags(&c->pinned_ev[i], cudaEventDisableTiming));
   }
+}
+
+void load_aos_pageable(psg_context* c, const uint8_t* body, uint64_t n_events) {
+  constexpr uint64_t kBufEv = kRingEvents, kBufBytes = kRingBytes;
+  constexpr int kBufs = kRingBufs;
+  ensure_pinned_ring(c);
   uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, 2 * kBufBytes));
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const unsigned nthreads = std::min(8u, hw);
@@ -397,6 +413,58 @@ void load_aos_pageable(psg_context* c, const uint8_t* body, uint64_t n_events) {
     std::memcpy(dst, src, std::min(bytes, part));
     for (auto& t : th) t.join();
     uint8_t* dev = stage + static_cast<uint64_t>(i % 2) * kBufBytes;
+    PSG_CUDA(cudaMemcpyAsync(dev, dst, bytes, cudaMemcpyHostToDevice, c->stream));
+    PSG_CUDA(cudaEventRecord(c->pinned_ev[slot], c->stream));
+    launch_aos_to_soa(dev, ev, c->d_ts.p + done, c->d_ctx.p + done, c->stream);
+    done += ev;
+  }
+}
+
+// A byte range of a file (trace.db bodies): host threads pread() straight into
+// the pinned ring (no page faults on an mmap), the DMA engine moves the
+// previous buffer meanwhile, then K1 transposes on the stream.
+void load_aos_file(psg_context* c, const std::string& path, uint64_t offset, uint64_t n_events) {
+  c->n_events = n_events;
+  c->d_ts.ensure(n_events + kEventPad);
+  c->d_ctx.ensure(n_events + kEventPad);
+  ensure_pinned_ring(c);
+  const int fd = ::open(path.c_str(), O_RDONLY);
+  if (fd < 0) fail(PS_E_IO, "cannot open " + path);
+  struct fd_closer {
+    int fd;
+    ~fd_closer() { ::close(fd); }
+  } closer{fd};
+  uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, 2 * kRingBytes));
+  const unsigned nthreads = std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+  uint64_t done = 0;
+  for (int i = 0; done < n_events; ++i) {
+    const uint64_t ev = std::min(kRingEvents, n_events - done);
+    const int slot = i % kRingBufs;
+    PSG_CUDA(cudaEventSynchronize(c->pinned_ev[slot]));
+    uint8_t* dst = c->pinned[slot];
+    const uint64_t bytes = ev * 12, part = ((bytes + nthreads - 1) / nthreads + 4095) & ~4095ull;
+    const uint64_t base = offset + done * 12;
+    std::vector<int> ok(nthreads, 1);
+    std::vector<std::thread> th;
+    for (unsigned k = 0; k < nthreads; ++k) {
+      const uint64_t a = std::min(bytes, k * part), e = std::min(bytes, a + part);
+      if (a >= e) break;
+      th.emplace_back([&, k, a, e] {
+        uint64_t got = a;
+        while (got < e) {
+          const ssize_t r = ::pread(fd, dst + got, e - got, static_cast<off_t>(base + got));
+          if (r <= 0) {
+            ok[k] = 0;
+            return;
+          }
+          got += static_cast<uint64_t>(r);
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int v : ok)
+      if (!v) fail(PS_E_IO, "short read of " + path);
+    uint8_t* dev = stage + static_cast<uint64_t>(i % 2) * kRingBytes;
     PSG_CUDA(cudaMemcpyAsync(dev, dst, bytes, cudaMemcpyHostToDevice, c->stream));
     PSG_CUDA(cudaEventRecord(c->pinned_ev[slot], c->stream));
     launch_aos_to_soa(dev, ev, c->d_ts.p + done, c->d_ctx.p + done, c->stream);
@@ -672,6 +740,7 @@ ps_status psg_load_traces_aos(psg_context* c, const void* body, uint64_t n_event
     c->h_off.assign(event_off, event_off + n_traces + 1);
     c->h_tend.assign(t_end_ns, t_end_ns + n_traces);
     c->h_pid.assign(profile_ids, profile_ids + n_traces);
+    c->h_tbegin.clear();
     for (uint32_t i = 0; i < n_traces; ++i)
       require(event_off[i] <= event_off[i + 1], "event_off must be non-decreasing");
     load_aos(c, static_cast<const uint8_t*>(body), n_events);
@@ -756,17 +825,12 @@ ps_status psg_load_trace_db(psg_context* c, const char* dir, const uint32_t* pid
         contiguous = false;
     }
     const uint64_t n_ev = c->h_off.back();
-    // first event must equal the indexed t_begin (store.cpp:750-751)
-    for (auto* e : sel)
-      if (e->event_count > 0) {
-        uint64_t ts0;
-        std::memcpy(&ts0, db.map.data() + e->offset, 8);
-        if (ts0 != e->t_begin_ns)
-          fail(PS_E_FORMAT, "trace " + std::to_string(e->profile_id) +
-                                " event 0: first event does not match indexed t_begin");
-      }
+    // first event == indexed t_begin (store.cpp:750-751) is checked on the device
+    c->h_tbegin.clear();
+    for (auto* e : sel) c->h_tbegin.push_back(e->t_begin_ns);
     if (contiguous || sel.empty()) {
-      load_aos(c, sel.empty() ? nullptr : db.map.data() + sel.front()->offset, n_ev);
+      if (n_ev) load_aos_file(c, db.dir + "/trace.db", sel.front()->offset, n_ev);
+      else load_aos(c, nullptr, 0);
     } else {
       std::vector<uint8_t> gathered(n_ev * 12);
       uint64_t o = 0;
@@ -837,6 +901,7 @@ ps_status psg_generate_iterative(psg_context* c, const psg_iter_scenario* s, uin
     c->h_pid.resize(n_local);
     for (uint32_t r = 0; r < n_local; ++r) c->h_pid[r] = rank_lo + r + 1;
     c->h_tend.assign(n_local, 0);
+    c->h_tbegin.clear();
 
     if (!c->jump.p) {
       auto mats = jump_matrices();

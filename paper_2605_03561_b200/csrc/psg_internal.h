@@ -184,8 +184,8 @@ void launch_soa_to_aos(const uint64_t* ts, const uint32_t* ctx, uint64_t n_event
 
 void launch_aos_to_soa(const uint8_t* body, uint64_t n_events, uint64_t* ts, uint32_t* ctx,
                        cudaStream_t s);
-void launch_validate(const trace_view& tr, uint32_t n_ctx, unsigned long long* bad,
-                     unsigned long long* first_bad, cudaStream_t s);
+void launch_validate(const trace_view& tr, uint32_t n_ctx, const uint64_t* t_begin,
+                     unsigned long long* bad, unsigned long long* first_bad, cudaStream_t s);
 void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_ranks,
                           uint32_t n_it, uint32_t n_k, const double* mean, const double* jitter,
                           const double* spread, uint64_t spread_kstride, uint64_t copy_ns,

@@ -125,8 +125,8 @@ void launch_soa_to_aos(const uint64_t* ts, const uint32_t* ctx, uint64_t n_event
 }
 
 // K1v: one warp per trace checks the invariants validate_database reports.
-__global__ void k_validate(trace_view tr, uint32_t n_ctx, unsigned long long* bad,
-                           unsigned long long* first_bad) {
+__global__ void k_validate(trace_view tr, uint32_t n_ctx, const uint64_t* t_begin,
+                           unsigned long long* bad, unsigned long long* first_bad) {
   uint32_t t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   int lane = threadIdx.x & 31;
   if (t >= tr.n) return;
@@ -137,6 +137,7 @@ __global__ void k_validate(trace_view tr, uint32_t n_ctx, unsigned long long* ba
     if (__ldg(tr.ctx + i) >= n_ctx) ok = false;
     if (i + 1 < e && ldg_u64(tr.ts + i + 1) < x) ok = false;
     if (i + 1 == e && tr.t_end[t] < x) ok = false;
+    if (i == b && t_begin && t_begin[t] != x) ok = false;  // store.cpp:750-751
   }
   if (!__all_sync(FULL, ok) && lane == 0) {
     atomicAdd(bad, 1ull);
@@ -144,10 +145,10 @@ __global__ void k_validate(trace_view tr, uint32_t n_ctx, unsigned long long* ba
   }
 }
 
-void launch_validate(const trace_view& tr, uint32_t n_ctx, unsigned long long* bad,
-                     unsigned long long* first_bad, cudaStream_t s) {
+void launch_validate(const trace_view& tr, uint32_t n_ctx, const uint64_t* t_begin,
+                     unsigned long long* bad, unsigned long long* first_bad, cudaStream_t s) {
   if (tr.n == 0) return;
-  k_validate<<<(tr.n + 7) / 8, 256, 0, s>>>(tr, n_ctx, bad, first_bad);
+  k_validate<<<(tr.n + 7) / 8, 256, 0, s>>>(tr, n_ctx, t_begin, bad, first_bad);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }

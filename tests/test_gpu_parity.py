@@ -6,13 +6,14 @@ ids; 1e-9 relative for the fp64 diagnostics (savings, CV)."""
 from __future__ import annotations
 
 import json
+import os
 
 import numpy as np
 import pytest
 
 import oracle
 from paper_2605_03561_b200 import Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_OUTLIERS, Q_STATS, Q_WINDOW, PsgError, scenarios
-from tests.helpers import assert_rel, random_cct, random_traces, ref_db, to_aos
+from tests.helpers import ROOT, assert_rel, random_cct, random_traces, ref_db, to_aos
 
 pytestmark = pytest.mark.gpu
 
@@ -361,3 +362,29 @@ def test_auto_anchor_on_device_matches_reference(gpu_ctx_factory):
         ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
         info = ctx.query(Q_CUBE | Q_STATS, anchor=ANCHOR_AUTO)
         assert info["anchor"] == int(g["auto_anchor"][0])
+
+
+def test_trace_db_ingest_multi_buffer(gpu_ctx_factory, tmp_path):
+    """psg_load_trace_db through the pread -> pinned ring -> HBM pipeline over
+    several 4 Mi-event buffers, and the page-cache-free gathered path for a
+    subset: the loaded events equal the ones written."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from load_bench import write_db
+    ctx = gpu_ctx_factory()
+    ctx.generate_iterative(scenarios.device_scenario(260, 746, seed=4))  # 13.0 M events
+    want = ctx.traces()
+    parent = np.array([0xFFFFFFFF, 0] + [1] * 64 + [0], np.uint32)
+    d = str(tmp_path / "db")
+    write_db(ctx, d, parent)
+    ctx.load_trace_db(d)
+    got = ctx.traces()
+    for k in ("ts", "ctx", "off", "t_end", "pid"):
+        assert np.array_equal(got[k], want[k]), k
+    sub = [int(want["pid"][i]) for i in (3, 100, 257)]
+    ctx.load_trace_db(d, sub)
+    g2 = ctx.traces()
+    assert list(g2["pid"]) == sub
+    a = int(want["off"][100])
+    assert np.array_equal(g2["ts"][int(g2["off"][1]):int(g2["off"][2])],
+                          want["ts"][a:a + int(g2["off"][2] - g2["off"][1])])
