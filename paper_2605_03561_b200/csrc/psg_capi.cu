@@ -1167,9 +1167,10 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
                       sa, na, c->d_worst.p, c->site_ratio.p, 2, s);
       c->allreduce(na, 2ull * c->n_nodes, ncclUint64, ncclSum);
+      const size_t ssb = node_select_scratch_bytes(c->n_nodes);
       launch_node_select(na, c->n_nodes, q->top_k, q->z_min, c->node_mean.ensure(c->n_nodes),
                          c->node_z.ensure(c->n_nodes), c->d_order.ensure(c->n_nodes),
-                         c->d_nsel.ensure(1), s);
+                         c->d_nsel.ensure(1), c->scratch.ensure(ssb), ssb, s);
       const uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
       if (nr) {
         launch_topology(c->d_order.p, c->d_nsel.p, c->d_node_rack_idx.p, c->d_node_chassis.p,

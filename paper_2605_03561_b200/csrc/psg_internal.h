@@ -123,41 +123,47 @@ struct query_params {
 // loop can use native 32-bit shared reductions (RED) without return values;
 // the overflow guards are the time spans of iterations and block steps (see
 // psg_query.cu).
+//
+// Cube rows have stride nn + 1: column nn is a trash column that absorbs the
+// events of contexts outside the anchor subtree, so the interior loop adds
+// every event without a branch.  The ring holds 2G rows and the gap row (2G).
+//
+// The window table is one 36-byte record per ctx, so one address serves all
+// of an event's reductions: {cnt, pending 32-bit sum, min, max, byte offset of
+// the ctx's cube column in a row, count of durations >= 2^32, folded 64-bit
+// sum (lo, hi words), -}.  The odd stride of 9 words puts the same field of 32
+// consecutive contexts in 32 distinct banks.  The rare min/max of durations
+// >= 2^32 accumulate in the trace's global output row (64-bit global atomics).
+enum : uint32_t { WT_CNT = 0, WT_LO = 1, WT_MIN = 2, WT_MAX = 3, WT_PPO = 4, WT_NBIG = 5,
+                  WT_ACC = 6 /* lo, hi words */, WT_STRIDE = 9 };
+
 struct warp_smem_layout {
-  uint32_t off_rlo, off_rhi;  // (2G+1) x nn u32: cube rows by node position (ring of 2G + gap)
+  uint32_t nnp;               // cube row stride (nn + 1)
+  uint32_t off_rlo, off_rhi;  // (2G+1) x nnp u32: cube rows (ring of 2G, gap)
   uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
-  uint32_t off_inrows; // G x nn u64   inclusive rows kept for the statistics (generic trees)
   uint32_t off_bwin;   // 2G+2 u32     boundary window (event indices relative to the trace)
   uint32_t off_bts;    // 2G+2 u64     timestamps of those boundaries
-  uint32_t off_wcnt, off_wlo, off_wmin, off_wmax, off_wnbig;  // n_ctx u32 each
-  uint32_t off_wacc, off_wminb, off_wmaxb;                    // n_ctx u64 each
+  uint32_t off_wtab;   // n_ctx x 36 B window records (WT_*)
   uint32_t off_wsx, off_wsqlo, off_wsqhi;  // nn u64: within-trace sums over k < K
   uint32_t off_carry;  // {u64 ts, u64 dur, u64 (has << 32 | ctx)}
   uint32_t off_scan;   // 2 x (n_ctx + 1) u64 at finalize (aliases the rows)
   uint32_t bytes;
-  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G, bool root_only) {
+  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G, bool /*root_only*/) {
     uint32_t o = 0;
     auto take = [&](uint32_t b) {
       uint32_t r = o;
       o += (b + 15u) & ~15u;
       return r;
     };
-    const uint32_t rows = 4u * (2 * G + 1) * nn, scan = 16u * (n_ctx + 1);
+    nnp = nn + 1;
+    const uint32_t rows = 4u * (2 * G + 1) * nnp, scan = 16u * (n_ctx + 1);
     off_rlo = take(rows > scan ? rows : scan);
     off_scan = off_rlo;
     off_rhi = take(rows);
     off_pref = take(8u * (nn + 1));  // generic rows and the gap row
-    off_inrows = take(root_only ? 0u : 8u * G * nn);
     off_bwin = take(4u * (2 * G + 2));
     off_bts = take(8u * (2 * G + 2));
-    off_wcnt = take(4u * n_ctx);
-    off_wlo = take(4u * n_ctx);
-    off_wmin = take(4u * n_ctx);
-    off_wmax = take(4u * n_ctx);
-    off_wnbig = take(4u * n_ctx);
-    off_wacc = take(8u * n_ctx);
-    off_wminb = take(8u * n_ctx);
-    off_wmaxb = take(8u * n_ctx);
+    off_wtab = take(4u * WT_STRIDE * n_ctx);
     off_wsx = take(8u * nn);
     off_wsqlo = take(8u * nn);
     off_wsqhi = take(8u * nn);
@@ -224,9 +230,10 @@ void launch_outliers(const uint64_t* w_incl, uint32_t n_traces, uint32_t n_ctx,
                      uint32_t n_nodes, unsigned long long* site_acc /*[n_sites][2]*/,
                      unsigned long long* node_acc /*[n_nodes][2]*/, uint32_t* worst,
                      double* site_ratio, uint32_t phase, cudaStream_t s);
+size_t node_select_scratch_bytes(uint32_t n_nodes);
 void launch_node_select(const unsigned long long* node_acc, uint32_t n_nodes, uint32_t top_k,
                         double z_min, double* node_mean, double* node_z, uint32_t* order,
-                        uint32_t* n_sel, cudaStream_t s);
+                        uint32_t* n_sel, void* scratch, size_t scratch_bytes, cudaStream_t s);
 void launch_topology(const uint32_t* selected, const uint32_t* n_sel, const uint32_t* node_rack_idx,
                      const uint32_t* node_chassis, const uint32_t* uni_cnt, uint32_t n_racks,
                      uint32_t* rack_nodes, unsigned long long* rack_mask,

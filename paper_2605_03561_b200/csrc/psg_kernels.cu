@@ -631,20 +631,25 @@ __global__ void k_node_cut(const uint32_t* sorted_ids, const double* z, uint32_t
   if (threadIdx.x == 0) *n_sel = top_k ? min(first_bad, top_k) : first_bad;
 }
 
+size_t node_select_scratch_bytes(uint32_t n_nodes) {
+  size_t temp_bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, static_cast<const uint64_t*>(nullptr),
+                                            static_cast<uint64_t*>(nullptr),
+                                            static_cast<const uint32_t*>(nullptr),
+                                            static_cast<uint32_t*>(nullptr), static_cast<int>(n_nodes),
+                                            0, 64);
+  return sizeof(uint64_t) * n_nodes * 2 + sizeof(uint32_t) * (n_nodes + 8) + temp_bytes + 64;
+}
+
 void launch_node_select(const unsigned long long* node_acc, uint32_t n_nodes, uint32_t top_k,
                         double z_min, double* node_mean, double* node_z, uint32_t* order,
-                        uint32_t* n_sel, cudaStream_t s) {
-  // scratch: keys/ids (in + out) allocated per call (small: n_nodes entries)
-  uint64_t *k_in = nullptr, *k_out = nullptr;
-  uint32_t* ids_in = nullptr;
-  void* temp = nullptr;
-  size_t temp_bytes = 0;
-  PSG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, k_in, k_out, ids_in, order,
-                                                     static_cast<int>(n_nodes), 0, 64, s));
-  PSG_CUDA(cudaMallocAsync(&k_in, sizeof(uint64_t) * n_nodes * 2 + sizeof(uint32_t) * n_nodes + temp_bytes + 64, s));
-  k_out = k_in + n_nodes;
-  ids_in = reinterpret_cast<uint32_t*>(k_out + n_nodes);
-  temp = reinterpret_cast<uint8_t*>(ids_in + n_nodes + 8);
+                        uint32_t* n_sel, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  // scratch (owned by the context, reused across queries): keys/ids in + out, sort temp
+  uint64_t* k_in = static_cast<uint64_t*>(scratch);
+  uint64_t* k_out = k_in + n_nodes;
+  uint32_t* ids_in = reinterpret_cast<uint32_t*>(k_out + n_nodes);
+  void* temp = reinterpret_cast<uint8_t*>(ids_in + n_nodes + 8);
+  size_t temp_bytes = scratch_bytes - (sizeof(uint64_t) * n_nodes * 2 + sizeof(uint32_t) * (n_nodes + 8));
   k_node_stats<<<1, 1024, 0, s>>>(node_acc, n_nodes, node_mean, node_z, k_in, ids_in);
   count_launch();
   PSG_CUDA(cudaGetLastError());
@@ -653,7 +658,6 @@ void launch_node_select(const unsigned long long* node_acc, uint32_t n_nodes, ui
   k_node_cut<<<1, 1024, 0, s>>>(order, node_z, n_nodes, top_k, z_min, n_sel);
   count_launch();
   PSG_CUDA(cudaGetLastError());
-  PSG_CUDA(cudaFreeAsync(k_in, s));
 }
 
 // K8: topology.  Outlier nodes -> (rack index, chassis) histogram; a chassis

@@ -260,36 +260,46 @@ void launch_bounds(const bound_params& p, cudaStream_t s) {
 namespace {
 
 constexpr u64 kSpan32 = 1ull << 32;
-constexpr u64 kSpan31 = 1ull << 31;  // narrow chunks: 4 squares of cells < 2^31 fit 64 bits
+constexpr u64 kSpan30 = 1ull << 30;  // narrow chunks: G = 8 squares of cells < 2^30 fit 64 bits
 
 enum : int { WIN_NONE = 0, WIN_FULL = 1, WIN_PART = 2, WIN_WIDE = 3 };
 
 struct warp_tables {
-  uint32_t *wcnt, *wlo, *wmin, *wmax, *wnbig;
-  u64 *wacc, *wminb, *wmaxb;
+  uint32_t* wt;  // n_ctx records of WT_STRIDE words (psg_internal.h)
+  unsigned long long *gminb, *gmaxb;  // the trace's global w_min / w_max rows (durations >= 2^32)
   u64* carry;
+  __device__ __forceinline__ u64 acc(uint32_t c) const {
+    const uint32_t* r = wt + c * WT_STRIDE + WT_ACC;
+    return static_cast<u64>(r[0]) | (static_cast<u64>(r[1]) << 32);
+  }
+  __device__ __forceinline__ void set_acc(uint32_t c, u64 v) const {
+    uint32_t* r = wt + c * WT_STRIDE + WT_ACC;
+    r[0] = static_cast<uint32_t>(v);
+    r[1] = static_cast<uint32_t>(v >> 32);
+  }
 };
 
 // One window row of duration d for ctx c (frame::group_aggregate's
 // count/sum/min/max fold, order-free in integers).
 __device__ __forceinline__ void win_row32(const warp_tables& T, uint32_t c, uint32_t d) {
-  atomicAdd(T.wcnt + c, 1u);
-  atomicAdd(T.wlo + c, d);
-  atomicMin(T.wmin + c, d);
-  atomicMax(T.wmax + c, d);
+  uint32_t* r = T.wt + c * WT_STRIDE;
+  atomicAdd(r + WT_CNT, 1u);
+  atomicAdd(r + WT_LO, d);
+  atomicMin(r + WT_MIN, d);
+  atomicMax(r + WT_MAX, d);
 }
 
 __device__ __forceinline__ void win_row64(const warp_tables& T, uint32_t c, u64 d) {
-  atomicAdd(T.wcnt + c, 1u);
-  uint32_t* acc = reinterpret_cast<uint32_t*>(T.wacc + c);
-  sadd64(acc, acc + 1, d);
+  uint32_t* r = T.wt + c * WT_STRIDE;
+  atomicAdd(r + WT_CNT, 1u);
+  sadd64(r + WT_ACC, r + WT_ACC + 1, d);
   if (d >> 32) {
-    atomicAdd(T.wnbig + c, 1u);
-    atomicMin(reinterpret_cast<unsigned long long*>(T.wminb + c), d);
-    atomicMax(reinterpret_cast<unsigned long long*>(T.wmaxb + c), d);
+    atomicAdd(r + WT_NBIG, 1u);
+    atomicMin(T.gminb + c, d);
+    atomicMax(T.gmaxb + c, d);
   } else {
-    atomicMin(T.wmin + c, static_cast<uint32_t>(d));
-    atomicMax(T.wmax + c, static_cast<uint32_t>(d));
+    atomicMin(r + WT_MIN, static_cast<uint32_t>(d));
+    atomicMax(r + WT_MAX, static_cast<uint32_t>(d));
   }
 }
 
@@ -328,7 +338,7 @@ struct run_state {
   int nxt;        // local index of the next boundary
   bool cube_ok;   // k is a stored iteration (or the gap of a kept trace)
   uint32_t slot;  // ring slot of k
-  uint32_t rowb;  // slot * nn
+  uint32_t rowb;  // slot * nnp
 };
 
 struct run_ctx {
@@ -337,7 +347,7 @@ struct run_ctx {
   uint32_t *rlo, *rhi;
   uint32_t base3;  // block step start relative to the trace, + 3
   u64 tend, t0, t1w;
-  uint32_t R2, nn;
+  uint32_t R2, nnp;  // ring size, cube row stride
   int iters;  // iterations stored for this trace; -1 for a skipped trace (no gap row either)
   int lb, lo, hi, last_li;
   bool root_only;
@@ -361,7 +371,7 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
         ++st.cnt;
         st.nxt = st.cnt <= R.R2 ? local_of(R.bwin[st.cnt], R.base3) : INT_MAX;
         st.slot = st.k < 0 ? R.R2 : (static_cast<uint32_t>(st.k) & (R.R2 - 1));
-        st.rowb = st.slot * R.nn;
+        st.rowb = st.slot * R.nnp;
         st.cube_ok = st.k < R.iters;
       }
       const int pp = R.s_sub_pre[cj];
@@ -444,6 +454,101 @@ __device__ __forceinline__ void warp_prefix_row(const uint32_t* lo, const uint32
   __syncwarp();
 }
 
+// Interior block step, fast path: every event of the step is valid and none
+// is the trace's last, the chunk is narrow (cells and block spans fit 32
+// bits), the window class is FULL or NONE, and the lane's run holds at most
+// one iteration boundary (local index bpos; RM when none).  Per event: one
+// window-record address, one load of the ctx's cube column offset, one cube
+// RED into the row selected by bpos and, inside the window, the four window
+// REDs.  Events of contexts outside the anchor subtree land in the trash
+// column, events of unstored iterations in the trash row: no branches.
+template <int WM>
+__device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
+                                         uint8_t* sm, uint32_t wt_off, int bpos,
+                                         uint32_t rb_before, uint32_t rb_after) {
+  uint32_t ppo[RM];
+#pragma unroll
+  for (int j = 0; j < RM; ++j)  // all column loads first: they do not wait on the REDs
+    ppo[j] = *reinterpret_cast<const uint32_t*>(sm + wt_off + cv[j] * (4u * WT_STRIDE) + 4u * WT_PPO);
+#pragma unroll
+  for (int j = 0; j < RM; ++j) {
+    const uint32_t d = static_cast<uint32_t>(tv[j + 1]) - static_cast<uint32_t>(tv[j]);
+    const uint32_t rb = j >= bpos ? rb_after : rb_before;
+    atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + ppo[j]), d);
+    if (WM == WIN_FULL) {
+      uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + cv[j] * (4u * WT_STRIDE));
+      atomicAdd(r + WT_CNT, 1u);
+      atomicAdd(r + WT_LO, d);
+      atomicMin(r + WT_MIN, d);
+      atomicMax(r + WT_MAX, d);
+    }
+  }
+}
+
+// Flush of a full narrow chunk (G rows, every cell < 2^30) when the anchor is
+// the only internal node: a leaf's inclusive time IS its exclusive time, so a
+// lane owns leaves across the chunk's rows and copies them straight to the
+// cube (coalesced along the node axis), with the within-rank Σx / Σx² in
+// registers; the anchor's inclusive time is the row total (one REDUX per row).
+template <bool STATS>
+__device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows, uint32_t nnp,
+                                           uint32_t nn, u64 ob, u64 xbase, u64* wsx, u64* wsqlo,
+                                           u64* wsqhi, int lane) {
+  constexpr uint32_t G = GC;
+  uint32_t rs[GC];
+#pragma unroll
+  for (uint32_t r = 0; r < G; ++r) rs[r] = lane == 0 ? rows[r * nnp] : 0u;  // the anchor's own excl
+  const uint32_t ax = lane < static_cast<int>(G) ? rows[lane * nnp] : 0u;
+  for (uint32_t n = 1 + lane; n < nn; n += 32) {
+    u64 sx = 0, sq = 0;
+    uint64_t* dst = p.cube_incl + ob + n;
+#pragma unroll
+    for (uint32_t r = 0; r < G; ++r) {
+      const uint32_t ex = rows[r * nnp + n];
+      rs[r] += ex;
+      dst[static_cast<size_t>(r) * nn] = ex;
+      if (STATS) {
+        sx += ex;
+        sq += static_cast<u64>(ex) * ex;  // G squares < 2^60 each
+      }
+    }
+    if (STATS) {
+      wsx[n] += sx;
+      const u64 l2 = wsqlo[n] + sq;
+      wsqhi[n] += l2 < sq ? 1ull : 0ull;
+      wsqlo[n] = l2;
+    }
+  }
+  __syncwarp();
+  {  // zero the chunk's G contiguous rows (16-byte aligned, G * nnp a multiple of 4 words)
+    uint4* z = reinterpret_cast<uint4*>(rows);
+    const uint32_t nz = G * nnp / 4;
+    for (uint32_t i = lane; i < nz; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (uint32_t r = 0; r < G; ++r) rs[r] = __reduce_add_sync(FULL, rs[r]);  // < 2^30
+  uint32_t mine = rs[0];
+#pragma unroll
+  for (uint32_t r = 1; r < G; ++r)
+    if (static_cast<uint32_t>(lane) == r) mine = rs[r];
+  if (lane < static_cast<int>(G)) {
+    p.cube_incl[ob + static_cast<u64>(lane) * nn] = mine;
+    if (p.store_cube) p.cube_xint[xbase + lane] = ax;  // m == 1
+  }
+  if (STATS && lane == 0) {
+    u64 sx = 0, sq = 0;
+#pragma unroll
+    for (uint32_t r = 0; r < G; ++r) {
+      sx += rs[r];
+      sq += static_cast<u64>(rs[r]) * rs[r];
+    }
+    wsx[0] += sx;
+    const u64 l2 = wsqlo[0] + sq;
+    wsqhi[0] += l2 < sq ? 1ull : 0ull;
+    wsqlo[0] = l2;
+  }
+}
+
 template <bool WIN, bool CUBE>
 __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(query_params p) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -459,8 +564,9 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
 
   warp_smem_layout L;
   L.init(n_ctx, nn, G, root_only || !CUBE);
-  const uint32_t tbl = cta_table_bytes(n_ctx, nn, W);
-  uint8_t* wb = smem + tbl + static_cast<size_t>(warp) * L.bytes;
+  const uint32_t nnp = L.nnp;
+  const uint32_t wb_off = cta_table_bytes(n_ctx, nn, W) + static_cast<uint32_t>(warp) * L.bytes;
+  uint8_t* wb = smem + wb_off;
   uint32_t* rlo = reinterpret_cast<uint32_t*>(wb + L.off_rlo);
   uint32_t* rhi = reinterpret_cast<uint32_t*>(wb + L.off_rhi);
   u64* pref = reinterpret_cast<u64*>(wb + L.off_pref);
@@ -470,15 +576,12 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   u64* wsqlo = reinterpret_cast<u64*>(wb + L.off_wsqlo);
   u64* wsqhi = reinterpret_cast<u64*>(wb + L.off_wsqhi);
   warp_tables T;
-  T.wcnt = reinterpret_cast<uint32_t*>(wb + L.off_wcnt);
-  T.wlo = reinterpret_cast<uint32_t*>(wb + L.off_wlo);
-  T.wmin = reinterpret_cast<uint32_t*>(wb + L.off_wmin);
-  T.wmax = reinterpret_cast<uint32_t*>(wb + L.off_wmax);
-  T.wnbig = reinterpret_cast<uint32_t*>(wb + L.off_wnbig);
-  T.wacc = reinterpret_cast<u64*>(wb + L.off_wacc);
-  T.wminb = reinterpret_cast<u64*>(wb + L.off_wminb);
-  T.wmaxb = reinterpret_cast<u64*>(wb + L.off_wmaxb);
+  T.wt = reinterpret_cast<uint32_t*>(wb + L.off_wtab);
   T.carry = reinterpret_cast<u64*>(wb + L.off_carry);
+  // byte offsets from smem for the fast path
+  const uint32_t wt_off = wb_off + L.off_wtab;
+  const uint32_t rows_off = wb_off + L.off_rlo;
+  const uint32_t row_bytes = 4u * nnp;
 
   for (uint32_t i = threadIdx.x; i < n_ctx; i += blockDim.x) {
     s_sub_pre[i] = CUBE ? p.sub_pre[i] : -1;
@@ -487,22 +590,29 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   }
   if (CUBE) {
     for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) s_node[i] = p.node_tab[i];
-    for (uint32_t j = lane; j < (R2 + 1) * nn; j += 32) rlo[j] = rhi[j] = 0;
+    for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rlo[j] = rhi[j] = 0;
     for (uint32_t j = lane; j < nn; j += 32) wsx[j] = wsqlo[j] = wsqhi[j] = 0;
   }
-  if (WIN) {
-    for (uint32_t c = lane; c < n_ctx; c += 32) {
-      T.wcnt[c] = T.wlo[c] = T.wmax[c] = T.wnbig[c] = 0u;
-      T.wmin[c] = 0xFFFFFFFFu;
-      T.wacc[c] = 0ull;
-      T.wminb[c] = ~0ull;
-      T.wmaxb[c] = 0ull;
-    }
+  for (uint32_t c = lane; c < n_ctx; c += 32) {
+    uint32_t* r = T.wt + c * WT_STRIDE;
+    r[WT_CNT] = r[WT_LO] = r[WT_MAX] = r[WT_NBIG] = 0u;
+    r[WT_MIN] = 0xFFFFFFFFu;
+    const int32_t sp = CUBE ? p.sub_pre[c] : -1;
+    r[WT_PPO] = 4u * (sp >= 0 ? static_cast<uint32_t>(sp) : nn);  // trash column nn
+    T.set_acc(c, 0ull);
   }
   if (lane == 0) T.carry[0] = T.carry[1] = T.carry[2] = 0;
 
   const uint32_t t = blockIdx.x * W + warp;
   const bool active = t < p.tr.n;
+  if (WIN && active) {
+    T.gminb = reinterpret_cast<unsigned long long*>(p.w_min) + static_cast<size_t>(t) * n_ctx;
+    T.gmaxb = reinterpret_cast<unsigned long long*>(p.w_max) + static_cast<size_t>(t) * n_ctx;
+    for (uint32_t c = lane; c < n_ctx; c += 32) {
+      T.gminb[c] = ~0ull;
+      T.gmaxb[c] = 0ull;
+    }
+  }
   const u64 b = active ? p.tr.off[t] : 0, e = active ? p.tr.off[t + 1] : 0;
   const u64 n_t = e - b;
   const u64 tend = active ? p.tr.t_end[t] : 0;
@@ -525,6 +635,12 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   const u64 t0 = p.t0, t1w = (p.clamp_tend && tend < p.t1) ? tend : p.t1;
   u64 pos = 0;    // next unprocessed event, relative to b
   u64 wspan = 0;  // time span added to the 32-bit pending window sums since the last fold
+  uint32_t mybw = 0xFFFFFFFFu;  // lane j <= 2G: relative event index of boundary kb + j
+
+  // ring row of iteration k (byte offset from smem): the gap row for k < 0
+  auto row_of = [&](int k) -> uint32_t {
+    return rows_off + (k < 0 ? R2 : (static_cast<uint32_t>(k) & (R2 - 1))) * row_bytes;
+  };
 
   run_ctx R;
   R.s_sub_pre = s_sub_pre;
@@ -536,7 +652,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   R.t1w = t1w;
   R.R2 = R2;
   R.iters = kept ? static_cast<int>(iters) : -1;
-  R.nn = nn;
+  R.nnp = nnp;
   R.root_only = root_only;
   R.lb = lane * RM;
   __syncthreads();
@@ -551,6 +667,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         bwin[lane] = nx_idx + 3;  // stored + 3, see local_of
         bts[lane] = nx_ts;
       }
+      mybw = lane <= static_cast<int>(R2) ? nx_idx : 0xFFFFFFFFu;
       // prefetch the next chunk's window: its loads overlap this chunk's events
       const u64 k = static_cast<u64>(kb + G) + lane;
       const bool have = lane <= static_cast<int>(R2) && k < nbd;
@@ -560,12 +677,13 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       E1 = bwin[G] - 3;
       E2 = bwin[R2] - 3;
       // iteration spans of the ring (and the gap in chunk 0) decide 32- vs 64-bit cells
-      bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan31;
-      if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan31;
+      bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan30;
+      if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan30;
       cwide = __any_sync(FULL, w);
     } else if (CUBE && active) {
       // skipped trace: only the window runs; iterations are not stored
       if (lane <= static_cast<int>(R2)) bwin[lane] = static_cast<uint32_t>(n_t) + 3;
+      mybw = lane <= static_cast<int>(R2) ? static_cast<uint32_t>(n_t) : 0xFFFFFFFFu;
       __syncwarp();
     }
 
@@ -607,31 +725,37 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       u64 nf = __shfl_down_sync(FULL, tv[0], 1);
       if (lane == 31) nf = ldg64(p.tr.ts + s_abs + STEP_M);
       tv[RM] = nf;
+      const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
 
       // window class of this block step (warp-uniform)
       int wm = WIN_NONE;
       if (WIN) {
-        u64 f = tv[0];  // lo <= 3 < RM: lane 0 owns the first valid event
-        if (R.lo >= 1) f = tv[1];
-        if (R.lo >= 2) f = tv[2];
-        if (R.lo >= 3) f = tv[3];
-        // first valid event and the successor of the last valid one (index hi)
-        u64 a;
-        switch (R.hi & (RM - 1)) {  // warp-uniform; constant register indices
-          case 1: a = tv[1]; break;
-          case 2: a = tv[2]; break;
-          case 3: a = tv[3]; break;
+        u64 first, after;
+        if (all) {
+          first = __shfl_sync(FULL, tv[0], 0);
+          after = __shfl_sync(FULL, tv[RM], 31);
+        } else {
+          u64 f = tv[0];  // lo <= 3 < RM: lane 0 owns the first valid event
+          if (R.lo >= 1) f = tv[1];
+          if (R.lo >= 2) f = tv[2];
+          if (R.lo >= 3) f = tv[3];
+          // first valid event and the successor of the last valid one (index hi)
+          u64 a;
+          switch (R.hi & (RM - 1)) {  // warp-uniform; constant register indices
+            case 1: a = tv[1]; break;
+            case 2: a = tv[2]; break;
+            case 3: a = tv[3]; break;
 #if PSG_RM > 4
-          case 4: a = tv[4]; break;
-          case 5: a = tv[5]; break;
-          case 6: a = tv[6]; break;
-          case 7: a = tv[7]; break;
+            case 4: a = tv[4]; break;
+            case 5: a = tv[5]; break;
+            case 6: a = tv[6]; break;
+            case 7: a = tv[7]; break;
 #endif
-          default: a = tv[0]; break;
+            default: a = tv[0]; break;
+          }
+          first = __shfl_sync(FULL, f, 0);
+          after = R.hi >= STEP_M ? __shfl_sync(FULL, tv[RM], 31) : __shfl_sync(FULL, a, R.hi / RM);
         }
-        const u64 first = __shfl_sync(FULL, f, 0);
-        const u64 after = R.hi >= STEP_M ? __shfl_sync(FULL, tv[RM], 31)
-                                         : __shfl_sync(FULL, a, R.hi / RM);
         const bool has_end = R.last_li >= 0 && R.last_li < R.hi;
         if ((first >= t1w && first >= t0) || (!has_end && after < t0)) {
           wm = WIN_NONE;
@@ -642,8 +766,9 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           if (wspan + span >= kSpan32) {  // fold the pending 32-bit sums
             __syncwarp();
             for (uint32_t x = lane; x < n_ctx; x += 32) {
-              T.wacc[x] += T.wlo[x];
-              T.wlo[x] = 0;
+              uint32_t* r = T.wt + x * WT_STRIDE;
+              T.set_acc(x, T.acc(x) + r[WT_LO]);
+              r[WT_LO] = 0;
             }
             __syncwarp();
             wspan = 0;
@@ -653,29 +778,55 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         }
       }
 
-      run_state st;
-      st.k = -1;
-      st.cnt = 0;
-      st.nxt = INT_MAX;
-      st.cube_ok = false;
-      st.slot = R2;
-      st.rowb = R2 * nn;
-      if (CUBE) {
-        // iteration of this lane's first event: boundaries of the window at or before it
-        uint32_t cnt = 0;
-        const uint32_t lp3 = R.base3 + static_cast<uint32_t>(R.lb);
-        for (uint32_t j = 0; j <= R2; ++j) cnt += bwin[j] <= lp3 ? 1u : 0u;
-        st.cnt = cnt;
-        st.k = static_cast<int>(kb) - 1 + static_cast<int>(cnt);
-        st.nxt = cnt <= R2 ? local_of(bwin[cnt], R.base3) : INT_MAX;
-        st.slot = st.k < 0 ? R2 : (static_cast<uint32_t>(st.k) & (R2 - 1));
-        st.rowb = st.slot * nn;
-        st.cube_ok = st.k < R.iters;
+      bool done = false;
+      if (CUBE && kept && all && !cwide && (wm == WIN_FULL || wm == WIN_NONE)) {
+        // boundaries of this block step: lane j <= 2G holds boundary kb + j;
+        // H marks the lanes whose run holds one (fast path: at most one per
+        // run, and every iteration of the step is stored)
+        const uint32_t base32 = static_cast<uint32_t>(base);  // >= 0 here (lo == 0)
+        const uint32_t rel = mybw - base32;
+        const bool inb = mybw >= base32 && rel < static_cast<uint32_t>(STEP_M);
+        const uint32_t H = __reduce_or_sync(FULL, inb ? 1u << (rel / RM) : 0u);
+        const unsigned inm = __ballot_sync(FULL, inb);
+        const uint32_t nb0 = __popc(__ballot_sync(FULL, mybw < base32));
+        if (__popc(H) == __popc(inm) && kb + nb0 + __popc(inm) <= iters) {
+          const uint32_t jb = nb0 + __popc(H & lanemask_lt());  // first boundary at/after the run
+          const uint32_t bw = __shfl_sync(FULL, mybw, static_cast<int>(jb & 31));
+          const int bpos = ((H >> lane) & 1u) ? static_cast<int>(bw - base32) - lane * RM : RM;
+          const int k0 = static_cast<int>(kb) - 1 + static_cast<int>(jb);
+          const uint32_t rb0 = row_of(k0), rb1 = row_of(k0 + 1);
+          if (wm == WIN_FULL)
+            run_fast<WIN_FULL>(tv, cv, smem, wt_off, bpos, rb0, rb1);
+          else
+            run_fast<WIN_NONE>(tv, cv, smem, wt_off, bpos, rb0, rb1);
+          done = true;
+        }
       }
-      if (cwide)
-        run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
-      else
-        run_block<WIN, CUBE, false>(wm, tv, cv, R, st, T);
+      if (!done) {
+        run_state st;
+        st.k = -1;
+        st.cnt = 0;
+        st.nxt = INT_MAX;
+        st.cube_ok = false;
+        st.slot = R2;
+        st.rowb = R2 * nnp;
+        if (CUBE) {
+          // iteration of this lane's first event: boundaries of the window at or before it
+          uint32_t cnt = 0;
+          const uint32_t lp3 = R.base3 + static_cast<uint32_t>(R.lb);
+          for (uint32_t j = 0; j <= R2; ++j) cnt += bwin[j] <= lp3 ? 1u : 0u;
+          st.cnt = cnt;
+          st.k = static_cast<int>(kb) - 1 + static_cast<int>(cnt);
+          st.nxt = cnt <= R2 ? local_of(bwin[cnt], R.base3) : INT_MAX;
+          st.slot = st.k < 0 ? R2 : (static_cast<uint32_t>(st.k) & (R2 - 1));
+          st.rowb = st.slot * nnp;
+          st.cube_ok = st.k < R.iters;
+        }
+        if (cwide)
+          run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
+        else
+          run_block<WIN, CUBE, false>(wm, tv, cv, R, st, T);
+      }
       pos = lim;
     }
     __syncwarp();
@@ -688,30 +839,31 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     if (CUBE && kept) {
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
       const u64 ob = bo + static_cast<u64>(kb) * nn;
-      if (root_only && !cwide) {
-        // Narrow chunk (every iteration spans < 2^31 ns) and the anchor is the
-        // only internal node: rows are node-indexed, so a lane owns one leaf
-        // across the chunk's rows (a leaf's incl IS its excl: straight copies,
-        // coalesced along the node axis, within-rank sums in registers); the
-        // anchor's inclusive time is the row total, reduced across the warp.
+      if (root_only && !cwide && n_iter_rows == G && (kcap == 0 || kcap == G)) {
+        if (kcap)
+          flush_fast<true>(p, rlo + s0 * nnp, nnp, nn, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
+        else
+          flush_fast<false>(p, rlo + s0 * nnp, nnp, nn, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
+      } else if (root_only && !cwide) {
+        // narrow partial chunk (the trace's last): the same straight copies, row by row
         uint32_t rs[GC];
 #pragma unroll
         for (uint32_t r = 0; r < GC; ++r)
-          rs[r] = (lane == 0 && r < n_iter_rows) ? rlo[(s0 + r) * nn] : 0u;  // anchor's own excl
+          rs[r] = (lane == 0 && r < n_iter_rows) ? rlo[(s0 + r) * nnp] : 0u;  // anchor's own excl
         for (uint32_t n = 1 + lane; n < nn; n += 32) {
           u64 sx = 0, sq = 0;
           uint64_t* dst = p.cube_incl + ob + n;
 #pragma unroll
           for (uint32_t r = 0; r < GC; ++r) {
             if (r < n_iter_rows) {
-              const uint32_t idx = (s0 + r) * nn + n;
+              const uint32_t idx = (s0 + r) * nnp + n;
               const uint32_t ex = rlo[idx];
               rs[r] += ex;
               dst[r * nn] = ex;
               rlo[idx] = 0;
               if (r < kcap) {
                 sx += ex;
-                sq += static_cast<u64>(ex) * ex;  // < 4 * 2^62
+                sq += static_cast<u64>(ex) * ex;  // G squares < 2^60 each
               }
             }
           }
@@ -723,16 +875,14 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           }
         }
 #pragma unroll
-        for (uint32_t r = 0; r < GC; ++r)
-#pragma unroll
-          for (int d = 16; d > 0; d >>= 1) rs[r] += __shfl_xor_sync(FULL, rs[r], d);
+        for (uint32_t r = 0; r < GC; ++r) rs[r] = __reduce_add_sync(FULL, rs[r]);
         // the anchor's cells: lane r writes row r; lane 0 folds the within sums
         uint32_t mine = rs[0];
 #pragma unroll
         for (uint32_t r = 1; r < GC; ++r)
           if (static_cast<uint32_t>(lane) == r) mine = rs[r];
         if (static_cast<uint32_t>(lane) < n_iter_rows) {
-          const uint32_t idx = (s0 + lane) * nn;
+          const uint32_t idx = (s0 + lane) * nnp;
           p.cube_incl[ob + static_cast<u64>(lane) * nn] = mine;
           if (p.store_cube) p.cube_xint[ib + kb + lane] = rlo[idx];  // m == 1
           rlo[idx] = 0;
@@ -753,10 +903,10 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       } else {
         for (uint32_t r = 0; r < n_iter_rows; ++r) {
           const uint32_t slot = s0 + r;
-          warp_prefix_row(rlo + slot * nn, rhi + slot * nn, s_node, pref, nn, lane);
+          warp_prefix_row(rlo + slot * nnp, rhi + slot * nnp, s_node, pref, nn, lane);
           for (uint32_t n = lane; n < nn; n += 32) {
             const int4 nd = s_node[n];
-            const u64 ex = cell64(rlo, rhi, slot * nn + n);
+            const u64 ex = cell64(rlo, rhi, slot * nnp + n);
             const u64 in = nd.z ? pref[nd.x + nd.y] - pref[nd.x] : ex;
             p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
             if (nd.z && p.store_cube) p.cube_xint[(ib + kb + r) * p.m + (nd.z - 1)] = ex;
@@ -770,24 +920,23 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
             }
           }
           __syncwarp();
-          for (uint32_t n = lane; n < nn; n += 32) rlo[slot * nn + n] = rhi[slot * nn + n] = 0;
+          for (uint32_t n = lane; n < nn; n += 32) rlo[slot * nnp + n] = rhi[slot * nnp + n] = 0;
           __syncwarp();
         }
       }
       if (c == 0) {  // the gap row [first_ts, b_0) (itermodel.cpp:331-338)
         __syncwarp();
-        warp_prefix_row(rlo + R2 * nn, rhi + R2 * nn, s_node, pref, nn, lane);
+        warp_prefix_row(rlo + R2 * nnp, rhi + R2 * nnp, s_node, pref, nn, lane);
         for (uint32_t n = lane; n < nn; n += 32) {
           const int4 nd = s_node[n];
-          const u64 ex = cell64(rlo, rhi, R2 * nn + n);
+          const u64 ex = cell64(rlo, rhi, R2 * nnp + n);
           const u64 in = !nd.z ? ex : pref[nd.x + nd.y] - pref[nd.x];
           p.gap_excl[static_cast<size_t>(tp) * nn + n] = ex;
           p.gap_incl[static_cast<size_t>(tp) * nn + n] = in;
         }
         __syncwarp();
-        for (uint32_t n = lane; n < nn; n += 32) rlo[R2 * nn + n] = rhi[R2 * nn + n] = 0;
+        for (uint32_t n = lane; n < nn; n += 32) rlo[R2 * nnp + n] = rhi[R2 * nnp + n] = 0;
       }
-      __syncwarp();
       __syncwarp();
     }
     if (pos >= n_t && static_cast<u64>(kb) + G >= iters) break;
@@ -804,20 +953,24 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     const uint32_t c_ctx = static_cast<uint32_t>(T.carry[2]);
     const u64 c_d = T.carry[1];
     for (uint32_t c = lane; c < n_ctx; c += 32) {
-      const u64 sum = T.wacc[c] + T.wlo[c];
+      const u64 sum = T.acc(c) + T.wt[c * WT_STRIDE + WT_LO];
       tmp[s_cct_pre[c]] = sum + ((c_has && c == c_ctx) ? c_d : 0ull);
     }
     __syncwarp();
     warp_prefix(tmp, scan, n_ctx, lane);
+    __threadfence();  // the big min/max atomics of all lanes, before the read-back
+    __syncwarp();
     const size_t base = static_cast<size_t>(t) * n_ctx;
     for (uint32_t c = lane; c < n_ctx; c += 32) {
+      const uint32_t* r = T.wt + c * WT_STRIDE;
       const int pr = s_cct_pre[c], sz = s_cct_size[c];
-      const u64 cnt = T.wcnt[c], nbig = T.wnbig[c];
-      const u64 sum = T.wacc[c] + T.wlo[c];
+      const u64 cnt = r[WT_CNT], nbig = r[WT_NBIG];
+      const u64 sum = T.acc(c) + r[WT_LO];
+      const u64 minb = nbig ? __ldcg(T.gminb + c) : 0ull, maxb = nbig ? __ldcg(T.gmaxb + c) : 0ull;
       p.w_cnt[base + c] = cnt;
       p.w_sum[base + c] = sum;
-      p.w_min[base + c] = cnt == 0 ? 0ull : (cnt > nbig ? static_cast<u64>(T.wmin[c]) : T.wminb[c]);
-      p.w_max[base + c] = nbig ? T.wmaxb[c] : static_cast<u64>(T.wmax[c]);
+      p.w_min[base + c] = cnt == 0 ? 0ull : (cnt > nbig ? static_cast<u64>(r[WT_MIN]) : minb);
+      p.w_max[base + c] = nbig ? maxb : static_cast<u64>(r[WT_MAX]);
       p.w_mean[base + c] = cnt ? static_cast<double>(sum) / static_cast<double>(cnt) : 0.0;
       p.w_excl[base + c] = scan[pr + 1] - scan[pr];
       p.w_incl[base + c] = scan[pr + sz] - scan[pr];
