@@ -232,12 +232,13 @@ def main():
     # roofline of the dominant kernel (k_trace_query): algorithmic bytes per launch
     nn, n_ctx = info["n_nodes"], sh["n_ctx"]
     # algorithmic bytes of k_trace_query: events read once (12 B),
-    # the compact cube written (incl 8 B per cell + excl 8 B per internal node
-    # per iteration), boundary windows read (4 + 8 B per iteration), window rows
-    # (7 x 8 B per (trace, ctx)), gap rows (16 B per kept trace x node) and the
-    # within-rank CV outputs (9 B per kept trace x node)
+    # the compact cube written (incl as stored: 4 or 8 B per cell in rows of
+    # nn + 1 rounded to even, + excl 8 B per internal node per iteration),
+    # boundary windows read (4 + 8 B per iteration), window rows (7 x 8 B per
+    # (trace, ctx)), gap rows (16 B per kept trace x node) and the within-rank
+    # CV outputs (9 B per kept trace x node)
     rows = info["n_cells"] // max(1, nn)
-    alg_bytes = (12 * events_local + 8 * info["n_cells"] + 8 * rows * info["n_internal"] + 12 * rows
+    alg_bytes = (12 * events_local + info["cube_store_bytes"] + 8 * rows * info["n_internal"] + 12 * rows
                  + 56 * n_local * n_ctx + 16 * info["n_kept"] * nn + 9 * info["n_kept"] * nn)
     main_s = statistics.mean(main_ms) / 1000.0
     peak, peak_kind = measured_peak()
@@ -247,6 +248,7 @@ def main():
                 "frac": achieved / peak, "peak_kind": peak_kind,
                 "traffic": per_ev * events_local if per_ev else None,
                 "kernel": "k_trace_query", "alg_bytes_per_launch": alg_bytes,
+                "cube_cell_bytes": info["cube_cell_bytes"],
                 "kernel_ms": main_s * 1000.0, "kernel_share_of_step": main_s * 1000.0 / (ms / args.steps),
                 "pass1_k_bounds_ms": statistics.mean(bounds_ms)}
 

@@ -138,6 +138,9 @@ enum {
   PSG_Q_NO_CUBE_STORE = 1u << 8, /* store only the incl half of the cube (excl is dropped) */
   PSG_Q_CLAMP_TEND = 1u << 9,    /* window end = min(t1, trace t_end) per trace: whole-trace
                                     integration equals the trace's profile record exactly */
+  PSG_Q_CUBE64 = 1u << 10,       /* keep 64-bit cube cells in HBM even when every stored
+                                    iteration spans < 2^32 ns (default there: 32-bit cells,
+                                    exact, widened to int64 on copy-out) */
   PSG_Q_ALL = PSG_Q_WINDOW | PSG_Q_CUBE | PSG_Q_STATS | PSG_Q_OUTLIERS
 };
 
@@ -183,6 +186,10 @@ typedef struct psg_query_info {
   float ms_total;
   float ms_main;                 /* pass 2: the fused window+cube kernel (k_trace_query) */
   float ms_bounds;               /* pass 1: iteration boundaries (k_bounds), 0 without CUBE */
+  /* device cube storage: bytes per cell (4 when every stored iteration spans
+   * < 2^32 ns, else 8) and total bytes incl. the per-row pad column */
+  uint32_t cube_cell_bytes;
+  uint64_t cube_store_bytes;
 } psg_query_info;
 
 ps_status psg_query(psg_context* ctx, const psg_query_spec* spec, psg_query_info* info);

@@ -24,6 +24,7 @@ STATUS_NAMES = [
 Q_WINDOW, Q_CUBE, Q_STATS, Q_OUTLIERS = 1, 2, 4, 8
 Q_NO_CUBE_STORE = 1 << 8
 Q_CLAMP_TEND = 1 << 9
+Q_CUBE64 = 1 << 10
 Q_ALL = Q_WINDOW | Q_CUBE | Q_STATS | Q_OUTLIERS
 ANCHOR_AUTO = 0xFFFFFFFF
 
@@ -67,6 +68,7 @@ class QueryInfo(C.Structure):
         ("worst_site", C.c_uint32), ("worst_ratio", C.c_double),
         ("n_outliers", C.c_uint32), ("n_racks", C.c_uint32),
         ("ms_total", C.c_float), ("ms_main", C.c_float), ("ms_bounds", C.c_float),
+        ("cube_cell_bytes", C.c_uint32), ("cube_store_bytes", C.c_uint64),
     ]
 
 

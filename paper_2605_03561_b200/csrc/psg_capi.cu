@@ -221,7 +221,9 @@ struct psg_context {
   uint32_t n_kept = 0, n_kept_global = 0, K = 0;
   uint64_t n_cells = 0;
   dbuf<uint32_t> iter_count, tpos;
-  dbuf<uint64_t> block_off, kept_bo, cube_incl, cube_xint, gap_incl, gap_excl;
+  dbuf<uint64_t> block_off, iter_off, kept_bo, cube_incl, cube_xint, gap_incl, gap_excl;
+  uint64_t n_store = 0;  // storage cells of the cube (rows of stride row_stride(nn), blocks padded)
+  bool cube32 = false;   // 32-bit cells (every stored iteration spans < 2^32 ns)
   dbuf<unsigned long long> summary;
   dbuf<uint8_t> scratch;
   dbuf<unsigned long long> x_acc;  // x_sum [K nn] | x_max [K nn] | x_sq [3 K nn]
@@ -1024,8 +1026,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       nn = c->nn;
       uint32_t* ic = c->iter_count.ensure(n + 1);
       // pass 1: iteration boundaries (re-run with exact region bounds on overflow)
-      unsigned long long* sum = c->summary.ensure(4);
-      unsigned long long h[4];
+      unsigned long long* sum = c->summary.ensure(8);
+      unsigned long long h[8];
       PSG_CUDA(cudaEventRecord(c->ev[4], s));
       for (;;) {
         if (!c->caps_valid) build_caps(c);
@@ -1049,13 +1051,17 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       }
       PSG_CUDA(cudaEventRecord(c->ev[5], s));
       const size_t sb = cube_layout_scratch_bytes(n);
-      launch_cube_layout(ic, n, nn, c->tpos.ensure(n + 1), c->block_off.ensure(n + 1),
-                         c->kept_bo.ensure(n + 1), sum,
+      launch_cube_layout(ic, n, nn, row_stride(nn), c->tpos.ensure(n + 1), c->block_off.ensure(n + 1),
+                         c->iter_off.ensure(n + 1), c->kept_bo.ensure(n + 1), sum,
                          c->scratch.ensure(sb), sb, s);
-      PSG_CUDA(cudaMemcpyAsync(h, sum, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      PSG_CUDA(cudaMemsetAsync(sum + 5, 0, 8, s));
+      launch_iter_spans(c->d_cap_off.p, c->d_bts.p, ic, c->d_tend.p, n, sum + 5, s);
+      PSG_CUDA(cudaMemcpyAsync(h, sum, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       c->sync();
       c->n_kept = static_cast<uint32_t>(h[0]);
       c->n_cells = h[2];
+      c->n_store = h[4];
+      c->cube32 = h[5] < (1ull << 32) && !(f & PSG_Q_CUBE64);
       unsigned long long g[2] = {h[1], h[0]};  // min iterations, kept count
       if (c->multi()) {
         unsigned long long* d = c->summary.p;  // reuse as staging
@@ -1082,10 +1088,12 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       p.iter_count = ic;
       p.tpos = c->tpos.p;
       p.block_off = c->block_off.p;
+      p.iter_off = c->iter_off.p;
       p.K = c->K;
       // incl is always materialised (the cross-rank statistics stream it);
       // PSG_Q_NO_CUBE_STORE drops the excl half
-      p.cube_incl = c->cube_incl.ensure(c->n_cells + 1);
+      p.cube_incl = c->cube_incl.ensure((c->n_store * (c->cube32 ? 4 : 8) + 7) / 8 + 2);
+      p.cube32 = c->cube32 ? 1 : 0;
       p.m = static_cast<uint32_t>(c->internal_pos.size());
       if (store_cube) p.cube_xint = c->cube_xint.ensure((nn ? c->n_cells / nn : 0) * p.m + 1);
       c->have_excl = store_cube;
@@ -1108,6 +1116,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     L.init(c->n_ctx, nn, p.G, c->root_only != 0 || !do_cube);
     uint32_t W = choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16));
     p.warps = W;
+    p.L = L;
     uint32_t smem = cta_table_bytes(c->n_ctx, nn, W) + W * L.bytes;
     PSG_CUDA(cudaEventRecord(c->ev[1], s));
     launch_trace_query(p, smem, s);
@@ -1115,7 +1124,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
 
     if (do_stats && c->K > 0) {
       const size_t plane = static_cast<size_t>(c->K) * nn;
-      launch_cross_stats(c->cube_incl.p, c->kept_bo.p, c->n_kept, nn, c->K, c->x_acc.p,
+      launch_cross_stats(c->cube_incl.p, c->cube32, c->kept_bo.p, c->n_kept, nn, row_stride(nn), c->K, c->x_acc.p,
                          c->x_acc.p + plane, c->x_acc.p + 2 * plane, s);
       double* no = c->node_out.ensure(static_cast<size_t>(nn) * 10 + 1);
       // within-rank partial sums per node, then cross-GPU sums of everything
@@ -1191,6 +1200,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     info->min_iterations = c->K;
     info->n_kept_global = c->n_kept_global;
     info->n_cells = c->n_cells;
+    info->cube_cell_bytes = do_cube ? (c->cube32 ? 4u : 8u) : 0u;
+    info->cube_store_bytes = do_cube ? c->n_store * (c->cube32 ? 4u : 8u) : 0u;
     info->n_leaves = do_cube ? static_cast<uint32_t>(c->leaves.size()) : 0;
     info->n_internal = do_cube ? static_cast<uint32_t>(c->internal_pos.size()) : 0;
     if (do_out) {
@@ -1255,31 +1266,52 @@ ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts
     if (c->n_traces)
       PSG_CUDA(cudaMemcpy(ic.data(), c->iter_count.p, 4ull * c->n_traces, cudaMemcpyDeviceToHost));
     if (iter_counts) std::copy(ic.begin(), ic.end(), iter_counts);
-    if (block_offset) {
-      std::vector<uint64_t> bo(c->n_traces);
-      if (c->n_traces)
-        PSG_CUDA(cudaMemcpy(bo.data(), c->block_off.p, 8ull * c->n_traces, cudaMemcpyDeviceToHost));
+    if (block_offset) {  // dense cell offsets of the kept traces (itermodel.hpp:97-101)
+      uint64_t off = 0;
       size_t j = 0;
       for (uint32_t t = 0; t < c->n_traces; ++t)
-        if (ic[t] > 0) block_offset[j++] = bo[t];
+        if (ic[t] > 0) {
+          block_offset[j++] = off;
+          off += static_cast<uint64_t>(ic[t]) * c->nn;
+        }
     }
     if (excl && !c->have_excl)
       fail(PS_E_INVALID_ARGUMENT, "the excl cube was not stored (PSG_Q_NO_CUBE_STORE)");
-    if (incl && c->n_cells)
-      PSG_CUDA(cudaMemcpy(incl, c->cube_incl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
-    if (excl && c->n_cells) {
-      // expand the compact cube: a leaf's excl equals its incl; internal nodes
-      // come from the [iteration][internal node] table
-      if (incl)
-        std::memcpy(excl, incl, 8 * c->n_cells);
-      else
-        PSG_CUDA(cudaMemcpy(excl, c->cube_incl.p, 8 * c->n_cells, cudaMemcpyDeviceToHost));
-      const size_t rows = c->n_cells / c->nn, m = c->internal_pos.size();
-      if (m) {
-        std::vector<int64_t> xi(rows * m);
-        PSG_CUDA(cudaMemcpy(xi.data(), c->cube_xint.p, 8 * rows * m, cudaMemcpyDeviceToHost));
-        for (size_t r = 0; r < rows; ++r)
-          for (size_t q = 0; q < m; ++q) excl[r * c->nn + c->internal_pos[q]] = xi[r * m + q];
+    if ((incl || excl) && c->n_cells) {
+      // storage -> the reference's dense int64 layout: rows of stride row_stride(nn)
+      // (pad column dropped), trace blocks padded to 4 cells, 32- or 64-bit cells
+      const size_t cb = c->cube32 ? 4 : 8;
+      std::vector<uint8_t> raw(c->n_store * cb);
+      PSG_CUDA(cudaMemcpy(raw.data(), c->cube_incl.p, raw.size(), cudaMemcpyDeviceToHost));
+      int64_t* dst = incl ? incl : excl;
+      const uint32_t nn = c->nn, nnp = row_stride(nn);
+      uint64_t so = 0, d = 0;
+      for (uint32_t t = 0; t < c->n_traces; ++t) {
+        if (ic[t] == 0) continue;
+        for (uint32_t k = 0; k < ic[t]; ++k)
+          for (uint32_t n = 0; n < nn; ++n, ++d) {
+            const uint64_t i = so + static_cast<uint64_t>(k) * nnp + n;
+            if (c->cube32) {
+              uint32_t v;
+              std::memcpy(&v, raw.data() + 4 * i, 4);
+              dst[d] = static_cast<int64_t>(v);
+            } else {
+              std::memcpy(&dst[d], raw.data() + 8 * i, 8);
+            }
+          }
+        so += (static_cast<uint64_t>(ic[t]) * nnp + 3) & ~3ull;
+      }
+      if (excl) {
+        // a leaf's excl equals its incl; internal nodes come from the
+        // [iteration][internal node] table
+        if (incl) std::memcpy(excl, incl, 8 * c->n_cells);
+        const size_t rows = c->n_cells / c->nn, m = c->internal_pos.size();
+        if (m) {
+          std::vector<int64_t> xi(rows * m);
+          PSG_CUDA(cudaMemcpy(xi.data(), c->cube_xint.p, 8 * rows * m, cudaMemcpyDeviceToHost));
+          for (size_t r = 0; r < rows; ++r)
+            for (size_t q = 0; q < m; ++q) excl[r * c->nn + c->internal_pos[q]] = xi[r * m + q];
+        }
       }
     }
     const size_t g = static_cast<size_t>(c->n_kept) * c->nn;

@@ -76,6 +76,66 @@ struct bound_params {
   unsigned long long* overflow;  // traces whose boundaries did not fit their region
 };
 
+// Per-warp shared-memory carve-out (bytes), shared by host and device.
+// Cube cells and window sums are split into 32-bit words so that the hot
+// loop can use native 32-bit shared reductions (RED) without return values;
+// the overflow guards are the time spans of iterations and block steps (see
+// psg_query.cu).
+//
+// Cube rows are node-indexed with stride nnp = nn + 1 rounded up to even (the
+// cube's storage stride): a chunk's G rows are byte for byte its block in the cube, and the pad
+// column nn absorbs the events of contexts outside the anchor subtree, so the
+// interior loop adds every event without a branch.  The ring holds 2G rows
+// and the gap row (2G).
+//
+// The window table is one 36-byte record per ctx, so one address serves all
+// of an event's reductions: {cnt, pending 32-bit sum, min, max, byte offset of
+// the ctx's cube column in a row (the pad column outside the anchor subtree),
+// count of durations >= 2^32, folded 64-bit
+// sum (lo, hi words), -}.  The odd stride of 9 words puts the same field of 32
+// consecutive contexts in 32 distinct banks.  The rare min/max of durations
+// >= 2^32 accumulate in the trace's global output row (64-bit global atomics).
+enum : uint32_t { WT_CNT = 0, WT_LO = 1, WT_MIN = 2, WT_MAX = 3, WT_PPO = 4, WT_NBIG = 5,
+                  WT_ACC = 6 /* lo, hi words */, WT_STRIDE = 9 };
+
+// Cube row stride in cells: nn + 1 rounded up to even (pad columns).
+__host__ __device__ inline uint32_t row_stride(uint32_t nn) { return (nn + 2) & ~1u; }
+
+struct warp_smem_layout {
+  uint32_t nnp;               // cube row stride (nn + 1 rounded up to even)
+  uint32_t off_rlo, off_rhi;  // (2G+1) x nnp u32: cube rows (ring of 2G, gap)
+  uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
+  uint32_t off_bwin;   // 2G+2 u32     boundary window (event indices relative to the trace)
+  uint32_t off_bts;    // 2G+2 u64     timestamps of those boundaries
+  uint32_t off_wtab;   // n_ctx x 36 B window records (WT_*)
+  uint32_t off_wsx, off_wsqlo, off_wsqhi;  // nn u64: within-trace sums over k < K
+  uint32_t off_carry;  // {u64 ts, u64 dur, u64 (has << 32 | ctx)}
+  uint32_t off_scan;   // 2 x (n_ctx + 1) u64 at finalize (aliases the rows)
+  uint32_t bytes;
+  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G, bool /*root_only*/) {
+    uint32_t o = 0;
+    auto take = [&](uint32_t b) {
+      uint32_t r = o;
+      o += (b + 15u) & ~15u;
+      return r;
+    };
+    nnp = row_stride(nn);
+    const uint32_t rows = 4u * (2 * G + 1) * nnp, scan = 16u * (n_ctx + 1);
+    off_rlo = take(rows > scan ? rows : scan);
+    off_scan = off_rlo;
+    off_rhi = take(rows);
+    off_pref = take(8u * (nn + 1));  // generic rows and the gap row
+    off_bwin = take(4u * (2 * G + 2));
+    off_bts = take(8u * (2 * G + 2));
+    off_wtab = take(4u * WT_STRIDE * n_ctx);
+    off_wsx = take(8u * nn);
+    off_wsqlo = take(8u * nn);
+    off_wsqhi = take(8u * nn);
+    off_carry = take(24);
+    bytes = o;
+  }
+};
+
 // Pass 2 (k_trace_query): window + cube + stats in one read of the events.
 struct query_params {
   trace_view tr;
@@ -103,12 +163,16 @@ struct query_params {
   const uint32_t* n_bounds;
   const uint32_t* iter_count;  // [n] 0 = skipped
   const uint32_t* tpos;        // [n] position among kept traces
-  const uint64_t* block_off;   // [n] cell offset of the trace's first row (kept traces)
+  const uint64_t* block_off;   // [n] storage cell offset of the trace's first row (kept traces)
+  const uint64_t* iter_off;    // [n] iterations stored before the trace (kept traces)
   uint32_t K;                  // global min iterations over kept traces (0: none)
-  // The cube is stored compactly: incl dense [cells]; excl only for the m
+  // The cube is stored compactly: incl in rows of stride nnp (nn + 1 rounded
+  // up to even: pad columns), each trace's block padded to 16 bytes, as 32-bit cells when every
+  // stored iteration spans < 2^32 ns (cube32) else 64-bit; excl only for the m
   // internal nodes [Σ iters][m] (a leaf's exclusive time IS its inclusive
-  // time), expanded to the reference's dense layout on copy-out.
+  // time).  Copy-out rebuilds the reference's dense int64 layout.
   uint64_t *cube_incl, *cube_xint, *gap_incl, *gap_excl;
+  uint32_t cube32;
   uint32_t m;  // internal nodes of the anchor subtree
   // cross-rank stats accumulators (k < K) and within-trace CVs
   unsigned long long *x_sum, *x_max, *x_sq;  // [K][nn], x_sq = 3 limbs [3][K][nn]
@@ -116,60 +180,7 @@ struct query_params {
   uint8_t* within_ok;  // [n_kept][nn]
   uint32_t G;          // iterations per chunk (power of two); the row ring holds 2G + gap
   uint32_t warps;      // traces per CTA
-};
-
-// Per-warp shared-memory carve-out (bytes), shared by host and device.
-// Cube cells and window sums are split into 32-bit words so that the hot
-// loop can use native 32-bit shared reductions (RED) without return values;
-// the overflow guards are the time spans of iterations and block steps (see
-// psg_query.cu).
-//
-// Cube rows have stride nn + 1: column nn is a trash column that absorbs the
-// events of contexts outside the anchor subtree, so the interior loop adds
-// every event without a branch.  The ring holds 2G rows and the gap row (2G).
-//
-// The window table is one 36-byte record per ctx, so one address serves all
-// of an event's reductions: {cnt, pending 32-bit sum, min, max, byte offset of
-// the ctx's cube column in a row, count of durations >= 2^32, folded 64-bit
-// sum (lo, hi words), -}.  The odd stride of 9 words puts the same field of 32
-// consecutive contexts in 32 distinct banks.  The rare min/max of durations
-// >= 2^32 accumulate in the trace's global output row (64-bit global atomics).
-enum : uint32_t { WT_CNT = 0, WT_LO = 1, WT_MIN = 2, WT_MAX = 3, WT_PPO = 4, WT_NBIG = 5,
-                  WT_ACC = 6 /* lo, hi words */, WT_STRIDE = 9 };
-
-struct warp_smem_layout {
-  uint32_t nnp;               // cube row stride (nn + 1)
-  uint32_t off_rlo, off_rhi;  // (2G+1) x nnp u32: cube rows (ring of 2G, gap)
-  uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
-  uint32_t off_bwin;   // 2G+2 u32     boundary window (event indices relative to the trace)
-  uint32_t off_bts;    // 2G+2 u64     timestamps of those boundaries
-  uint32_t off_wtab;   // n_ctx x 36 B window records (WT_*)
-  uint32_t off_wsx, off_wsqlo, off_wsqhi;  // nn u64: within-trace sums over k < K
-  uint32_t off_carry;  // {u64 ts, u64 dur, u64 (has << 32 | ctx)}
-  uint32_t off_scan;   // 2 x (n_ctx + 1) u64 at finalize (aliases the rows)
-  uint32_t bytes;
-  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G, bool /*root_only*/) {
-    uint32_t o = 0;
-    auto take = [&](uint32_t b) {
-      uint32_t r = o;
-      o += (b + 15u) & ~15u;
-      return r;
-    };
-    nnp = nn + 1;
-    const uint32_t rows = 4u * (2 * G + 1) * nnp, scan = 16u * (n_ctx + 1);
-    off_rlo = take(rows > scan ? rows : scan);
-    off_scan = off_rlo;
-    off_rhi = take(rows);
-    off_pref = take(8u * (nn + 1));  // generic rows and the gap row
-    off_bwin = take(4u * (2 * G + 2));
-    off_bts = take(8u * (2 * G + 2));
-    off_wtab = take(4u * WT_STRIDE * n_ctx);
-    off_wsx = take(8u * nn);
-    off_wsqlo = take(8u * nn);
-    off_wsqhi = take(8u * nn);
-    off_carry = take(24);
-    bytes = o;
-  }
+  warp_smem_layout L;  // per-warp shared-memory carve-out (computed on the host)
 };
 
 // CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]
@@ -204,14 +215,23 @@ void launch_bounds(const bound_params& p, cudaStream_t s);
 uint32_t launch_suggest_anchor(const uint64_t* ts, const uint32_t* ctx, uint64_t n, uint64_t t_end,
                                const uint32_t* parent, const int32_t* pre, const int32_t* size,
                                uint32_t n_ctx, uint32_t min_iters, double cv_max, cudaStream_t s);
-void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t* tpos,
-                        uint64_t* block_off, uint64_t* kept_bo,
-                        unsigned long long* summary /*[0]=kept [1]=min_it [2]=cells*/,
-                        void* scratch, size_t scratch_bytes, cudaStream_t s);
+// Cube layout from the iteration counts: kept positions, storage offsets of
+// the trace blocks (rows of stride nnp, blocks padded to 4 cells), iteration
+// offsets, the compact list of kept block offsets.  summary: [0] kept,
+// [1] min iterations, [2] logical cells (Σ iters * nn), [4] storage cells.
+void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t nnp,
+                        uint32_t* tpos, uint64_t* block_off, uint64_t* iter_off, uint64_t* kept_bo,
+                        unsigned long long* summary, void* scratch, size_t scratch_bytes,
+                        cudaStream_t s);
+// Longest stored iteration of any trace (b_{k+1} - b_k, the last one ending at
+// t_end) into *max_span (atomicMax): decides 32- vs 64-bit cube cells.
+void launch_iter_spans(const uint64_t* cap_off, const uint64_t* bts, const uint32_t* iter_count,
+                       const uint64_t* t_end, uint32_t n, unsigned long long* max_span,
+                       cudaStream_t s);
 size_t cube_layout_scratch_bytes(uint32_t n);
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s);
-void launch_cross_stats(const uint64_t* incl, const uint64_t* kept_bo, uint32_t n_kept,
-                        uint32_t nn, uint32_t K, unsigned long long* x_sum,
+void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, uint32_t n_kept,
+                        uint32_t nn, uint32_t nnp, uint32_t K, unsigned long long* x_sum,
                         unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s);
 void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,
                            const unsigned long long* x_sq, uint32_t K, uint32_t nn,

@@ -296,18 +296,23 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
   PSG_CUDA(cudaGetLastError());
 }
 
-// Cube layout: kept flags, cell counts, then exclusive scans (CUB).
-__global__ void k_layout_prep(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint64_t* kept,
-                              uint64_t* cells, unsigned long long* summary) {
+// Cube layout: kept flags, storage cell counts (rows of stride nnp, each
+// trace block padded to a multiple of 4 cells = 16 bytes of 32-bit cells),
+// iteration counts, then exclusive scans (CUB).
+__global__ void k_layout_prep(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t nnp,
+                              uint64_t* kept, uint64_t* cells, uint64_t* iters,
+                              unsigned long long* summary) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   uint32_t it = iter_count[t];
   kept[t] = it > 0 ? 1 : 0;
-  cells[t] = static_cast<uint64_t>(it) * nn;
+  cells[t] = (static_cast<uint64_t>(it) * nnp + 3) & ~3ull;
+  iters[t] = it;
   if (it > 0) {
     atomicAdd(summary + 0, 1ull);
     atomicMin(summary + 1, static_cast<unsigned long long>(it));
     atomicAdd(summary + 2, static_cast<unsigned long long>(it) * nn);
+    atomicAdd(summary + 4, (static_cast<unsigned long long>(it) * nnp + 3) & ~3ull);
   }
 }
 
@@ -320,6 +325,33 @@ __global__ void k_finish_layout(const uint64_t* tpos64, const uint32_t* iter_cou
   const uint32_t tp = static_cast<uint32_t>(tpos64[t]);
   tpos[t] = tp;
   if (iter_count[t] > 0) kept_bo[tp] = block_off[t];
+}
+
+// One warp per trace: the longest stored iteration (itermodel.cpp:294-301:
+// iteration k = [b_k, b_{k+1}), the last one ends at t_end).
+__global__ void k_iter_spans(const uint64_t* cap_off, const uint64_t* bts, const uint32_t* iter_count,
+                             const uint64_t* t_end, uint32_t n, unsigned long long* max_span) {
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= n) return;
+  const uint32_t it = iter_count[t];
+  const uint64_t* b = bts + cap_off[t];
+  unsigned long long m = 0;
+  for (uint32_t j = lane; j < it; j += 32) {
+    const uint64_t b0 = b[j], b1 = j + 1 < it ? b[j + 1] : t_end[t];
+    m = max(m, static_cast<unsigned long long>(b1 - b0));
+  }
+  for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if (lane == 0 && it > 0) atomicMax(max_span, m);
+}
+
+void launch_iter_spans(const uint64_t* cap_off, const uint64_t* bts, const uint32_t* iter_count,
+                       const uint64_t* t_end, uint32_t n, unsigned long long* max_span,
+                       cudaStream_t s) {
+  if (n == 0) return;
+  k_iter_spans<<<(n + 7) / 8, 256, 0, s>>>(cap_off, bts, iter_count, t_end, n, max_span);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
 }
 
 size_t exclusive_scan_u64_scratch(uint32_t n) {
@@ -336,26 +368,30 @@ void launch_exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint32_t n, vo
 }
 
 size_t cube_layout_scratch_bytes(uint32_t n) {
-  // kept (n u64) + cells (n u64) + tpos64 (n u64) + scan temp
-  return 3ull * (n + 1) * sizeof(uint64_t) + exclusive_scan_u64_scratch(n) + 256;
+  // kept, cells, tpos64, iters (n u64 each) + scan temp
+  return 4ull * (n + 1) * sizeof(uint64_t) + exclusive_scan_u64_scratch(n) + 256;
 }
 
-void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t* tpos,
-                        uint64_t* block_off, uint64_t* kept_bo, unsigned long long* summary,
-                        void* scratch, size_t scratch_bytes, cudaStream_t s) {
+void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t nnp,
+                        uint32_t* tpos, uint64_t* block_off, uint64_t* iter_off, uint64_t* kept_bo,
+                        unsigned long long* summary, void* scratch, size_t scratch_bytes,
+                        cudaStream_t s) {
   if (n == 0) return;
   uint64_t* kept = static_cast<uint64_t*>(scratch);
   uint64_t* cells = kept + (n + 1);
   uint64_t* tpos64 = cells + (n + 1);
-  void* temp = tpos64 + (n + 1);
-  size_t temp_bytes = scratch_bytes - 3ull * (n + 1) * sizeof(uint64_t);
-  unsigned long long init[3] = {0ull, 0xFFFFFFFFull, 0ull};
-  PSG_CUDA(cudaMemcpyAsync(summary, init, sizeof(init), cudaMemcpyHostToDevice, s));
-  k_layout_prep<<<(n + 255) / 256, 256, 0, s>>>(iter_count, n, nn, kept, cells, summary);
+  uint64_t* iters = tpos64 + (n + 1);
+  void* temp = iters + (n + 1);
+  size_t temp_bytes = scratch_bytes - 4ull * (n + 1) * sizeof(uint64_t);
+  unsigned long long init[5] = {0ull, 0xFFFFFFFFull, 0ull, 0ull, 0ull};
+  PSG_CUDA(cudaMemcpyAsync(summary, init, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  PSG_CUDA(cudaMemcpyAsync(summary + 4, init + 4, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  k_layout_prep<<<(n + 255) / 256, 256, 0, s>>>(iter_count, n, nn, nnp, kept, cells, iters, summary);
   count_launch();
   PSG_CUDA(cudaGetLastError());
   launch_exclusive_scan_u64(kept, tpos64, n, temp, temp_bytes, s);
   launch_exclusive_scan_u64(cells, block_off, n, temp, temp_bytes, s);
+  launch_exclusive_scan_u64(iters, iter_off, n, temp, temp_bytes, s);
   k_finish_layout<<<(n + 255) / 256, 256, 0, s>>>(tpos64, iter_count, block_off, n, tpos, kept_bo);
   count_launch();
   PSG_CUDA(cudaGetLastError());

@@ -140,19 +140,31 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   bool have_c = false;   // a candidate has been seen ...
   u64 last_c = 0;        // ... with this timestamp
   u64 nb = 0, last_b = 0;
+  // software pipeline: the next block step's ctx words are loaded into
+  // registers while this one is processed (the arrays carry one block step of
+  // slack past the last event)
+  uint4 nxt[RB / 4];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(p.tr.ctx + (b & ~3ull) + static_cast<u64>(lane) * RB);
+#pragma unroll
+    for (int q = 0; q < RB / 4; ++q) nxt[q] = __ldg(src + q);
+  }
   for (u64 s = b & ~3ull; s < e; s += STEP_B) {
     const u64 r0 = s + static_cast<u64>(lane) * RB;
     if (lane == 0 && s + 3 * STEP_B <= e)
       prefetch_l2(p.tr.ctx + s + 2 * STEP_B, 4 * STEP_B);
     uint32_t cx[RB];
-    const uint4* src = reinterpret_cast<const uint4*>(p.tr.ctx + r0);
 #pragma unroll
     for (int q = 0; q < RB / 4; ++q) {
-      const uint4 v = __ldg(src + q);
-      cx[4 * q] = v.x;
-      cx[4 * q + 1] = v.y;
-      cx[4 * q + 2] = v.z;
-      cx[4 * q + 3] = v.w;
+      cx[4 * q] = nxt[q].x;
+      cx[4 * q + 1] = nxt[q].y;
+      cx[4 * q + 2] = nxt[q].z;
+      cx[4 * q + 3] = nxt[q].w;
+    }
+    if (s + STEP_B < e) {
+      const uint4* src = reinterpret_cast<const uint4*>(p.tr.ctx + r0 + STEP_B);
+#pragma unroll
+      for (int q = 0; q < RB / 4; ++q) nxt[q] = __ldg(src + q);
     }
     // events of this trace in the lane's run: local indices [lo, hi) of [0, RB)
     const int64_t lo64 = static_cast<int64_t>(b) - static_cast<int64_t>(r0);
@@ -431,7 +443,16 @@ __device__ __forceinline__ void run_block(int wm, const u64 (&tv)[RM + 1], const
 }
 
 __device__ __forceinline__ u64 cell64(const uint32_t* lo, const uint32_t* hi, uint32_t i) {
-  return static_cast<u64>(lo[i]) | (static_cast<u64>(hi[i]) << 32);
+  return static_cast<u64>(lo[i]) | (hi ? static_cast<u64>(hi[i]) << 32 : 0ull);
+}
+
+// One cube cell into HBM storage (32-bit cells when the query's iterations all
+// span < 2^32 ns, else 64-bit); idx counts storage cells (rows of stride nnp).
+__device__ __forceinline__ void store_cell(const query_params& p, u64 idx, u64 v) {
+  if (p.cube32)
+    reinterpret_cast<uint32_t*>(p.cube_incl)[idx] = static_cast<uint32_t>(v);
+  else
+    p.cube_incl[idx] = v;
 }
 
 // Exclusive prefix, in subtree preorder, over a node-indexed (lo, hi) word row
@@ -459,9 +480,9 @@ __device__ __forceinline__ void warp_prefix_row(const uint32_t* lo, const uint32
 // bits), the window class is FULL or NONE, and the lane's run holds at most
 // one iteration boundary (local index bpos; RM when none).  Per event: one
 // window-record address, one load of the ctx's cube column offset, one cube
-// RED into the row selected by bpos and, inside the window, the four window
-// REDs.  Events of contexts outside the anchor subtree land in the trash
-// column, events of unstored iterations in the trash row: no branches.
+// RED into the row selected by bpos (contexts outside the anchor subtree land
+// in the rows' pad column) and, inside the window, the four window REDs; no
+// branches.
 template <int WM>
 __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
                                          uint8_t* sm, uint32_t wt_off, int bpos,
@@ -486,27 +507,29 @@ __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t
 }
 
 // Flush of a full narrow chunk (G rows, every cell < 2^30) when the anchor is
-// the only internal node: a leaf's inclusive time IS its exclusive time, so a
-// lane owns leaves across the chunk's rows and copies them straight to the
-// cube (coalesced along the node axis), with the within-rank Σx / Σx² in
-// registers; the anchor's inclusive time is the row total (one REDUX per row).
+// the only internal node.  A leaf's inclusive time IS its exclusive time, and
+// the chunk's G ring rows (stride nnp = nn + 1) are byte for byte the cube
+// block of its G iterations (same stride; the pad column is zeroed), so:
+//  1. a lane owns leaves across the rows: row sums and the within-rank Σx, Σx²
+//     in registers;
+//  2. the anchor's inclusive time (row total, one REDUX per row) replaces its
+//     exclusive time in the block (that one goes to the compact excl cube);
+//  3. the block is copied to the cube with 16-byte stores, then zeroed.
 template <bool STATS>
-__device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows, uint32_t nnp,
-                                           uint32_t nn, u64 ob, u64 xbase, u64* wsx, u64* wsqlo,
+__device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows, uint32_t nn,
+                                           uint32_t nnp, u64 ob, u64 xbase, u64* wsx, u64* wsqlo,
                                            u64* wsqhi, int lane) {
   constexpr uint32_t G = GC;
   uint32_t rs[GC];
 #pragma unroll
-  for (uint32_t r = 0; r < G; ++r) rs[r] = lane == 0 ? rows[r * nnp] : 0u;  // the anchor's own excl
-  const uint32_t ax = lane < static_cast<int>(G) ? rows[lane * nnp] : 0u;
+  for (uint32_t r = 0; r < G; ++r) rs[r] = 0u;
+  const uint32_t ax = lane < static_cast<int>(G) ? rows[lane * nnp] : 0u;  // the anchor's excl
   for (uint32_t n = 1 + lane; n < nn; n += 32) {
     u64 sx = 0, sq = 0;
-    uint64_t* dst = p.cube_incl + ob + n;
 #pragma unroll
     for (uint32_t r = 0; r < G; ++r) {
       const uint32_t ex = rows[r * nnp + n];
       rs[r] += ex;
-      dst[static_cast<size_t>(r) * nn] = ex;
       if (STATS) {
         sx += ex;
         sq += static_cast<u64>(ex) * ex;  // G squares < 2^60 each
@@ -519,34 +542,55 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
       wsqlo[n] = l2;
     }
   }
-  __syncwarp();
-  {  // zero the chunk's G contiguous rows (16-byte aligned, G * nnp a multiple of 4 words)
-    uint4* z = reinterpret_cast<uint4*>(rows);
-    const uint32_t nz = G * nnp / 4;
-    for (uint32_t i = lane; i < nz; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
-  }
 #pragma unroll
-  for (uint32_t r = 0; r < G; ++r) rs[r] = __reduce_add_sync(FULL, rs[r]);  // < 2^30
+  for (uint32_t r = 0; r < G; ++r) rs[r] = __reduce_add_sync(FULL, rs[r]);  // leaves, < 2^30
   uint32_t mine = rs[0];
 #pragma unroll
   for (uint32_t r = 1; r < G; ++r)
     if (static_cast<uint32_t>(lane) == r) mine = rs[r];
+  mine += ax;  // lane r < G: the anchor's inclusive time in row r
   if (lane < static_cast<int>(G)) {
-    p.cube_incl[ob + static_cast<u64>(lane) * nn] = mine;
+    rows[lane * nnp] = mine;
+    rows[lane * nnp + nn] = 0u;  // pad column
     if (p.store_cube) p.cube_xint[xbase + lane] = ax;  // m == 1
   }
-  if (STATS && lane == 0) {
-    u64 sx = 0, sq = 0;
+  if (STATS) {  // the anchor's within-rank sums: lanes r < G hold its G cells
+    u64 sx = lane < static_cast<int>(G) ? mine : 0u;
+    u64 sq = sx * sx;
 #pragma unroll
-    for (uint32_t r = 0; r < G; ++r) {
-      sx += rs[r];
-      sq += static_cast<u64>(rs[r]) * rs[r];
+    for (int d = 1; d < static_cast<int>(G); d <<= 1) {
+      sx += __shfl_xor_sync(FULL, sx, d);
+      sq += __shfl_xor_sync(FULL, sq, d);
     }
-    wsx[0] += sx;
-    const u64 l2 = wsqlo[0] + sq;
-    wsqhi[0] += l2 < sq ? 1ull : 0ull;
-    wsqlo[0] = l2;
+    if (lane == 0) {
+      wsx[0] += sx;
+      const u64 l2 = wsqlo[0] + sq;
+      wsqhi[0] += l2 < sq ? 1ull : 0ull;
+      wsqlo[0] = l2;
+    }
   }
+  __syncwarp();
+  // the block: G * nnp cells, a multiple of 4; 16-byte aligned on both sides
+  // (ring rows from a 16-byte boundary, trace blocks padded to 4 cells, kb * nnp
+  // a multiple of 8)
+  const uint4* src = reinterpret_cast<const uint4*>(rows);
+  const uint32_t nq = G * nnp / 4;
+  if (p.cube32) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.cube_incl) + ob);
+#pragma unroll 4
+    for (uint32_t i = lane; i < nq; i += 32) dst[i] = src[i];
+  } else {
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(p.cube_incl + ob);
+#pragma unroll 4
+    for (uint32_t i = lane; i < nq; i += 32) {
+      const uint4 v = src[i];
+      dst[2 * i] = make_ulonglong2(v.x, v.y);
+      dst[2 * i + 1] = make_ulonglong2(v.z, v.w);
+    }
+  }
+  __syncwarp();
+  uint4* z = reinterpret_cast<uint4*>(rows);
+  for (uint32_t i = lane; i < nq; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 template <bool WIN, bool CUBE>
@@ -562,8 +606,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   int32_t* s_cct_pre = s_sub_pre + n_ctx;
   int32_t* s_cct_size = s_cct_pre + n_ctx;
 
-  warp_smem_layout L;
-  L.init(n_ctx, nn, G, root_only || !CUBE);
+  const warp_smem_layout& L = p.L;
   const uint32_t nnp = L.nnp;
   const uint32_t wb_off = cta_table_bytes(n_ctx, nn, W) + static_cast<uint32_t>(warp) * L.bytes;
   uint8_t* wb = smem + wb_off;
@@ -598,7 +641,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     r[WT_CNT] = r[WT_LO] = r[WT_MAX] = r[WT_NBIG] = 0u;
     r[WT_MIN] = 0xFFFFFFFFu;
     const int32_t sp = CUBE ? p.sub_pre[c] : -1;
-    r[WT_PPO] = 4u * (sp >= 0 ? static_cast<uint32_t>(sp) : nn);  // trash column nn
+    r[WT_PPO] = 4u * (sp >= 0 ? static_cast<uint32_t>(sp) : nn);  // pad column nn
     T.set_acc(c, 0ull);
   }
   if (lane == 0) T.carry[0] = T.carry[1] = T.carry[2] = 0;
@@ -621,7 +664,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   const bool kept = iters > 0;
   const uint32_t tp = kept ? p.tpos[t] : 0;
   const u64 bo = kept ? p.block_off[t] : 0;
-  const u64 ib = kept ? bo / nn : 0;  // iterations stored before this trace
+  const u64 ib = kept ? p.iter_off[t] : 0;  // iterations stored before this trace
   const u64 region = (CUBE && active) ? p.cap_off[t] : 0;
   const uint32_t* bt = p.bidx + region;
   const uint64_t* btt = p.bts + region;
@@ -721,10 +764,10 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           cv[4 * q + 2] = v.z;
           cv[4 * q + 3] = v.w;
         }
+        u64 nf = __shfl_down_sync(FULL, tv[0], 1);
+        if (lane == 31) nf = ldg64(p.tr.ts + s_abs + STEP_M);
+        tv[RM] = nf;
       }
-      u64 nf = __shfl_down_sync(FULL, tv[0], 1);
-      if (lane == 31) nf = ldg64(p.tr.ts + s_abs + STEP_M);
-      tv[RM] = nf;
       const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
 
       // window class of this block step (warp-uniform)
@@ -838,12 +881,13 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     const uint32_t kcap = (CUBE && p.do_stats && kb < p.K) ? min(n_iter_rows, p.K - kb) : 0;
     if (CUBE && kept) {
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
-      const u64 ob = bo + static_cast<u64>(kb) * nn;
+      uint32_t* rhw = cwide ? rhi : nullptr;  // high words (all zero in narrow chunks)
+      const u64 ob = bo + static_cast<u64>(kb) * nnp;  // storage cell of the chunk's first row
       if (root_only && !cwide && n_iter_rows == G && (kcap == 0 || kcap == G)) {
         if (kcap)
-          flush_fast<true>(p, rlo + s0 * nnp, nnp, nn, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
+          flush_fast<true>(p, rlo + s0 * nnp, nn, nnp, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
         else
-          flush_fast<false>(p, rlo + s0 * nnp, nnp, nn, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
+          flush_fast<false>(p, rlo + s0 * nnp, nn, nnp, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
       } else if (root_only && !cwide) {
         // narrow partial chunk (the trace's last): the same straight copies, row by row
         uint32_t rs[GC];
@@ -852,14 +896,13 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           rs[r] = (lane == 0 && r < n_iter_rows) ? rlo[(s0 + r) * nnp] : 0u;  // anchor's own excl
         for (uint32_t n = 1 + lane; n < nn; n += 32) {
           u64 sx = 0, sq = 0;
-          uint64_t* dst = p.cube_incl + ob + n;
 #pragma unroll
           for (uint32_t r = 0; r < GC; ++r) {
             if (r < n_iter_rows) {
               const uint32_t idx = (s0 + r) * nnp + n;
               const uint32_t ex = rlo[idx];
               rs[r] += ex;
-              dst[r * nn] = ex;
+              store_cell(p, ob + r * nnp + n, ex);
               rlo[idx] = 0;
               if (r < kcap) {
                 sx += ex;
@@ -883,7 +926,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           if (static_cast<uint32_t>(lane) == r) mine = rs[r];
         if (static_cast<uint32_t>(lane) < n_iter_rows) {
           const uint32_t idx = (s0 + lane) * nnp;
-          p.cube_incl[ob + static_cast<u64>(lane) * nn] = mine;
+          store_cell(p, ob + static_cast<u64>(lane) * nnp, mine);
           if (p.store_cube) p.cube_xint[ib + kb + lane] = rlo[idx];  // m == 1
           rlo[idx] = 0;
         }
@@ -903,12 +946,12 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       } else {
         for (uint32_t r = 0; r < n_iter_rows; ++r) {
           const uint32_t slot = s0 + r;
-          warp_prefix_row(rlo + slot * nnp, rhi + slot * nnp, s_node, pref, nn, lane);
+          warp_prefix_row(rlo + slot * nnp, rhw ? rhw + slot * nnp : nullptr, s_node, pref, nn, lane);
           for (uint32_t n = lane; n < nn; n += 32) {
             const int4 nd = s_node[n];
-            const u64 ex = cell64(rlo, rhi, slot * nnp + n);
+            const u64 ex = cell64(rlo, rhw, slot * nnp + n);
             const u64 in = nd.z ? pref[nd.x + nd.y] - pref[nd.x] : ex;
-            p.cube_incl[ob + static_cast<u64>(r) * nn + n] = in;
+            store_cell(p, ob + static_cast<u64>(r) * nnp + n, in);
             if (nd.z && p.store_cube) p.cube_xint[(ib + kb + r) * p.m + (nd.z - 1)] = ex;
             if (r < kcap) {
               wsx[n] += in;
@@ -920,22 +963,28 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
             }
           }
           __syncwarp();
-          for (uint32_t n = lane; n < nn; n += 32) rlo[slot * nnp + n] = rhi[slot * nnp + n] = 0;
+          for (uint32_t n = lane; n < nn; n += 32) {
+            rlo[slot * nnp + n] = 0;
+            if (rhw) rhw[slot * nnp + n] = 0;
+          }
           __syncwarp();
         }
       }
       if (c == 0) {  // the gap row [first_ts, b_0) (itermodel.cpp:331-338)
         __syncwarp();
-        warp_prefix_row(rlo + R2 * nnp, rhi + R2 * nnp, s_node, pref, nn, lane);
+        warp_prefix_row(rlo + R2 * nnp, rhw ? rhw + R2 * nnp : nullptr, s_node, pref, nn, lane);
         for (uint32_t n = lane; n < nn; n += 32) {
           const int4 nd = s_node[n];
-          const u64 ex = cell64(rlo, rhi, R2 * nnp + n);
+          const u64 ex = cell64(rlo, rhw, R2 * nnp + n);
           const u64 in = !nd.z ? ex : pref[nd.x + nd.y] - pref[nd.x];
           p.gap_excl[static_cast<size_t>(tp) * nn + n] = ex;
           p.gap_incl[static_cast<size_t>(tp) * nn + n] = in;
         }
         __syncwarp();
-        for (uint32_t n = lane; n < nn; n += 32) rlo[R2 * nnp + n] = rhi[R2 * nnp + n] = 0;
+        for (uint32_t n = lane; n < nn; n += 32) {
+          rlo[R2 * nnp + n] = 0;
+          if (rhw) rhw[R2 * nnp + n] = 0;
+        }
       }
       __syncwarp();
     }
@@ -1027,77 +1076,129 @@ void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t
 // sufficient statistics of node_matrix / savings_report / iteration_cv_report
 // (diagnostics.cpp:83-158) — per cell Σx, max x and Σx² over the kept traces,
 // for k < K (the ordinal intersection).  Grid = (k tiles) x (trace tiles): a
-// thread owns one (k, node) cell of its tile and streams it over the tile's
-// traces (a trace's tile is kt*nn contiguous values, so the loads coalesce);
-// the global atomics happen once per cell per trace tile.
-__global__ void __launch_bounds__(512) k_cross_stats(const uint64_t* __restrict__ incl,
+// thread owns two adjacent cells (k, 2q), (k, 2q + 1) of its tile (rows have
+// an even stride nnp, so the pair is one 8- or 16-byte load) and streams them
+// over the tile's traces (a trace's tile is kt rows of nnp contiguous cells,
+// so the loads coalesce); the global atomics happen once per cell per tile.
+template <typename CELL> struct cell_pair;
+template <> struct cell_pair<uint32_t> {
+  __device__ static void get(const uint32_t* p, uint32_t& a, uint32_t& b) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    a = v.x;
+    b = v.y;
+  }
+};
+template <> struct cell_pair<unsigned long long> {
+  __device__ static void get(const unsigned long long* p, unsigned long long& a,
+                             unsigned long long& b) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    a = v.x;
+    b = v.y;
+  }
+};
+
+struct cell_acc {
+  u64 sum = 0, mx = 0, ql = 0, qh = 0;
+  __device__ __forceinline__ void add32(u64 v) {  // squares on the 32-bit fast path
+    sum += v;
+    mx = max(mx, v);
+    const u64 q = static_cast<u64>(static_cast<uint32_t>(v)) * static_cast<uint32_t>(v);
+    ql += q;
+    qh += ql < q ? 1ull : 0ull;
+  }
+};
+
+template <typename CELL>
+__global__ void __launch_bounds__(512) k_cross_stats(const CELL* __restrict__ incl,
                                                      const uint64_t* __restrict__ kept_bo,
-                                                     uint32_t n_kept, uint32_t nn, uint32_t K,
-                                                     uint32_t kt, uint32_t per_tile,
+                                                     uint32_t n_kept, uint32_t nn, uint32_t nnp,
+                                                     uint32_t K, uint32_t kt, uint32_t per_tile,
                                                      unsigned long long* x_sum,
                                                      unsigned long long* x_max,
                                                      unsigned long long* x_sq) {
-  constexpr int U = 16;  // independent loads in flight per thread
+  // independent pair loads in flight per thread (128 B of 32-bit cells, 128 B
+  // of 64-bit ones); the next batch's block offsets load during this batch
+  constexpr int U = sizeof(CELL) == 4 ? 16 : 8;
   const uint32_t k0 = blockIdx.x * kt;
   const uint32_t kc = min(kt, K - k0);
   const uint32_t t_lo = blockIdx.y * per_tile, t_hi = min(n_kept, t_lo + per_tile);
   const size_t plane = static_cast<size_t>(K) * nn;
-  for (uint32_t cell = threadIdx.x; cell < kc * nn; cell += blockDim.x) {
-    const u64 off = static_cast<u64>(k0) * nn + cell;
-    u64 sum = 0, mx = 0, ql = 0, qh = 0;
-    // squares on the 32-bit fast path (one IMAD.WIDE each); the maximum says
-    // whether any value reached 2^32, in which case the cell is redone exactly
+  const uint32_t hp = nnp / 2;  // pairs per row
+  for (uint32_t pr = threadIdx.x; pr < kc * hp; pr += blockDim.x) {
+    const uint32_t kk = pr / hp, n0 = 2 * (pr - kk * hp);
+    const u64 off = static_cast<u64>(k0 + kk) * nnp + n0;  // storage cell within the trace block
+    cell_acc A, B;
     uint32_t t = t_lo;
-    for (; t + U <= t_hi; t += U) {
-      u64 v[U];
+    if (t + U <= t_hi) {
+      u64 bo[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = ldg64(incl + ldg64(kept_bo + t + u) + off);
+      for (int u = 0; u < U; ++u) bo[u] = ldg64(kept_bo + t + u);
+      for (; t + U <= t_hi; t += U) {
+        CELL a[U], b[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        sum += v[u];
-        mx = max(mx, v[u]);
-        const u64 q = static_cast<u64>(static_cast<uint32_t>(v[u])) * static_cast<uint32_t>(v[u]);
-        ql += q;
-        qh += ql < q ? 1ull : 0ull;
+        for (int u = 0; u < U; ++u) cell_pair<CELL>::get(incl + bo[u] + off, a[u], b[u]);
+        const bool more = t + 2 * U <= t_hi;
+#pragma unroll
+        for (int u = 0; u < U; ++u) bo[u] = more ? ldg64(kept_bo + t + U + u) : 0ull;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          A.add32(a[u]);
+          B.add32(b[u]);
+        }
       }
     }
     for (; t < t_hi; ++t) {
-      const u64 v = ldg64(incl + ldg64(kept_bo + t) + off);
-      sum += v;
-      mx = max(mx, v);
-      const u64 q = static_cast<u64>(static_cast<uint32_t>(v)) * static_cast<uint32_t>(v);
-      ql += q;
-      qh += ql < q ? 1ull : 0ull;
+      CELL a, b;
+      cell_pair<CELL>::get(incl + ldg64(kept_bo + t) + off, a, b);
+      A.add32(a);
+      B.add32(b);
     }
-    if (mx >> 32) {  // a value >= 2^32: exact 128-bit squares
-      ql = qh = 0;
-      for (t = t_lo; t < t_hi; ++t) acc_sq(ql, qh, ldg64(incl + ldg64(kept_bo + t) + off));
+    // a value >= 2^32 (64-bit cells only): exact 128-bit squares for that cell
+    if ((A.mx >> 32) || (B.mx >> 32)) {
+      A.ql = A.qh = B.ql = B.qh = 0;
+      for (t = t_lo; t < t_hi; ++t) {
+        CELL a, b;
+        cell_pair<CELL>::get(incl + ldg64(kept_bo + t) + off, a, b);
+        acc_sq(A.ql, A.qh, a);
+        acc_sq(B.ql, B.qh, b);
+      }
     }
     if (t_hi > t_lo) {
-      const size_t ci = static_cast<size_t>(off);
       const u64 mask43 = (1ull << 43) - 1;
-      atomicAdd(x_sum + ci, sum);
-      atomicMax(x_max + ci, mx);
-      atomicAdd(x_sq + ci, ql & mask43);
-      atomicAdd(x_sq + plane + ci, ((ql >> 43) | (qh << 21)) & mask43);
-      const u64 top = qh >> 22;
-      if (top) atomicAdd(x_sq + 2 * plane + ci, top);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const cell_acc& C = h ? B : A;
+        if (n0 + h >= nn) continue;  // pad column
+        const size_t ci = static_cast<size_t>(k0 + kk) * nn + n0 + h;
+        atomicAdd(x_sum + ci, C.sum);
+        atomicMax(x_max + ci, C.mx);
+        atomicAdd(x_sq + ci, C.ql & mask43);
+        atomicAdd(x_sq + plane + ci, ((C.ql >> 43) | (C.qh << 21)) & mask43);
+        const u64 top = C.qh >> 22;
+        if (top) atomicAdd(x_sq + 2 * plane + ci, top);
+      }
     }
   }
 }
 
-void launch_cross_stats(const uint64_t* incl, const uint64_t* kept_bo, uint32_t n_kept,
-                        uint32_t nn, uint32_t K, unsigned long long* x_sum,
+void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, uint32_t n_kept,
+                        uint32_t nn, uint32_t nnp, uint32_t K, unsigned long long* x_sum,
                         unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s) {
   if (n_kept == 0 || K == 0 || nn == 0) return;
-  const uint32_t kt = nn >= 512 ? 1u : 512u / nn;
+  const uint32_t kt = nnp >= 1024 ? 1u : 1024u / nnp;  // ~512 pairs per CTA
   const uint32_t gx = (K + kt - 1) / kt;
   uint32_t gy = (4u * 148u + gx - 1) / gx;  // ~4 CTAs per SM in total
   gy = std::max(1u, std::min(gy, (n_kept + 63) / 64));
   const uint32_t per_tile = (n_kept + gy - 1) / gy;
   gy = (n_kept + per_tile - 1) / per_tile;
-  k_cross_stats<<<dim3(gx, gy), 512, 0, s>>>(incl, kept_bo, n_kept, nn, K, kt, per_tile, x_sum,
-                                            x_max, x_sq);
+  if (cube32)
+    k_cross_stats<uint32_t><<<dim3(gx, gy), 512, 0, s>>>(static_cast<const uint32_t*>(incl), kept_bo,
+                                                         n_kept, nn, nnp, K, kt, per_tile, x_sum,
+                                                         x_max, x_sq);
+  else
+    k_cross_stats<unsigned long long><<<dim3(gx, gy), 512, 0, s>>>(
+        static_cast<const unsigned long long*>(incl), kept_bo, n_kept, nn, nnp, K, kt, per_tile,
+        x_sum, x_max, x_sq);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_2605_03561_b200 import Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_OUTLIERS, Q_STATS, Q_WINDOW, PsgError, scenarios
+from paper_2605_03561_b200 import Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_CUBE64, Q_OUTLIERS, Q_STATS, Q_WINDOW, PsgError, scenarios
 from tests.helpers import ROOT, assert_rel, random_cct, random_traces, ref_db, to_aos
 
 pytestmark = pytest.mark.gpu
@@ -32,22 +32,27 @@ def check_window(ctx, tr, parent, t0, t1):
 
 
 def check_cube(ctx, tr, parent, anchor, stats=True):
-    info = ctx.query(Q_CUBE | (Q_STATS if stats else 0), anchor=anchor)
-    g = ctx.cube()
+    """Both HBM cube formats (32-bit cells where every iteration spans < 2^32
+    ns, and forced 64-bit cells) against the oracle."""
     o = oracle.cube(tr, parent, anchor)
-    for k in ("node_ids", "iter_counts", "block_offset", "incl", "excl", "gap_incl", "gap_excl"):
-        assert np.array_equal(g[k], o[k]), f"cube {k} differs (anchor {anchor})"
     kept = int((o["iter_counts"] > 0).sum())
-    assert info["n_kept"] == kept
-    if stats and kept > 0:
-        s = ctx.stats(1.0)
-        for j, leaf in enumerate(s["leaves"]):
-            npos = int(np.searchsorted(o["node_ids"], leaf))
-            want, ok = oracle.node_stats(o, npos)
-            assert_rel(s["savings"][j], want[:4], 1e-9, f"savings leaf {leaf}")
-            assert bool(s["cv_ok"][j]) == ok, f"cv_ok leaf {leaf}"
-            if ok:
-                assert_rel(s["cv"][j], want[4:], 1e-9, f"cv leaf {leaf}")
+    for extra in (0, Q_CUBE64):
+        info = ctx.query(Q_CUBE | (Q_STATS if stats else 0) | extra, anchor=anchor)
+        if extra or kept == 0:
+            assert info["cube_cell_bytes"] == 8 or kept == 0
+        g = ctx.cube()
+        for k in ("node_ids", "iter_counts", "block_offset", "incl", "excl", "gap_incl", "gap_excl"):
+            assert np.array_equal(g[k], o[k]), f"cube {k} differs (anchor {anchor}, flags {extra})"
+        assert info["n_kept"] == kept
+        if stats and kept > 0:
+            s = ctx.stats(1.0)
+            for j, leaf in enumerate(s["leaves"]):
+                npos = int(np.searchsorted(o["node_ids"], leaf))
+                want, ok = oracle.node_stats(o, npos)
+                assert_rel(s["savings"][j], want[:4], 1e-9, f"savings leaf {leaf}")
+                assert bool(s["cv_ok"][j]) == ok, f"cv_ok leaf {leaf}"
+                if ok:
+                    assert_rel(s["cv"][j], want[4:], 1e-9, f"cv leaf {leaf}")
     return g, o
 
 
@@ -307,10 +312,12 @@ def test_wide_durations(gpu_ctx_factory, seed):
         check_cube(ctx, tr, parent, anchor)
 
 
-def test_narrow_and_wide_iterations_mixed(gpu_ctx_factory):
-    """One trace whose iterations alternate between short (< 2^31 ns) and
-    long (> 2^32 ns) spans: chunks switch between the 32-bit and the 64-bit
-    cube paths inside one trace."""
+@pytest.mark.parametrize("long_span", [3 * 2**31, 2**30])
+def test_narrow_and_wide_iterations_mixed(gpu_ctx_factory, long_span):
+    """One trace whose iterations alternate between short (< 2^30 ns) and
+    long spans: chunks switch between the 32-bit and the 64-bit shared-memory
+    cube paths inside one trace.  Long iterations > 2^32 ns force 64-bit HBM
+    cells; 2^31 ns ones keep 32-bit HBM cells with 64-bit shared rows."""
     parent = np.array([0xFFFFFFFF, 0, 1, 1, 0], np.uint32)
     ts, cx = [], []
     t = 1000
@@ -319,7 +326,7 @@ def test_narrow_and_wide_iterations_mixed(gpu_ctx_factory):
         ts.append(t); cx.append(1)
         for k in (2, 3):
             ts.append(t); cx.append(k)
-            t += (3 * 2**31 if long_it else 10_000 + 37 * it) + k
+            t += (long_span if long_it else 10_000 + 37 * it) + k
         ts.append(t); cx.append(4)
         t += 5
         ts.append(t); cx.append(0)
