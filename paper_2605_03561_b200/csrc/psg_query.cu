@@ -45,6 +45,9 @@ typedef unsigned __int128 u128;
 #ifndef PSG_RM
 #define PSG_RM 8
 #endif
+#ifndef PSG_PIPE
+#define PSG_PIPE 1  // register software pipeline of block-step loads in k_trace_query
+#endif
 #ifndef PSG_LB_THREADS
 #define PSG_LB_THREADS 512
 #endif
@@ -77,6 +80,19 @@ __device__ __forceinline__ u64 ldg64(const uint64_t* p) {
 // TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16).
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// One block step's events for this lane (RM timestamps + ctx words from r0)
+// and, on lane 31, the timestamp after the step.
+__device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_abs, int lane,
+                                          ulonglong2 (&ts)[RM / 2], uint4 (&cx)[RM / 4], u64& nf) {
+  const ulonglong2* tsrc = reinterpret_cast<const ulonglong2*>(tr.ts + r0);
+#pragma unroll
+  for (int q = 0; q < RM / 2; ++q) ts[q] = __ldg(tsrc + q);
+  const uint4* csrc = reinterpret_cast<const uint4*>(tr.ctx + r0);
+#pragma unroll
+  for (int q = 0; q < RM / 4; ++q) cx[q] = __ldg(csrc + q);
+  if (lane == 31) nf = ldg64(tr.ts + s_abs + 32 * RM);
 }
 
 // 64-bit add into shared memory through two 32-bit words (lo, hi) with
@@ -134,6 +150,11 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   if (t >= p.tr.n) return;
   const u64 b = p.tr.off[t], e = p.tr.off[t + 1];
   const u64 cap = p.cap_off[t + 1] - p.cap_off[t];
+#ifdef PSG_BOUNDS_FAKE_TS  // A/B only: candidate timestamps = event indices (no ts loads)
+#define BTS(i) static_cast<u64>(i)
+#else
+#define BTS(i) ldg64(p.tr.ts + (i))
+#endif
   uint32_t* out = p.bidx + p.cap_off[t];
   uint64_t* out_ts = p.bts + p.cap_off[t];
   uint32_t prev_in = 0;  // containment of the event before the block step
@@ -151,8 +172,10 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   }
   for (u64 s = b & ~3ull; s < e; s += STEP_B) {
     const u64 r0 = s + static_cast<u64>(lane) * RB;
+#ifndef PSG_NO_BOUNDS_PREFETCH
     if (lane == 0 && s + 3 * STEP_B <= e)
       prefetch_l2(p.tr.ctx + s + 2 * STEP_B, 4 * STEP_B);
+#endif
     uint32_t cx[RB];
 #pragma unroll
     for (int q = 0; q < RB / 4; ++q) {
@@ -193,7 +216,7 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
     // timestamp of this lane's last candidate; the previous candidate before
     // this lane's first one comes from the nearest lower lane with candidates
     u64 my_last = 0;
-    if (candm) my_last = ldg64(p.tr.ts + r0 + (31 - __clz(candm)));
+    if (candm) my_last = BTS(r0 + (31 - __clz(candm)));
     const unsigned lower = any & lanemask_lt();
     u64 prv = __shfl_sync(FULL, my_last, lower ? 31 - __clz(lower) : lane);
     bool has_prv = lower != 0 || have_c;
@@ -202,7 +225,7 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
     u64 lb = 0;
     for (uint32_t m = candm; m; m &= m - 1) {
       const int j = __ffs(m) - 1;
-      const u64 tj = (m & (m - 1)) ? ldg64(p.tr.ts + r0 + j) : my_last;
+      const u64 tj = (m & (m - 1)) ? BTS(r0 + j) : my_last;
       if (!has_prv || prv < tj) {
         bm |= 1u << j;
         ++nbl;
@@ -223,7 +246,7 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
       if (kk < cap) {
         const int j = __ffs(m) - 1;
         out[kk] = static_cast<uint32_t>(r0 + j - b);
-        out_ts[kk] = ldg64(p.tr.ts + r0 + j);
+        out_ts[kk] = BTS(r0 + j);
       }
     nb += tot;
     last_c = __shfl_sync(FULL, my_last, 31 - __clz(any));
@@ -239,6 +262,7 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
     if (nb > cap) atomicAdd(p.overflow, 1ull);
   }
 }
+#undef BTS
 
 void launch_bounds(const bound_params& p, cudaStream_t s) {
   if (p.tr.n == 0) return;
@@ -699,6 +723,12 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   R.root_only = root_only;
   R.lb = lane * RM;
   __syncthreads();
+#if PSG_PIPE
+  ulonglong2 pts[RM / 2];
+  uint4 pcx[RM / 4];
+  u64 pnf = 0;
+  u64 pf_pos = ~0ull;  // block start whose events sit in pts/pcx/pnf
+#endif
 
   for (uint32_t c = 0;; ++c) {
     const uint32_t kb = c * G;
@@ -747,6 +777,36 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       }
       u64 tv[RM + 1];
       uint32_t cv[RM];
+#if PSG_PIPE
+      // software pipeline: this block step's events were loaded into registers
+      // while the previous one was processed; load the next one now
+      if (pf_pos != s_abs) {
+        load_step(p.tr, r0, s_abs, lane, pts, pcx, pnf);
+      }
+#pragma unroll
+      for (int q = 0; q < RM / 2; ++q) {
+        tv[2 * q] = pts[q].x;
+        tv[2 * q + 1] = pts[q].y;
+      }
+#pragma unroll
+      for (int q = 0; q < RM / 4; ++q) {
+        cv[4 * q] = pcx[q].x;
+        cv[4 * q + 1] = pcx[q].y;
+        cv[4 * q + 2] = pcx[q].z;
+        cv[4 * q + 3] = pcx[q].w;
+      }
+      {
+        u64 nf = __shfl_down_sync(FULL, tv[0], 1);
+        if (lane == 31) nf = pnf;
+        tv[RM] = nf;
+      }
+      if (lim < n_t) {
+        pf_pos = (b + lim) & ~3ull;
+        load_step(p.tr, pf_pos + static_cast<u64>(R.lb), pf_pos, lane, pts, pcx, pnf);
+      } else {
+        pf_pos = ~0ull;
+      }
+#else
       {
         const ulonglong2* tsrc = reinterpret_cast<const ulonglong2*>(p.tr.ts + r0);
 #pragma unroll
@@ -768,6 +828,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         if (lane == 31) nf = ldg64(p.tr.ts + s_abs + STEP_M);
         tv[RM] = nf;
       }
+#endif
       const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
 
       // window class of this block step (warp-uniform)
@@ -1109,74 +1170,79 @@ struct cell_acc {
 };
 
 template <typename CELL>
-__global__ void __launch_bounds__(512) k_cross_stats(const CELL* __restrict__ incl,
-                                                     const uint64_t* __restrict__ kept_bo,
-                                                     uint32_t n_kept, uint32_t nn, uint32_t nnp,
-                                                     uint32_t K, uint32_t kt, uint32_t per_tile,
-                                                     unsigned long long* x_sum,
-                                                     unsigned long long* x_max,
-                                                     unsigned long long* x_sq) {
-  // independent pair loads in flight per thread (128 B of 32-bit cells, 128 B
-  // of 64-bit ones); the next batch's block offsets load during this batch
+__global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__ incl,
+                                                        const uint64_t* __restrict__ kept_bo,
+                                                        uint32_t n_kept, uint32_t nn, uint32_t nnp,
+                                                        uint32_t K, uint32_t kt, uint32_t per_tile,
+                                                        unsigned long long* x_sum,
+                                                        unsigned long long* x_max,
+                                                        unsigned long long* x_sq) {
+  // The tile's trace block offsets are staged in shared memory in batches and
+  // read as broadcasts; U independent pair loads are in flight per thread.
   constexpr int U = sizeof(CELL) == 4 ? 16 : 8;
+  constexpr uint32_t TB = 512;
+  __shared__ u64 s_bo[TB];
   const uint32_t k0 = blockIdx.x * kt;
   const uint32_t kc = min(kt, K - k0);
   const uint32_t t_lo = blockIdx.y * per_tile, t_hi = min(n_kept, t_lo + per_tile);
   const size_t plane = static_cast<size_t>(K) * nn;
   const uint32_t hp = nnp / 2;  // pairs per row
-  for (uint32_t pr = threadIdx.x; pr < kc * hp; pr += blockDim.x) {
-    const uint32_t kk = pr / hp, n0 = 2 * (pr - kk * hp);
+  const uint32_t npairs = kc * hp;
+  for (uint32_t pr0 = 0; pr0 < npairs; pr0 += blockDim.x) {
+    const uint32_t pr = pr0 + threadIdx.x;
+    const bool mine = pr < npairs;
+    const uint32_t kk = mine ? pr / hp : 0, n0 = mine ? 2 * (pr - kk * hp) : 0;
     const u64 off = static_cast<u64>(k0 + kk) * nnp + n0;  // storage cell within the trace block
     cell_acc A, B;
-    uint32_t t = t_lo;
-    if (t + U <= t_hi) {
-      u64 bo[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) bo[u] = ldg64(kept_bo + t + u);
-      for (; t + U <= t_hi; t += U) {
+    bool wide = false;
+    for (uint32_t tb = t_lo; tb < t_hi; tb += TB) {
+      const uint32_t nb = min(TB, t_hi - tb);
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) s_bo[i] = kept_bo[tb + i];
+      __syncthreads();
+      if (!mine) continue;
+      uint32_t i = 0;
+      for (; i + U <= nb; i += U) {
         CELL a[U], b[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) cell_pair<CELL>::get(incl + bo[u] + off, a[u], b[u]);
-        const bool more = t + 2 * U <= t_hi;
-#pragma unroll
-        for (int u = 0; u < U; ++u) bo[u] = more ? ldg64(kept_bo + t + U + u) : 0ull;
+        for (int u = 0; u < U; ++u) cell_pair<CELL>::get(incl + s_bo[i + u] + off, a[u], b[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           A.add32(a[u]);
           B.add32(b[u]);
         }
       }
+      for (; i < nb; ++i) {
+        CELL a, b;
+        cell_pair<CELL>::get(incl + s_bo[i] + off, a, b);
+        A.add32(a);
+        B.add32(b);
+      }
     }
-    for (; t < t_hi; ++t) {
-      CELL a, b;
-      cell_pair<CELL>::get(incl + ldg64(kept_bo + t) + off, a, b);
-      A.add32(a);
-      B.add32(b);
-    }
+    if (!mine || t_hi <= t_lo) continue;
     // a value >= 2^32 (64-bit cells only): exact 128-bit squares for that cell
-    if ((A.mx >> 32) || (B.mx >> 32)) {
+    wide = (A.mx >> 32) || (B.mx >> 32);
+    if (wide) {
       A.ql = A.qh = B.ql = B.qh = 0;
-      for (t = t_lo; t < t_hi; ++t) {
+      for (uint32_t t = t_lo; t < t_hi; ++t) {
         CELL a, b;
         cell_pair<CELL>::get(incl + ldg64(kept_bo + t) + off, a, b);
         acc_sq(A.ql, A.qh, a);
         acc_sq(B.ql, B.qh, b);
       }
     }
-    if (t_hi > t_lo) {
-      const u64 mask43 = (1ull << 43) - 1;
+    const u64 mask43 = (1ull << 43) - 1;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const cell_acc& C = h ? B : A;
-        if (n0 + h >= nn) continue;  // pad column
-        const size_t ci = static_cast<size_t>(k0 + kk) * nn + n0 + h;
-        atomicAdd(x_sum + ci, C.sum);
-        atomicMax(x_max + ci, C.mx);
-        atomicAdd(x_sq + ci, C.ql & mask43);
-        atomicAdd(x_sq + plane + ci, ((C.ql >> 43) | (C.qh << 21)) & mask43);
-        const u64 top = C.qh >> 22;
-        if (top) atomicAdd(x_sq + 2 * plane + ci, top);
-      }
+    for (int h = 0; h < 2; ++h) {
+      const cell_acc& C = h ? B : A;
+      if (n0 + h >= nn) continue;  // pad column
+      const size_t ci = static_cast<size_t>(k0 + kk) * nn + n0 + h;
+      atomicAdd(x_sum + ci, C.sum);
+      atomicMax(x_max + ci, C.mx);
+      atomicAdd(x_sq + ci, C.ql & mask43);
+      atomicAdd(x_sq + plane + ci, ((C.ql >> 43) | (C.qh << 21)) & mask43);
+      const u64 top = C.qh >> 22;
+      if (top) atomicAdd(x_sq + 2 * plane + ci, top);
     }
   }
 }
@@ -1187,7 +1253,7 @@ void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, 
   if (n_kept == 0 || K == 0 || nn == 0) return;
   const uint32_t kt = nnp >= 1024 ? 1u : 1024u / nnp;  // ~512 pairs per CTA
   const uint32_t gx = (K + kt - 1) / kt;
-  uint32_t gy = (4u * 148u + gx - 1) / gx;  // ~4 CTAs per SM in total
+  uint32_t gy = (8u * 148u + gx - 1) / gx;  // ~8 CTAs per SM in total (2 resident)
   gy = std::max(1u, std::min(gy, (n_kept + 63) / 64));
   const uint32_t per_tile = (n_kept + gy - 1) / gy;
   gy = (n_kept + per_tile - 1) / per_tile;
