@@ -141,6 +141,9 @@ enum {
   PSG_Q_CUBE64 = 1u << 10,       /* keep 64-bit cube cells in HBM even when every stored
                                     iteration spans < 2^32 ns (default there: 32-bit cells,
                                     exact, widened to int64 on copy-out) */
+  PSG_Q_EXACT_BOUNDS = 1u << 11, /* run pass 1 in its exact mode (boundary timestamps loaded
+                                    and deduplicated there) instead of the optimistic one
+                                    verified by pass 2 */
   PSG_Q_ALL = PSG_Q_WINDOW | PSG_Q_CUBE | PSG_Q_STATS | PSG_Q_OUTLIERS
 };
 

@@ -14,11 +14,11 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import (ANCHOR_AUTO, PsgError, Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_CUBE64, Q_NO_CUBE_STORE, Q_OUTLIERS, Q_STATS, Q_WINDOW,
+from ._lib import (ANCHOR_AUTO, PsgError, Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_CUBE64, Q_EXACT_BOUNDS, Q_NO_CUBE_STORE, Q_OUTLIERS, Q_STATS, Q_WINDOW,
                    check, load)
 from . import scenarios
 
-__all__ = ["ANCHOR_AUTO", "Context", "PsgError", "Q_ALL", "Q_CLAMP_TEND", "Q_CUBE", "Q_CUBE64", "Q_NO_CUBE_STORE", "Q_OUTLIERS", "Q_STATS",
+__all__ = ["ANCHOR_AUTO", "Context", "PsgError", "Q_ALL", "Q_CLAMP_TEND", "Q_CUBE", "Q_CUBE64", "Q_EXACT_BOUNDS", "Q_NO_CUBE_STORE", "Q_OUTLIERS", "Q_STATS",
            "Q_WINDOW", "load", "scenarios"]
 
 

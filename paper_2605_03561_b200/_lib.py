@@ -25,6 +25,7 @@ Q_WINDOW, Q_CUBE, Q_STATS, Q_OUTLIERS = 1, 2, 4, 8
 Q_NO_CUBE_STORE = 1 << 8
 Q_CLAMP_TEND = 1 << 9
 Q_CUBE64 = 1 << 10
+Q_EXACT_BOUNDS = 1 << 11
 Q_ALL = Q_WINDOW | Q_CUBE | Q_STATS | Q_OUTLIERS
 ANCHOR_AUTO = 0xFFFFFFFF
 

@@ -204,6 +204,9 @@ struct psg_context {
   // pass-1 boundary regions: trace t owns bidx[cap_off[t], cap_off[t+1])
   uint32_t cap_div = 32;  // capacity = n_t / cap_div + 32 (exact bound after an overflow)
   bool caps_valid = false;
+  // the optimistic pass 1 missed on the loaded traces: start the next queries
+  // in the exact mode (reset when traces are loaded)
+  bool exact_hint = false;
   dbuf<uint64_t> d_cap_off;
   dbuf<uint32_t> d_bidx, d_nbounds;
   dbuf<uint64_t> d_bts;
@@ -353,6 +356,7 @@ void finish_load(psg_context* c) {
       fail(PS_E_INVALID_ARGUMENT, "trace " + std::to_string(c->h_pid[t]) +
                                       " has 2^32 - 4096 or more events (event indices are 32-bit)");
   c->caps_valid = false;
+  c->exact_hint = false;
   c->cap_div = 32;
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(c->summary.ensure(4));
   unsigned long long init[2] = {0ull, ~0ull};
@@ -1021,6 +1025,9 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     uint32_t anchor = q->anchor_ctx;
     if (do_cube && anchor == PSG_ANCHOR_AUTO) anchor = auto_anchor(c);
     info->anchor = do_cube ? anchor : 0;
+    bool exact_bounds = c->exact_hint || (f & PSG_Q_EXACT_BOUNDS) != 0;
+    const bool force64 = (f & PSG_Q_CUBE64) != 0;
+    for (;;) {  // optimistic pass 1 / 32-bit cells, verified by pass 2 (re-run on a miss)
     if (do_cube) {
       compute_subtree(c, anchor);
       nn = c->nn;
@@ -1042,7 +1049,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
         bp.iter_count = ic;
         bp.overflow = sum + 3;
         PSG_CUDA(cudaMemsetAsync(sum + 3, 0, 8, s));
-        launch_bounds(bp, s);
+        launch_bounds(bp, exact_bounds, s);
         PSG_CUDA(cudaMemcpyAsync(&h[3], sum + 3, 8, cudaMemcpyDeviceToHost, s));
         c->sync();
         if (h[3] == 0 || c->cap_div <= 2) break;
@@ -1054,14 +1061,15 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       launch_cube_layout(ic, n, nn, row_stride(nn), c->tpos.ensure(n + 1), c->block_off.ensure(n + 1),
                          c->iter_off.ensure(n + 1), c->kept_bo.ensure(n + 1), sum,
                          c->scratch.ensure(sb), sb, s);
-      PSG_CUDA(cudaMemsetAsync(sum + 5, 0, 8, s));
-      launch_iter_spans(c->d_cap_off.p, c->d_bts.p, ic, c->d_tend.p, n, sum + 5, s);
+      PSG_CUDA(cudaMemsetAsync(sum + 5, 0, 16, s));  // [5] longest iteration, [6] pass-2 verdict
+      if (exact_bounds) launch_iter_spans(c->d_cap_off.p, c->d_bts.p, ic, c->d_tend.p, n, sum + 5, s);
       PSG_CUDA(cudaMemcpyAsync(h, sum, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       c->sync();
       c->n_kept = static_cast<uint32_t>(h[0]);
       c->n_cells = h[2];
       c->n_store = h[4];
-      c->cube32 = h[5] < (1ull << 32) && !(f & PSG_Q_CUBE64);
+      // 32-bit cells: exact spans from pass 1, or optimistic (verified by pass 2)
+      c->cube32 = !force64 && (!exact_bounds || h[5] < (1ull << 32));
       unsigned long long g[2] = {h[1], h[0]};  // min iterations, kept count
       if (c->multi()) {
         unsigned long long* d = c->summary.p;  // reuse as staging
@@ -1094,6 +1102,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       // PSG_Q_NO_CUBE_STORE drops the excl half
       p.cube_incl = c->cube_incl.ensure((c->n_store * (c->cube32 ? 4 : 8) + 7) / 8 + 2);
       p.cube32 = c->cube32 ? 1 : 0;
+      p.exact_bounds = exact_bounds ? 1 : 0;
       p.m = static_cast<uint32_t>(c->internal_pos.size());
       if (store_cube) p.cube_xint = c->cube_xint.ensure((nn ? c->n_cells / nn : 0) * p.m + 1);
       c->have_excl = store_cube;
@@ -1121,6 +1130,22 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     PSG_CUDA(cudaEventRecord(c->ev[1], s));
     launch_trace_query(p, smem, s);
     PSG_CUDA(cudaEventRecord(c->ev[2], s));
+    if (do_cube && !exact_bounds) {
+      // the optimistic pass 1 (and its 32-bit cells) against the boundary
+      // timestamps pass 2 recorded; a miss re-runs both passes exactly
+      unsigned long long* v = c->summary.p + 6;
+      launch_verify_bounds(c->view(), c->d_cap_off.p, c->d_bts.p, c->d_nbounds.p, c->iter_count.p, v, s);
+      if (c->multi()) c->allreduce(v, 1, ncclUint64, ncclMax);  // every rank re-runs together
+      unsigned long long hv = 0;
+      PSG_CUDA(cudaMemcpyAsync(&hv, v, 8, cudaMemcpyDeviceToHost, s));
+      c->sync();
+      if (hv) {  // duplicate boundary timestamps, or an iteration >= 2^32 ns
+        exact_bounds = c->exact_hint = true;
+        continue;
+      }
+    }
+    break;
+    }
 
     if (do_stats && c->K > 0) {
       const size_t plane = static_cast<size_t>(c->K) * nn;

@@ -159,7 +159,7 @@ struct query_params {
   uint32_t root_only;        // the only internal node is the anchor: incl(anchor) = row total
   const uint64_t* cap_off;     // pass-1 boundary regions
   const uint32_t* bidx;
-  const uint64_t* bts;
+  uint64_t* bts;               // boundary timestamps (written by pass 2 after an optimistic pass 1)
   const uint32_t* n_bounds;
   const uint32_t* iter_count;  // [n] 0 = skipped
   const uint32_t* tpos;        // [n] position among kept traces
@@ -173,6 +173,8 @@ struct query_params {
   // time).  Copy-out rebuilds the reference's dense int64 layout.
   uint64_t *cube_incl, *cube_xint, *gap_incl, *gap_excl;
   uint32_t cube32;
+  uint32_t exact_bounds;        // pass 1 ran exact (boundary timestamps in bts)
+
   uint32_t m;  // internal nodes of the anchor subtree
   // cross-rank stats accumulators (k < K) and within-trace CVs
   unsigned long long *x_sum, *x_max, *x_sq;  // [K][nn], x_sq = 3 limbs [3][K][nn]
@@ -209,7 +211,12 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
                           uint32_t rank_lo, uint32_t n_local, uint64_t events_per_trace,
                           uint64_t* chunk_scratch, uint64_t* ts, uint32_t* ctx, uint64_t* t_end,
                           cudaStream_t s);
-void launch_bounds(const bound_params& p, cudaStream_t s);
+void launch_bounds(const bound_params& p, bool exact, cudaStream_t s);
+// After pass 2 on an optimistic pass 1: duplicate boundary timestamps (bit 0)
+// or a gap / iteration >= 2^32 ns (bit 1), OR-ed into *verify.
+void launch_verify_bounds(const trace_view& tr, const uint64_t* cap_off, const uint64_t* bts,
+                          const uint32_t* n_bounds, const uint32_t* iter_count,
+                          unsigned long long* verify, cudaStream_t s);
 // itermodel::suggest_anchor on one trace (psg_anchor.cu); returns the anchor
 // ctx or 0xFFFFFFFF when no context shows periodic entries.
 uint32_t launch_suggest_anchor(const uint64_t* ts, const uint32_t* ctx, uint64_t n, uint64_t t_end,

@@ -38,6 +38,7 @@ namespace psg {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr unsigned long long kSpan32 = 1ull << 32;
 typedef unsigned long long u64;
 typedef unsigned __int128 u128;
 
@@ -137,13 +138,20 @@ __device__ __forceinline__ void warp_prefix(const u64* src, u64* dst, uint32_t n
 // kept).  The number of iterations drops a zero-length last interval
 // (boundary at t_end).  Boundary event indices are relative to the trace's
 // first event.
-template <bool SMALL>  // SMALL: the CCT has <= 64 contexts, membership bits live in a register
+//
+// EXACT = false is the optimistic pass: it reads only ctx words (4 B/event)
+// and takes every candidate as a boundary, with no timestamp loads (each one
+// costs a whole 128-byte line from HBM) except the last candidate's.  It is
+// exact unless two candidates share a timestamp; pass 2 reads every
+// boundary's timestamp from its own stream, flags that case, and the host
+// re-runs both passes with EXACT = true.
+template <bool SMALL, bool EXACT>  // SMALL: <= 128 contexts, membership bits live in registers
 __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   extern __shared__ uint32_t s_bits[];
   for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) s_bits[i] = p.contains[i];
-  const u64 bits64 = SMALL ? (static_cast<u64>(p.contains[0]) |
-                              (p.words > 1 ? static_cast<u64>(p.contains[1]) << 32 : 0ull))
-                           : 0ull;
+  auto word = [&](uint32_t w) -> u64 { return w < p.words ? static_cast<u64>(p.contains[w]) : 0ull; };
+  const u64 bits_lo = SMALL ? (word(0) | (word(1) << 32)) : 0ull;
+  const u64 bits_hi = SMALL ? (word(2) | (word(3) << 32)) : 0ull;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -200,8 +208,8 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
     for (int j = 0; j < RB; ++j) {
       const uint32_t c = cx[j];
       uint32_t in;
-      if (SMALL)
-        in = static_cast<uint32_t>(bits64 >> (c & 63)) & 1u;  // ctx < 64 on real events
+      if (SMALL)  // ctx < 128 on real events
+        in = static_cast<uint32_t>((c & 64 ? bits_hi : bits_lo) >> (c & 63)) & 1u;
       else
         in = (s_bits[min(c, p.words * 32 - 1) >> 5] >> (c & 31)) & 1u;
       inm |= in << j;
@@ -213,6 +221,20 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
     prev_in = __shfl_sync(FULL, (inm >> (RB - 1)) & 1u, 31);
     const unsigned any = __ballot_sync(FULL, candm != 0);
     if (!any) continue;
+    if (!EXACT) {  // every candidate is a boundary (verified by pass 2)
+      const uint32_t nbl = __popc(candm);
+      uint32_t inc = nbl;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, inc, d);
+        if (lane >= d) inc += y;
+      }
+      u64 kk = nb + inc - nbl;
+      for (uint32_t m = candm; m; m &= m - 1, ++kk)
+        if (kk < cap) out[kk] = static_cast<uint32_t>(r0 + (__ffs(m) - 1) - b);
+      nb += __shfl_sync(FULL, inc, 31);
+      continue;
+    }
     // timestamp of this lane's last candidate; the previous candidate before
     // this lane's first one comes from the nearest lower lane with candidates
     u64 my_last = 0;
@@ -254,6 +276,10 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
     const unsigned bl = __ballot_sync(FULL, nbl != 0);
     if (bl) last_b = __shfl_sync(FULL, lb, 31 - __clz(bl));
   }
+  if (!EXACT) {
+    __syncwarp();  // the other lanes' boundary indices are visible to lane 0
+    if (lane == 0 && nb > 0 && nb <= cap) last_b = ldg64(p.tr.ts + b + out[nb - 1]);
+  }
   if (lane == 0) {
     uint32_t it = static_cast<uint32_t>(nb);
     if (nb > 0 && last_b >= p.tr.t_end[t]) it -= 1;  // empty last interval dropped
@@ -264,12 +290,56 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
 }
 #undef BTS
 
-void launch_bounds(const bound_params& p, cudaStream_t s) {
+void launch_bounds(const bound_params& p, bool exact, cudaStream_t s) {
   if (p.tr.n == 0) return;
-  if (p.words <= 2)
-    k_bounds<true><<<(p.tr.n + 7) / 8, 256, 4u * p.words, s>>>(p);
-  else
-    k_bounds<false><<<(p.tr.n + 7) / 8, 256, 4u * p.words, s>>>(p);
+  const unsigned g = (p.tr.n + 7) / 8, sm = 4u * p.words;
+  if (p.words <= 4) {
+    if (exact)
+      k_bounds<true, true><<<g, 256, sm, s>>>(p);
+    else
+      k_bounds<true, false><<<g, 256, sm, s>>>(p);
+  } else {
+    if (exact)
+      k_bounds<false, true><<<g, 256, sm, s>>>(p);
+    else
+      k_bounds<false, false><<<g, 256, sm, s>>>(p);
+  }
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
+// Verdict on an optimistic pass 1 after pass 2 recorded every boundary's
+// timestamp: bit 0 = two boundaries on one timestamp (the exact pass drops the
+// second, itermodel.cpp:121-130), bit 1 = the gap or a stored iteration spans
+// >= 2^32 ns (32-bit cells could have wrapped).  One warp per trace.
+__global__ void k_verify_bounds(trace_view tr, const uint64_t* cap_off, const uint64_t* bts,
+                                const uint32_t* n_bounds, const uint32_t* iter_count,
+                                unsigned long long* verify) {
+  const uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= tr.n) return;
+  const uint32_t it = iter_count[t], nbd = n_bounds[t];
+  if (it == 0) return;  // skipped trace: no cube rows
+  const uint64_t* bt = bts + cap_off[t];
+  const u64 first = ldg64(tr.ts + tr.off[t]), tend = tr.t_end[t];
+  bool dup = false, wide = false;
+  for (uint32_t j = lane; j < nbd; j += 32) {
+    const u64 tj = bt[j];
+    const u64 prev = j > 0 ? bt[j - 1] : first;
+    if (j > 0) dup |= tj == prev;
+    else wide |= tj - prev >= kSpan32;  // the gap row [first, b_0)
+    const u64 nx = j + 1 < nbd ? bt[j + 1] : tend;
+    if (j < it) wide |= nx - tj >= kSpan32;
+  }
+  const unsigned v = (__ballot_sync(FULL, dup) ? 1u : 0u) | (__ballot_sync(FULL, wide) ? 2u : 0u);
+  if (v && lane == 0) atomicOr(verify, static_cast<unsigned long long>(v));
+}
+
+void launch_verify_bounds(const trace_view& tr, const uint64_t* cap_off, const uint64_t* bts,
+                          const uint32_t* n_bounds, const uint32_t* iter_count,
+                          unsigned long long* verify, cudaStream_t s) {
+  if (tr.n == 0) return;
+  k_verify_bounds<<<(tr.n + 7) / 8, 256, 0, s>>>(tr, cap_off, bts, n_bounds, iter_count, verify);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
@@ -295,8 +365,6 @@ void launch_bounds(const bound_params& p, cudaStream_t s) {
 // path.
 namespace {
 
-constexpr u64 kSpan32 = 1ull << 32;
-constexpr u64 kSpan30 = 1ull << 30;  // narrow chunks: G = 8 squares of cells < 2^30 fit 64 bits
 
 enum : int { WIN_NONE = 0, WIN_FULL = 1, WIN_PART = 2, WIN_WIDE = 3 };
 
@@ -387,6 +455,8 @@ struct run_ctx {
   int iters;  // iterations stored for this trace; -1 for a skipped trace (no gap row either)
   int lb, lo, hi, last_li;
   bool root_only;
+  uint64_t* bts_out;  // optimistic pass 1: boundary timestamps are recorded here (k < nbd)
+  uint32_t nbd;
 };
 
 // ALL: every event of the block step is valid and none is the trace's last
@@ -405,6 +475,7 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
       if (li >= st.nxt) {  // boundaries are distinct events: at most one per event
         ++st.k;
         ++st.cnt;
+        if (R.bts_out && static_cast<uint32_t>(st.k) < R.nbd) R.bts_out[st.k] = tsj;
         st.nxt = st.cnt <= R.R2 ? local_of(R.bwin[st.cnt], R.base3) : INT_MAX;
         st.slot = st.k < 0 ? R.R2 : (static_cast<uint32_t>(st.k) & (R.R2 - 1));
         st.rowb = st.slot * R.nnp;
@@ -530,12 +601,13 @@ __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t
   }
 }
 
-// Flush of a full narrow chunk (G rows, every cell < 2^30) when the anchor is
+// Flush of a full narrow chunk (G rows, every cell < 2^32) when the anchor is
 // the only internal node.  A leaf's inclusive time IS its exclusive time, and
-// the chunk's G ring rows (stride nnp = nn + 1) are byte for byte the cube
-// block of its G iterations (same stride; the pad column is zeroed), so:
+// the chunk's G ring rows (stride nnp) are byte for byte the cube block of its
+// G iterations (same stride; the pad columns are zeroed), so:
 //  1. a lane owns leaves across the rows: row sums and the within-rank Σx, Σx²
-//     in registers;
+//     in registers (G squares in 64 bits while its cells are < 2^30, else
+//     redone in 128 bits);
 //  2. the anchor's inclusive time (row total, one REDUX per row) replaces its
 //     exclusive time in the block (that one goes to the compact excl cube);
 //  3. the block is copied to the cube with 16-byte stores, then zeroed.
@@ -544,30 +616,39 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
                                            uint32_t nnp, u64 ob, u64 xbase, u64* wsx, u64* wsqlo,
                                            u64* wsqhi, int lane) {
   constexpr uint32_t G = GC;
+  const uint4* src = reinterpret_cast<const uint4*>(rows);
+  const uint32_t nq = G * nnp / 4;
   uint32_t rs[GC];
 #pragma unroll
   for (uint32_t r = 0; r < G; ++r) rs[r] = 0u;
   const uint32_t ax = lane < static_cast<int>(G) ? rows[lane * nnp] : 0u;  // the anchor's excl
   for (uint32_t n = 1 + lane; n < nn; n += 32) {
-    u64 sx = 0, sq = 0;
+    u64 sx = 0, sq = 0, sqh = 0;
+    uint32_t orv = 0;
 #pragma unroll
     for (uint32_t r = 0; r < G; ++r) {
       const uint32_t ex = rows[r * nnp + n];
       rs[r] += ex;
       if (STATS) {
         sx += ex;
-        sq += static_cast<u64>(ex) * ex;  // G squares < 2^60 each
+        sq += static_cast<u64>(ex) * ex;  // G squares fit 64 bits while every cell < 2^30
+        orv |= ex;
       }
     }
     if (STATS) {
+      if (orv >> 30) {  // a cell >= 2^30: redo the squares in 128 bits
+        sq = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < G; ++r) acc_sq(sq, sqh, rows[r * nnp + n]);
+      }
       wsx[n] += sx;
       const u64 l2 = wsqlo[n] + sq;
-      wsqhi[n] += l2 < sq ? 1ull : 0ull;
+      wsqhi[n] += sqh + (l2 < sq ? 1ull : 0ull);
       wsqlo[n] = l2;
     }
   }
 #pragma unroll
-  for (uint32_t r = 0; r < G; ++r) rs[r] = __reduce_add_sync(FULL, rs[r]);  // leaves, < 2^30
+  for (uint32_t r = 0; r < G; ++r) rs[r] = __reduce_add_sync(FULL, rs[r]);  // leaves, < 2^32
   uint32_t mine = rs[0];
 #pragma unroll
   for (uint32_t r = 1; r < G; ++r)
@@ -580,16 +661,28 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   }
   if (STATS) {  // the anchor's within-rank sums: lanes r < G hold its G cells
     u64 sx = lane < static_cast<int>(G) ? mine : 0u;
-    u64 sq = sx * sx;
+    u64 sq = sx * sx, sqh = 0;
+    if (!__any_sync(FULL, (sx >> 30) != 0)) {
 #pragma unroll
-    for (int d = 1; d < static_cast<int>(G); d <<= 1) {
-      sx += __shfl_xor_sync(FULL, sx, d);
-      sq += __shfl_xor_sync(FULL, sq, d);
+      for (int d = 1; d < static_cast<int>(G); d <<= 1) {
+        sx += __shfl_xor_sync(FULL, sx, d);
+        sq += __shfl_xor_sync(FULL, sq, d);
+      }
+    } else {  // a row total >= 2^30: 128-bit squares
+      sq = 0;
+      acc_sq(sq, sqh, sx);
+#pragma unroll
+      for (int d = 1; d < static_cast<int>(G); d <<= 1) {
+        sx += __shfl_xor_sync(FULL, sx, d);
+        const u64 ol = __shfl_xor_sync(FULL, sq, d), oh = __shfl_xor_sync(FULL, sqh, d);
+        sq += ol;
+        sqh += oh + (sq < ol ? 1ull : 0ull);
+      }
     }
     if (lane == 0) {
       wsx[0] += sx;
       const u64 l2 = wsqlo[0] + sq;
-      wsqhi[0] += l2 < sq ? 1ull : 0ull;
+      wsqhi[0] += sqh + (l2 < sq ? 1ull : 0ull);
       wsqlo[0] = l2;
     }
   }
@@ -597,8 +690,6 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   // the block: G * nnp cells, a multiple of 4; 16-byte aligned on both sides
   // (ring rows from a 16-byte boundary, trace blocks padded to 4 cells, kb * nnp
   // a multiple of 8)
-  const uint4* src = reinterpret_cast<const uint4*>(rows);
-  const uint32_t nq = G * nnp / 4;
   if (p.cube32) {
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.cube_incl) + ob);
 #pragma unroll 4
@@ -692,12 +783,24 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   const u64 region = (CUBE && active) ? p.cap_off[t] : 0;
   const uint32_t* bt = p.bidx + region;
   const uint64_t* btt = p.bts + region;
-  uint32_t nx_idx = static_cast<uint32_t>(n_t);  // this lane's entry of the next boundary window
+  // this lane's entry of the boundary windows of the next chunk (index and
+  // timestamp) and of the one after (index): the timestamp load depends on
+  // the index, so indices run one chunk further ahead
+  uint32_t nx_idx = static_cast<uint32_t>(n_t), nn_idx = static_cast<uint32_t>(n_t);
   u64 nx_ts = tend;
+  // Boundary timestamps come from pass 1 in its exact mode.  After the
+  // optimistic pass 1 there are none: every chunk runs with 32-bit cells
+  // (exact while iterations span < 2^32 ns), each boundary's timestamp is
+  // written out as its event is processed, and k_verify_bounds checks the
+  // optimistic assumptions afterwards.
+  const bool optimistic = !p.exact_bounds;
+  uint64_t* bts_out = optimistic ? p.bts + region : nullptr;
   if (CUBE && kept && lane <= static_cast<int>(2 * G)) {
     const bool have = static_cast<uint32_t>(lane) < nbd;
     nx_idx = have ? __ldg(bt + lane) : static_cast<uint32_t>(n_t);
-    nx_ts = have ? ldg64(btt + lane) : tend;
+    nx_ts = (have && !optimistic) ? ldg64(btt + lane) : tend;
+    const bool have2 = static_cast<uint32_t>(lane) + G < nbd;
+    nn_idx = have2 ? __ldg(bt + G + lane) : static_cast<uint32_t>(n_t);
   }
   const u64 t0 = p.t0, t1w = (p.clamp_tend && tend < p.t1) ? tend : p.t1;
   u64 pos = 0;    // next unprocessed event, relative to b
@@ -722,6 +825,8 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   R.nnp = nnp;
   R.root_only = root_only;
   R.lb = lane * RM;
+  R.bts_out = kept ? bts_out : nullptr;
+  R.nbd = nbd;
   __syncthreads();
 #if PSG_PIPE
   ulonglong2 pts[RM / 2];
@@ -744,15 +849,20 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       // prefetch the next chunk's window: its loads overlap this chunk's events
       const u64 k = static_cast<u64>(kb + G) + lane;
       const bool have = lane <= static_cast<int>(R2) && k < nbd;
-      nx_idx = have ? __ldg(bt + k) : static_cast<uint32_t>(n_t);
-      nx_ts = have ? ldg64(btt + k) : tend;
+      nx_idx = nn_idx;
+      nx_ts = (have && !optimistic) ? ldg64(btt + k) : tend;
+      const bool have2 = lane <= static_cast<int>(R2) && k + G < nbd;
+      nn_idx = have2 ? __ldg(bt + k + G) : static_cast<uint32_t>(n_t);
       __syncwarp();
       E1 = bwin[G] - 3;
       E2 = bwin[R2] - 3;
-      // iteration spans of the ring (and the gap in chunk 0) decide 32- vs 64-bit cells
-      bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan30;
-      if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan30;
-      cwide = __any_sync(FULL, w);
+      // iteration spans of the ring (and the gap in chunk 0) decide 32- vs
+      // 64-bit cells (exact mode; the optimistic mode runs 32-bit throughout)
+      if (!optimistic) {
+        bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan32;
+        if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan32;
+        cwide = __any_sync(FULL, w);
+      }
     } else if (CUBE && active) {
       // skipped trace: only the window runs; iterations are not stored
       if (lane <= static_cast<int>(R2)) bwin[lane] = static_cast<uint32_t>(n_t) + 3;
@@ -899,6 +1009,8 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           const int bpos = ((H >> lane) & 1u) ? static_cast<int>(bw - base32) - lane * RM : RM;
           const int k0 = static_cast<int>(kb) - 1 + static_cast<int>(jb);
           const uint32_t rb0 = row_of(k0), rb1 = row_of(k0 + 1);
+          if (bts_out && bpos < RM && static_cast<uint32_t>(k0 + 1) < nbd)
+            bts_out[k0 + 1] = ldg64(p.tr.ts + b + bw);
           if (wm == WIN_FULL)
             run_fast<WIN_FULL>(tv, cv, smem, wt_off, bpos, rb0, rb1);
           else
@@ -920,6 +1032,10 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           const uint32_t lp3 = R.base3 + static_cast<uint32_t>(R.lb);
           for (uint32_t j = 0; j <= R2; ++j) cnt += bwin[j] <= lp3 ? 1u : 0u;
           st.cnt = cnt;
+          // a boundary on the lane's first event is counted here, not crossed
+          // in run_events: record its timestamp (optimistic pass 1)
+          if (R.bts_out && cnt > 0 && bwin[cnt - 1] == lp3 && kb - 1 + cnt < nbd)
+            R.bts_out[kb - 1 + cnt] = tv[0];
           st.k = static_cast<int>(kb) - 1 + static_cast<int>(cnt);
           st.nxt = cnt <= R2 ? local_of(bwin[cnt], R.base3) : INT_MAX;
           st.slot = st.k < 0 ? R2 : (static_cast<uint32_t>(st.k) & (R2 - 1));
@@ -956,7 +1072,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         for (uint32_t r = 0; r < GC; ++r)
           rs[r] = (lane == 0 && r < n_iter_rows) ? rlo[(s0 + r) * nnp] : 0u;  // anchor's own excl
         for (uint32_t n = 1 + lane; n < nn; n += 32) {
-          u64 sx = 0, sq = 0;
+          u64 sx = 0, sq = 0, sqh = 0;
 #pragma unroll
           for (uint32_t r = 0; r < GC; ++r) {
             if (r < n_iter_rows) {
@@ -967,14 +1083,14 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
               rlo[idx] = 0;
               if (r < kcap) {
                 sx += ex;
-                sq += static_cast<u64>(ex) * ex;  // G squares < 2^60 each
+                acc_sq(sq, sqh, ex);
               }
             }
           }
           if (kcap) {
             wsx[n] += sx;
             const u64 l2 = wsqlo[n] + sq;
-            wsqhi[n] += l2 < sq ? 1ull : 0ull;
+            wsqhi[n] += sqh + (l2 < sq ? 1ull : 0ull);
             wsqlo[n] = l2;
           }
         }
@@ -992,16 +1108,16 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           rlo[idx] = 0;
         }
         if (kcap && lane == 0) {
-          u64 sx = 0, sq = 0;
+          u64 sx = 0, sq = 0, sqh = 0;
 #pragma unroll
           for (uint32_t r = 0; r < GC; ++r)
             if (r < kcap) {
               sx += rs[r];
-              sq += static_cast<u64>(rs[r]) * rs[r];
+              acc_sq(sq, sqh, rs[r]);
             }
           wsx[0] += sx;
           const u64 l2 = wsqlo[0] + sq;
-          wsqhi[0] += l2 < sq ? 1ull : 0ull;
+          wsqhi[0] += sqh + (l2 < sq ? 1ull : 0ull);
           wsqlo[0] = l2;
         }
       } else {

@@ -8,7 +8,7 @@ import os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
-from paper_2605_03561_b200 import Q_CUBE, Q_NO_CUBE_STORE, Q_STATS, Q_WINDOW, Context, scenarios  # noqa: E402
+from paper_2605_03561_b200 import Q_CUBE, Q_EXACT_BOUNDS, Q_NO_CUBE_STORE, Q_STATS, Q_WINDOW, Context, scenarios  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
 only = sys.argv[2] if len(sys.argv) > 2 else None  # run one flavour (for ncu)
@@ -19,7 +19,8 @@ ev = ctx.shard()["n_events"]
 res = {}
 for name, fl in [("window", Q_WINDOW), ("cube", Q_CUBE), ("cube_nostore", Q_CUBE | Q_NO_CUBE_STORE),
                  ("cube_stats", Q_CUBE | Q_STATS), ("window_cube", Q_WINDOW | Q_CUBE),
-                 ("full", Q_WINDOW | Q_CUBE | Q_STATS)]:
+                 ("full", Q_WINDOW | Q_CUBE | Q_STATS),
+                 ("full_exact", Q_WINDOW | Q_CUBE | Q_STATS | Q_EXACT_BOUNDS)]:
     if only and name != only:
         continue
     ms, mb, mt = [], [], []
