@@ -234,6 +234,42 @@ ps_status psg_get_outliers(psg_context* ctx, double* site_ratio, double* node_me
 ps_status psg_window_rows(psg_context* ctx, uint64_t t0_ns, uint64_t t1_ns, uint64_t* n_rows,
                           uint32_t* row_pid, uint64_t* row_ts, uint32_t* row_ctx);
 
+/* ---- profile records (profile.db) ---------------- */
+/* Loads profile-record bodies into HBM.  `records` holds the packed 14-byte
+ * records {u32 ctx, u16 metric, f64 value} of n_profiles profiles back to back
+ * (host or device memory; each profile's run sorted by ctx, as the reference's
+ * binary search requires, store.cpp:601-613 -- else PS_E_FORMAT),
+ * rec_off[n_profiles + 1] their record offsets, pid[] strictly ascending
+ * profile ids, rank[] their MPI ranks (-1: not a rank, e.g. the summary
+ * profile), node_of_profile[] their node ids in the psg_set_nodes numbering
+ * (NULL: no psg_profile_outliers). */
+ps_status psg_load_profiles(psg_context* ctx, const void* records, const uint64_t* rec_off,
+                            const uint32_t* pid, const int32_t* rank,
+                            const uint32_t* node_of_profile, uint32_t n_profiles);
+/* meta.bin + profile.db of a reference database directory (db_handle::open,
+ * store.cpp:484-503): all profiles; nodes = the hostnames of the ranks, sorted
+ * (node_correlate's order), with rack / chassis parsed from Slingshot names. */
+ps_status psg_load_profile_db(psg_context* ctx, const char* dir);
+/* ingest::ingest_profiles / read_slices (ingest.cpp:122-176) on the device:
+ * the records of the requested profiles (sorted, deduplicated; an unknown id
+ * is PS_E_NOT_FOUND) whose ctx is in ctx_ids (NULL: all) and metric in
+ * metric_ids (NULL: all), profile-id ascending, record order within a profile.
+ * Call with NULL row arrays to get *n_rows, then again to copy. */
+ps_status psg_slice(psg_context* ctx, const uint32_t* pids, uint32_t n_pids, const uint32_t* ctx_ids,
+                    uint32_t n_ctx_ids, const uint16_t* metric_ids, uint32_t n_metrics,
+                    uint64_t* n_rows, uint32_t* row_pid, uint32_t* row_ctx, uint16_t* row_metric,
+                    double* row_value);
+/* congestion_report's numeric core over profile records (workflows.cpp:413-539):
+ * per candidate site the rank_vector of `metric` (rank profiles in rank order,
+ * absent records as 0; workflows.cpp:42-62), its balance ratio
+ * (diagnostics.cpp:10-19), the worst (first minimal) site, the node means of
+ * its values (node_correlate, diagnostics.cpp:378-403), then z-scores and the
+ * top-k (mean desc, node asc) among z >= z_min, and the rack / chassis
+ * localisation.  Results: info (worst_site, worst_ratio, n_outliers, n_racks,
+ * ms_total) and psg_get_outliers. */
+ps_status psg_profile_outliers(psg_context* ctx, uint16_t metric, const uint32_t* site_ctx,
+                               uint32_t n_sites, uint32_t top_k, double z_min, psg_query_info* info);
+
 #ifdef __cplusplus
 }
 #endif

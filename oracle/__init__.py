@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import os
+import struct
 import subprocess
 import tempfile
 
@@ -266,6 +267,98 @@ def ref_congestion_report(db: str, glob: str = "MPI_*", method: str = "dbscan", 
     return _take(p)
 
 
+def ref_slices(db: str, pids, ctx_ids=None, metric_ids=None, jobs: int = 1) -> dict:
+    """The reference's ingest_profiles (ingest.cpp:155-176) through oracle/_ref."""
+    p = np.ascontiguousarray(pids, np.uint32)
+    cx = np.ascontiguousarray([] if ctx_ids is None else ctx_ids, np.uint32)
+    mt = np.ascontiguousarray([] if metric_ids is None else metric_ids, np.uint16)
+    lib = ref()
+    lib.refh_slices.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(C.c_uint32),
+                                C.c_uint32, C.c_int, C.POINTER(C.c_uint16), C.c_uint32, C.c_uint,
+                                C.c_char_p]
+    with tempfile.TemporaryDirectory() as d:
+        _chk(lib.refh_slices(db.encode(), _p(p, C.c_uint32), len(p), _p(cx, C.c_uint32), len(cx),
+                             int(ctx_ids is None), _p(mt, C.c_uint16), len(mt), jobs, d.encode()))
+        return _load_bins(d, {"pid": np.uint32, "ctx": np.uint32, "metric": np.uint16,
+                              "value": np.float64})
+
+
+def read_profile_db(db: str) -> dict:
+    """Tiny independent reader of profile.db (store.hpp:11-14): per profile its
+    id and the packed 14-byte records, plus the whole body as bytes."""
+    raw = open(os.path.join(db, "profile.db"), "rb").read()
+    assert raw[:4] == b"HPPR"
+    n = struct.unpack_from("<I", raw, 8)[0]
+    pids, offs, cnts = [], [], []
+    for i in range(n):
+        pid, off, cnt = struct.unpack_from("<IQQ", raw, 12 + 20 * i)
+        pids.append(pid), offs.append(off), cnts.append(cnt)
+    rec = np.dtype([("ctx", "<u4"), ("metric", "<u2"), ("value", "<f8")])
+    body = b"".join(raw[o:o + 14 * c] for o, c in zip(offs, cnts))
+    recs = np.frombuffer(body, dtype=rec)
+    return {"pid": np.array(pids, np.uint32),
+            "rec_off": np.concatenate([[0], np.cumsum(cnts)]).astype(np.uint64),
+            "body": np.frombuffer(body, np.uint8), "ctx": recs["ctx"].astype(np.uint32),
+            "metric": recs["metric"].astype(np.uint16), "value": recs["value"].astype(np.float64)}
+
+
+def slices(pdb: dict, pids, ctx_ids=None, metric_ids=None) -> dict:
+    """CPU restatement of read_slices (ingest.cpp:122-153) over read_profile_db
+    arrays: sorted unique profiles, records in order, filtered by ctx and metric
+    (records are ctx-sorted, so the reference's per-ctx binary-search runs
+    visit them in record order, store.cpp:598-628)."""
+    out = {"pid": [], "ctx": [], "metric": [], "value": []}
+    cset = None if ctx_ids is None else set(int(c) for c in ctx_ids)
+    mset = None if metric_ids is None else set(int(m) for m in metric_ids)
+    for p in sorted(set(int(x) for x in pids)):
+        i = int(np.searchsorted(pdb["pid"], p))
+        assert i < len(pdb["pid"]) and pdb["pid"][i] == p, f"profile {p} not in database"
+        a, b = int(pdb["rec_off"][i]), int(pdb["rec_off"][i + 1])
+        for r in range(a, b):
+            c, m = int(pdb["ctx"][r]), int(pdb["metric"][r])
+            if (cset is None or c in cset) and (mset is None or m in mset):
+                out["pid"].append(p), out["ctx"].append(c), out["metric"].append(m)
+                out["value"].append(float(pdb["value"][r]))
+    return {"pid": np.array(out["pid"], np.uint32), "ctx": np.array(out["ctx"], np.uint32),
+            "metric": np.array(out["metric"], np.uint16), "value": np.array(out["value"], np.float64)}
+
+
+def profile_sites(pdb: dict, meta: dict, metric: int, sites) -> dict:
+    """congestion_report's numeric core over profile records
+    (workflows.cpp:42-62, 442-471; diagnostics.cpp:10-19, 378-403): per site the
+    rank_vector (rank profiles sorted by (rank, value), absent records as 0),
+    its balance ratio, the worst (first minimal) site and the node means of
+    its values over the sorted host list."""
+    ranks = {int(pid): (int(r), h) for (pid, r, h) in meta["profiles"]}
+    rank_host = {}
+    for (pid, r, h) in meta["profiles"]:
+        if r >= 0 and r not in rank_host:
+            rank_host[r] = h
+    ratios, vectors = [], []
+    for s in sites:
+        by_profile = {}
+        sl = slices(pdb, [p for p in pdb["pid"] if ranks.get(int(p), (-1, ""))[0] >= 0], [s], [metric])
+        for p, v in zip(sl["pid"], sl["value"]):
+            by_profile[int(p)] = float(v)
+        rv = sorted((ranks[int(p)][0], by_profile.get(int(p), 0.0)) for p in pdb["pid"]
+                    if ranks.get(int(p), (-1, ""))[0] >= 0)
+        vals = [v for _, v in rv]
+        mx, sm = vals[0], 0.0
+        for v in vals:
+            mx, sm = max(mx, v), sm + v
+        ratios.append(1.0 if mx == 0.0 else sm / len(vals) / mx)
+        vectors.append(rv)
+    w = min(range(len(sites)), key=lambda i: (ratios[i], i))
+    acc = {}
+    for r, v in vectors[w]:
+        a = acc.setdefault(rank_host[r], [0.0, 0])
+        a[0] += v
+        a[1] += 1
+    hosts = sorted(acc)
+    return {"ratio": np.array(ratios), "worst": w, "hosts": hosts,
+            "node_mean": np.array([acc[h][0] / acc[h][1] for h in hosts])}
+
+
 def read_trace_db(db: str) -> dict:
     """Tiny independent reader of trace.db (format store.hpp:15-18) for tests."""
     raw = np.fromfile(os.path.join(db, "trace.db"), dtype=np.uint8)
@@ -305,8 +398,10 @@ def read_meta(db: str) -> dict:
         pos += ln
         return r
 
+    metrics = []
     for _ in range(u(np.uint32, 4)):
-        u(np.uint32, 4); u(np.uint8, 1); s(); s()
+        mid = u(np.uint32, 4); scope = u(np.uint8, 1); name = s(); s()
+        metrics.append((mid, scope, name))
     profiles = []
     for _ in range(u(np.uint32, 4)):
         pid = u(np.uint32, 4); rank = u(np.int32, 4); u(np.int32, 4); host = s(); u(np.uint64, 8)
@@ -314,4 +409,5 @@ def read_meta(db: str) -> dict:
     parent, names = [], []
     for _ in range(u(np.uint32, 4)):
         u(np.uint32, 4); parent.append(u(np.uint32, 4)); u(np.uint8, 1); names.append(s())
-    return {"parent": np.array(parent, np.uint32), "names": names, "profiles": profiles}
+    return {"parent": np.array(parent, np.uint32), "names": names, "profiles": profiles,
+            "metrics": metrics}

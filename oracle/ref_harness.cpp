@@ -228,6 +228,48 @@ int refh_window(const char* dir, uint64_t t0, uint64_t t1, unsigned jobs,
   });
 }
 
+// ingest::ingest_profiles (ingest.cpp:155-176): the profile-record slice of
+// the requested profiles; all_ctx = a keep set covering the whole tree.
+int refh_slices(const char* dir, const uint32_t* pids, uint32_t n_pids, const uint32_t* ctxs,
+                uint32_t n_ctx, int all_ctx, const uint16_t* metrics, uint32_t n_metrics,
+                unsigned jobs, const char* outdir) {
+  return guarded([&] {
+    auto h = store::db_handle::open(dir);
+    ingest::keep_set keep;
+    if (all_ctx) {
+      for (uint32_t i = 0; i < h.meta().contexts.size(); ++i) keep.ids.push_back(i);
+    } else {
+      keep.ids.assign(ctxs, ctxs + n_ctx);
+    }
+    std::vector<uint16_t> m(metrics, metrics + n_metrics);
+    auto t = ingest::ingest_profiles(h, std::vector<uint32_t>(pids, pids + n_pids), keep, m, jobs);
+    std::string o = outdir;
+    std::filesystem::create_directories(o);
+    dump(o, "pid", t.profile_id);
+    dump(o, "ctx", t.ctx_id);
+    dump(o, "metric", t.metric_id);
+    dump(o, "value", t.value);
+  });
+}
+
+// Mean wall time of ingest_profiles over all rank profiles for the given ctx
+// set and metric (the CPU baseline of the profile slice path).
+double refh_time_slices(const char* dir, const uint32_t* ctxs, uint32_t n_ctx, uint16_t metric,
+                        unsigned jobs, unsigned repeat) {
+  try {
+    auto h = store::db_handle::open(dir);
+    std::vector<uint32_t> pids;
+    for (const auto& p : h.meta().profiles)
+      if (p.rank >= 0) pids.push_back(p.id);
+    ingest::keep_set keep;
+    keep.ids.assign(ctxs, ctxs + n_ctx);
+    return time_mean(repeat, [&] { ingest::ingest_profiles(h, pids, keep, {metric}, jobs); });
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
 // itermodel::build_tri_model (itermodel.cpp:242-360) + savings_report /
 // iteration_cv_report on the subtree leaves (diagnostics.cpp:100-158).
 int refh_trimodel(const char* dir, int64_t anchor, unsigned jobs, double total_time,

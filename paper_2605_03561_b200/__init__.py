@@ -250,6 +250,47 @@ class Context:
                 "selected": sel[: info["n_outliers"]], "racks": rows[:nr],
                 "chassis_mask": cm[:nr], "full_mask": fm[:nr]}
 
+    # ---- profile records (profile.db) -----------------------------------
+    def load_profiles(self, records, rec_off, pids, ranks, node_of_profile=None):
+        """records: uint8 array of packed 14-byte {u32 ctx, u16 metric, f64} records."""
+        off = np.ascontiguousarray(rec_off, dtype=np.uint64)
+        pid = np.ascontiguousarray(pids, dtype=np.uint32)
+        rk = np.ascontiguousarray(ranks, dtype=np.int32)
+        rec = np.ascontiguousarray(records, dtype=np.uint8)
+        nd = None if node_of_profile is None else np.ascontiguousarray(node_of_profile, dtype=np.uint32)
+        check(self.lib.psg_load_profiles(self.h, C.c_void_p(rec.ctypes.data if rec.size else 0),
+                                         _ptr(off, C.c_uint64), _ptr(pid, C.c_uint32), _ptr(rk, C.c_int32),
+                                         _ptr(nd, C.c_uint32) if nd is not None else None, len(pid)))
+
+    def load_profile_db(self, path: str):
+        check(self.lib.psg_load_profile_db(self.h, path.encode()))
+
+    def slice(self, pids, ctx_ids=None, metric_ids=None) -> dict:
+        """ingest_profiles / read_slices: rows (pid, ctx, metric, value)."""
+        p = np.ascontiguousarray(pids, dtype=np.uint32)
+        cx = None if ctx_ids is None else np.ascontiguousarray(ctx_ids, dtype=np.uint32)
+        mt = None if metric_ids is None else np.ascontiguousarray(metric_ids, dtype=np.uint16)
+        args = [self.h, _ptr(p, C.c_uint32), len(p),
+                _ptr(cx, C.c_uint32) if cx is not None else None, 0 if cx is None else len(cx),
+                _ptr(mt, C.c_uint16) if mt is not None else None, 0 if mt is None else len(mt)]
+        n = C.c_uint64()
+        check(self.lib.psg_slice(*args, C.byref(n), None, None, None, None))
+        m = n.value
+        out = {"pid": np.empty(max(1, m), np.uint32), "ctx": np.empty(max(1, m), np.uint32),
+               "metric": np.empty(max(1, m), np.uint16), "value": np.empty(max(1, m), np.float64)}
+        check(self.lib.psg_slice(*args, C.byref(n), _ptr(out["pid"], C.c_uint32),
+                                 _ptr(out["ctx"], C.c_uint32), _ptr(out["metric"], C.c_uint16),
+                                 _ptr(out["value"], C.c_double)))
+        return {k: v[:m] for k, v in out.items()}
+
+    def profile_outliers(self, metric: int, sites, top_k: int = 0, z_min: float = float("-inf")) -> dict:
+        self._sites = np.ascontiguousarray(sites, dtype=np.uint32)
+        info = _lib.QueryInfo()
+        check(self.lib.psg_profile_outliers(self.h, metric, _ptr(self._sites, C.c_uint32),
+                                            len(self._sites), top_k, z_min, C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in info._fields_}
+        return self.info
+
     def export_aos(self, body_addr: int):
         """Writes the loaded traces as packed trace.db bytes to host address body_addr."""
         check(self.lib.psg_export_aos(self.h, C.c_void_p(body_addr)))

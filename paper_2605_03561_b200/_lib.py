@@ -80,6 +80,7 @@ ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.
 
 P = C.c_void_p
 U8P, U32P, U64P = C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+U16P = C.POINTER(C.c_uint16)
 I32P, I64P, F64P = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_double)
 
 _SIGS = {
@@ -109,6 +110,12 @@ _SIGS = {
     "psg_window_rows": (C.c_int, [P, C.c_uint64, C.c_uint64, U64P, U32P, U64P, U32P]),
     "psg_export_aos": (C.c_int, [P, P]),
     "psg_kernel_launches": (C.c_uint64, []),
+    "psg_load_profiles": (C.c_int, [P, P, U64P, U32P, I32P, U32P, C.c_uint32]),
+    "psg_load_profile_db": (C.c_int, [P, C.c_char_p]),
+    "psg_slice": (C.c_int, [P, U32P, C.c_uint32, U32P, C.c_uint32, U16P, C.c_uint32, U64P, U32P, U32P,
+                            U16P, F64P]),
+    "psg_profile_outliers": (C.c_int, [P, C.c_uint16, U32P, C.c_uint32, C.c_uint32, C.c_double,
+                                       C.POINTER(QueryInfo)]),
 }
 
 EXPORTED = sorted(_SIGS)

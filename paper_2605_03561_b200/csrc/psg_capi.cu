@@ -242,6 +242,29 @@ struct psg_context {
   dbuf<unsigned long long> site_acc, node_acc, rack_mask, rack_full;
   dbuf<double> site_ratio, node_mean, node_z;
 
+  // profile records (profile.db; psg_profiles.cu)
+  uint32_t n_prof = 0;
+  uint64_t n_rec = 0;
+  std::vector<uint32_t> h_prof_pid;
+  std::vector<int32_t> h_prof_rank;
+  dbuf<uint64_t> prof_off;
+  dbuf<uint32_t> prof_pid, prec_ctx;
+  dbuf<uint16_t> prec_metric;
+  dbuf<double> prec_value;
+  uint32_t n_rank_prof = 0;                    // profiles with rank >= 0 ...
+  dbuf<uint32_t> d_rank_slot;                  // ... in (rank, id) order -> profile slot
+  bool have_prof_nodes = false;
+  dbuf<uint32_t> d_pnode_off, d_pnode_rank;    // node -> its rank profiles (CSR, rank order)
+  dbuf<double> pvals;                          // [n_rank_prof][n_sites] rank_vector values
+  dbuf<uint32_t> d_slot, d_ctx_bits, d_metric_bits;
+  dbuf<unsigned long long> d_counts, d_row_off;
+  dbuf<uint32_t> d_row_pid, d_row_ctx;
+  dbuf<uint16_t> d_row_metric;
+  dbuf<double> d_row_value;
+  profile_view pview() const {
+    return {prof_off.p, prof_pid.p, prec_ctx.p, prec_metric.p, prec_value.p, n_prof};
+  }
+
   dbuf<uint64_t> jump;
   dbuf<double> gen_params;
   dbuf<uint64_t> gen_chunks;
@@ -614,6 +637,35 @@ uint32_t choose_warps(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table
 
 }  // namespace
 
+// The node universe shared by the trace and profile paths: n_nodes, and when
+// given, each node's rack and chassis (topology.cpp:54-92 universe counts).
+static void set_node_tables(psg_context* c, uint32_t n_nodes, const uint32_t* node_rack,
+                     const uint32_t* node_chassis) {
+  c->n_nodes = n_nodes;
+  {
+    c->h_rack_ids.clear();
+    if (node_rack && node_chassis) {
+      std::set<uint32_t> racks(node_rack, node_rack + n_nodes);
+      c->h_rack_ids.assign(racks.begin(), racks.end());
+      std::vector<uint32_t> ridx(n_nodes), uni(c->h_rack_ids.size() * 64, 0);
+      for (uint32_t i = 0; i < n_nodes; ++i) {
+        ridx[i] = static_cast<uint32_t>(
+            std::lower_bound(c->h_rack_ids.begin(), c->h_rack_ids.end(), node_rack[i]) -
+            c->h_rack_ids.begin());
+        require(node_chassis[i] < 64, "chassis ids >= 64 are not supported");
+        uni[ridx[i] * 64 + node_chassis[i]] += 1;
+      }
+      PSG_CUDA(cudaMemcpyAsync(c->d_node_rack_idx.ensure(n_nodes), ridx.data(), 4ull * n_nodes,
+                               cudaMemcpyHostToDevice, c->stream));
+      PSG_CUDA(cudaMemcpyAsync(c->d_node_chassis.ensure(n_nodes), node_chassis, 4ull * n_nodes,
+                               cudaMemcpyHostToDevice, c->stream));
+      PSG_CUDA(cudaMemcpyAsync(c->d_uni_cnt.ensure(uni.size()), uni.data(), 4ull * uni.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+    }
+  }
+  c->sync();
+}
+
 extern "C" {
 
 const char* psg_version(void) { return "0.1.0-sm100a"; }
@@ -766,26 +818,252 @@ ps_status psg_set_nodes(psg_context* c, const uint32_t* node_of_trace, uint32_t 
     c->h_node_of_trace.assign(node_of_trace, node_of_trace + c->n_traces);
     PSG_CUDA(cudaMemcpyAsync(c->d_node_of_trace.ensure(c->n_traces + 1), node_of_trace,
                              4ull * c->n_traces, cudaMemcpyHostToDevice, c->stream));
-    c->h_rack_ids.clear();
-    if (node_rack && node_chassis) {
-      std::set<uint32_t> racks(node_rack, node_rack + n_nodes);
-      c->h_rack_ids.assign(racks.begin(), racks.end());
-      std::vector<uint32_t> ridx(n_nodes), uni(c->h_rack_ids.size() * 64, 0);
-      for (uint32_t i = 0; i < n_nodes; ++i) {
-        ridx[i] = static_cast<uint32_t>(
-            std::lower_bound(c->h_rack_ids.begin(), c->h_rack_ids.end(), node_rack[i]) -
-            c->h_rack_ids.begin());
-        require(node_chassis[i] < 64, "chassis ids >= 64 are not supported");
-        uni[ridx[i] * 64 + node_chassis[i]] += 1;
-      }
-      PSG_CUDA(cudaMemcpyAsync(c->d_node_rack_idx.ensure(n_nodes), ridx.data(), 4ull * n_nodes,
-                               cudaMemcpyHostToDevice, c->stream));
-      PSG_CUDA(cudaMemcpyAsync(c->d_node_chassis.ensure(n_nodes), node_chassis, 4ull * n_nodes,
-                               cudaMemcpyHostToDevice, c->stream));
-      PSG_CUDA(cudaMemcpyAsync(c->d_uni_cnt.ensure(uni.size()), uni.data(), 4ull * uni.size(),
-                               cudaMemcpyHostToDevice, c->stream));
-    }
+    set_node_tables(c, n_nodes, node_rack, node_chassis);
     c->sync();
+  });
+}
+
+
+// ---- profile records ------------------------------
+
+namespace {
+// Uploads n_rec packed records (host or device bytes) and the profile index,
+// transposes to SoA on the device and checks the ctx order of every run.
+void load_profiles_impl(psg_context* c, const uint8_t* records, const uint64_t* rec_off,
+                        const uint32_t* pid, const int32_t* rank, const uint32_t* node_of_profile,
+                        uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i) {
+    require(rec_off[i + 1] >= rec_off[i], "record offsets must be non-decreasing");
+    if (i > 0 && pid[i] <= pid[i - 1]) fail(PS_E_FORMAT, "profile ids must be strictly ascending");
+  }
+  const uint64_t n_rec = n ? rec_off[n] - rec_off[0] : 0;
+  c->n_prof = n;
+  c->n_rec = n_rec;
+  c->h_prof_pid.assign(pid, pid + n);
+  c->h_prof_rank.assign(rank, rank + n);
+  std::vector<uint64_t> off(n + 1);
+  for (uint32_t i = 0; i <= n; ++i) off[i] = n ? rec_off[i] - rec_off[0] : 0;
+  cudaStream_t s = c->stream;
+  PSG_CUDA(cudaMemcpyAsync(c->prof_off.ensure(n + 1), off.data(), 8ull * (n + 1), cudaMemcpyHostToDevice, s));
+  PSG_CUDA(cudaMemcpyAsync(c->prof_pid.ensure(n + 1), pid, 4ull * n, cudaMemcpyHostToDevice, s));
+  uint8_t* stage = c->d_stage.ensure(n_rec * 14 + 16);
+  if (n_rec)
+    PSG_CUDA(cudaMemcpyAsync(stage, records, n_rec * 14, cudaMemcpyDefault, s));
+  launch_records_to_soa(stage, n_rec, c->prec_ctx.ensure(n_rec + 1), c->prec_metric.ensure(n_rec + 1),
+                        c->prec_value.ensure(n_rec + 1), s);
+  unsigned long long* bad = c->summary.ensure(8) + 7;
+  PSG_CUDA(cudaMemsetAsync(bad, 0, 8, s));
+  launch_records_check(c->prec_ctx.p, c->prof_off.p, n, bad, s);
+  unsigned long long hb = 0;
+  PSG_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, s));
+  c->sync();
+  if (hb) fail(PS_E_FORMAT, "profile records must be sorted by ctx within a profile (store.cpp:601-613)");
+  // rank profiles in (rank, id) order: rank_vector's order (workflows.cpp:42-62)
+  std::vector<uint32_t> rs;
+  for (uint32_t i = 0; i < n; ++i)
+    if (rank[i] >= 0) rs.push_back(i);
+  std::stable_sort(rs.begin(), rs.end(), [&](uint32_t a, uint32_t b) { return rank[a] < rank[b]; });
+  c->n_rank_prof = static_cast<uint32_t>(rs.size());
+  PSG_CUDA(cudaMemcpyAsync(c->d_rank_slot.ensure(rs.size() + 1), rs.data(), 4ull * rs.size(),
+                           cudaMemcpyHostToDevice, s));
+  c->have_prof_nodes = false;
+  if (node_of_profile && c->n_nodes > 0) {
+    // node -> its rank profiles in rank order (node_correlate sums in that order)
+    std::vector<uint32_t> cnt(c->n_nodes + 1, 0), members(rs.size());
+    for (uint32_t r = 0; r < rs.size(); ++r) {
+      const uint32_t nd = node_of_profile[rs[r]];
+      require(nd < c->n_nodes, "node_of_profile entry out of range");
+      ++cnt[nd + 1];
+    }
+    for (uint32_t i = 0; i < c->n_nodes; ++i) cnt[i + 1] += cnt[i];
+    std::vector<uint32_t> fill(cnt.begin(), cnt.end() - 1);
+    for (uint32_t r = 0; r < rs.size(); ++r) members[fill[node_of_profile[rs[r]]]++] = r;
+    PSG_CUDA(cudaMemcpyAsync(c->d_pnode_off.ensure(c->n_nodes + 1), cnt.data(), 4ull * (c->n_nodes + 1),
+                             cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(c->d_pnode_rank.ensure(members.size() + 1), members.data(),
+                             4ull * members.size(), cudaMemcpyHostToDevice, s));
+    c->have_prof_nodes = true;
+  }
+  c->sync();
+}
+}  // namespace
+
+ps_status psg_load_profiles(psg_context* c, const void* records, const uint64_t* rec_off,
+                            const uint32_t* pid, const int32_t* rank,
+                            const uint32_t* node_of_profile, uint32_t n_profiles) {
+  if (!c || (n_profiles && (!rec_off || !pid || !rank))) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    if (n_profiles && rec_off[n_profiles] > rec_off[0]) require(records != nullptr, "records are required");
+    load_profiles_impl(c, static_cast<const uint8_t*>(records), rec_off, pid, rank, node_of_profile,
+                       n_profiles);
+  });
+}
+
+ps_status psg_load_profile_db(psg_context* c, const char* dir) {
+  if (!c || !dir) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    store::profile_db db;
+    store::open_profile_db(dir, db);
+    const uint32_t n = static_cast<uint32_t>(db.index.size());
+    std::vector<uint64_t> off(n + 1, 0);
+    std::vector<uint32_t> pid(n);
+    std::vector<int32_t> rank(n, -1);
+    bool contiguous = true;
+    for (uint32_t i = 0; i < n; ++i) {
+      const auto& e = db.index[i];
+      off[i + 1] = off[i] + e.record_count;
+      pid[i] = e.profile_id;
+      const auto* pd = db.meta.find_profile(e.profile_id);
+      rank[i] = pd ? pd->rank : -1;
+      if (i > 0 && e.offset != db.index[i - 1].offset + db.index[i - 1].record_count * store::k_record_size)
+        contiguous = false;
+    }
+    std::vector<uint8_t> gathered;
+    const uint8_t* body = nullptr;
+    if (n && off[n]) {
+      if (contiguous) {
+        body = db.map.data() + db.index[0].offset;
+      } else {
+        gathered.resize(off[n] * store::k_record_size);
+        for (uint32_t i = 0; i < n; ++i)
+          std::memcpy(gathered.data() + off[i] * store::k_record_size, db.map.data() + db.index[i].offset,
+                      db.index[i].record_count * store::k_record_size);
+        body = gathered.data();
+      }
+    }
+    // nodes: rank -> hostname from the first profile with that rank, node id =
+    // position in the sorted host list (node_correlate, diagnostics.cpp:381-398)
+    std::map<int32_t, const std::string*> rank_host;
+    for (const auto& p : db.meta.profiles)
+      if (p.rank >= 0 && !rank_host.count(p.rank)) rank_host[p.rank] = &p.hostname;
+    std::set<std::string> hosts;
+    for (const auto& [r, h] : rank_host) hosts.insert(*h);
+    std::vector<std::string> host_list(hosts.begin(), hosts.end());
+    std::vector<uint32_t> node_of(n, 0), rack(host_list.size()), chassis(host_list.size());
+    for (uint32_t i = 0; i < n; ++i)
+      if (rank[i] >= 0)
+        node_of[i] = static_cast<uint32_t>(std::lower_bound(host_list.begin(), host_list.end(),
+                                                            *rank_host[rank[i]]) - host_list.begin());
+    bool topo = !host_list.empty();
+    for (size_t i = 0; i < host_list.size() && topo; ++i)
+      topo = store::parse_node_name(host_list[i], &rack[i], &chassis[i]) && chassis[i] < 64;
+    if (!host_list.empty())
+      set_node_tables(c, static_cast<uint32_t>(host_list.size()), topo ? rack.data() : nullptr,
+                      topo ? chassis.data() : nullptr);
+    load_profiles_impl(c, body, off.data(), pid.data(), rank.data(),
+                       host_list.empty() ? nullptr : node_of.data(), n);
+  });
+}
+
+ps_status psg_slice(psg_context* c, const uint32_t* pids, uint32_t n_pids, const uint32_t* ctx_ids,
+                    uint32_t n_ctx_ids, const uint16_t* metric_ids, uint32_t n_metrics,
+                    uint64_t* n_rows, uint32_t* row_pid, uint32_t* row_ctx, uint16_t* row_metric,
+                    double* row_value) {
+  if (!c || !n_rows || (n_pids && !pids)) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    cudaStream_t s = c->stream;
+    // ingest_profiles: sorted unique profile ids (ingest.cpp:161-163); an
+    // unknown id is not_found (store.cpp:588-590)
+    std::vector<uint32_t> ids(pids, pids + n_pids);
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    std::vector<uint32_t> slot(ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) {
+      auto it = std::lower_bound(c->h_prof_pid.begin(), c->h_prof_pid.end(), ids[i]);
+      if (it == c->h_prof_pid.end() || *it != ids[i])
+        fail(PS_E_NOT_FOUND, "profile " + std::to_string(ids[i]) + " not in database");
+      slot[i] = static_cast<uint32_t>(it - c->h_prof_pid.begin());
+    }
+    const uint32_t nr = static_cast<uint32_t>(ids.size());
+    PSG_CUDA(cudaMemcpyAsync(c->d_slot.ensure(nr + 1), slot.data(), 4ull * nr, cudaMemcpyHostToDevice, s));
+    // filters as bit sets (id_filter / metric_filter "all" = no set)
+    const uint32_t* cb = nullptr;
+    uint32_t cw = 0;
+    if (ctx_ids) {
+      uint32_t mx = 0;
+      for (uint32_t i = 0; i < n_ctx_ids; ++i) mx = std::max(mx, ctx_ids[i]);
+      cw = n_ctx_ids ? mx / 32 + 1 : 1;
+      std::vector<uint32_t> bits(cw, 0);
+      for (uint32_t i = 0; i < n_ctx_ids; ++i) bits[ctx_ids[i] >> 5] |= 1u << (ctx_ids[i] & 31);
+      PSG_CUDA(cudaMemcpyAsync(c->d_ctx_bits.ensure(cw), bits.data(), 4ull * cw, cudaMemcpyHostToDevice, s));
+      cb = c->d_ctx_bits.p;
+    }
+    const uint32_t* mb = nullptr;
+    if (metric_ids) {
+      std::vector<uint32_t> bits(2048, 0);
+      for (uint32_t i = 0; i < n_metrics; ++i) bits[metric_ids[i] >> 5] |= 1u << (metric_ids[i] & 31);
+      PSG_CUDA(cudaMemcpyAsync(c->d_metric_bits.ensure(2048), bits.data(), 4ull * 2048,
+                               cudaMemcpyHostToDevice, s));
+      mb = c->d_metric_bits.p;
+    }
+    unsigned long long* counts = c->d_counts.ensure(nr + 1);
+    launch_slice(c->pview(), c->d_slot.p, nr, cb, cw, mb, counts, nullptr, nullptr, nullptr, nullptr,
+                 nullptr, s);
+    unsigned long long* ro = c->d_row_off.ensure(nr + 1);
+    const size_t sb = exclusive_scan_u64_scratch(nr + 1);
+    PSG_CUDA(cudaMemsetAsync(counts + nr, 0, 8, s));
+    launch_exclusive_scan_u64(reinterpret_cast<const uint64_t*>(counts), reinterpret_cast<uint64_t*>(ro),
+                              nr + 1, c->scratch.ensure(sb), sb, s);
+    unsigned long long total = 0;
+    PSG_CUDA(cudaMemcpyAsync(&total, ro + nr, 8, cudaMemcpyDeviceToHost, s));
+    c->sync();
+    const bool want = row_pid || row_ctx || row_metric || row_value;
+    if (want && total) {
+      launch_slice(c->pview(), c->d_slot.p, nr, cb, cw, mb, counts, ro, c->d_row_pid.ensure(total),
+                   c->d_row_ctx.ensure(total), c->d_row_metric.ensure(total), c->d_row_value.ensure(total), s);
+      if (row_pid) PSG_CUDA(cudaMemcpyAsync(row_pid, c->d_row_pid.p, 4 * total, cudaMemcpyDeviceToHost, s));
+      if (row_ctx) PSG_CUDA(cudaMemcpyAsync(row_ctx, c->d_row_ctx.p, 4 * total, cudaMemcpyDeviceToHost, s));
+      if (row_metric)
+        PSG_CUDA(cudaMemcpyAsync(row_metric, c->d_row_metric.p, 2 * total, cudaMemcpyDeviceToHost, s));
+      if (row_value)
+        PSG_CUDA(cudaMemcpyAsync(row_value, c->d_row_value.p, 8 * total, cudaMemcpyDeviceToHost, s));
+      c->sync();
+    }
+    *n_rows = total;
+  });
+}
+
+ps_status psg_profile_outliers(psg_context* c, uint16_t metric, const uint32_t* site_ctx,
+                               uint32_t n_sites, uint32_t top_k, double z_min, psg_query_info* info) {
+  if (!c || !info || !site_ctx || n_sites == 0) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_device(c);
+    if (c->n_rank_prof == 0) fail(PS_E_INSUFFICIENT_DATA, "balance_ratio of empty vector (no rank profiles loaded)");
+    require(c->have_prof_nodes, "profile outliers need the profile -> node mapping (psg_load_profile_db or node_of_profile)");
+    invalidate_results(c);
+    std::memset(info, 0, sizeof(*info));
+    cudaStream_t s = c->stream;
+    PSG_CUDA(cudaEventRecord(c->ev[0], s));
+    c->sites.assign(site_ctx, site_ctx + n_sites);
+    PSG_CUDA(cudaMemcpyAsync(c->d_sites.ensure(n_sites), site_ctx, 4ull * n_sites, cudaMemcpyHostToDevice, s));
+    launch_profile_outliers(c->pview(), c->d_rank_slot.p, c->n_rank_prof, c->d_sites.p, n_sites, metric,
+                            c->pvals.ensure(static_cast<size_t>(c->n_rank_prof) * n_sites),
+                            c->site_ratio.ensure(n_sites), c->d_worst.ensure(2), c->d_pnode_off.p,
+                            c->d_pnode_rank.p, c->n_nodes, c->node_mean.ensure(c->n_nodes), s);
+    const size_t ssb = node_select_scratch_bytes(c->n_nodes);
+    launch_node_select(nullptr, c->n_nodes, top_k, z_min, c->node_mean.p, c->node_z.ensure(c->n_nodes),
+                       c->d_order.ensure(c->n_nodes), c->d_nsel.ensure(1), c->scratch.ensure(ssb), ssb, s);
+    const uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
+    if (nr)
+      launch_topology(c->d_order.p, c->d_nsel.p, c->d_node_rack_idx.p, c->d_node_chassis.p, c->d_uni_cnt.p,
+                      nr, c->d_rack_nodes.ensure(nr), c->rack_mask.ensure(nr), c->rack_full.ensure(nr), s);
+    PSG_CUDA(cudaEventRecord(c->ev[3], s));
+    c->sync();
+    c->have_outliers = true;
+    uint32_t w = 0;
+    PSG_CUDA(cudaMemcpy(&w, c->d_worst.p, 4, cudaMemcpyDeviceToHost));
+    PSG_CUDA(cudaMemcpy(&info->n_outliers, c->d_nsel.p, 4, cudaMemcpyDeviceToHost));
+    info->worst_site = c->sites[w];
+    PSG_CUDA(cudaMemcpy(&info->worst_ratio, c->site_ratio.p + w, 8, cudaMemcpyDeviceToHost));
+    if (nr) {
+      std::vector<uint32_t> rn(nr);
+      PSG_CUDA(cudaMemcpy(rn.data(), c->d_rack_nodes.p, 4ull * nr, cudaMemcpyDeviceToHost));
+      for (uint32_t x : rn) info->n_racks += x > 0;
+    }
+    PSG_CUDA(cudaEventElapsedTime(&info->ms_total, c->ev[0], c->ev[3]));
   });
 }
 

@@ -63,6 +63,16 @@ struct trace_view {
   uint32_t n;
 };
 
+// Profile records in HBM (profile.db bodies as SoA; store.cpp:563-571).
+struct profile_view {
+  const uint64_t* off;    // [n+1] record offsets per profile slot
+  const uint32_t* pid;    // [n] ascending profile ids
+  const uint32_t* ctx;    // [R] sorted by ctx within a profile
+  const uint16_t* metric; // [R]
+  const double* value;    // [R]
+  uint32_t n;
+};
+
 // Pass 1 (k_bounds): iteration boundaries per trace (itermodel.cpp:111-143).
 struct bound_params {
   trace_view tr;
@@ -258,9 +268,26 @@ void launch_outliers(const uint64_t* w_incl, uint32_t n_traces, uint32_t n_ctx,
                      unsigned long long* node_acc /*[n_nodes][2]*/, uint32_t* worst,
                      double* site_ratio, uint32_t phase, cudaStream_t s);
 size_t node_select_scratch_bytes(uint32_t n_nodes);
+// node means from node_acc ({Σ ns, count} per node), or given in node_mean
+// when node_acc is null; then z-scores and the (mean desc, id asc) order, cut
+// at top_k / z_min.
 void launch_node_select(const unsigned long long* node_acc, uint32_t n_nodes, uint32_t top_k,
                         double z_min, double* node_mean, double* node_z, uint32_t* order,
                         uint32_t* n_sel, void* scratch, size_t scratch_bytes, cudaStream_t s);
+// profile-record path (psg_profiles.cu)
+void launch_records_to_soa(const uint8_t* body, uint64_t n, uint32_t* ctx, uint16_t* metric,
+                           double* value, cudaStream_t s);
+void launch_records_check(const uint32_t* ctx, const uint64_t* off, uint32_t n_prof,
+                          unsigned long long* bad, cudaStream_t s);
+void launch_slice(const profile_view& pv, const uint32_t* slot, uint32_t n_req,
+                  const uint32_t* ctx_bits, uint32_t ctx_words, const uint32_t* metric_bits,
+                  unsigned long long* counts, const unsigned long long* row_off, uint32_t* out_pid,
+                  uint32_t* out_ctx, uint16_t* out_metric, double* out_value, cudaStream_t s);
+void launch_profile_outliers(const profile_view& pv, const uint32_t* rank_slot, uint32_t n_ranks,
+                             const uint32_t* site, uint32_t n_sites, uint16_t metric, double* vals,
+                             double* ratio, uint32_t* worst, const uint32_t* node_off,
+                             const uint32_t* node_rank, uint32_t n_nodes, double* node_mean,
+                             cudaStream_t s);
 void launch_topology(const uint32_t* selected, const uint32_t* n_sel, const uint32_t* node_rack_idx,
                      const uint32_t* node_chassis, const uint32_t* uni_cnt, uint32_t n_racks,
                      uint32_t* rack_nodes, unsigned long long* rack_mask,

@@ -627,9 +627,14 @@ __global__ void k_node_stats(const unsigned long long* node_acc, uint32_t n_node
   __shared__ double red[1024];
   double s = 0.0;
   for (uint32_t i = threadIdx.x; i < n_nodes; i += blockDim.x) {
-    u64 c = node_acc[2 * i + 1];
-    double m = c ? (static_cast<double>(node_acc[2 * i]) / 1e9) / static_cast<double>(c) : 0.0;
-    mean[i] = m;
+    double m;
+    if (node_acc) {
+      u64 c = node_acc[2 * i + 1];
+      m = c ? (static_cast<double>(node_acc[2 * i]) / 1e9) / static_cast<double>(c) : 0.0;
+      mean[i] = m;
+    } else {
+      m = mean[i];  // given (profile-record path)
+    }
     s += m;
   }
   red[threadIdx.x] = s;
@@ -651,7 +656,9 @@ __global__ void k_node_stats(const unsigned long long* node_acc, uint32_t n_node
   const double sd = sqrt(red[0] / static_cast<double>(n_nodes));
   for (uint32_t i = threadIdx.x; i < n_nodes; i += blockDim.x) {
     z[i] = sd > 0.0 ? (mean[i] - mu) / sd : 0.0;
-    key[i] = __double_as_longlong(mean[i]);  // means are >= 0: bit order == value order
+    // order-preserving map of doubles to unsigned keys (negative: all bits flipped)
+    const u64 bits = static_cast<u64>(__double_as_longlong(mean[i]));
+    key[i] = (bits >> 63) ? ~bits : (bits | (1ull << 63));
     ids[i] = i;
   }
 }

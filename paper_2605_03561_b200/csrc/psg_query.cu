@@ -955,17 +955,12 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           if (R.lo >= 3) f = tv[3];
           // first valid event and the successor of the last valid one (index hi)
           u64 a;
-          switch (R.hi & (RM - 1)) {  // warp-uniform; constant register indices
-            case 1: a = tv[1]; break;
-            case 2: a = tv[2]; break;
-            case 3: a = tv[3]; break;
-#if PSG_RM > 4
-            case 4: a = tv[4]; break;
-            case 5: a = tv[5]; break;
-            case 6: a = tv[6]; break;
-            case 7: a = tv[7]; break;
-#endif
-            default: a = tv[0]; break;
+          {  // warp-uniform index; constant register indices
+            const int hx = R.hi & (RM - 1);
+            a = tv[0];
+#pragma unroll
+            for (int q = 1; q < RM; ++q)
+              if (hx == q) a = tv[q];
           }
           first = __shfl_sync(FULL, f, 0);
           after = R.hi >= STEP_M ? __shfl_sync(FULL, tv[RM], 31) : __shfl_sync(FULL, a, R.hi / RM);

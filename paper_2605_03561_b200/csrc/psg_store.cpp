@@ -22,6 +22,7 @@ namespace {
 
 constexpr char k_meta_magic[4] = {'H', 'P', 'A', 'N'};
 constexpr char k_trace_magic[4] = {'H', 'P', 'T', 'R'};
+constexpr char k_profile_magic[4] = {'H', 'P', 'P', 'R'};
 constexpr uint32_t k_version = 1;
 constexpr uint64_t k_event_size = 12;
 
@@ -102,8 +103,8 @@ const trace_index_entry* trace_db::find(uint32_t pid) const {
   return (it == index.end() || it->profile_id != pid) ? nullptr : &*it;
 }
 
-void open_trace_db(const std::string& dir, trace_db& db) {
-  db.dir = dir;
+void read_meta(const std::string& dir, meta_data& meta) {
+  meta = meta_data{};
   std::ifstream mf(dir + "/meta.bin", std::ios::binary);
   if (!mf) fail(PS_E_IO, "cannot open " + dir + "/meta.bin");
   std::string bytes((std::istreambuf_iterator<char>(mf)), std::istreambuf_iterator<char>());
@@ -118,7 +119,7 @@ void open_trace_db(const std::string& dir, trace_db& db) {
     if (m.scope > 1) fail(PS_E_FORMAT, "meta.bin: bad metric scope");
     m.name = mc.str();
     m.unit = mc.str();
-    db.meta.metrics.push_back(std::move(m));
+    meta.metrics.push_back(std::move(m));
   }
   uint32_t n_profiles = mc.get<uint32_t>();
   for (uint32_t i = 0; i < n_profiles; ++i) {
@@ -128,7 +129,7 @@ void open_trace_db(const std::string& dir, trace_db& db) {
     p.thread = mc.get<int32_t>();
     p.hostname = mc.str();
     p.posix_node_id = mc.get<uint64_t>();
-    db.meta.profiles.push_back(std::move(p));
+    meta.profiles.push_back(std::move(p));
   }
   uint32_t n_ctx = mc.get<uint32_t>();
   for (uint32_t i = 0; i < n_ctx; ++i) {
@@ -137,9 +138,13 @@ void open_trace_db(const std::string& dir, trace_db& db) {
     n.parent = mc.get<uint32_t>();
     n.kind = mc.get<uint8_t>();
     n.name = mc.str();
-    db.meta.contexts.push_back(std::move(n));
+    meta.contexts.push_back(std::move(n));
   }
+}
 
+void open_trace_db(const std::string& dir, trace_db& db) {
+  db.dir = dir;
+  read_meta(dir, db.meta);
   db.map.open(dir + "/trace.db");
   cursor tc{db.map.data(), db.map.size(), 0, "trace.db"};
   tc.magic(k_trace_magic);
@@ -159,6 +164,37 @@ void open_trace_db(const std::string& dir, trace_db& db) {
       fail(PS_E_FORMAT, "trace.db: t_begin after t_end for trace " + std::to_string(e.profile_id));
     if (i > 0 && e.profile_id <= db.index[i - 1].profile_id)
       fail(PS_E_FORMAT, "trace.db: index not sorted by profile id");
+    db.index.push_back(e);
+  }
+}
+
+const profile_index_entry* profile_db::find(uint32_t pid) const {
+  auto it = std::lower_bound(index.begin(), index.end(), pid,
+                             [](const profile_index_entry& e, uint32_t x) { return e.profile_id < x; });
+  return (it == index.end() || it->profile_id != pid) ? nullptr : &*it;
+}
+
+// profile.db: magic "HPPR", u32 version, u32 count, 20-byte index entries
+// {u32 profile_id, u64 offset, u64 record_count}, then packed 14-byte records
+// (the reference's open, store.cpp:484-503, with its validation).
+void open_profile_db(const std::string& dir, profile_db& db) {
+  db.dir = dir;
+  read_meta(dir, db.meta);
+  db.map.open(dir + "/profile.db");
+  cursor pc{db.map.data(), db.map.size(), 0, "profile.db"};
+  pc.magic(k_profile_magic);
+  pc.version();
+  uint32_t count = pc.get<uint32_t>();
+  db.index.reserve(count);
+  for (uint32_t i = 0; i < count; ++i) {
+    profile_index_entry e;
+    e.profile_id = pc.get<uint32_t>();
+    e.offset = pc.get<uint64_t>();
+    e.record_count = pc.get<uint64_t>();
+    if (e.offset + e.record_count * k_record_size > db.map.size())
+      fail(PS_E_FORMAT, "profile.db: body out of bounds for profile " + std::to_string(e.profile_id));
+    if (i > 0 && e.profile_id <= db.index[i - 1].profile_id)
+      fail(PS_E_FORMAT, "profile.db: index not sorted by profile id");
     db.index.push_back(e);
   }
 }

@@ -67,8 +67,26 @@ struct trace_db {
   const trace_index_entry* find(uint32_t pid) const;
 };
 
+constexpr uint64_t k_record_size = 14;  // profile record: u32 ctx + u16 metric + f64 value
+
+struct profile_index_entry {
+  uint32_t profile_id = 0;
+  uint64_t offset = 0, record_count = 0;
+};
+
+// db_handle::open (store.cpp:436-534) restricted to meta.bin + profile.db.
+struct profile_db {
+  std::string dir;
+  meta_data meta;
+  std::vector<profile_index_entry> index;  // sorted by profile id
+  mapped_file map;
+  const profile_index_entry* find(uint32_t pid) const;
+};
+
 // Throws psg::failure(PS_E_IO / PS_E_FORMAT) like the reference's errc.
+void read_meta(const std::string& dir, meta_data& out);
 void open_trace_db(const std::string& dir, trace_db& out);
+void open_profile_db(const std::string& dir, profile_db& out);
 
 // x<rack>c<chassis>s<slot>b<blade>n<node>, strict decimal (topology.cpp:33-46).
 bool parse_node_name(const std::string& name, uint32_t* rack, uint32_t* chassis);

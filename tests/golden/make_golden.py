@@ -193,6 +193,38 @@ def congestion_fixture(name: str, ranks_per_node: int, seed: int) -> None:
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
 
 
+def profile_fixture(name: str, ranks_per_node: int, seed: int) -> None:
+    """profile.db of the aurora-like scenario with the reference's
+    ingest_profiles slices (all / filtered) and congestion_report ratios."""
+    cfg = scenarios.aurora(ranks_per_node=ranks_per_node, seed=seed)
+    with tempfile.TemporaryDirectory() as d:
+        truth = oracle.ref_generate(cfg, d)
+        meta = oracle.read_meta(d)
+        pdb = oracle.read_profile_db(d)
+        rep = json.loads(oracle.ref_congestion_report(d))
+        pids = [p for (p, _, _) in meta["profiles"]]
+        some = pids[::7]
+        ctxs = [0, 1] + list(truth["callsite_ctx"])
+        all_rows = oracle.ref_slices(d, some)
+        filt = oracle.ref_slices(d, some, sorted(ctxs), [1])
+        out = {
+            "body": pdb["body"], "rec_off": pdb["rec_off"], "pid": pdb["pid"],
+            "prof_pid": np.array(pids, np.uint32),
+            "prof_rank": np.array([r for (_, r, _) in meta["profiles"]], np.int32),
+            "prof_host": np.array([h for (_, _, h) in meta["profiles"]]),
+            "req_pids": np.array(some, np.uint32), "req_ctx": np.array(sorted(ctxs), np.uint32),
+            "site_ctx": np.array(truth["callsite_ctx"], np.uint32),
+            "ref_ratio": np.array([s["balance_ratio"] for s in rep["callsites"]], np.float64),
+            "ref_worst_ctx": np.array([rep["worst"]["ctx_id"]], np.uint32),
+            "ref_outliers": np.array(sorted(rep["outlier_group"]["hostnames"])),
+        }
+        for k, v in all_rows.items():
+            out["all_" + k] = v
+        for k, v in filt.items():
+            out["filt_" + k] = v
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+
+
 def main() -> None:
     if not oracle.ref_available():
         raise SystemExit("oracle/_ref missing: run oracle/build_ref.sh first")
@@ -205,6 +237,7 @@ def main() -> None:
         random_fixture(f"random_{s}", s)
     anchor_cases()
     congestion_fixture("congestion_rpn2", ranks_per_node=2, seed=2025)
+    profile_fixture("profiles_rpn1", ranks_per_node=1, seed=2025)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f"{f:28s} {os.path.getsize(os.path.join(HERE, f)):8d} B")

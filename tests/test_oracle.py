@@ -235,3 +235,33 @@ def test_suggest_anchor_oracle_matches_reference():
     for i in range(int(z["n_cases"][0])):
         tr = {k: z[f"case{i}_{k}"] for k in ("ts", "ctx", "off", "t_end", "pid")}
         assert oracle.suggest_anchor(tr, z["parent"], 0) == int(z[f"case{i}_anchor"][0]), i
+
+
+def _fixture_pdb(g: dict) -> dict:
+    rec = np.dtype([("ctx", "<u4"), ("metric", "<u2"), ("value", "<f8")])
+    r = np.frombuffer(g["body"].tobytes(), dtype=rec)
+    return {"pid": g["pid"], "rec_off": g["rec_off"], "ctx": r["ctx"].astype(np.uint32),
+            "metric": r["metric"].astype(np.uint16), "value": r["value"].astype(np.float64)}
+
+
+def test_profile_slice_oracle_matches_ingest_profiles():
+    """read_slices / ingest_profiles restated (oracle.slices) == the reference's
+    own rows, all contexts and a keep set + metric filter (tests/golden)."""
+    g = load("profiles_rpn1")
+    pdb = _fixture_pdb(g)
+    for pre, cx, mt in (("all_", None, None), ("filt_", g["req_ctx"], [1])):
+        o = oracle.slices(pdb, g["req_pids"], cx, mt)
+        for k in ("pid", "ctx", "metric", "value"):
+            assert np.array_equal(o[k], g[pre + k]), f"{pre}{k}"
+
+
+def test_profile_congestion_oracle_matches_reference():
+    """rank_vector + balance_ratio + node_correlate over profile records ==
+    congestion_report's call-site ratios and worst site (tests/golden)."""
+    g = load("profiles_rpn1")
+    pdb = _fixture_pdb(g)
+    meta = {"profiles": list(zip(g["prof_pid"].tolist(), g["prof_rank"].tolist(),
+                                 g["prof_host"].tolist()))}
+    o = oracle.profile_sites(pdb, meta, 1, g["site_ctx"])
+    assert_rel(o["ratio"], g["ref_ratio"], 1e-12, "balance ratios")
+    assert int(g["site_ctx"][o["worst"]]) == int(g["ref_worst_ctx"][0])
