@@ -302,17 +302,28 @@ void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_r
 __global__ void k_layout_prep(const uint32_t* iter_count, uint32_t n, uint32_t nn, uint32_t nnp,
                               uint64_t* kept, uint64_t* cells, uint64_t* iters,
                               unsigned long long* summary) {
-  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  uint32_t it = iter_count[t];
-  kept[t] = it > 0 ? 1 : 0;
-  cells[t] = (static_cast<uint64_t>(it) * nnp + 3) & ~3ull;
-  iters[t] = it;
-  if (it > 0) {
-    atomicAdd(summary + 0, 1ull);
-    atomicMin(summary + 1, static_cast<unsigned long long>(it));
-    atomicAdd(summary + 2, static_cast<unsigned long long>(it) * nn);
-    atomicAdd(summary + 4, (static_cast<unsigned long long>(it) * nnp + 3) & ~3ull);
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // the grid covers whole warps
+  const uint32_t it = t < n ? iter_count[t] : 0;
+  if (t < n) {
+    kept[t] = it > 0 ? 1 : 0;
+    cells[t] = (static_cast<uint64_t>(it) * nnp + 3) & ~3ull;
+    iters[t] = it;
+  }
+  // warp-aggregated summary atomics: kept count, min iterations, cells, storage cells
+  unsigned long long k1 = it > 0 ? 1ull : 0ull, m1 = it > 0 ? it : 0xFFFFFFFFull;
+  unsigned long long c2 = static_cast<unsigned long long>(it) * nn;
+  unsigned long long c4 = (static_cast<unsigned long long>(it) * nnp + 3) & ~3ull;
+  for (int d = 16; d > 0; d >>= 1) {
+    k1 += __shfl_xor_sync(FULL, k1, d);
+    m1 = min(m1, __shfl_xor_sync(FULL, m1, d));
+    c2 += __shfl_xor_sync(FULL, c2, d);
+    c4 += __shfl_xor_sync(FULL, c4, d);
+  }
+  if ((threadIdx.x & 31) == 0 && k1) {
+    atomicAdd(summary + 0, k1);
+    atomicMin(summary + 1, m1);
+    atomicAdd(summary + 2, c2);
+    atomicAdd(summary + 4, c4);
   }
 }
 
@@ -400,23 +411,53 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
 // ===========================================================================
 // K6b: within-rank CV mean over kept traces (fixed-order tree per node), then
 // the per-node savings / across-rank CV rows.
-__global__ void k_within_reduce(const double* within_cv, const uint8_t* within_ok, uint32_t n_kept,
-                                uint32_t nn, double* out_sum, double* out_bad) {
-  const uint32_t n = blockIdx.x;
-  double s = 0.0, bad = 0.0;
-  for (uint32_t t = threadIdx.x; t < n_kept; t += blockDim.x) {
-    s += within_cv[static_cast<size_t>(t) * nn + n];
-    bad += within_ok[static_cast<size_t>(t) * nn + n] ? 0.0 : 1.0;
+// Stage 1: one CTA per tile of kept traces.  Threads cover (sub-row j, node
+// n) so that consecutive threads read consecutive cells of a trace's row
+// (coalesced); each thread sums its node over the tile's traces j, j + S, ...
+// in order, and sub-row partials are added in fixed order: deterministic.
+__global__ void __launch_bounds__(256) k_within_partial(const double* within_cv,
+                                                        const uint8_t* within_ok, uint32_t n_kept,
+                                                        uint32_t nn, uint32_t per_tile,
+                                                        double* part /*[tiles][2][nn]*/) {
+  __shared__ double s_sum[256], s_bad[256];
+  const uint32_t ne = min(nn, blockDim.x), S = blockDim.x / ne;
+  const uint32_t j = threadIdx.x / ne, nl = threadIdx.x % ne;
+  const uint32_t t0 = blockIdx.x * per_tile, t1 = min(n_kept, t0 + per_tile);
+  for (uint32_t nb = 0; nb < nn; nb += ne) {
+    const uint32_t n = nb + nl;
+    double sm = 0.0, bad = 0.0;
+    if (j < S && n < nn)
+      for (uint32_t t = t0 + j; t < t1; t += S) {
+        sm += within_cv[static_cast<size_t>(t) * nn + n];
+        bad += within_ok[static_cast<size_t>(t) * nn + n] ? 0.0 : 1.0;
+      }
+    s_sum[threadIdx.x] = sm;
+    s_bad[threadIdx.x] = bad;
+    __syncthreads();
+    if (j == 0 && n < nn) {
+      for (uint32_t q = 1; q < S; ++q) {
+        sm += s_sum[q * ne + nl];
+        bad += s_bad[q * ne + nl];
+      }
+      part[(static_cast<size_t>(blockIdx.x) * 2) * nn + n] = sm;
+      part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * nn + n] = bad;
+    }
+    __syncthreads();
   }
-  typedef cub::BlockReduce<double, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  double ts = BR(tmp).Sum(s);
-  __syncthreads();
-  double tb = BR(tmp).Sum(bad);
-  if (threadIdx.x == 0) {
-    out_sum[n] = ts;
-    out_bad[n] = tb;
+}
+
+// Stage 2: per node, the tile partials in tile order.
+__global__ void k_within_finish(const double* part, uint32_t tiles, uint32_t nn, double* out_sum,
+                                double* out_bad) {
+  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= nn) return;
+  double sm = 0.0, bad = 0.0;
+  for (uint32_t b = 0; b < tiles; ++b) {
+    sm += part[(static_cast<size_t>(b) * 2) * nn + n];
+    bad += part[(static_cast<size_t>(b) * 2 + 1) * nn + n];
   }
+  out_sum[n] = sm;
+  out_bad[n] = bad;
 }
 
 // One CTA per node: the per-iteration terms are summed with a fixed-order
@@ -474,8 +515,13 @@ void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long 
   double* wsum = node_out + static_cast<size_t>(nn) * 8;
   double* wbad = wsum + nn;
   if (within_cv) {
-    k_within_reduce<<<nn, 256, 0, s>>>(within_cv, within_ok, n_kept_local, nn, wsum, wbad);
-    count_launch();
+    // tile partials live after the bad counts in node_out (sized by the caller)
+    const uint32_t tiles = std::max(1u, std::min(148u, (n_kept_local + 63) / 64));
+    const uint32_t per_tile = (std::max(1u, n_kept_local) + tiles - 1) / tiles;
+    double* part = wbad + nn;
+    k_within_partial<<<tiles, 256, 0, s>>>(within_cv, within_ok, n_kept_local, nn, per_tile, part);
+    k_within_finish<<<(nn + 127) / 128, 128, 0, s>>>(part, tiles, nn, wsum, wbad);
+    count_launch(2);
     PSG_CUDA(cudaGetLastError());
   }
   if (x_sum) {
