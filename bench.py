@@ -260,6 +260,11 @@ def main():
         ctx.export_aos(host.data_ptr())
         idx = ctx.index()
         off, pids, tend = idx["off"], idx["pid"], idx["t_end"]
+        # pinned host buffers for the window copy-out (allocated once, reused)
+        n_cells = n_local * sh["n_ctx"]
+        pin = {k: torch.empty(n_cells * 8, dtype=torch.uint8, pin_memory=True)
+               for k, _ in Context.WINDOW_DTYPES}
+        wout = {k: pin[k].numpy().view(dt).reshape(n_local, sh["n_ctx"]) for k, dt in Context.WINDOW_DTYPES}
         d2h = 0
         secs = []
         for i in range(args.e2e_steps + 1):
@@ -269,7 +274,7 @@ def main():
             ctx.load_aos(host.data_ptr(), off, pids, tend)
             ctx.set_nodes(node_of, n_nodes, 4000 + node // 32, (node // 8) % 4)
             inf = ctx.query(**q)
-            w = ctx.window()
+            w = ctx.window(wout)
             st = ctx.stats(1.0)
             ou = ctx.outliers(n_nodes)
             cb = ctx.cube(with_cells=False)

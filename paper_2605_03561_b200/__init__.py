@@ -179,12 +179,19 @@ class Context:
         self._flags = flags
         return self.info
 
-    def window(self) -> dict:
+    WINDOW_DTYPES = [("count", np.uint64), ("sum", np.int64), ("min", np.int64), ("max", np.int64),
+                     ("mean", np.float64), ("excl", np.int64), ("incl", np.int64)]
+
+    def window(self, out: Optional[dict] = None) -> dict:
+        """Dense [trace][ctx] window aggregates; `out` may supply the seven host
+        arrays (e.g. views of pinned buffers, for a fast copy-out)."""
         sh = self.shard()
         shape = (sh["n_traces"], sh["n_ctx"])
-        out = {k: np.empty(shape, dt) for k, dt in [
-            ("count", np.uint64), ("sum", np.int64), ("min", np.int64), ("max", np.int64),
-            ("mean", np.float64), ("excl", np.int64), ("incl", np.int64)]}
+        if out is None:
+            out = {k: np.empty(shape, dt) for k, dt in self.WINDOW_DTYPES}
+        for k, dt in self.WINDOW_DTYPES:
+            a = out[k]
+            assert a.dtype == dt and a.size == shape[0] * shape[1] and a.flags.c_contiguous, k
         check(self.lib.psg_get_window(
             self.h, _ptr(out["count"], C.c_uint64), _ptr(out["sum"], C.c_int64),
             _ptr(out["min"], C.c_int64), _ptr(out["max"], C.c_int64),

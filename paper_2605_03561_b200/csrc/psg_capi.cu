@@ -183,6 +183,8 @@ struct psg_context {
   dbuf<uint8_t> d_stage;
   uint8_t* pinned[3] = {nullptr, nullptr, nullptr};  // pageable-source staging ring
   cudaEvent_t pinned_ev[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;  // H2D of pinned trace bodies (load_aos)
+  cudaEvent_t stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
   // nodes / topology
   uint32_t n_nodes = 0;
@@ -274,6 +276,9 @@ struct psg_context {
       if (pinned_ev[i]) cudaEventDestroy(pinned_ev[i]);
       if (pinned[i]) cudaFreeHost(pinned[i]);
     }
+    for (auto& e : stage_ev)
+      if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (comm) nccl().comm_destroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -517,13 +522,30 @@ void load_aos(psg_context* c, const uint8_t* body, uint64_t n_events) {
   const uint64_t chunk_ev = 4ull << 24;  // 64 Mi events = 768 MB per chunk
   const uint64_t chunk_bytes = chunk_ev * 12;
   uint8_t* stage = c->d_stage.ensure(std::min<uint64_t>(2 * chunk_bytes, n_events * 12 + 64));
+  const bool two = c->d_stage.n >= 2 * chunk_bytes;
+  // H2D copies on their own stream, transposes on the context's stream: copy
+  // i + 1 runs while transpose i does (two staging slots, events in between),
+  // so the copy engine stays busy at the PCIe rate
+  if (!c->copy_stream) {
+    PSG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : c->stage_ev) PSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t* copied = c->stage_ev;      // [2] slot filled
+  cudaEvent_t* consumed = c->stage_ev + 2;  // [2] slot transposed
+  PSG_CUDA(cudaEventRecord(consumed[0], c->stream));  // earlier work on the staging buffer
+  PSG_CUDA(cudaEventRecord(consumed[1], c->stream));
   uint64_t done = 0;
   int slot = 0;
   while (done < n_events) {
     uint64_t ev = std::min(chunk_ev, n_events - done);
-    uint8_t* dst = stage + (c->d_stage.n >= 2 * chunk_bytes ? slot * chunk_bytes : 0);
-    PSG_CUDA(cudaMemcpyAsync(dst, body + done * 12, ev * 12, cudaMemcpyHostToDevice, c->stream));
+    const int sl = two ? slot : 0;
+    uint8_t* dst = stage + sl * chunk_bytes;
+    PSG_CUDA(cudaStreamWaitEvent(c->copy_stream, consumed[sl], 0));
+    PSG_CUDA(cudaMemcpyAsync(dst, body + done * 12, ev * 12, cudaMemcpyHostToDevice, c->copy_stream));
+    PSG_CUDA(cudaEventRecord(copied[sl], c->copy_stream));
+    PSG_CUDA(cudaStreamWaitEvent(c->stream, copied[sl], 0));
     launch_aos_to_soa(dst, ev, c->d_ts.p + done, c->d_ctx.p + done, c->stream);
+    PSG_CUDA(cudaEventRecord(consumed[sl], c->stream));
     done += ev;
     slot ^= 1;
   }

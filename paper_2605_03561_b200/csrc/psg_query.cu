@@ -46,6 +46,9 @@ typedef unsigned __int128 u128;
 #ifndef PSG_RM
 #define PSG_RM 8
 #endif
+#ifndef PSG_PIPE_CROSS
+#define PSG_PIPE_CROSS 1  // the register pipeline also runs across a chunk flush
+#endif
 #ifndef PSG_PIPE
 #define PSG_PIPE 1  // register software pipeline of block-step loads in k_trace_query
 #endif
@@ -910,7 +913,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         if (lane == 31) nf = pnf;
         tv[RM] = nf;
       }
-      if (lim < n_t) {
+      if (lim < n_t && (PSG_PIPE_CROSS || lim < E1)) {
         pf_pos = (b + lim) & ~3ull;
         load_step(p.tr, pf_pos + static_cast<u64>(R.lb), pf_pos, lane, pts, pcx, pnf);
       } else {
