@@ -270,6 +270,56 @@ ps_status psg_slice(psg_context* ctx, const uint32_t* pids, uint32_t n_pids, con
 ps_status psg_profile_outliers(psg_context* ctx, uint16_t metric, const uint32_t* site_ctx,
                                uint32_t n_sites, uint32_t top_k, double z_min, psg_query_info* info);
 
+/* ---- frame operators (frame.hpp) ------------------
+ * The reference's columnar engine for numeric columns on the device, with its
+ * determinism contract (frame.hpp:3-10): every result is the reference's,
+ * bit for bit.  Column data pointers are DEVICE pointers (e.g. CUDA tensors);
+ * n = rows.  Index outputs (perm, starts, idx, lidx, ridx) are device u64. */
+enum { PSG_I64 = 0, PSG_U64 = 1, PSG_F64 = 2 };                      /* frame::dtype */
+enum { PSG_LT = 0, PSG_LE = 1, PSG_EQ = 2, PSG_GE = 3, PSG_GT = 4, PSG_NE = 5 }; /* frame::cmp_op */
+enum { PSG_AGG_SUM = 0, PSG_AGG_MIN = 1, PSG_AGG_MAX = 2, PSG_AGG_MEAN = 3, PSG_AGG_COUNT = 4 };
+typedef struct psg_col {
+  uint32_t dtype;
+  const void* data;
+} psg_col;
+/* sort's permutation (frame.cpp:62-117, 410-422): stable multi-key argsort,
+ * ascending[k] = 0 for a descending key (NULL: all ascending). */
+ps_status psg_frame_argsort(psg_context* ctx, const psg_col* keys, uint32_t n_keys,
+                            const uint8_t* ascending, uint64_t n, uint64_t* perm);
+/* group_aggregate's grouping (frame.cpp:290-318): perm[n] sorted by the key
+ * tuple, starts[*n_groups] = first sorted position of each group. */
+ps_status psg_frame_group(psg_context* ctx, const psg_col* keys, uint32_t n_keys, uint64_t n,
+                          uint64_t* perm, uint64_t* starts, uint64_t* n_groups);
+/* one aggregate column per group (frame.cpp:320-392): sum / min / max in the
+ * source dtype (integer sums wrap), mean in f64, count in u64; NaN in an f64
+ * source is PS_E_INVALID_ARGUMENT (require_numeric). */
+ps_status psg_frame_group_agg(psg_context* ctx, psg_col src, const uint64_t* perm,
+                              const uint64_t* starts, uint64_t n_groups, uint64_t n, uint32_t fn,
+                              void* out);
+/* out[i] = src[idx[i]] (any 8-byte dtype). */
+ps_status psg_frame_gather(psg_context* ctx, psg_col src, const uint64_t* idx, uint64_t n_idx,
+                           void* out);
+/* filter (frame.cpp:424-470): idx[*n_out] = rows with (col <op> *literal), in
+ * order; literal is a host i64 / u64 / f64 of the column's dtype. */
+ps_status psg_frame_filter(psg_context* ctx, psg_col col, uint32_t op, const void* literal,
+                           uint64_t n, uint64_t* idx, uint64_t* n_out);
+/* merge (frame.cpp:472-572): inner-join row pairs ordered by (left row, right
+ * row).  *n_out is always set; the pairs are written when it fits capacity. */
+ps_status psg_frame_merge(psg_context* ctx, const psg_col* lkeys, const psg_col* rkeys,
+                          uint32_t n_keys, uint64_t n_left, uint64_t n_right, uint64_t capacity,
+                          uint64_t* lidx, uint64_t* ridx, uint64_t* n_out);
+/* vector_add, in_place_multiply, scalar_compare (0/1 i64), reduce_sum and
+ * cumulative_sum (fold-left in 4096-element blocks, then across blocks;
+ * frame.cpp:574-657) over f64 columns. */
+ps_status psg_frame_vector_add(psg_context* ctx, const double* a, const double* b, uint64_t n,
+                               double* out);
+ps_status psg_frame_multiply(psg_context* ctx, const double* a, double scalar, uint64_t n,
+                             double* out);
+ps_status psg_frame_scalar_compare(psg_context* ctx, const double* a, uint32_t op, double scalar,
+                                   uint64_t n, int64_t* out);
+ps_status psg_frame_reduce_sum(psg_context* ctx, const double* a, uint64_t n, double* result);
+ps_status psg_frame_cumsum(psg_context* ctx, const double* a, uint64_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -411,3 +411,125 @@ def read_meta(db: str) -> dict:
         u(np.uint32, 4); parent.append(u(np.uint32, 4)); u(np.uint8, 1); names.append(s())
     return {"parent": np.array(parent, np.uint32), "names": names, "profiles": profiles,
             "metrics": metrics}
+
+
+# ---- frame operators (frame.cpp) --------------------------------------------
+_FRAME_DT = {np.dtype(np.int64): 0, np.dtype(np.uint64): 1, np.dtype(np.float64): 2}
+FRAME_OPS = {"lt": 0, "le": 1, "eq": 2, "ge": 3, "gt": 4, "ne": 5}
+FRAME_AGGS = {"sum": 0, "min": 1, "max": 2, "mean": 3, "count": 4}
+
+
+def _ptrs(cols):
+    arr = (C.c_void_p * max(1, len(cols)))(*[c.ctypes.data for c in cols])
+    dts = (C.c_int * max(1, len(cols)))(*[_FRAME_DT[c.dtype] for c in cols])
+    return arr, dts
+
+
+def ref_frame_sort(keys, ascending=None, jobs: int = 1) -> np.ndarray:
+    """The reference's frame::sort permutation (oracle/_ref)."""
+    keys = [np.ascontiguousarray(k) for k in keys]
+    n = len(keys[0])
+    arr, dts = _ptrs(keys)
+    asc = None if ascending is None else np.array([1 if a else 0 for a in ascending], np.uint8)
+    perm = np.empty(max(1, n), np.uint64)
+    _chk(ref().refh_frame_sort(C.c_uint64(n), len(keys), dts, arr,
+                               asc.ctypes.data_as(C.c_void_p) if asc is not None else None, jobs,
+                               perm.ctypes.data_as(C.c_void_p)))
+    return perm[:n]
+
+
+def ref_frame_group(keys, src, fn: str, jobs: int = 1):
+    keys = [np.ascontiguousarray(k) for k in keys]
+    src = np.ascontiguousarray(src)
+    n = len(src)
+    arr, dts = _ptrs(keys)
+    ng = C.c_uint64()
+    lib = ref()
+    _chk(lib.refh_frame_group(C.c_uint64(n), len(keys), dts, arr, _FRAME_DT[src.dtype], C.c_void_p(src.ctypes.data),
+                              FRAME_AGGS[fn], jobs, C.byref(ng), None, None))
+    g = ng.value
+    kout = [np.empty(max(1, g), k.dtype) for k in keys]
+    odt = np.float64 if fn == "mean" else (np.uint64 if fn == "count" else src.dtype)
+    agg = np.empty(max(1, g), odt)
+    karr = (C.c_void_p * max(1, len(keys)))(*[k.ctypes.data for k in kout])
+    _chk(lib.refh_frame_group(C.c_uint64(n), len(keys), dts, arr, _FRAME_DT[src.dtype], C.c_void_p(src.ctypes.data),
+                              FRAME_AGGS[fn], jobs, C.byref(ng), karr, C.c_void_p(agg.ctypes.data)))
+    return [k[:g] for k in kout], agg[:g]
+
+
+def ref_frame_filter(col, op: str, literal, jobs: int = 1) -> np.ndarray:
+    col = np.ascontiguousarray(col)
+    lit = np.array([literal], col.dtype)
+    m = C.c_uint64()
+    idx = np.empty(max(1, len(col)), np.uint64)
+    _chk(ref().refh_frame_filter(C.c_uint64(len(col)), _FRAME_DT[col.dtype], C.c_void_p(col.ctypes.data),
+                                 FRAME_OPS[op], C.c_void_p(lit.ctypes.data), jobs, C.byref(m),
+                                 C.c_void_p(idx.ctypes.data)))
+    return idx[:m.value]
+
+
+def ref_frame_merge(lkeys, rkeys, jobs: int = 1):
+    lkeys = [np.ascontiguousarray(k) for k in lkeys]
+    rkeys = [np.ascontiguousarray(k) for k in rkeys]
+    la, dts = _ptrs(lkeys)
+    ra, _ = _ptrs(rkeys)
+    m = C.c_uint64()
+    lib = ref()
+    nl, nr = len(lkeys[0]), len(rkeys[0])
+    _chk(lib.refh_frame_merge(C.c_uint64(nl), C.c_uint64(nr), len(lkeys), dts, la, ra, jobs, C.byref(m), None, None))
+    li = np.empty(max(1, m.value), np.uint64)
+    ri = np.empty(max(1, m.value), np.uint64)
+    _chk(lib.refh_frame_merge(C.c_uint64(nl), C.c_uint64(nr), len(lkeys), dts, la, ra, jobs, C.byref(m),
+                              C.c_void_p(li.ctypes.data), C.c_void_p(ri.ctypes.data)))
+    return li[:m.value], ri[:m.value]
+
+
+def ref_frame_vec(op: str, a, b=None, scalar: float = 0.0, cmp: str = "lt", jobs: int = 1):
+    a = np.ascontiguousarray(a, np.float64)
+    code = {"vector_add": 0, "multiply": 1, "scalar_compare": 2, "cumsum": 3, "reduce_sum": 4}[op]
+    out = np.empty(max(1, len(a)), np.int64 if op == "scalar_compare" else np.float64)
+    bb = np.ascontiguousarray(b if b is not None else a, np.float64)
+    lib = ref()
+    lib.refh_frame_vec.argtypes = [C.c_int, C.c_uint64, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_uint,
+                                   C.c_void_p]
+    _chk(lib.refh_frame_vec(code, len(a), a.ctypes.data, bb.ctypes.data, scalar, FRAME_OPS[cmp], jobs,
+                            out.ctypes.data))
+    return out[0] if op == "reduce_sum" else out[:len(a)]
+
+
+# CPU restatement (test infrastructure), pinned to the reference by tests/test_oracle.py
+def frame_key(col: np.ndarray, descending: bool = False) -> np.ndarray:
+    """Order-preserving u64 key (frame.cpp:19-25: NaN above every number and
+    equal to itself; -0 == +0)."""
+    if col.dtype == np.int64:
+        k = col.view(np.uint64) ^ np.uint64(1 << 63)
+    elif col.dtype == np.uint64:
+        k = col.copy()
+    else:
+        v = np.where(col == 0.0, 0.0, col)
+        b = v.view(np.uint64)
+        k = np.where(b >> np.uint64(63), ~b, b | np.uint64(1 << 63))
+        k = np.where(np.isnan(col), np.uint64(~np.uint64(0)), k)
+    return ~k if descending else k
+
+
+def frame_argsort(keys, ascending=None) -> np.ndarray:
+    ks = [frame_key(k, ascending is not None and not ascending[i]) for i, k in enumerate(keys)]
+    return np.lexsort(ks[::-1]).astype(np.uint64)  # stable; keys[0] most significant
+
+
+def frame_block_scan(a: np.ndarray):
+    """reduce_sum and cumulative_sum (frame.cpp:599-647): fold left inside
+    4096-element blocks, then across the block sums."""
+    a = np.asarray(a, np.float64)
+    out = np.empty_like(a)
+    blocks = [a[i:i + 4096] for i in range(0, len(a), 4096)]
+    sums = [np.cumsum(b)[-1] for b in blocks]
+    carry = 0.0
+    total = 0.0
+    for i, b in enumerate(blocks):
+        run = np.cumsum(b)
+        out[i * 4096:i * 4096 + len(b)] = run if i == 0 else carry + run
+        total = sums[0] if i == 0 else total + sums[i]
+        carry = total
+    return (total if len(a) else 0.0), out

@@ -456,4 +456,125 @@ double refh_time_congestion(const char* dir, unsigned jobs, unsigned repeat) {
   return t;
 }
 
+// ---- frame operators (frame.cpp) on raw columns: dtype 0 i64, 1 u64, 2 f64 ----
+namespace {
+frame::column make_col(const std::string& name, int dt, const void* data, uint64_t n) {
+  if (dt == 0) {
+    const int64_t* p = static_cast<const int64_t*>(data);
+    return frame::column::of_i64(name, std::vector<int64_t>(p, p + n));
+  }
+  if (dt == 1) {
+    const uint64_t* p = static_cast<const uint64_t*>(data);
+    return frame::column::of_u64(name, std::vector<uint64_t>(p, p + n));
+  }
+  const double* p = static_cast<const double*>(data);
+  return frame::column::of_f64(name, std::vector<double>(p, p + n));
+}
+std::vector<uint64_t> iota_u64(uint64_t n) {
+  std::vector<uint64_t> v(n);
+  for (uint64_t i = 0; i < n; ++i) v[i] = i;
+  return v;
+}
+void copy_col(const frame::column& c, void* out) {
+  switch (c.type()) {
+    case frame::dtype::i64: std::memcpy(out, c.i64s().data(), 8 * c.size()); break;
+    case frame::dtype::u64: std::memcpy(out, c.u64s().data(), 8 * c.size()); break;
+    case frame::dtype::f64: std::memcpy(out, c.f64s().data(), 8 * c.size()); break;
+    default: throw std::runtime_error("string column");
+  }
+}
+frame::backend be_of(unsigned jobs) { return jobs > 1 ? frame::backend::par(jobs) : frame::backend::seq(); }
+}  // namespace
+
+// frame::sort -> the permutation (gathered row ids)
+int refh_frame_sort(uint64_t n, uint32_t nk, const int* dts, const void* const* keys, const uint8_t* asc,
+                    unsigned jobs, uint64_t* perm) {
+  return guarded([&] {
+    frame::table t;
+    std::vector<std::string> names;
+    std::vector<bool> a;
+    for (uint32_t k = 0; k < nk; ++k) {
+      names.push_back("k" + std::to_string(k));
+      t.add(make_col(names.back(), dts[k], keys[k], n));
+      a.push_back(asc ? asc[k] != 0 : true);
+    }
+    t.add(frame::column::of_u64("_row", iota_u64(n)));
+    frame::table o = frame::sort(t, names, asc ? a : std::vector<bool>{}, be_of(jobs));
+    copy_col(o.col("_row"), perm);
+  });
+}
+
+// frame::group_aggregate with one aggregate; outputs the group keys' first
+// key column as row ids of the group heads is not available, so the keys are
+// returned as columns (each 8 bytes) plus the aggregate column
+int refh_frame_group(uint64_t n, uint32_t nk, const int* dts, const void* const* keys, int sdt,
+                     const void* src, int fn, unsigned jobs, uint64_t* n_groups, void* const* key_out,
+                     void* agg_out) {
+  return guarded([&] {
+    frame::table t;
+    std::vector<std::string> names;
+    for (uint32_t k = 0; k < nk; ++k) {
+      names.push_back("k" + std::to_string(k));
+      t.add(make_col(names.back(), dts[k], keys[k], n));
+    }
+    t.add(make_col("v", sdt, src, n));
+    const frame::agg_fn fns[5] = {frame::agg_fn::sum, frame::agg_fn::min, frame::agg_fn::max,
+                                  frame::agg_fn::mean, frame::agg_fn::count};
+    frame::table o = frame::group_aggregate(t, names, {{"v", fns[fn]}}, be_of(jobs));
+    *n_groups = o.n_rows();
+    if (key_out)
+      for (uint32_t k = 0; k < nk; ++k) copy_col(o.col(names[k]), key_out[k]);
+    if (agg_out) copy_col(o.columns().back(), agg_out);
+  });
+}
+
+int refh_frame_filter(uint64_t n, int dt, const void* col, int op, const void* lit, unsigned jobs,
+                      uint64_t* n_out, uint64_t* idx) {
+  return guarded([&] {
+    frame::table t;
+    t.add(make_col("c", dt, col, n));
+    t.add(frame::column::of_u64("_row", iota_u64(n)));
+    frame::literal l;
+    if (dt == 0) l = *static_cast<const int64_t*>(lit);
+    else if (dt == 1) l = *static_cast<const uint64_t*>(lit);
+    else l = *static_cast<const double*>(lit);
+    frame::table o = frame::filter(t, "c", static_cast<frame::cmp_op>(op), l, be_of(jobs));
+    *n_out = o.n_rows();
+    if (idx) copy_col(o.col("_row"), idx);
+  });
+}
+
+int refh_frame_merge(uint64_t nl, uint64_t nr, uint32_t nk, const int* dts, const void* const* lkeys,
+                     const void* const* rkeys, unsigned jobs, uint64_t* n_out, uint64_t* lidx, uint64_t* ridx) {
+  return guarded([&] {
+    frame::table l, r;
+    std::vector<std::string> names;
+    for (uint32_t k = 0; k < nk; ++k) {
+      names.push_back("k" + std::to_string(k));
+      l.add(make_col(names.back(), dts[k], lkeys[k], nl));
+      r.add(make_col(names.back(), dts[k], rkeys[k], nr));
+    }
+    l.add(frame::column::of_u64("_l", iota_u64(nl)));
+    r.add(frame::column::of_u64("_r", iota_u64(nr)));
+    frame::table o = frame::merge(l, r, names, be_of(jobs));
+    *n_out = o.n_rows();
+    if (lidx) copy_col(o.col("_l"), lidx);
+    if (ridx) copy_col(o.col("_r"), ridx);
+  });
+}
+
+// op 0 vector_add, 1 in_place_multiply, 2 scalar_compare (cmp), 3 cumulative_sum, 4 reduce_sum
+int refh_frame_vec(int op, uint64_t n, const double* a, const double* b, double scalar, int cmp, unsigned jobs,
+                   void* out) {
+  return guarded([&] {
+    frame::column ca = frame::column::of_f64("a", std::vector<double>(a, a + n));
+    frame::backend bk = be_of(jobs);
+    if (op == 0) copy_col(frame::vector_add(ca, frame::column::of_f64("b", std::vector<double>(b, b + n)), bk), out);
+    else if (op == 1) copy_col(frame::in_place_multiply(ca, scalar, bk), out);
+    else if (op == 2) copy_col(frame::scalar_compare(ca, static_cast<frame::cmp_op>(cmp), scalar, bk), out);
+    else if (op == 3) copy_col(frame::cumulative_sum(ca, bk), out);
+    else *static_cast<double*>(out) = frame::reduce_sum(ca, bk);
+  });
+}
+
 }  // extern "C"

@@ -60,6 +60,10 @@ class QuerySpec(C.Structure):
     ]
 
 
+class PsgCol(C.Structure):
+    _fields_ = [("dtype", C.c_uint32), ("data", C.c_void_p)]
+
+
 class QueryInfo(C.Structure):
     _fields_ = [
         ("n_window_groups", C.c_uint64), ("n_window_rows", C.c_uint64),
@@ -116,6 +120,18 @@ _SIGS = {
                             U16P, F64P]),
     "psg_profile_outliers": (C.c_int, [P, C.c_uint16, U32P, C.c_uint32, C.c_uint32, C.c_double,
                                        C.POINTER(QueryInfo)]),
+    "psg_frame_argsort": (C.c_int, [P, C.POINTER(PsgCol), C.c_uint32, U8P, C.c_uint64, P]),
+    "psg_frame_group": (C.c_int, [P, C.POINTER(PsgCol), C.c_uint32, C.c_uint64, P, P, U64P]),
+    "psg_frame_group_agg": (C.c_int, [P, PsgCol, P, P, C.c_uint64, C.c_uint64, C.c_uint32, P]),
+    "psg_frame_gather": (C.c_int, [P, PsgCol, P, C.c_uint64, P]),
+    "psg_frame_filter": (C.c_int, [P, PsgCol, C.c_uint32, P, C.c_uint64, P, U64P]),
+    "psg_frame_merge": (C.c_int, [P, C.POINTER(PsgCol), C.POINTER(PsgCol), C.c_uint32, C.c_uint64,
+                                  C.c_uint64, C.c_uint64, P, P, U64P]),
+    "psg_frame_vector_add": (C.c_int, [P, P, P, C.c_uint64, P]),
+    "psg_frame_multiply": (C.c_int, [P, P, C.c_double, C.c_uint64, P]),
+    "psg_frame_scalar_compare": (C.c_int, [P, P, C.c_uint32, C.c_double, C.c_uint64, P]),
+    "psg_frame_reduce_sum": (C.c_int, [P, P, C.c_uint64, C.POINTER(C.c_double)]),
+    "psg_frame_cumsum": (C.c_int, [P, P, C.c_uint64, P]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -51,6 +51,12 @@ void require(bool ok, const char* msg) {
   if (!ok) fail(PS_E_INVALID_ARGUMENT, msg);
 }
 
+}  // namespace
+
+void psg::set_last_error(const std::string& m) { t_last_error = m; }
+
+namespace {
+
 // ---- NCCL, resolved at runtime ---------------------------------------------
 // Loaded with dlopen so that a process which already holds torch's bundled
 // libnccl.so.2 reuses it (RTLD_NOLOAD first) instead of mixing two copies.

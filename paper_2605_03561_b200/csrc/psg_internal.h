@@ -22,6 +22,9 @@ struct failure : std::runtime_error {
 
 [[noreturn]] inline void fail(ps_status s, const std::string& m) { throw failure(s, m); }
 
+// The thread-local message behind psg_last_error (psg_capi.cu).
+void set_last_error(const std::string& m);
+
 inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     fail(PS_E_INTERNAL, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));

@@ -265,3 +265,29 @@ def test_profile_congestion_oracle_matches_reference():
     o = oracle.profile_sites(pdb, meta, 1, g["site_ctx"])
     assert_rel(o["ratio"], g["ref_ratio"], 1e-12, "balance ratios")
     assert int(g["site_ctx"][o["worst"]]) == int(g["ref_worst_ctx"][0])
+
+
+def _frame_inputs(seed: int, n: int):
+    rng = np.random.default_rng(seed)
+    a = rng.integers(-6, 6, n).astype(np.int64)
+    b = rng.random(n)
+    b[::7] = np.nan
+    b[::11] = -0.0
+    b[::13] = 0.0
+    c = rng.integers(0, 4, n).astype(np.uint64)
+    return a, b, c
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(3))
+def test_frame_oracle_matches_reference(seed):
+    """Stable multi-key argsort over NaN / +-0 / duplicate keys and the
+    4096-block fold of reduce_sum / cumulative_sum, restated in numpy, equal
+    the reference's frame::sort / reduce_sum / cumulative_sum bit for bit."""
+    a, b, c = _frame_inputs(seed, 9000)
+    for asc in (None, [True, False, True], [False, True, False]):
+        assert np.array_equal(oracle.frame_argsort([a, b, c], asc), oracle.ref_frame_sort([a, b, c], asc))
+    x = np.random.default_rng(seed).random(50_000) * 1e3 - 500
+    tot, cs = oracle.frame_block_scan(x)
+    assert tot == oracle.ref_frame_vec("reduce_sum", x)
+    assert np.array_equal(cs, oracle.ref_frame_vec("cumsum", x))
