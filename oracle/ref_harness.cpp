@@ -577,4 +577,43 @@ int refh_frame_vec(int op, uint64_t n, const double* a, const double* b, double 
   });
 }
 
+// Mean wall time of one frame operator on the reference engine (par backend
+// with `jobs` workers): op 0 group_aggregate(keys k0,k1; v sum,min,max,mean,count),
+// 1 sort(k0 asc, k2 desc), 2 filter(k2 >= lit), 3 merge(on k0 with a [m] table),
+// 4 vector_add, 5 in_place_multiply, 6 scalar_compare, 7 reduce_sum, 8 cumulative_sum.
+double refh_time_frame(int op, uint64_t n, const uint64_t* k0, const uint64_t* k1, const uint64_t* k2,
+                       const double* v, uint64_t m, const uint64_t* mk, const double* mv, uint64_t lit,
+                       unsigned jobs, unsigned repeat) {
+  try {
+    frame::table t;
+    t.add(frame::column::of_u64("k0", std::vector<uint64_t>(k0, k0 + n)));
+    t.add(frame::column::of_u64("k1", std::vector<uint64_t>(k1, k1 + n)));
+    t.add(frame::column::of_u64("k2", std::vector<uint64_t>(k2, k2 + n)));
+    t.add(frame::column::of_f64("v", std::vector<double>(v, v + n)));
+    frame::table r;
+    r.add(frame::column::of_u64("k0", std::vector<uint64_t>(mk, mk + m)));
+    r.add(frame::column::of_f64("w", std::vector<double>(mv, mv + m)));
+    const frame::column& cv = t.col("v");
+    frame::backend bk = be_of(jobs);
+    return time_mean(repeat, [&] {
+      switch (op) {
+        case 0: frame::group_aggregate(t, {"k0", "k1"}, {{"v", frame::agg_fn::sum}, {"v", frame::agg_fn::min},
+                                                         {"v", frame::agg_fn::max}, {"v", frame::agg_fn::mean},
+                                                         {"v", frame::agg_fn::count}}, bk); break;
+        case 1: frame::sort(t, {"k0", "k2"}, {true, false}, bk); break;
+        case 2: frame::filter(t, "k2", frame::cmp_op::ge, frame::literal{lit}, bk); break;
+        case 3: frame::merge(t, r, {"k0"}, bk); break;
+        case 4: frame::vector_add(cv, cv, bk); break;
+        case 5: frame::in_place_multiply(cv, 1.5, bk); break;
+        case 6: frame::scalar_compare(cv, frame::cmp_op::gt, 0.5, bk); break;
+        case 7: frame::reduce_sum(cv, bk); break;
+        default: frame::cumulative_sum(cv, bk); break;
+      }
+    });
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
 }  // extern "C"
