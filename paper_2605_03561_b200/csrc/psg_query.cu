@@ -1004,15 +1004,18 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         if (__popc(H) == __popc(inm) && kb + nb0 + __popc(inm) <= iters) {
           const uint32_t jb = nb0 + __popc(H & lanemask_lt());  // first boundary at/after the run
           const uint32_t bw = __shfl_sync(FULL, mybw, static_cast<int>(jb & 31));
-          const int bpos = ((H >> lane) & 1u) ? static_cast<int>(bw - base32) - lane * RM : RM;
+          const int bpos = ((H >> lane) & 1u) ? static_cast<int>(bw - base32) - R.lb : RM;
           const int k0 = static_cast<int>(kb) - 1 + static_cast<int>(jb);
           const uint32_t rb0 = row_of(k0), rb1 = row_of(k0 + 1);
-          if (bts_out && bpos < RM && static_cast<uint32_t>(k0 + 1) < nbd)
-            bts_out[k0 + 1] = ldg64(p.tr.ts + b + bw);
+          // the boundary's timestamp (optimistic pass 1): loaded now, stored
+          // after the step's reductions so its latency is hidden behind them
+          const bool rec = bts_out && bpos < RM && static_cast<uint32_t>(k0 + 1) < nbd;
+          const u64 bval = rec ? ldg64(p.tr.ts + b + bw) : 0ull;
           if (wm == WIN_FULL)
             run_fast<WIN_FULL>(tv, cv, smem, wt_off, bpos, rb0, rb1);
           else
             run_fast<WIN_NONE>(tv, cv, smem, wt_off, bpos, rb0, rb1);
+          if (rec) bts_out[k0 + 1] = bval;
           done = true;
         }
       }
