@@ -137,6 +137,38 @@ void device::bind(const store::db_handle& h, std::vector<uint32_t> profile_ids) 
   pids_ = std::move(profile_ids);
 }
 
+void device::bind_profiles(const store::db_handle& h) {
+  if (bound_profiles_ == &h) return;
+  check(psg_load_profile_db(ctx_, (h.path()).c_str()));
+  bound_profiles_ = &h;
+}
+
+ingest::slice_table ingest_profiles(const store::db_handle& h, std::vector<uint32_t> profile_ids,
+                                    const ingest::keep_set& keep,
+                                    const std::vector<uint16_t>& metric_ids, unsigned /*jobs*/) {
+  device& d = default_device();
+  d.bind_profiles(h);
+  const bool all_ctx = keep.size() == h.meta().contexts.size();
+  uint64_t n = 0;
+  const uint32_t* cx = all_ctx ? nullptr : keep.ids.data();
+  const uint32_t ncx = all_ctx ? 0 : static_cast<uint32_t>(keep.ids.size());
+  static const uint32_t k_none = 0;
+  if (!all_ctx && keep.ids.empty()) cx = &k_none;  // an empty keep set keeps nothing
+  const uint16_t* mt = metric_ids.empty() ? nullptr : metric_ids.data();
+  const uint32_t nmt = static_cast<uint32_t>(metric_ids.size());
+  const uint32_t np = static_cast<uint32_t>(profile_ids.size());
+  check(psg_slice(d.ctx(), profile_ids.data(), np, cx, ncx, mt, nmt, &n, nullptr, nullptr, nullptr, nullptr));
+  ingest::slice_table out;
+  out.profile_id.resize(n);
+  out.ctx_id.resize(n);
+  out.metric_id.resize(n);
+  out.value.resize(n);
+  if (n)
+    check(psg_slice(d.ctx(), profile_ids.data(), np, cx, ncx, mt, nmt, &n, out.profile_id.data(),
+                    out.ctx_id.data(), out.metric_id.data(), out.value.data()));
+  return out;
+}
+
 device& default_device() {
   thread_local std::unique_ptr<device> d;
   if (!d) d = std::make_unique<device>(0);

@@ -42,12 +42,15 @@ class device {
   // empty) of `h` unless they are already resident.  Raises not_found for an
   // id without a trace (store.cpp:639-642).
   void bind(const store::db_handle& h, std::vector<uint32_t> profile_ids);
+  // Loads every profile's records (profile.db of h) unless already resident.
+  void bind_profiles(const store::db_handle& h);
   psg_context* ctx() const { return ctx_; }
   const std::vector<uint32_t>& profile_ids() const { return pids_; }
 
  private:
   psg_context* ctx_ = nullptr;
   const store::db_handle* bound_ = nullptr;
+  const store::db_handle* bound_profiles_ = nullptr;
   std::vector<uint32_t> pids_;
 };
 
@@ -67,6 +70,13 @@ ingest::trace_ingest_result ingest_traces(const store::db_handle& h,
 // frame::table, column for column.
 frame::table window_aggregate(const store::db_handle& h, std::vector<uint32_t> profile_ids,
                               uint64_t t0_ns, uint64_t t1_ns);
+
+// ingest::ingest_profiles (ingest.hpp:83-87, ingest.cpp:155-176): the
+// profile-record slice of the requested profiles, filtered by the keep set and
+// metric ids, on the device (psg_slice).  `jobs` is accepted and ignored.
+ingest::slice_table ingest_profiles(const store::db_handle& h, std::vector<uint32_t> profile_ids,
+                                    const ingest::keep_set& keep,
+                                    const std::vector<uint16_t>& metric_ids, unsigned jobs);
 
 // itermodel::build_tri_model (itermodel.hpp:118-120, itermodel.cpp:242-360).
 // An automatic anchor is chosen by the reference's suggest_anchor on the first

@@ -200,6 +200,31 @@ void check_everything(const db& d, const std::string& tag, std::vector<uint32_t>
     });
 }
 
+void check_profiles(const db& d, const std::string& tag) {
+  run(tag + ": ingest_profiles == reference (keep sets x metric filters)", [&] {
+    const auto& meta = d.h->meta();
+    std::vector<uint32_t> all_pids;
+    for (const auto& p : meta.profiles) all_pids.push_back(p.id);
+    ingest::keep_set all_ctx, some, none;
+    for (uint32_t c = 0; c < meta.contexts.size(); ++c) {
+      all_ctx.ids.push_back(c);
+      if (c % 3 != 1) some.ids.push_back(c);
+    }
+    std::vector<uint32_t> sub = {all_pids.back(), all_pids.front(), all_pids.back()};
+    for (const auto* pids : {&all_pids, &sub})
+      for (const auto* keep : {&all_ctx, &some, &none})
+        for (const std::vector<uint16_t>& m : {std::vector<uint16_t>{}, std::vector<uint16_t>{0},
+                                               std::vector<uint16_t>{1}, std::vector<uint16_t>{0, 1}}) {
+          auto a = ingest::ingest_profiles(*d.h, *pids, *keep, m, 2);
+          auto b = gpu::ingest_profiles(*d.h, *pids, *keep, m, 2);
+          expect(a == b, "slice table");
+        }
+    expect(raised([&] { gpu::ingest_profiles(*d.h, {all_pids.back() + 1000}, all_ctx, {}, 1); }) ==
+               errc::not_found,
+           "missing profile");
+  });
+}
+
 void check_diagnostics(const db& d, const std::string& tag, uint32_t anchor, double total) {
   run(tag + ": savings_report + iteration_cv_report == reference (1e-9)", [&] {
     const auto ids = d.ids();
@@ -241,6 +266,7 @@ int main() {
     db d(image);
     check_everything(d, "small_iter", {0, 1, 2});
     check_diagnostics(d, "small_iter", 1, 10.0);
+    check_profiles(d, "small_iter");
     run("small_iter: auto anchor == reference (itermodel.cpp:253-255)", [&] {
       auto pol = itermodel::anchor_policy::auto_detect();
       same_model(itermodel::build_tri_model(*d.h, d.ids(), pol, 1),
