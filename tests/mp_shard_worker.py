@@ -36,9 +36,62 @@ def run(ctx: Context, lo: int, hi: int, T: int) -> dict:
     return out
 
 
-def main(out_dir: str) -> None:
+def dup_traces():
+    """N_TRACES traces of anchor(1) / kernels 2..4 / root(0) iterations; trace 3
+    re-enters the anchor subtree on the timestamp it left it (a candidate the
+    exact pass 1 drops): only the rank owning trace 3 sees the optimistic pass
+    miss, and every rank must re-run with it."""
+    parent = np.array([0xFFFFFFFF, 0, 1, 1, 1, 0], np.uint32)
+    rng = np.random.default_rng(11)
+    ts, cx, off, tend = [], [], [0], []
+    for t in range(N_TRACES):
+        now = int(rng.integers(0, 50))
+        for it in range(12):
+            cx.append(1); ts.append(now)
+            if t == 3 and it == 5:                # leave and re-enter on the same timestamp
+                cx.append(5); ts.append(now)
+                cx.append(1); ts.append(now)
+            for k in (2, 3, 4):
+                cx.append(k); ts.append(now)
+                now += int(rng.integers(10, 100))
+            cx.append(5); ts.append(now)          # leave the subtree
+            now += 7
+            cx.append(0); ts.append(now)
+            now += 3
+        off.append(len(ts))
+        tend.append(now + 5)
+    body = np.zeros(len(ts) * 12, np.uint8)
+    body.reshape(-1, 12)[:, :8] = np.array(ts, np.uint64).view(np.uint8).reshape(-1, 8)
+    body.reshape(-1, 12)[:, 8:] = np.array(cx, np.uint32).view(np.uint8).reshape(-1, 4)
+    return parent, body, np.array(off, np.uint64), np.array(tend, np.uint64)
+
+
+def load_dup(ctx: Context, lo: int, hi: int) -> None:
+    parent, body, off, tend = dup_traces()
+    ctx.set_cct(parent)
+    sub = body[int(off[lo]) * 12:int(off[hi]) * 12]
+    ctx.load_aos(sub, off[lo:hi + 1] - off[lo], np.arange(lo, hi, dtype=np.uint32) + 1, tend[lo:hi])
+
+
+def main(out_dir: str, mode: str = "gen") -> None:
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
+    if mode == "dup":
+        with Context(0) as single:
+            load_dup(single, 0, N_TRACES)
+            T = int(single.shard()["t_max"])
+            if rank == 0:
+                np.savez(os.path.join(out_dir, "single.npz"), **run(single, 0, N_TRACES, T))
+        lo, hi = pdist.shard_range(N_TRACES, world, rank)
+        with Context(0) as ctx:
+            ctx.comm_init_host(world, rank, pdist.torch_reducer())
+            load_dup(ctx, lo, hi)
+            res = run(ctx, lo, hi, T)
+            res["range"] = np.array([lo, hi], np.int64)
+            np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **res)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     cfg = scenarios.iterative(N_TRACES, 9, n_kernels=6, seed=3, jitter=0.25)
     T = 0
     with Context(0) as single:  # to learn T (and, on rank 0, the reference run)
@@ -58,4 +111,4 @@ def main(out_dir: str) -> None:
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "gen")

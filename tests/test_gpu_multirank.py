@@ -18,11 +18,13 @@ from tests.helpers import ROOT, assert_rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_query_equals_single_context(tmp_path, world):
+@pytest.mark.parametrize("world,mode", [(2, "gen"), (3, "gen"), (2, "dup"), (3, "dup")])
+def test_sharded_query_equals_single_context(tmp_path, world, mode):
+    """mode "dup": one rank's traces make the optimistic pass 1 miss; the
+    verdict is all-reduced, so every rank re-runs both passes exactly."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
            f"--nproc-per-node={world}", os.path.join(ROOT, "tests", "mp_shard_worker.py"),
-           str(tmp_path)]
+           str(tmp_path), mode]
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
