@@ -40,6 +40,17 @@ with Context(0) as ctx:
     ms = [ctx.profile_outliers(metric, sites, top_k=0, z_min=1.0)["ms_total"] for _ in range(10)]
     out["gpu_profile_outliers_ms_device"] = float(np.median(ms))
     out["n_outliers"] = ctx.info["n_outliers"]
+    # parity with the reference's congestion_report at this size
+    rep = json.loads(oracle.ref_congestion_report(d))
+    hosts = sorted({h for (_, r, h) in meta["profiles"] if r >= 0})
+    o = ctx.outliers(len(hosts))
+    want = [s["balance_ratio"] for s in rep["callsites"]]
+    out["parity"] = {
+        "worst_site": ctx.info["worst_site"] == rep["worst"]["ctx_id"],
+        "balance_ratio_max_rel_err": float(np.max(np.abs(o["site_ratio"] - want) / np.abs(want))),
+        "outliers_equal_dbscan_group": sorted(hosts[i] for i in o["selected"]) == sorted(rep["outlier_group"]["hostnames"]),
+        "racks": [int(r[0]) for r in o["racks"]] == [r["rack"] for r in rep["topology"]["racks"]],
+    }
 lib = oracle.ref()
 lib.refh_time_slices.restype = C.c_double
 lib.refh_time_slices.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.c_uint32, C.c_uint16, C.c_uint, C.c_uint]
