@@ -77,6 +77,14 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// TMA bulk prefetch issued by lane 0 only, without a branch (predicated).
+__device__ __forceinline__ void prefetch_l2_lane0(const void* p, uint32_t bytes, bool on) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(p),
+      "r"(bytes), "r"(static_cast<uint32_t>(on))
+      : "memory");
+}
+
 __device__ __forceinline__ u64 ldg64(const uint64_t* p) {
   return static_cast<u64>(__ldg(reinterpret_cast<const unsigned long long*>(p)));
 }
@@ -884,9 +892,10 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       const int64_t lr = static_cast<int64_t>(n_t) - 1 - base;
       R.last_li = lr < STEP_M ? static_cast<int>(lr) : -1;
       const u64 r0 = s_abs + static_cast<u64>(R.lb);
-      if (lane == 0 && s_abs + 3 * STEP_M <= e) {
-        prefetch_l2(p.tr.ts + s_abs + 2 * STEP_M, 8 * STEP_M);
-        prefetch_l2(p.tr.ctx + s_abs + 2 * STEP_M, 4 * STEP_M);
+      {
+        const bool pf = lane == 0 && s_abs + 3 * STEP_M <= e;
+        prefetch_l2_lane0(p.tr.ts + s_abs + 2 * STEP_M, 8 * STEP_M, pf);
+        prefetch_l2_lane0(p.tr.ctx + s_abs + 2 * STEP_M, 4 * STEP_M, pf);
       }
       u64 tv[RM + 1];
       uint32_t cv[RM];
