@@ -1,15 +1,21 @@
 // The fused trace query on sm_100a: two passes over the event stream.
 //
 //   k_bounds       pass 1 — iteration boundaries per trace (itermodel.cpp:111-143):
-//                  reads ctx only (4 B/event) plus the timestamp of each
-//                  boundary candidate, writes the boundary event indices.
+//                  optimistic mode (default) reads ctx only (4 B/event) and
+//                  takes every subtree entry as a boundary; exact mode also
+//                  reads each candidate's timestamp and drops same-timestamp
+//                  re-entries.  Writes the boundary event indices.
+//   k_verify_bounds  after an optimistic pass 1: checks the boundary
+//                  timestamps pass 2 recorded (no two equal, gap and
+//                  iterations < 2^32 ns); a miss re-runs both passes exactly.
 //   k_trace_query  pass 2 — ONE read of ts+ctx (12 B/event) computing
 //                    * the window filter + per-(trace, ctx) count/sum/min/max/mean
 //                      (ingest.cpp:178-208 + frame.cpp:290-408),
 //                    * the time-integrated excl/incl of the window incl. the
 //                      carry-in segment (itermodel.cpp:145-183),
 //                    * the trace x iteration x node cube incl/excl + gap rows
-//                      (itermodel.cpp:242-360),
+//                      (itermodel.cpp:242-360), stored with 32-bit cells when
+//                      every iteration spans < 2^32 ns,
 //                    * exact integer sufficient statistics for the cross-rank and
 //                      within-rank diagnostics (diagnostics.cpp:83-158).
 //
@@ -27,6 +33,9 @@
 // Everything on the event stream is integer arithmetic in nanoseconds, which
 // is exact and order-free, so the results are bit-identical to the reference
 // regardless of thread order.
+//
+//   k_cross_stats  the cross-rank (iteration, node) Σx, max, Σx² over the
+//                  stored cube (diagnostics.cpp:83-158).
 #include <algorithm>
 #include <climits>
 #include <cstdint>
