@@ -110,6 +110,17 @@ struct bound_params {
 // >= 2^32 accumulate in the trace's global output row (64-bit global atomics).
 enum : uint32_t { WT_CNT = 0, WT_LO = 1, WT_MIN = 2, WT_MAX = 3, WT_PPO = 4, WT_NBIG = 5,
                   WT_ACC = 6 /* lo, hi words */, WT_STRIDE = 9 };
+// First word of ctx c's record.  Lanes hold runs of 8 consecutive events, so
+// in an iterative trace the lanes of one iteration touch contexts 8 apart;
+// with a stride of 9 words those share a bank every 4 lanes (3-way conflicts
+// measured).  Leaving one record slot free after every 8 contexts makes
+// contexts 8 apart 81 words apart: 17 banks, distinct for all 32 lanes.
+#ifndef PSG_WT_SWIZZLE
+#define PSG_WT_SWIZZLE 1
+#endif
+__host__ __device__ inline uint32_t wt_word(uint32_t c) {
+  return WT_STRIDE * (PSG_WT_SWIZZLE ? c + (c >> 3) : c);
+}
 
 // Cube row stride in cells: nn + 1 rounded up to even (pad columns).
 __host__ __device__ inline uint32_t row_stride(uint32_t nn) { return (nn + 2) & ~1u; }
@@ -140,7 +151,7 @@ struct warp_smem_layout {
     off_pref = take(8u * (nn + 1));  // generic rows and the gap row
     off_bwin = take(4u * (2 * G + 2));
     off_bts = take(8u * (2 * G + 2));
-    off_wtab = take(4u * WT_STRIDE * n_ctx);
+    off_wtab = take(4u * WT_STRIDE * (n_ctx + n_ctx / 8 + 1));
     off_wsx = take(8u * nn);
     off_wsqlo = take(8u * nn);
     off_wsqhi = take(8u * nn);

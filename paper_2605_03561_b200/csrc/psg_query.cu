@@ -393,11 +393,11 @@ struct warp_tables {
   unsigned long long *gminb, *gmaxb;  // the trace's global w_min / w_max rows (durations >= 2^32)
   u64* carry;
   __device__ __forceinline__ u64 acc(uint32_t c) const {
-    const uint32_t* r = wt + c * WT_STRIDE + WT_ACC;
+    const uint32_t* r = wt + wt_word(c) + WT_ACC;
     return static_cast<u64>(r[0]) | (static_cast<u64>(r[1]) << 32);
   }
   __device__ __forceinline__ void set_acc(uint32_t c, u64 v) const {
-    uint32_t* r = wt + c * WT_STRIDE + WT_ACC;
+    uint32_t* r = wt + wt_word(c) + WT_ACC;
     r[0] = static_cast<uint32_t>(v);
     r[1] = static_cast<uint32_t>(v >> 32);
   }
@@ -406,7 +406,7 @@ struct warp_tables {
 // One window row of duration d for ctx c (frame::group_aggregate's
 // count/sum/min/max fold, order-free in integers).
 __device__ __forceinline__ void win_row32(const warp_tables& T, uint32_t c, uint32_t d) {
-  uint32_t* r = T.wt + c * WT_STRIDE;
+  uint32_t* r = T.wt + wt_word(c);
   atomicAdd(r + WT_CNT, 1u);
   atomicAdd(r + WT_LO, d);
   atomicMin(r + WT_MIN, d);
@@ -414,7 +414,7 @@ __device__ __forceinline__ void win_row32(const warp_tables& T, uint32_t c, uint
 }
 
 __device__ __forceinline__ void win_row64(const warp_tables& T, uint32_t c, u64 d) {
-  uint32_t* r = T.wt + c * WT_STRIDE;
+  uint32_t* r = T.wt + wt_word(c);
   atomicAdd(r + WT_CNT, 1u);
   sadd64(r + WT_ACC, r + WT_ACC + 1, d);
   if (d >> 32) {
@@ -602,22 +602,28 @@ template <int WM>
 __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
                                          uint8_t* sm, uint32_t wt_off, int bpos,
                                          uint32_t rb_before, uint32_t rb_after) {
-  uint32_t ppo[RM];
+  uint32_t ppo[RM], d[RM];
 #pragma unroll
-  for (int j = 0; j < RM; ++j)  // all column loads first: they do not wait on the REDs
-    ppo[j] = *reinterpret_cast<const uint32_t*>(sm + wt_off + cv[j] * (4u * WT_STRIDE) + 4u * WT_PPO);
+  for (int j = 0; j < RM; ++j) {  // all column loads first: they do not wait on the REDs
+    ppo[j] = *reinterpret_cast<const uint32_t*>(sm + wt_off + 4u * (wt_word(cv[j]) + WT_PPO));
+    d[j] = static_cast<uint32_t>(tv[j + 1]) - static_cast<uint32_t>(tv[j]);
+  }
+  // the window reductions first (they need no column offset): the column
+  // loads' latency is hidden behind them
+  if (WM == WIN_FULL) {
+#pragma unroll
+    for (int j = 0; j < RM; ++j) {
+      uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word(cv[j]));
+      atomicAdd(r + WT_CNT, 1u);
+      atomicAdd(r + WT_LO, d[j]);
+      atomicMin(r + WT_MIN, d[j]);
+      atomicMax(r + WT_MAX, d[j]);
+    }
+  }
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
-    const uint32_t d = static_cast<uint32_t>(tv[j + 1]) - static_cast<uint32_t>(tv[j]);
     const uint32_t rb = j >= bpos ? rb_after : rb_before;
-    atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + ppo[j]), d);
-    if (WM == WIN_FULL) {
-      uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + cv[j] * (4u * WT_STRIDE));
-      atomicAdd(r + WT_CNT, 1u);
-      atomicAdd(r + WT_LO, d);
-      atomicMin(r + WT_MIN, d);
-      atomicMax(r + WT_MAX, d);
-    }
+    atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + ppo[j]), d[j]);
   }
 }
 
@@ -638,6 +644,14 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   constexpr uint32_t G = GC;
   const uint4* src = reinterpret_cast<const uint4*>(rows);
   const uint32_t nq = G * nnp / 4;
+#ifdef PSG_AB_NO_FLUSH  // A/B timing experiment only (wrong results): zero the rows, nothing else
+  {
+    __syncwarp();
+    uint4* z = reinterpret_cast<uint4*>(rows);
+    for (uint32_t i = lane; i < nq; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    return;
+  }
+#endif
   uint32_t rs[GC];
 #pragma unroll
   for (uint32_t r = 0; r < G; ++r) rs[r] = 0u;
@@ -772,7 +786,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     for (uint32_t j = lane; j < nn; j += 32) wsx[j] = wsqlo[j] = wsqhi[j] = 0;
   }
   for (uint32_t c = lane; c < n_ctx; c += 32) {
-    uint32_t* r = T.wt + c * WT_STRIDE;
+    uint32_t* r = T.wt + wt_word(c);
     r[WT_CNT] = r[WT_LO] = r[WT_MAX] = r[WT_NBIG] = 0u;
     r[WT_MIN] = 0xFFFFFFFFu;
     const int32_t sp = CUBE ? p.sub_pre[c] : -1;
@@ -996,7 +1010,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           if (wspan + span >= kSpan32) {  // fold the pending 32-bit sums
             __syncwarp();
             for (uint32_t x = lane; x < n_ctx; x += 32) {
-              uint32_t* r = T.wt + x * WT_STRIDE;
+              uint32_t* r = T.wt + wt_word(x);
               T.set_acc(x, T.acc(x) + r[WT_LO]);
               r[WT_LO] = 0;
             }
@@ -1061,10 +1075,12 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           st.rowb = st.slot * nnp;
           st.cube_ok = st.k < R.iters;
         }
+#ifndef PSG_AB_NO_SLOW  // A/B timing experiment only (wrong results): no general block path
         if (cwide)
           run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
         else
           run_block<WIN, CUBE, false>(wm, tv, cv, R, st, T);
+#endif
       }
       pos = lim;
     }
@@ -1198,7 +1214,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     const uint32_t c_ctx = static_cast<uint32_t>(T.carry[2]);
     const u64 c_d = T.carry[1];
     for (uint32_t c = lane; c < n_ctx; c += 32) {
-      const u64 sum = T.acc(c) + T.wt[c * WT_STRIDE + WT_LO];
+      const u64 sum = T.acc(c) + T.wt[wt_word(c) + WT_LO];
       tmp[s_cct_pre[c]] = sum + ((c_has && c == c_ctx) ? c_d : 0ull);
     }
     __syncwarp();
@@ -1207,7 +1223,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     __syncwarp();
     const size_t base = static_cast<size_t>(t) * n_ctx;
     for (uint32_t c = lane; c < n_ctx; c += 32) {
-      const uint32_t* r = T.wt + c * WT_STRIDE;
+      const uint32_t* r = T.wt + wt_word(c);
       const int pr = s_cct_pre[c], sz = s_cct_size[c];
       const u64 cnt = r[WT_CNT], nbig = r[WT_NBIG];
       const u64 sum = T.acc(c) + r[WT_LO];
