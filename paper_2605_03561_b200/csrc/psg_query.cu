@@ -601,13 +601,11 @@ __device__ __forceinline__ void warp_prefix_row(const uint32_t* lo, const uint32
 template <int WM>
 __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
                                          uint8_t* sm, uint32_t wt_off, int bpos,
-                                         uint32_t rb_before, uint32_t rb_after) {
-  uint32_t ppo[RM], d[RM];
+                                         uint32_t rb_before, uint32_t rb_after,
+                                         const uint32_t (&ppo)[RM]) {
+  uint32_t d[RM];
 #pragma unroll
-  for (int j = 0; j < RM; ++j) {  // all column loads first: they do not wait on the REDs
-    ppo[j] = *reinterpret_cast<const uint32_t*>(sm + wt_off + 4u * (wt_word(cv[j]) + WT_PPO));
-    d[j] = static_cast<uint32_t>(tv[j + 1]) - static_cast<uint32_t>(tv[j]);
-  }
+  for (int j = 0; j < RM; ++j) d[j] = static_cast<uint32_t>(tv[j + 1]) - static_cast<uint32_t>(tv[j]);
   // the window reductions first (they need no column offset): the column
   // loads' latency is hidden behind them
   if (WM == WIN_FULL) {
@@ -656,7 +654,14 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
 #pragma unroll
   for (uint32_t r = 0; r < G; ++r) rs[r] = 0u;
   const uint32_t ax = lane < static_cast<int>(G) ? rows[lane * nnp] : 0u;  // the anchor's excl
-  for (uint32_t n = 1 + lane; n < nn; n += 32) {
+  // leaves 1..nn-1: whole groups of 32 columns one column per lane; a tail
+  // of at most 32/G columns (65 leaves = 2 groups + 1 in the iterative
+  // scenarios) one cell per lane instead, so the warp does not run a G-row
+  // pass for a handful of active lanes
+  constexpr uint32_t TW = 32 / GC;  // tail columns per pass
+  const uint32_t nl = nn - 1, tail = nl & 31u;
+  const uint32_t n_cols = (tail != 0 && tail <= TW) ? nn - tail : nn;
+  for (uint32_t n = 1 + lane; n < n_cols; n += 32) {
     u64 sx = 0, sq = 0, sqh = 0;
     uint32_t orv = 0;
 #pragma unroll
@@ -681,13 +686,45 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
       wsqlo[n] = l2;
     }
   }
+  uint32_t trs = 0;  // tail cells of row lane % G
+  if (n_cols < nn) {
+    const uint32_t n = n_cols + static_cast<uint32_t>(lane) / G, r = static_cast<uint32_t>(lane) % G;
+    const u64 ex = n < nn ? rows[r * nnp + n] : 0u;
+    trs = static_cast<uint32_t>(ex);
+    if (STATS) {  // the G lanes of a column (aligned group): its within-rank sums
+      u64 sx = ex, sq = ex * ex, sqh = 0;
+      if (!__any_sync(FULL, (ex >> 30) != 0)) {
+#pragma unroll
+        for (int d = 1; d < static_cast<int>(G); d <<= 1) {
+          sx += __shfl_xor_sync(FULL, sx, d);
+          sq += __shfl_xor_sync(FULL, sq, d);
+        }
+      } else {
+#pragma unroll
+        for (int d = 1; d < static_cast<int>(G); d <<= 1) {
+          sx += __shfl_xor_sync(FULL, sx, d);
+          const u64 ol = __shfl_xor_sync(FULL, sq, d), oh = __shfl_xor_sync(FULL, sqh, d);
+          sq += ol;
+          sqh += oh + (sq < ol ? 1ull : 0ull);
+        }
+      }
+      if (r == 0 && n < nn) {
+        wsx[n] += sx;
+        const u64 l2 = wsqlo[n] + sq;
+        wsqhi[n] += sqh + (l2 < sq ? 1ull : 0ull);
+        wsqlo[n] = l2;
+      }
+    }
+#pragma unroll
+    for (int d = G; d < 32; d <<= 1) trs += __shfl_xor_sync(FULL, trs, d);  // row lane % G
+  }
 #pragma unroll
   for (uint32_t r = 0; r < G; ++r) rs[r] = __reduce_add_sync(FULL, rs[r]);  // leaves, < 2^32
   uint32_t mine = rs[0];
 #pragma unroll
   for (uint32_t r = 1; r < G; ++r)
     if (static_cast<uint32_t>(lane) == r) mine = rs[r];
-  mine += ax;  // lane r < G: the anchor's inclusive time in row r
+  mine += ax + trs;  // lane r < G: the anchor's inclusive time in row r
   if (lane < static_cast<int>(G)) {
     rows[lane * nnp] = mine;
     rows[lane * nnp + nn] = 0u;  // pad column
@@ -724,22 +761,27 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   // the block: G * nnp cells, a multiple of 4; 16-byte aligned on both sides
   // (ring rows from a 16-byte boundary, trace blocks padded to 4 cells, kb * nnp
   // a multiple of 8)
+  // each lane zeroes the 16 bytes it has just read
+  uint4* z = reinterpret_cast<uint4*>(rows);
   if (p.cube32) {
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.cube_incl) + ob);
 #pragma unroll 4
-    for (uint32_t i = lane; i < nq; i += 32) dst[i] = src[i];
+    for (uint32_t i = lane; i < nq; i += 32) {
+      const uint4 v = src[i];
+      z[i] = make_uint4(0u, 0u, 0u, 0u);
+      dst[i] = v;
+    }
   } else {
     ulonglong2* dst = reinterpret_cast<ulonglong2*>(p.cube_incl + ob);
 #pragma unroll 4
     for (uint32_t i = lane; i < nq; i += 32) {
       const uint4 v = src[i];
+      z[i] = make_uint4(0u, 0u, 0u, 0u);
       dst[2 * i] = make_ulonglong2(v.x, v.y);
       dst[2 * i + 1] = make_ulonglong2(v.z, v.w);
     }
   }
   __syncwarp();
-  uint4* z = reinterpret_cast<uint4*>(rows);
-  for (uint32_t i = lane; i < nq; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 template <bool WIN, bool CUBE>
@@ -1043,10 +1085,16 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           // after the step's reductions so its latency is hidden behind them
           const bool rec = bts_out && bpos < RM && static_cast<uint32_t>(k0 + 1) < nbd;
           const u64 bval = rec ? ldg64(p.tr.ts + b + bw) : 0ull;
+          // column offsets of the step's events (loading them earlier, before
+          // the window classification, measured slower: register pressure)
+          uint32_t ppo[RM];
+#pragma unroll
+          for (int j = 0; j < RM; ++j)
+            ppo[j] = *reinterpret_cast<const uint32_t*>(smem + wt_off + 4u * (wt_word(cv[j]) + WT_PPO));
           if (wm == WIN_FULL)
-            run_fast<WIN_FULL>(tv, cv, smem, wt_off, bpos, rb0, rb1);
+            run_fast<WIN_FULL>(tv, cv, smem, wt_off, bpos, rb0, rb1, ppo);
           else
-            run_fast<WIN_NONE>(tv, cv, smem, wt_off, bpos, rb0, rb1);
+            run_fast<WIN_NONE>(tv, cv, smem, wt_off, bpos, rb0, rb1, ppo);
           if (rec) bts_out[k0 + 1] = bval;
           done = true;
         }
