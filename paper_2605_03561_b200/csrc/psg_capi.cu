@@ -1428,11 +1428,12 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     }
     // launch geometry
     warp_smem_layout L;
-    L.init(c->n_ctx, nn, p.G, c->root_only != 0 || !do_cube);
+    L.init(c->n_ctx, nn, p.G, do_cube && exact_bounds);
     uint32_t W = choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16));
     p.warps = W;
     p.L = L;
-    uint32_t smem = cta_table_bytes(c->n_ctx, nn, W) + W * L.bytes;
+    p.cta_bytes = cta_table_bytes(c->n_ctx, nn, W);
+    uint32_t smem = p.cta_bytes + W * L.bytes;
     PSG_CUDA(cudaEventRecord(c->ev[1], s));
     launch_trace_query(p, smem, s);
     PSG_CUDA(cudaEventRecord(c->ev[2], s));

@@ -127,7 +127,7 @@ __host__ __device__ inline uint32_t row_stride(uint32_t nn) { return (nn + 2) & 
 
 struct warp_smem_layout {
   uint32_t nnp;               // cube row stride (nn + 1 rounded up to even)
-  uint32_t off_rlo, off_rhi;  // (2G+1) x nnp u32: cube rows (ring of 2G, gap)
+  uint32_t off_rlo, off_rhi;  // (2G+1) x nnp u32: cube rows (ring of 2G, gap), high words
   uint32_t off_pref;   // nn+1 u64     prefix scratch for the generic inclusive roll-up
   uint32_t off_bwin;   // 2G+2 u32     boundary window (event indices relative to the trace)
   uint32_t off_bts;    // 2G+2 u64     timestamps of those boundaries
@@ -136,7 +136,9 @@ struct warp_smem_layout {
   uint32_t off_carry;  // {u64 ts, u64 dur, u64 (has << 32 | ctx)}
   uint32_t off_scan;   // 2 x (n_ctx + 1) u64 at finalize (aliases the rows)
   uint32_t bytes;
-  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G, bool /*root_only*/) {
+  // wide_rows: 64-bit cells possible (exact pass 1), so the rows need their
+  // high words; the optimistic mode runs 32-bit throughout and aliases them
+  __host__ __device__ void init(uint32_t n_ctx, uint32_t nn, uint32_t G, bool wide_rows) {
     uint32_t o = 0;
     auto take = [&](uint32_t b) {
       uint32_t r = o;
@@ -147,7 +149,7 @@ struct warp_smem_layout {
     const uint32_t rows = 4u * (2 * G + 1) * nnp, scan = 16u * (n_ctx + 1);
     off_rlo = take(rows > scan ? rows : scan);
     off_scan = off_rlo;
-    off_rhi = take(rows);
+    off_rhi = wide_rows ? take(rows) : off_rlo;
     off_pref = take(8u * (nn + 1));  // generic rows and the gap row
     off_bwin = take(4u * (2 * G + 2));
     off_bts = take(8u * (2 * G + 2));
@@ -207,6 +209,7 @@ struct query_params {
   uint32_t G;          // iterations per chunk (power of two); the row ring holds 2G + gap
   uint32_t warps;      // traces per CTA
   warp_smem_layout L;  // per-warp shared-memory carve-out (computed on the host)
+  uint32_t cta_bytes;  // cta_table_bytes(n_ctx, nn, warps), computed on the host
 };
 
 // CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]

@@ -105,14 +105,42 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 
 // One block step's events for this lane (RM timestamps + ctx words from r0)
 // and, on lane 31, the timestamp after the step.
+#ifndef PSG_LD256
+#define PSG_LD256 1
+#endif
+#ifndef PSG_SA
+#define PSG_SA 8  // block steps start on multiples of SA events (4 or 8)
+#endif
+constexpr int SA = PSG_SA, SOFF = SA - 1;
+// 32-byte read-only load (one LDG.256: every instruction fills whole 32-byte
+// sectors, so no sector is fetched twice when L1 cannot hold it in between)
+__device__ __forceinline__ void ldg256(const uint64_t* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p));
+}
+
 __device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_abs, int lane,
                                           ulonglong2 (&ts)[RM / 2], uint4 (&cx)[RM / 4], u64& nf) {
-  const ulonglong2* tsrc = reinterpret_cast<const ulonglong2*>(tr.ts + r0);
+  if (PSG_LD256) {  // r0 is a multiple of 4 events: 32-byte aligned timestamps
 #pragma unroll
-  for (int q = 0; q < RM / 2; ++q) ts[q] = __ldg(tsrc + q);
-  const uint4* csrc = reinterpret_cast<const uint4*>(tr.ctx + r0);
+    for (int q = 0; q < RM / 4; ++q)
+      ldg256(tr.ts + r0 + 4 * q, ts[2 * q].x, ts[2 * q].y, ts[2 * q + 1].x, ts[2 * q + 1].y);
+  } else {
+    const ulonglong2* tsrc = reinterpret_cast<const ulonglong2*>(tr.ts + r0);
 #pragma unroll
-  for (int q = 0; q < RM / 4; ++q) cx[q] = __ldg(csrc + q);
+    for (int q = 0; q < RM / 2; ++q) ts[q] = __ldg(tsrc + q);
+  }
+  if (PSG_LD256 && SA == 8 && RM == 8) {  // r0 a multiple of 8 events: 32-byte aligned ctx words
+    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(cx[0].x), "=r"(cx[0].y), "=r"(cx[0].z), "=r"(cx[0].w), "=r"(cx[1].x),
+                   "=r"(cx[1].y), "=r"(cx[1].z), "=r"(cx[1].w)
+                 : "l"(tr.ctx + r0));
+  } else {
+    const uint4* csrc = reinterpret_cast<const uint4*>(tr.ctx + r0);
+#pragma unroll
+    for (int q = 0; q < RM / 4; ++q) cx[q] = __ldg(csrc + q);
+  }
   if (lane == 31) nf = ldg64(tr.ts + s_abs + 32 * RM);
 }
 
@@ -447,8 +475,8 @@ __device__ __forceinline__ void acc_sq(u64& lo, u64& hi, u64 x) {
   }
 }
 
-// Boundary windows hold event indices relative to the trace plus 3 (the block
-// step start is aligned down by at most 3 events), so all index arithmetic is
+// Boundary windows hold event indices relative to the trace plus SOFF (the block
+// step start is aligned down by at most SOFF events), so all index arithmetic is
 // unsigned 32-bit (traces have < 2^32 - 4096 events).  Local index of a
 // boundary in the block step starting at base3 (clamped past the step).
 __device__ __forceinline__ int local_of(uint32_t bw3, uint32_t base3) {
@@ -469,7 +497,7 @@ struct run_ctx {
   const int32_t* s_sub_pre;
   const uint32_t* bwin;
   uint32_t *rlo, *rhi;
-  uint32_t base3;  // block step start relative to the trace, + 3
+  uint32_t base3;  // block step start relative to the trace, + SOFF
   u64 tend, t0, t1w;
   uint32_t R2, nnp;  // ring size, cube row stride
   int iters;  // iterations stored for this trace; -1 for a skipped trace (no gap row either)
@@ -799,7 +827,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
 
   const warp_smem_layout& L = p.L;
   const uint32_t nnp = L.nnp;
-  const uint32_t wb_off = cta_table_bytes(n_ctx, nn, W) + static_cast<uint32_t>(warp) * L.bytes;
+  const uint32_t wb_off = p.cta_bytes + static_cast<uint32_t>(warp) * L.bytes;
   uint8_t* wb = smem + wb_off;
   uint32_t* rlo = reinterpret_cast<uint32_t*>(wb + L.off_rlo);
   uint32_t* rhi = reinterpret_cast<uint32_t*>(wb + L.off_rhi);
@@ -824,7 +852,9 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   }
   if (CUBE) {
     for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) s_node[i] = p.node_tab[i];
-    for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rlo[j] = rhi[j] = 0;
+    for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rlo[j] = 0;
+    if (p.exact_bounds)
+      for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rhi[j] = 0;
     for (uint32_t j = lane; j < nn; j += 32) wsx[j] = wsqlo[j] = wsqhi[j] = 0;
   }
   for (uint32_t c = lane; c < n_ctx; c += 32) {
@@ -918,7 +948,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
     if (CUBE && kept) {
       // boundary window of this chunk (prefetched during the previous one)
       if (lane <= static_cast<int>(R2)) {
-        bwin[lane] = nx_idx + 3;  // stored + 3, see local_of
+        bwin[lane] = nx_idx + SOFF;  // stored + SOFF, see local_of
         bts[lane] = nx_ts;
       }
       mybw = lane <= static_cast<int>(R2) ? nx_idx : 0xFFFFFFFFu;
@@ -930,8 +960,8 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       const bool have2 = lane <= static_cast<int>(R2) && k + G < nbd;
       nn_idx = have2 ? __ldg(bt + k + G) : static_cast<uint32_t>(n_t);
       __syncwarp();
-      E1 = bwin[G] - 3;
-      E2 = bwin[R2] - 3;
+      E1 = bwin[G] - SOFF;
+      E2 = bwin[R2] - SOFF;
       // iteration spans of the ring (and the gap in chunk 0) decide 32- vs
       // 64-bit cells (exact mode; the optimistic mode runs 32-bit throughout)
       if (!optimistic) {
@@ -941,17 +971,17 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       }
     } else if (CUBE && active) {
       // skipped trace: only the window runs; iterations are not stored
-      if (lane <= static_cast<int>(R2)) bwin[lane] = static_cast<uint32_t>(n_t) + 3;
+      if (lane <= static_cast<int>(R2)) bwin[lane] = static_cast<uint32_t>(n_t) + SOFF;
       mybw = lane <= static_cast<int>(R2) ? static_cast<uint32_t>(n_t) : 0xFFFFFFFFu;
       __syncwarp();
     }
 
     // ---- phase 1: consume events [pos, E1), possibly running ahead to E2 ----
     while (pos < E1) {
-      const u64 s_abs = (b + pos) & ~3ull;
-      const int64_t base = static_cast<int64_t>(s_abs) - static_cast<int64_t>(b);  // >= -3
+      const u64 s_abs = (b + pos) & ~static_cast<u64>(SOFF);
+      const int64_t base = static_cast<int64_t>(s_abs) - static_cast<int64_t>(b);  // >= -SOFF
       const u64 lim = min(static_cast<u64>(base + STEP_M), E2);
-      R.base3 = static_cast<uint32_t>(base + 3);
+      R.base3 = static_cast<uint32_t>(base + SOFF);
       R.lo = static_cast<int>(static_cast<int64_t>(pos) - base);
       R.hi = static_cast<int>(static_cast<int64_t>(lim) - base);
       const int64_t lr = static_cast<int64_t>(n_t) - 1 - base;
@@ -988,7 +1018,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         tv[RM] = nf;
       }
       if (lim < n_t && (PSG_PIPE_CROSS || lim < E1)) {
-        pf_pos = (b + lim) & ~3ull;
+        pf_pos = (b + lim) & ~static_cast<u64>(SOFF);
         load_step(p.tr, pf_pos + static_cast<u64>(R.lb), pf_pos, lane, pts, pcx, pnf);
       } else {
         pf_pos = ~0ull;
@@ -1026,10 +1056,10 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
           first = __shfl_sync(FULL, tv[0], 0);
           after = __shfl_sync(FULL, tv[RM], 31);
         } else {
-          u64 f = tv[0];  // lo <= 3 < RM: lane 0 owns the first valid event
-          if (R.lo >= 1) f = tv[1];
-          if (R.lo >= 2) f = tv[2];
-          if (R.lo >= 3) f = tv[3];
+          u64 f = tv[0];  // lo <= SOFF < RM: lane 0 owns the first valid event
+#pragma unroll
+          for (int q = 1; q < SA; ++q)
+            if (R.lo == q) f = tv[q];
           // first valid event and the successor of the last valid one (index hi)
           u64 a;
           {  // warp-uniform index; constant register indices
