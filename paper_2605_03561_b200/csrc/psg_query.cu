@@ -38,6 +38,7 @@
 //                  stored cube (diagnostics.cpp:83-158).
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdint>
 
 #include "psg_internal.h"
@@ -1017,7 +1018,18 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
         if (lane == 31) nf = pnf;
         tv[RM] = nf;
       }
-      if (lim < n_t && (PSG_PIPE_CROSS || lim < E1)) {
+#ifndef PSG_PIPE_UNCOND
+#define PSG_PIPE_UNCOND 1
+#endif
+      if (PSG_PIPE_UNCOND) {
+        // always load (this step again past the trace end: no branch, so the
+        // loaded registers need no copies to join the paths)
+        const bool more = lim < n_t && (PSG_PIPE_CROSS || lim < E1);
+        const u64 nxt = (b + lim) & ~static_cast<u64>(SOFF);
+        const u64 lp = more ? nxt : s_abs;
+        pf_pos = more ? nxt : ~0ull;
+        load_step(p.tr, lp + static_cast<u64>(R.lb), lp, lane, pts, pcx, pnf);
+      } else if (lim < n_t && (PSG_PIPE_CROSS || lim < E1)) {
         pf_pos = (b + lim) & ~static_cast<u64>(SOFF);
         load_step(p.tr, pf_pos + static_cast<u64>(R.lb), pf_pos, lane, pts, pcx, pnf);
       } else {
@@ -1396,6 +1408,13 @@ struct cell_acc {
     ql += q;
     qh += ql < q ? 1ull : 0ull;
   }
+  // a batch's sum, maximum and (non-overflowing) sum of squares
+  __device__ __forceinline__ void add_batch(uint32_t s, uint32_t m, u64 q) {
+    sum += s;
+    mx = max(mx, static_cast<u64>(m));
+    ql += q;
+    qh += ql < q ? 1ull : 0ull;
+  }
 };
 
 template <typename CELL>
@@ -1435,6 +1454,33 @@ __global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__
         CELL a[U], b[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) cell_pair<CELL>::get(incl + s_bo[i + u] + off, a[u], b[u]);
+        if (sizeof(CELL) == 4) {
+          // 32-bit cells: the batch's maxima first; below 2^28 the U sums fit
+          // 32 bits and the U squares 64 bits, so the wide accumulators are
+          // touched once per batch instead of once per cell
+          uint32_t ma = 0, mb = 0;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            ma = max(ma, static_cast<uint32_t>(a[u]));
+            mb = max(mb, static_cast<uint32_t>(b[u]));
+          }
+          static_assert(U <= 16, "U sums of values < 2^28 must fit 32 bits");
+          if (((ma | mb) >> 28) == 0) {
+            uint32_t sa = 0, sb = 0;
+            u64 qa = 0, qb = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t x = static_cast<uint32_t>(a[u]), y = static_cast<uint32_t>(b[u]);
+              sa += x;
+              sb += y;
+              qa += static_cast<u64>(x) * x;
+              qb += static_cast<u64>(y) * y;
+            }
+            A.add_batch(sa, ma, qa);
+            B.add_batch(sb, mb, qb);
+            continue;
+          }
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           A.add32(a[u]);
@@ -1481,11 +1527,33 @@ void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, 
                         unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s) {
   if (n_kept == 0 || K == 0 || nn == 0) return;
   const uint32_t kt = nnp >= 1024 ? 1u : 1024u / nnp;  // ~512 pairs per CTA
-  const uint32_t gx = (K + kt - 1) / kt;
-  uint32_t gy = (8u * 148u + gx - 1) / gx;  // ~8 CTAs per SM in total (2 resident)
-  gy = std::max(1u, std::min(gy, (n_kept + 63) / 64));
-  const uint32_t per_tile = (n_kept + gy - 1) / gy;
-  gy = (n_kept + per_tile - 1) / per_tile;
+  const uint32_t gx = (K + kt - 1) / kt;  // iteration tiles
+  // trace ranges: the CTA count fills whole waves of the resident slots as
+  // closely as possible (a last wave of a few CTAs would leave the GPU idle
+  // for a whole CTA duration)
+  int dev = 0, sms = 148, per_sm = 2;
+  PSG_CUDA(cudaGetDevice(&dev));
+  PSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (cube32)
+    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cross_stats<uint32_t>, 512, 0));
+  else
+    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cross_stats<unsigned long long>, 512, 0));
+  const uint32_t slots = static_cast<uint32_t>(std::max(1, sms * std::max(1, per_sm)));
+  const uint32_t gy_cap = std::max(1u, (n_kept + 63) / 64);  // >= 64 traces per CTA
+  uint32_t gy = 1, per_tile = n_kept;
+  double best = -1.0;
+  for (uint32_t w = 2; w <= 8; ++w) {
+    uint32_t g = std::min(gy_cap, std::max(1u, w * slots / gx));
+    const uint32_t pt = (n_kept + g - 1) / g;
+    g = (n_kept + pt - 1) / pt;
+    const double ctas = static_cast<double>(gx) * g;
+    const double eff = ctas / (std::ceil(ctas / slots) * slots);
+    if (eff > best + 0.01) {
+      best = eff;
+      gy = g;
+      per_tile = pt;
+    }
+  }
   if (cube32)
     k_cross_stats<uint32_t><<<dim3(gx, gy), 512, 0, s>>>(static_cast<const uint32_t*>(incl), kept_bo,
                                                          n_kept, nn, nnp, K, kt, per_tile, x_sum,

@@ -12,7 +12,7 @@ while [ $# -ge 2 ]; do
   o=build/variants/$name; mkdir -p $o
   for f in paper_2605_03561_b200/csrc/*.cu; do
     $NVCC $ARCH -O3 -std=c++17 -Iinclude -Ipaper_2605_03561_b200/csrc -lineinfo -Xcompiler -fPIC \
-      --expt-relaxed-constexpr $defs -c $f -o $o/$(basename $f).o &
+      --expt-relaxed-constexpr -diag-suppress 186 $defs -c $f -o $o/$(basename $f).o &
   done
   g++ -O3 -std=c++17 -Iinclude -Ipaper_2605_03561_b200/csrc -fPIC -I/usr/local/cuda/include $defs \
     -c paper_2605_03561_b200/csrc/psg_store.cpp -o $o/psg_store.cpp.o &
