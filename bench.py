@@ -250,7 +250,15 @@ def main():
                 "kernel": "k_trace_query", "alg_bytes_per_launch": alg_bytes,
                 "cube_cell_bytes": info["cube_cell_bytes"],
                 "kernel_ms": main_s * 1000.0, "kernel_share_of_step": main_s * 1000.0 / (ms / args.steps),
-                "pass1_k_bounds_ms": statistics.mean(bounds_ms)}
+                "pass1_k_bounds_ms": statistics.mean(bounds_ms),
+                "frac_of_nominal_8tbs": achieved / 8000.0}
+    # the whole query step against the same peak: pass 1 reads the ctx words
+    # (4 B per event), pass 2 its algorithmic bytes, k_cross_stats re-reads the
+    # stored cube (k < K; all iterations here)
+    step_bytes = 4 * events_local + alg_bytes + info["cube_store_bytes"]
+    step_s = ms / args.steps / 1000.0
+    roofline["step"] = {"alg_bytes": step_bytes, "achieved": step_bytes / step_s / 1e9,
+                        "frac": step_bytes / step_s / 1e9 / peak}
 
     # end to end through the public API: pinned host trace.db bytes -> HBM ->
     # query -> results back to host, every step.

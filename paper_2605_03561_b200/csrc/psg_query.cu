@@ -1409,7 +1409,7 @@ struct cell_acc {
     qh += ql < q ? 1ull : 0ull;
   }
   // a batch's sum, maximum and (non-overflowing) sum of squares
-  __device__ __forceinline__ void add_batch(uint32_t s, uint32_t m, u64 q) {
+  __device__ __forceinline__ void add_batch(u64 s, uint32_t m, u64 q) {
     sum += s;
     mx = max(mx, static_cast<u64>(m));
     ql += q;
@@ -1455,19 +1455,20 @@ __global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__
 #pragma unroll
         for (int u = 0; u < U; ++u) cell_pair<CELL>::get(incl + s_bo[i + u] + off, a[u], b[u]);
         if (sizeof(CELL) == 4) {
-          // 32-bit cells: the batch's maxima first; below 2^28 the U sums fit
-          // 32 bits and the U squares 64 bits, so the wide accumulators are
-          // touched once per batch instead of once per cell
+          // 32-bit cells: the batch's maxima first; below 2^30 the U squares
+          // fit 64 bits, so the 128-bit accumulators are touched once per
+          // batch instead of once per cell (2^30 ns = 1.07 s: the anchor's
+          // inclusive cells, ~2^28 here, stay on this path with the leaves,
+          // so warps do not diverge over the anchor column)
           uint32_t ma = 0, mb = 0;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             ma = max(ma, static_cast<uint32_t>(a[u]));
             mb = max(mb, static_cast<uint32_t>(b[u]));
           }
-          static_assert(U <= 16, "U sums of values < 2^28 must fit 32 bits");
-          if (((ma | mb) >> 28) == 0) {
-            uint32_t sa = 0, sb = 0;
-            u64 qa = 0, qb = 0;
+          static_assert(U <= 16, "U squares of values < 2^30 must fit 64 bits");
+          if (((ma | mb) >> 30) == 0) {
+            u64 sa = 0, sb = 0, qa = 0, qb = 0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const uint32_t x = static_cast<uint32_t>(a[u]), y = static_cast<uint32_t>(b[u]);
