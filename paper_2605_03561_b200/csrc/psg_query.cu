@@ -75,7 +75,7 @@ typedef unsigned __int128 u128;
 #ifndef PSG_RB
 #define PSG_RB 16
 #endif
-constexpr int RB = PSG_RB;  // events per lane per block step, pass 1 (ctx: RB/4 x 128-bit loads)
+constexpr int RB = PSG_RB;  // events per lane per block step, pass 1 (ctx: RB/8 x 256-bit loads)
 constexpr int RM = PSG_RM;  // events per lane per block step, pass 2 (ts: RM/2, ctx: RM/4 x 128-bit)
 constexpr int STEP_B = 32 * RB;
 constexpr uint32_t GC = PSG_G;  // iterations per chunk of pass 2 (the host passes the same G)
@@ -121,6 +121,13 @@ __device__ __forceinline__ void ldg256(const uint64_t* p, u64& a, u64& b, u64& c
                : "l"(p));
 }
 
+// 32 ctx-word bytes (two uint4) in one LDG.256; p 32-byte aligned
+__device__ __forceinline__ void ldg256x(const uint32_t* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
 __device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_abs, int lane,
                                           ulonglong2 (&ts)[RM / 2], uint4 (&cx)[RM / 4], u64& nf) {
   if (PSG_LD256) {  // r0 is a multiple of 4 events: 32-byte aligned timestamps
@@ -133,10 +140,7 @@ __device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_ab
     for (int q = 0; q < RM / 2; ++q) ts[q] = __ldg(tsrc + q);
   }
   if (PSG_LD256 && SA == 8 && RM == 8) {  // r0 a multiple of 8 events: 32-byte aligned ctx words
-    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(cx[0].x), "=r"(cx[0].y), "=r"(cx[0].z), "=r"(cx[0].w), "=r"(cx[1].x),
-                   "=r"(cx[1].y), "=r"(cx[1].z), "=r"(cx[1].w)
-                 : "l"(tr.ctx + r0));
+    ldg256x(tr.ctx + r0, cx[0], cx[1]);
   } else {
     const uint4* csrc = reinterpret_cast<const uint4*>(tr.ctx + r0);
 #pragma unroll
@@ -221,13 +225,16 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   // software pipeline: the next block step's ctx words are loaded into
   // registers while this one is processed (the arrays carry one block step of
   // slack past the last event)
+  // block steps start on multiples of 8 events: each lane's 16 ctx words are
+  // two 32-byte aligned LDG.256 (whole sectors per instruction)
+  static_assert(RB % 8 == 0, "RB must be a multiple of 8");
   uint4 nxt[RB / 4];
   {
-    const uint4* src = reinterpret_cast<const uint4*>(p.tr.ctx + (b & ~3ull) + static_cast<u64>(lane) * RB);
+    const uint32_t* src = p.tr.ctx + (b & ~7ull) + static_cast<u64>(lane) * RB;
 #pragma unroll
-    for (int q = 0; q < RB / 4; ++q) nxt[q] = __ldg(src + q);
+    for (int q = 0; q < RB / 8; ++q) ldg256x(src + 8 * q, nxt[2 * q], nxt[2 * q + 1]);
   }
-  for (u64 s = b & ~3ull; s < e; s += STEP_B) {
+  for (u64 s = b & ~7ull; s < e; s += STEP_B) {
     const u64 r0 = s + static_cast<u64>(lane) * RB;
 #ifndef PSG_NO_BOUNDS_PREFETCH
     if (lane == 0 && s + 3 * STEP_B <= e)
@@ -242,9 +249,9 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
       cx[4 * q + 3] = nxt[q].w;
     }
     if (s + STEP_B < e) {
-      const uint4* src = reinterpret_cast<const uint4*>(p.tr.ctx + r0 + STEP_B);
+      const uint32_t* src = p.tr.ctx + r0 + STEP_B;
 #pragma unroll
-      for (int q = 0; q < RB / 4; ++q) nxt[q] = __ldg(src + q);
+      for (int q = 0; q < RB / 8; ++q) ldg256x(src + 8 * q, nxt[2 * q], nxt[2 * q + 1]);
     }
     // events of this trace in the lane's run: local indices [lo, hi) of [0, RB)
     const int64_t lo64 = static_cast<int64_t>(b) - static_cast<int64_t>(r0);
