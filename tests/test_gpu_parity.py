@@ -427,3 +427,42 @@ def test_candidates_sharing_a_timestamp(gpu_ctx_factory):
     for _ in range(2):
         g, o = check_cube(ctx, tr, parent, 1)
     assert list(o["iter_counts"][:1]) == [3]
+
+
+@pytest.mark.parametrize("n_kernels", [1, 2, 3, 4, 33, 36])
+def test_flush_tail_columns(gpu_ctx_factory, n_kernels):
+    """Leaf counts whose last group of 32 columns holds 1..4 leaves: the fast
+    flush takes those columns one cell per lane (row sums, within-rank sums)
+    -- cube, savings and CVs still equal the reference."""
+    cfg = scenarios.iterative(6, 21, n_kernels=n_kernels, seed=60 + n_kernels, jitter=0.2)
+    d = ref_db(cfg)
+    tr = oracle.read_trace_db(d)
+    parent = oracle.read_meta(d)["parent"]
+    ctx = gpu_ctx_factory()
+    ctx.set_cct(parent)
+    ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    check_cube(ctx, tr, parent, 1)
+
+
+def test_flush_tail_columns_with_large_cells(gpu_ctx_factory):
+    """Tail leaves with cells >= 2^30 ns (and < 2^32: 32-bit cells): the tail's
+    squares are summed in 128 bits."""
+    parent = np.array([0xFFFFFFFF, 0, 1, 1, 0], np.uint32)
+    ts, cx = [], []
+    t = 1000
+    for it in range(26):
+        ts.append(t); cx.append(1)
+        for k in (2, 3):
+            ts.append(t); cx.append(k)
+            t += (2**30 + 12345 * it + k) if (it + k) % 3 else 777 + it
+        ts.append(t); cx.append(4)
+        t += 5
+        ts.append(t); cx.append(0)
+        t += 3
+    tr = {"ts": np.array(ts, np.uint64), "ctx": np.array(cx, np.uint32),
+          "off": np.array([0, len(ts)], np.uint64), "t_end": np.array([t + 7], np.uint64),
+          "pid": np.array([1], np.uint32)}
+    ctx = gpu_ctx_factory()
+    ctx.set_cct(parent)
+    ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    check_cube(ctx, tr, parent, 1)
