@@ -470,6 +470,13 @@ __device__ __forceinline__ void carry_in(const warp_tables& T, uint32_t c, u64 t
 }
 
 // x^2 accumulated into a 128-bit (hi, lo) pair; one IMAD.WIDE when x < 2^32.
+// a * b + c in one IMAD.WIDE.U32 (64-bit addend)
+__device__ __forceinline__ u64 mad_wide(uint32_t a, uint32_t b, u64 c) {
+  u64 d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
 __device__ __forceinline__ void acc_sq(u64& lo, u64& hi, u64 x) {
   if ((x >> 32) == 0) {
     const u64 q = static_cast<u64>(static_cast<uint32_t>(x)) * static_cast<uint32_t>(x);
@@ -698,23 +705,30 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   const uint32_t nl = nn - 1, tail = nl & 31u;
   const uint32_t n_cols = (tail != 0 && tail <= TW) ? nn - tail : nn;
   for (uint32_t n = 1 + lane; n < n_cols; n += 32) {
-    u64 sx = 0, sq = 0, sqh = 0;
-    uint32_t orv = 0;
+    u64 sq = 0, sqh = 0;
+    uint32_t sx32 = 0, orv = 0;
 #pragma unroll
     for (uint32_t r = 0; r < G; ++r) {
       const uint32_t ex = rows[r * nnp + n];
       rs[r] += ex;
       if (STATS) {
-        sx += ex;
-        sq += static_cast<u64>(ex) * ex;  // G squares fit 64 bits while every cell < 2^30
+        sx32 += ex;  // exact while every cell < 2^29 (G = 8)
+        sq = mad_wide(ex, ex, sq);  // G squares fit 64 bits while every cell < 2^30
         orv |= ex;
       }
     }
+    static_assert(GC <= 8, "32-bit sums of G cells < 2^29");
     if (STATS) {
-      if (orv >> 30) {  // a cell >= 2^30: redo the squares in 128 bits
+      u64 sx = sx32;
+      if (orv >> 29) {  // a cell >= 2^29: redo the sum in 64 bits and the squares in 128
         sq = 0;
+        sx = 0;
 #pragma unroll
-        for (uint32_t r = 0; r < G; ++r) acc_sq(sq, sqh, rows[r * nnp + n]);
+        for (uint32_t r = 0; r < G; ++r) {
+          const uint32_t ex = rows[r * nnp + n];
+          sx += ex;
+          acc_sq(sq, sqh, ex);
+        }
       }
       wsx[n] += sx;
       const u64 l2 = wsqlo[n] + sq;
@@ -1481,8 +1495,8 @@ __global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__
               const uint32_t x = static_cast<uint32_t>(a[u]), y = static_cast<uint32_t>(b[u]);
               sa += x;
               sb += y;
-              qa += static_cast<u64>(x) * x;
-              qb += static_cast<u64>(y) * y;
+              qa = mad_wide(x, x, qa);
+              qb = mad_wide(y, y, qb);
             }
             A.add_batch(sa, ma, qa);
             B.add_batch(sb, mb, qb);
