@@ -606,7 +606,11 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
 }
 
 #ifndef PSG_WMAX
+#if PSG_WARP_CTA
+#define PSG_WMAX 1  // one warp (trace) per CTA of k_trace_query
+#else
 #define PSG_WMAX 16  // warps (traces) per CTA of k_trace_query (<= its launch bound / 32)
+#endif
 #endif
 #ifndef PSG_G
 #define PSG_G 8  // iterations per chunk of k_trace_query (power of two, <= 15)

@@ -214,7 +214,11 @@ struct query_params {
 
 // CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]
 // (int4), then sub_pre, cct_pre, cct_size [n_ctx], then per-warp kept flags.
+#ifndef PSG_WARP_CTA
+#define PSG_WARP_CTA 1  // k_trace_query with one warp (one trace) per CTA, tables read from global
+#endif
 __host__ __device__ inline uint32_t cta_table_bytes(uint32_t n_ctx, uint32_t nn, uint32_t warps) {
+  if (PSG_WARP_CTA) return 0;
   uint32_t b = 16u * nn + 4u * n_ctx * 3 + 4u * warps;
   return (b + 15u) & ~15u;
 }

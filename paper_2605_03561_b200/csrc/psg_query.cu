@@ -62,11 +62,23 @@ typedef unsigned __int128 u128;
 #ifndef PSG_PIPE
 #define PSG_PIPE 1  // register software pipeline of block-step loads in k_trace_query
 #endif
+// k_trace_query launch bounds: one-warp CTAs (PSG_WARP_CTA), 17 resident per
+// SM (96 registers per thread; 17 carve-outs of ~10.6 KB keep the 196 KB
+// shared-memory configuration, so 60 KB of L1 remain for the table reads)
+#if PSG_WARP_CTA
+#ifndef PSG_LB_THREADS
+#define PSG_LB_THREADS 32
+#endif
+#ifndef PSG_LB_MINB
+#define PSG_LB_MINB 17
+#endif
+#else
 #ifndef PSG_LB_THREADS
 #define PSG_LB_THREADS 512
 #endif
 #ifndef PSG_LB_MINB
 #define PSG_LB_MINB 1
+#endif
 #endif
 #ifndef PSG_G
 #define PSG_G 8
@@ -837,15 +849,32 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
 template <bool WIN, bool CUBE>
 __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(query_params p) {
   extern __shared__ __align__(16) uint8_t smem[];
+#if PSG_WARP_CTA
+  // one-warp CTAs: the trace index and everything derived from it are
+  // uniform across the CTA, so they live in uniform registers
+  const int lane = threadIdx.x, warp = 0;
+  constexpr uint32_t CT = 32;  // threads per CTA
+#else
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t CT = blockDim.x;
+#endif
   const uint32_t W = p.warps, n_ctx = p.n_ctx, nn = p.nn;
   constexpr uint32_t G = GC, R2 = 2 * GC;  // p.G == GC (same PSG_G on both sides)
   const bool root_only = p.root_only != 0;
 
+#if PSG_WARP_CTA
+  // read-only tables straight from global memory (L1-cached): the fast path
+  // never reads them, and the carve-out stays small enough for 20 CTAs per SM
+  const int4* s_node = p.node_tab;
+  const int32_t* s_sub_pre = p.sub_pre;
+  const int32_t* s_cct_pre = p.cct_pre;
+  const int32_t* s_cct_size = p.cct_size;
+#else
   int4* s_node = reinterpret_cast<int4*>(smem);
   int32_t* s_sub_pre = reinterpret_cast<int32_t*>(s_node + nn);
   int32_t* s_cct_pre = s_sub_pre + n_ctx;
   int32_t* s_cct_size = s_cct_pre + n_ctx;
+#endif
 
   const warp_smem_layout& L = p.L;
   const uint32_t nnp = L.nnp;
@@ -867,13 +896,17 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   const uint32_t rows_off = wb_off + L.off_rlo;
   const uint32_t row_bytes = 4u * nnp;
 
-  for (uint32_t i = threadIdx.x; i < n_ctx; i += blockDim.x) {
+#if !PSG_WARP_CTA
+  for (uint32_t i = threadIdx.x; i < n_ctx; i += CT) {
     s_sub_pre[i] = CUBE ? p.sub_pre[i] : -1;
     s_cct_pre[i] = WIN ? p.cct_pre[i] : 0;
     s_cct_size[i] = WIN ? p.cct_size[i] : 0;
   }
+#endif
   if (CUBE) {
-    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) s_node[i] = p.node_tab[i];
+#if !PSG_WARP_CTA
+    for (uint32_t i = threadIdx.x; i < nn; i += CT) s_node[i] = p.node_tab[i];
+#endif
     for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rlo[j] = 0;
     if (p.exact_bounds)
       for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rhi[j] = 0;
