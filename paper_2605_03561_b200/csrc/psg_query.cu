@@ -83,6 +83,10 @@ typedef unsigned __int128 u128;
 #ifndef PSG_G
 #define PSG_G 8
 #endif
+#ifndef PSG_FLUSH_UNROLL
+#define PSG_FLUSH_UNROLL 2
+#endif
+constexpr int kFlushUnroll = PSG_FLUSH_UNROLL;
 
 #ifndef PSG_RB
 #define PSG_RB 16
@@ -716,6 +720,7 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   constexpr uint32_t TW = 32 / GC;  // tail columns per pass
   const uint32_t nl = nn - 1, tail = nl & 31u;
   const uint32_t n_cols = (tail != 0 && tail <= TW) ? nn - tail : nn;
+#pragma unroll kFlushUnroll  // two columns per lane at once (latency of the row chains)
   for (uint32_t n = 1 + lane; n < n_cols; n += 32) {
     u64 sq = 0, sqh = 0;
     uint32_t sx32 = 0, orv = 0;
