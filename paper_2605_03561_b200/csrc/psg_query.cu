@@ -253,8 +253,12 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   for (u64 s = b & ~7ull; s < e; s += STEP_B) {
     const u64 r0 = s + static_cast<u64>(lane) * RB;
 #ifndef PSG_NO_BOUNDS_PREFETCH
-    if (lane == 0 && s + 3 * STEP_B <= e)
-      prefetch_l2(p.tr.ctx + s + 2 * STEP_B, 4 * STEP_B);
+#ifndef PSG_B_PF_DIST
+#define PSG_B_PF_DIST 0  // block steps of L2 prefetch run-ahead in pass 1 (0: none;
+                         // with the 256-bit loads it no longer pays: 3.07 vs 3.04 ms)
+#endif
+    if (PSG_B_PF_DIST > 0 && lane == 0 && s + (PSG_B_PF_DIST + 1) * STEP_B <= e)
+      prefetch_l2(p.tr.ctx + s + PSG_B_PF_DIST * STEP_B, 4 * STEP_B);
 #endif
     uint32_t cx[RB];
 #pragma unroll
