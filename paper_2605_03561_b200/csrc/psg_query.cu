@@ -855,8 +855,14 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   __syncwarp();
 }
 
-template <bool WIN, bool CUBE>
-__global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(query_params p) {
+// EXACT: pass 1 ran in the exact mode (p.exact_bounds): boundary timestamps
+// are known and chunks may need 64-bit cells.  The optimistic instantiation
+// runs 32-bit throughout and carries none of the 64-bit cell code (a third
+// smaller, which the instruction cache notices).
+template <bool WIN, bool CUBE, bool EXACT>
+// (the optimistic cube-only instantiation spills at 96 registers: 16 CTAs per SM, 128)
+__global__ void __launch_bounds__(PSG_LB_THREADS, (PSG_WARP_CTA && !WIN && !EXACT) ? 16 : PSG_LB_MINB)
+    k_trace_query(query_params p) {
   extern __shared__ __align__(16) uint8_t smem[];
 #if PSG_WARP_CTA
   // one-warp CTAs: the trace index and everything derived from it are
@@ -963,7 +969,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   // (exact while iterations span < 2^32 ns), each boundary's timestamp is
   // written out as its event is processed, and k_verify_bounds checks the
   // optimistic assumptions afterwards.
-  const bool optimistic = !p.exact_bounds;
+  constexpr bool optimistic = !EXACT;  // == !p.exact_bounds (launch_variant)
   uint64_t* bts_out = optimistic ? p.bts + region : nullptr;
   if (CUBE && kept && lane <= static_cast<int>(2 * G)) {
     const bool have = static_cast<uint32_t>(lane) < nbd;
@@ -1028,7 +1034,7 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
       E2 = bwin[R2] - SOFF;
       // iteration spans of the ring (and the gap in chunk 0) decide 32- vs
       // 64-bit cells (exact mode; the optimistic mode runs 32-bit throughout)
-      if (!optimistic) {
+      if (EXACT) {
         bool w = lane < static_cast<int>(R2) && bts[lane + 1] - bts[lane] >= kSpan32;
         if (c == 0 && lane == 0 && n_t) w = w || bts[0] - ldg64(p.tr.ts + b) >= kSpan32;
         cwide = __any_sync(FULL, w);
@@ -1411,17 +1417,17 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, PSG_LB_MINB) k_trace_query(que
   }
 }
 
-template <bool WIN, bool CUBE>
+template <bool WIN, bool CUBE, bool EXACT>
 void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
   static int configured_bytes = 0;
   if (static_cast<int>(smem_bytes) > configured_bytes) {
-    PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE>,
+    PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem_bytes)));
     configured_bytes = static_cast<int>(smem_bytes);
   }
   const unsigned blocks = (p.tr.n + p.warps - 1) / p.warps;
-  k_trace_query<WIN, CUBE><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
+  k_trace_query<WIN, CUBE, EXACT><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
 }
 
 }  // namespace
@@ -1429,12 +1435,13 @@ void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) 
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
   if (p.tr.n == 0) return;
   if (p.G != GC) fail(PS_E_INTERNAL, "chunk size mismatch between host and kernel (PSG_G)");
+  const bool exact = p.do_cube && p.exact_bounds;
   if (p.do_window && p.do_cube)
-    launch_variant<true, true>(p, smem_bytes, s);
+    exact ? launch_variant<true, true, true>(p, smem_bytes, s) : launch_variant<true, true, false>(p, smem_bytes, s);
   else if (p.do_window)
-    launch_variant<true, false>(p, smem_bytes, s);
+    launch_variant<true, false, false>(p, smem_bytes, s);
   else
-    launch_variant<false, true>(p, smem_bytes, s);
+    exact ? launch_variant<false, true, true>(p, smem_bytes, s) : launch_variant<false, true, false>(p, smem_bytes, s);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
