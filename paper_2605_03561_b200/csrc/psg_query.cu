@@ -227,11 +227,7 @@ __global__ void __launch_bounds__(256) k_bounds(bound_params p) {
   if (t >= p.tr.n) return;
   const u64 b = p.tr.off[t], e = p.tr.off[t + 1];
   const u64 cap = p.cap_off[t + 1] - p.cap_off[t];
-#ifdef PSG_BOUNDS_FAKE_TS  // A/B only: candidate timestamps = event indices (no ts loads)
-#define BTS(i) static_cast<u64>(i)
-#else
 #define BTS(i) ldg64(p.tr.ts + (i))
-#endif
   uint32_t* out = p.bidx + p.cap_off[t];
   uint64_t* out_ts = p.bts + p.cap_off[t];
   uint32_t prev_in = 0;  // containment of the event before the block step
@@ -705,14 +701,6 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   constexpr uint32_t G = GC;
   const uint4* src = reinterpret_cast<const uint4*>(rows);
   const uint32_t nq = G * nnp / 4;
-#ifdef PSG_AB_NO_FLUSH  // A/B timing experiment only (wrong results): zero the rows, nothing else
-  {
-    __syncwarp();
-    uint4* z = reinterpret_cast<uint4*>(rows);
-    for (uint32_t i = lane; i < nq; i += 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
-    return;
-  }
-#endif
   uint32_t rs[GC];
 #pragma unroll
   for (uint32_t r = 0; r < G; ++r) rs[r] = 0u;
@@ -1237,12 +1225,10 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, (PSG_WARP_CTA && !WIN && !EXAC
           st.rowb = st.slot * nnp;
           st.cube_ok = st.k < R.iters;
         }
-#ifndef PSG_AB_NO_SLOW  // A/B timing experiment only (wrong results): no general block path
         if (cwide)
           run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
         else
           run_block<WIN, CUBE, false>(wm, tv, cv, R, st, T);
-#endif
       }
       pos = lim;
     }
