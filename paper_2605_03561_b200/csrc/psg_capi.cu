@@ -606,12 +606,12 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
 }
 
 #ifndef PSG_WMAX
-#if PSG_WARP_CTA
-#define PSG_WMAX 1  // one warp (trace) per CTA of k_trace_query
-#else
-#define PSG_WMAX 16  // warps (traces) per CTA of k_trace_query (<= its launch bound / 32)
+#define PSG_WMAX 16  // warps (traces) per CTA of k_trace_query's wide shape (<= its launch bound / 32)
 #endif
+#ifndef PSG_ONE_WARP_MIN_EVENTS
+#define PSG_ONE_WARP_MIN_EVENTS 40000  // average events per trace from which one-warp CTAs are used (measured crossover 33.5k-50k)
 #endif
+static constexpr uint64_t kOneWarpMinEvents = PSG_ONE_WARP_MIN_EVENTS;
 #ifndef PSG_G
 #define PSG_G 8  // iterations per chunk of k_trace_query (power of two, <= 15)
 #endif
@@ -1433,10 +1433,21 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     // launch geometry
     warp_smem_layout L;
     L.init(c->n_ctx, nn, p.G, do_cube && exact_bounds);
-    uint32_t W = choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16));
+    // CTA shape: one warp per CTA for long traces (17 resident per SM, no
+    // CTA tail), 16-warp CTAs for short ones (their per-trace prologue and
+    // epilogue run better in warps that start together); PSG_CTA_SHAPE=one|wide
+    // overrides (A/B)
+    bool one = c->n_events >= kOneWarpMinEvents * static_cast<uint64_t>(n);
+    if (const char* e = std::getenv("PSG_CTA_SHAPE")) {
+      if (!std::strcmp(e, "one")) one = true;
+      if (!std::strcmp(e, "wide")) one = false;
+    }
+    uint32_t W = one ? choose_warps(1, L.bytes, 0) : choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false));
+    if (one) W = 1;
+    p.one_warp = one ? 1u : 0u;
     p.warps = W;
     p.L = L;
-    p.cta_bytes = cta_table_bytes(c->n_ctx, nn, W);
+    p.cta_bytes = cta_table_bytes(c->n_ctx, nn, W, one);
     uint32_t smem = p.cta_bytes + W * L.bytes;
     PSG_CUDA(cudaEventRecord(c->ev[1], s));
     launch_trace_query(p, smem, s);

@@ -210,15 +210,15 @@ struct query_params {
   uint32_t warps;      // traces per CTA
   warp_smem_layout L;  // per-warp shared-memory carve-out (computed on the host)
   uint32_t cta_bytes;  // cta_table_bytes(n_ctx, nn, warps), computed on the host
+  uint32_t one_warp;   // CTA shape: one warp per CTA (long traces) or up to 16
 };
 
 // CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]
 // (int4), then sub_pre, cct_pre, cct_size [n_ctx], then per-warp kept flags.
-#ifndef PSG_WARP_CTA
-#define PSG_WARP_CTA 1  // k_trace_query with one warp (one trace) per CTA, tables read from global
-#endif
-__host__ __device__ inline uint32_t cta_table_bytes(uint32_t n_ctx, uint32_t nn, uint32_t warps) {
-  if (PSG_WARP_CTA) return 0;
+// One-warp CTAs read the tables from global memory instead (no CTA tables).
+__host__ __device__ inline uint32_t cta_table_bytes(uint32_t n_ctx, uint32_t nn, uint32_t warps,
+                                                   bool one_warp) {
+  if (one_warp) return 0;
   uint32_t b = 16u * nn + 4u * n_ctx * 3 + 4u * warps;
   return (b + 15u) & ~15u;
 }

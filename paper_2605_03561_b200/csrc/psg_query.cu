@@ -62,23 +62,14 @@ typedef unsigned __int128 u128;
 #ifndef PSG_PIPE
 #define PSG_PIPE 1  // register software pipeline of block-step loads in k_trace_query
 #endif
-// k_trace_query launch bounds: one-warp CTAs (PSG_WARP_CTA), 17 resident per
-// SM (96 registers per thread; 17 carve-outs of ~10.6 KB keep the 196 KB
-// shared-memory configuration, so 60 KB of L1 remain for the table reads)
-#if PSG_WARP_CTA
-#ifndef PSG_LB_THREADS
-#define PSG_LB_THREADS 32
-#endif
-#ifndef PSG_LB_MINB
-#define PSG_LB_MINB 17
-#endif
-#else
-#ifndef PSG_LB_THREADS
-#define PSG_LB_THREADS 512
-#endif
-#ifndef PSG_LB_MINB
-#define PSG_LB_MINB 1
-#endif
+// k_trace_query CTA shapes (query_params::one_warp, chosen per query on the
+// host): one-warp CTAs, 17 resident per SM (96 registers per thread; 17
+// carve-outs of ~10.6 KB keep the 196 KB shared-memory configuration, so
+// 60 KB of L1 remain for the table reads) for long traces; 16-warp CTAs with
+// the tables in shared memory for short ones (warps of a CTA start together:
+// fewer instruction-cache misses in the per-trace prologue and epilogue).
+#ifndef PSG_ONE_MINB
+#define PSG_ONE_MINB 17
 #endif
 #ifndef PSG_G
 #define PSG_G 8
@@ -847,37 +838,32 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
 // are known and chunks may need 64-bit cells.  The optimistic instantiation
 // runs 32-bit throughout and carries none of the 64-bit cell code (a third
 // smaller, which the instruction cache notices).
-template <bool WIN, bool CUBE, bool EXACT>
-// (the optimistic cube-only instantiation spills at 96 registers: 16 CTAs per SM, 128)
-__global__ void __launch_bounds__(PSG_LB_THREADS, (PSG_WARP_CTA && !WIN && !EXACT) ? 16 : PSG_LB_MINB)
+// ONE: one warp per CTA (else up to 16).
+// (the optimistic cube-only one-warp instantiation spills at 96 registers: 16 CTAs per SM, 128)
+template <bool WIN, bool CUBE, bool EXACT, bool ONE>
+__global__ void __launch_bounds__(ONE ? 32 : 512, ONE ? ((!WIN && !EXACT) ? 16 : PSG_ONE_MINB) : 1)
     k_trace_query(query_params p) {
   extern __shared__ __align__(16) uint8_t smem[];
-#if PSG_WARP_CTA
   // one-warp CTAs: the trace index and everything derived from it are
   // uniform across the CTA, so they live in uniform registers
-  const int lane = threadIdx.x, warp = 0;
-  constexpr uint32_t CT = 32;  // threads per CTA
-#else
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t CT = blockDim.x;
-#endif
+  const int lane = ONE ? static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x & 31);
+  const int warp = ONE ? 0 : static_cast<int>(threadIdx.x >> 5);
+  const uint32_t CT = ONE ? 32u : blockDim.x;  // threads per CTA
   const uint32_t W = p.warps, n_ctx = p.n_ctx, nn = p.nn;
   constexpr uint32_t G = GC, R2 = 2 * GC;  // p.G == GC (same PSG_G on both sides)
   const bool root_only = p.root_only != 0;
 
-#if PSG_WARP_CTA
-  // read-only tables straight from global memory (L1-cached): the fast path
-  // never reads them, and the carve-out stays small enough for 20 CTAs per SM
-  const int4* s_node = p.node_tab;
-  const int32_t* s_sub_pre = p.sub_pre;
-  const int32_t* s_cct_pre = p.cct_pre;
-  const int32_t* s_cct_size = p.cct_size;
-#else
-  int4* s_node = reinterpret_cast<int4*>(smem);
-  int32_t* s_sub_pre = reinterpret_cast<int32_t*>(s_node + nn);
-  int32_t* s_cct_pre = s_sub_pre + n_ctx;
-  int32_t* s_cct_size = s_cct_pre + n_ctx;
-#endif
+  // one-warp CTAs read the tables straight from global memory (L1-cached: the
+  // fast path never reads them, and the carve-out stays small); wider CTAs
+  // share one copy in shared memory
+  int4* t_node = reinterpret_cast<int4*>(smem);
+  int32_t* t_sub_pre = reinterpret_cast<int32_t*>(t_node + nn);
+  int32_t* t_cct_pre = t_sub_pre + n_ctx;
+  int32_t* t_cct_size = t_cct_pre + n_ctx;
+  const int4* s_node = ONE ? p.node_tab : t_node;
+  const int32_t* s_sub_pre = ONE ? p.sub_pre : t_sub_pre;
+  const int32_t* s_cct_pre = ONE ? p.cct_pre : t_cct_pre;
+  const int32_t* s_cct_size = ONE ? p.cct_size : t_cct_size;
 
   const warp_smem_layout& L = p.L;
   const uint32_t nnp = L.nnp;
@@ -899,17 +885,15 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, (PSG_WARP_CTA && !WIN && !EXAC
   const uint32_t rows_off = wb_off + L.off_rlo;
   const uint32_t row_bytes = 4u * nnp;
 
-#if !PSG_WARP_CTA
-  for (uint32_t i = threadIdx.x; i < n_ctx; i += CT) {
-    s_sub_pre[i] = CUBE ? p.sub_pre[i] : -1;
-    s_cct_pre[i] = WIN ? p.cct_pre[i] : 0;
-    s_cct_size[i] = WIN ? p.cct_size[i] : 0;
-  }
-#endif
+  if (!ONE)
+    for (uint32_t i = threadIdx.x; i < n_ctx; i += CT) {
+      t_sub_pre[i] = CUBE ? p.sub_pre[i] : -1;
+      t_cct_pre[i] = WIN ? p.cct_pre[i] : 0;
+      t_cct_size[i] = WIN ? p.cct_size[i] : 0;
+    }
   if (CUBE) {
-#if !PSG_WARP_CTA
-    for (uint32_t i = threadIdx.x; i < nn; i += CT) s_node[i] = p.node_tab[i];
-#endif
+    if (!ONE)
+      for (uint32_t i = threadIdx.x; i < nn; i += CT) t_node[i] = p.node_tab[i];
     for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rlo[j] = 0;
     if (p.exact_bounds)
       for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rhi[j] = 0;
@@ -1403,17 +1387,28 @@ __global__ void __launch_bounds__(PSG_LB_THREADS, (PSG_WARP_CTA && !WIN && !EXAC
   }
 }
 
-template <bool WIN, bool CUBE, bool EXACT>
-void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
+template <bool WIN, bool CUBE, bool EXACT, bool ONE>
+void launch_shape(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
   static int configured_bytes = 0;
   if (static_cast<int>(smem_bytes) > configured_bytes) {
-    PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT>,
+    PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT, ONE>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem_bytes)));
     configured_bytes = static_cast<int>(smem_bytes);
   }
   const unsigned blocks = (p.tr.n + p.warps - 1) / p.warps;
-  k_trace_query<WIN, CUBE, EXACT><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
+  k_trace_query<WIN, CUBE, EXACT, ONE><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
+}
+
+template <bool WIN, bool CUBE, bool EXACT>
+void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
+  if (p.one_warp) {
+    if (p.warps != 1) fail(PS_E_INTERNAL, "one-warp CTA shape with warps != 1");
+    launch_shape<WIN, CUBE, EXACT, true>(p, smem_bytes, s);
+  } else {
+    if (p.warps > 16) fail(PS_E_INTERNAL, "more than 16 warps per CTA");
+    launch_shape<WIN, CUBE, EXACT, false>(p, smem_bytes, s);
+  }
 }
 
 }  // namespace

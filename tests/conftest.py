@@ -24,3 +24,18 @@ def gpu_ctx_factory():
     yield make
     for c in made:
         c.close()
+
+
+def pytest_generate_tests(metafunc):
+    # every GPU test runs under both CTA shapes of the fused kernel (one warp
+    # per CTA, the long-trace shape; 16-warp CTAs, the short-trace shape): the
+    # shape follows the average trace length, which the test inputs do not span
+    if metafunc.definition.get_closest_marker("gpu") is not None:
+        metafunc.fixturenames.append("cta_shape")
+        metafunc.parametrize("cta_shape", ["one", "wide"], indirect=True)
+
+
+@pytest.fixture
+def cta_shape(request, monkeypatch):
+    monkeypatch.setenv("PSG_CTA_SHAPE", request.param)
+    return request.param
