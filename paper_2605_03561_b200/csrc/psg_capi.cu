@@ -1438,6 +1438,13 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     // epilogue run better in warps that start together); PSG_CTA_SHAPE=one|wide
     // overrides (A/B)
     bool one = c->n_events >= kOneWarpMinEvents * static_cast<uint64_t>(n);
+    {  // few traces: 16-warp CTAs (one per SM) would leave a part-filled last wave
+      int dev = 0, sms = 148;
+      PSG_CUDA(cudaGetDevice(&dev));
+      PSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const double ctas = std::ceil(n / 16.0), waves = std::ceil(ctas / sms);
+      if (ctas / (waves * sms) < 0.9) one = true;
+    }
     if (const char* e = std::getenv("PSG_CTA_SHAPE")) {
       if (!std::strcmp(e, "one")) one = true;
       if (!std::strcmp(e, "wide")) one = false;
