@@ -68,6 +68,12 @@ typedef unsigned __int128 u128;
 // 60 KB of L1 remain for the table reads) for long traces; 16-warp CTAs with
 // the tables in shared memory for short ones (warps of a CTA start together:
 // fewer instruction-cache misses in the per-trace prologue and epilogue).
+#ifndef PSG_WIDE_THREADS
+#define PSG_WIDE_THREADS 512  // launch bound of the wide shape (PSG_WMAX warps per CTA)
+#endif
+#ifndef PSG_WIDE_MINB
+#define PSG_WIDE_MINB 1
+#endif
 #ifndef PSG_ONE_MINB
 #define PSG_ONE_MINB 17
 #endif
@@ -841,7 +847,7 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
 // ONE: one warp per CTA (else up to 16).
 // (the optimistic cube-only one-warp instantiation spills at 96 registers: 16 CTAs per SM, 128)
 template <bool WIN, bool CUBE, bool EXACT, bool ONE>
-__global__ void __launch_bounds__(ONE ? 32 : 512, ONE ? ((!WIN && !EXACT) ? 16 : PSG_ONE_MINB) : 1)
+__global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !EXACT) ? 16 : PSG_ONE_MINB) : PSG_WIDE_MINB)
     k_trace_query(query_params p) {
   extern __shared__ __align__(16) uint8_t smem[];
   // one-warp CTAs: the trace index and everything derived from it are
@@ -1406,7 +1412,7 @@ void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) 
     if (p.warps != 1) fail(PS_E_INTERNAL, "one-warp CTA shape with warps != 1");
     launch_shape<WIN, CUBE, EXACT, true>(p, smem_bytes, s);
   } else {
-    if (p.warps > 16) fail(PS_E_INTERNAL, "more than 16 warps per CTA");
+    if (p.warps * 32 > PSG_WIDE_THREADS) fail(PS_E_INTERNAL, "more warps per CTA than the launch bound");
     launch_shape<WIN, CUBE, EXACT, false>(p, smem_bytes, s);
   }
 }
