@@ -68,6 +68,9 @@ typedef unsigned __int128 u128;
 // 60 KB of L1 remain for the table reads) for long traces; 16-warp CTAs with
 // the tables in shared memory for short ones (warps of a CTA start together:
 // fewer instruction-cache misses in the per-trace prologue and epilogue).
+#ifndef PSG_B_MINB
+#define PSG_B_MINB 1  // k_bounds: resident 256-thread CTAs per SM the registers must allow
+#endif
 #ifndef PSG_WIDE_THREADS
 #define PSG_WIDE_THREADS 512  // launch bound of the wide shape (PSG_WMAX warps per CTA)
 #endif
@@ -212,7 +215,7 @@ __device__ __forceinline__ void warp_prefix(const u64* src, u64* dst, uint32_t n
 // boundary's timestamp from its own stream, flags that case, and the host
 // re-runs both passes with EXACT = true.
 template <bool SMALL, bool EXACT>  // SMALL: <= 128 contexts, membership bits live in registers
-__global__ void __launch_bounds__(256) k_bounds(bound_params p) {
+__global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
   extern __shared__ uint32_t s_bits[];
   for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) s_bits[i] = p.contains[i];
   auto word = [&](uint32_t w) -> u64 { return w < p.words ? static_cast<u64>(p.contains[w]) : 0ull; };
