@@ -71,6 +71,9 @@ typedef unsigned __int128 u128;
 #ifndef PSG_B_MINB
 #define PSG_B_MINB 1  // k_bounds: resident 256-thread CTAs per SM the registers must allow
 #endif
+#ifndef PSG_X_U
+#define PSG_X_U 16  // k_cross_stats: 32-bit cell pairs in flight per thread (the batch size)
+#endif
 #ifndef PSG_WIDE_THREADS
 #define PSG_WIDE_THREADS 512  // launch bound of the wide shape (PSG_WMAX warps per CTA)
 #endif
@@ -1490,7 +1493,7 @@ __global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__
                                                         unsigned long long* x_sq) {
   // The tile's trace block offsets are staged in shared memory in batches and
   // read as broadcasts; U independent pair loads are in flight per thread.
-  constexpr int U = sizeof(CELL) == 4 ? 16 : 8;
+  constexpr int U = sizeof(CELL) == 4 ? PSG_X_U : 8;
   constexpr uint32_t TB = 512;
   __shared__ u64 s_bo[TB];
   const uint32_t k0 = blockIdx.x * kt;
