@@ -223,10 +223,18 @@ ps_status psg_get_stats(psg_context* ctx, double total_time_s, uint32_t* leaves,
 /* Outliers: per site balance ratio [n_sites]; node means [n_nodes] (s);
  * node z-scores; selected node ids [n_outliers] (value desc, id asc); topology
  * rows [n_racks][3] = rack, affected nodes, n_chassis and chassis masks per
- * rack: affected [n_racks], fully affected [n_racks] (bit c = chassis c). */
+ * rack: affected [n_racks], fully affected [n_racks] (bit c = chassis c).
+ * Outlier queries raise PS_E_PARSE when a hostname of the node universe read
+ * from a database is not a Slingshot name (topology.cpp:14-46). */
 ps_status psg_get_outliers(psg_context* ctx, double* site_ratio, double* node_mean, double* node_z,
                            uint32_t* selected, uint32_t* rack_rows, uint64_t* chassis_mask,
                            uint64_t* full_mask);
+
+/* localize_outliers' rows (topology.cpp:54-92) for any chassis ids: one row
+ * [rack, chassis, outlier nodes, fully affected 0/1] per affected (rack,
+ * chassis), ascending.  Call with rows = NULL for *n_rows first.  (The masks of
+ * psg_get_outliers have bit c = chassis c and need chassis ids < 64.) */
+ps_status psg_get_topology(psg_context* ctx, uint32_t* n_rows, uint32_t* rows);
 
 /* ingest::ingest_traces (ingest.cpp:178-208) on the device: the events with
  * t0 <= ts < t1 of every loaded trace in load order, as SoA rows, plus the

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "core/common.hpp"
@@ -43,7 +44,24 @@ errc errc_of(ps_status s) {
 }
 
 void check(ps_status s) {
-  if (s != PS_OK) raise(errc_of(s), std::string("psg: ") + psg_last_error());
+  if (s == PS_OK) return;
+  const std::string msg = psg_last_error();
+  errc e = errc_of(s);
+  // ps_status folds several errc into one; the library's message names the
+  // reference condition where the C++ caller can tell them apart
+  if (s == PS_E_INVALID_ARGUMENT && msg.find("trace has no events") != std::string::npos)
+    e = errc::empty_input;  // suggest_anchor on an empty trace (itermodel.cpp:48)
+  raise(e, "psg: " + msg);
+}
+
+// Identity of a database's on-disk files: a reopened or replaced database at
+// the same path (or a new handle at a reused address) is a different key.
+std::string db_key(const store::db_handle& h, const char* file) {
+  struct stat st{};
+  const std::filesystem::path p = h.path() / file;
+  if (::stat(p.c_str(), &st) != 0) return p.string();
+  return p.string() + "|" + std::to_string(st.st_size) + "|" + std::to_string(st.st_mtim.tv_sec) +
+         "." + std::to_string(st.st_mtim.tv_nsec) + "|" + std::to_string(st.st_ino);
 }
 
 std::vector<uint32_t> sorted_unique(std::vector<uint32_t> v) {
@@ -89,7 +107,9 @@ device::~device() { psg_close(ctx_); }
 
 void device::bind(const store::db_handle& h, std::vector<uint32_t> profile_ids) {
   profile_ids = sorted_unique(std::move(profile_ids));
-  if (bound_ == &h && profile_ids == pids_) return;
+  const std::string key = db_key(h, "trace.db") + "|" + db_key(h, "meta.bin");
+  if (key == bound_key_ && profile_ids == pids_) return;
+  bound_key_.clear();
   std::vector<const store::trace_index_entry*> sel;
   sel.reserve(profile_ids.size());
   for (uint32_t id : profile_ids) {
@@ -133,20 +153,23 @@ void device::bind(const store::db_handle& h, std::vector<uint32_t> profile_ids) 
   }
   check(psg_load_traces_aos(ctx_, body, n_ev, off.data(), pid.data(), t_end.data(),
                             static_cast<uint32_t>(pid.size())));
-  bound_ = &h;
+  bound_key_ = key;
   pids_ = std::move(profile_ids);
 }
 
 void device::bind_profiles(const store::db_handle& h) {
-  if (bound_profiles_ == &h) return;
+  const std::string key = db_key(h, "profile.db") + "|" + db_key(h, "meta.bin");
+  if (key == bound_profiles_key_) return;
+  bound_profiles_key_.clear();
   check(psg_load_profile_db(ctx_, (h.path()).c_str()));
-  bound_profiles_ = &h;
+  bound_profiles_key_ = key;
 }
 
 ingest::slice_table ingest_profiles(const store::db_handle& h, std::vector<uint32_t> profile_ids,
                                     const ingest::keep_set& keep,
                                     const std::vector<uint16_t>& metric_ids, unsigned /*jobs*/) {
-  device& d = default_device();
+  device_lease lease = acquire_device();
+  device& d = lease.dev;
   d.bind_profiles(h);
   const bool all_ctx = keep.size() == h.meta().contexts.size();
   uint64_t n = 0;
@@ -169,10 +192,21 @@ ingest::slice_table ingest_profiles(const store::db_handle& h, std::vector<uint3
   return out;
 }
 
+namespace {
+std::mutex g_device_mu;
+std::unique_ptr<device> g_device;
+}  // namespace
+
 device& default_device() {
-  thread_local std::unique_ptr<device> d;
-  if (!d) d = std::make_unique<device>(0);
-  return *d;
+  std::lock_guard<std::mutex> lk(g_device_mu);
+  if (!g_device) g_device = std::make_unique<device>(0);
+  return *g_device;
+}
+
+device_lease acquire_device() {
+  std::unique_lock<std::mutex> lk(g_device_mu);
+  if (!g_device) g_device = std::make_unique<device>(0);
+  return device_lease{std::move(lk), *g_device};
 }
 
 ingest::trace_ingest_result ingest_traces(const store::db_handle& h,
@@ -182,7 +216,8 @@ ingest::trace_ingest_result ingest_traces(const store::db_handle& h,
   ingest::trace_ingest_result out;
   profile_ids = sorted_unique(std::move(profile_ids));
   if (profile_ids.empty()) return out;
-  device& d = default_device();
+  device_lease lease = acquire_device();
+  device& d = lease.dev;
   d.bind(h, profile_ids);
   uint64_t n = 0;
   check(psg_window_rows(d.ctx(), t0_ns, t1_ns, &n, nullptr, nullptr, nullptr));
@@ -210,7 +245,8 @@ frame::table window_aggregate(const store::db_handle& h, std::vector<uint32_t> p
   std::vector<int64_t> sum, mn, mx;
   std::vector<double> mean;
   if (!profile_ids.empty()) {
-    device& d = default_device();
+    device_lease lease = acquire_device();
+    device& d = lease.dev;
     d.bind(h, profile_ids);
     psg_query_spec q{};
     q.flags = PSG_Q_WINDOW;
@@ -259,13 +295,15 @@ struct cube_run {
   std::vector<uint32_t> pids;
 };
 
-cube_run run_cube(const store::db_handle& h, const std::vector<uint32_t>& profile_ids,
+// One cube query on the bound device (the caller holds the device lease).
+// anchor = PSG_ANCHOR_AUTO runs suggest_anchor on the device on the first
+// requested trace (itermodel.cpp:253-255); info.anchor is the one used.
+cube_run run_cube(device& d, const store::db_handle& h, const std::vector<uint32_t>& profile_ids,
                   uint32_t anchor, bool stats) {
   cube_run r;
   r.pids = sorted_unique(profile_ids);
-  if (anchor >= h.meta().contexts.size())  // itermodel.cpp:258-260
+  if (anchor != PSG_ANCHOR_AUTO && anchor >= h.meta().contexts.size())  // itermodel.cpp:258-260
     raise(errc::not_found, "anchor ctx " + std::to_string(anchor) + " not in tree");
-  device& d = default_device();
   d.bind(h, r.pids);
   psg_query_spec q{};
   q.flags = static_cast<uint32_t>(PSG_Q_CUBE) | (stats ? static_cast<uint32_t>(PSG_Q_STATS) : 0u);
@@ -282,14 +320,10 @@ itermodel::tri_model build_tri_model(const store::db_handle& h,
   if (profile_ids.empty()) raise(errc::invalid_argument, "no traces requested");
   const std::vector<uint32_t> pids = sorted_unique(profile_ids);
   itermodel::tri_model model;
-  if (policy.automatic) {  // itermodel.cpp:253-255: the first requested trace only
-    auto [events, t_end] = h.read_trace_full(pids.front());
-    model.anchor_ctx = itermodel::suggest_anchor(events, t_end, h.meta());
-  } else {
-    model.anchor_ctx = policy.ctx;
-  }
-  cube_run r = run_cube(h, pids, model.anchor_ctx, false);
-  device& d = default_device();
+  device_lease lease = acquire_device();
+  device& d = lease.dev;
+  cube_run r = run_cube(d, h, pids, policy.automatic ? PSG_ANCHOR_AUTO : policy.ctx, false);
+  model.anchor_ctx = r.info.anchor;
   const psg_query_info& info = r.info;
   const size_t n = pids.size(), nn = info.n_nodes, kept = info.n_kept;
   model.node_ids.resize(nn);
@@ -319,8 +353,9 @@ iteration_diagnostics iteration_report(const store::db_handle& h,
   if (profile_ids.empty()) raise(errc::invalid_argument, "no traces requested");
   if (!(total_time_s > 0.0))  // diagnostics.cpp:124-125
     raise(errc::invalid_total, "total time must be positive");
-  cube_run r = run_cube(h, profile_ids, anchor_ctx, true);
-  device& d = default_device();
+  device_lease lease = acquire_device();
+  device& d = lease.dev;
+  cube_run r = run_cube(d, h, profile_ids, anchor_ctx, true);
   if (r.info.n_kept_global == 0 || r.info.min_iterations == 0)
     raise(errc::insufficient_data, "model has no iterations");
   const uint32_t nl = r.info.n_leaves;

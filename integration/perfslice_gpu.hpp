@@ -16,6 +16,8 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
+#include <string>
 #include <optional>
 #include <vector>
 
@@ -49,13 +51,23 @@ class device {
 
  private:
   psg_context* ctx_ = nullptr;
-  const store::db_handle* bound_ = nullptr;
-  const store::db_handle* bound_profiles_ = nullptr;
+  // what is resident: database identity (path, size, mtime, inode of its
+  // files) + profile ids; empty = nothing
+  std::string bound_key_, bound_profiles_key_;
   std::vector<uint32_t> pids_;
 };
 
-// The calling thread's device (CUDA device 0), created on first use.
+// The process-wide device (CUDA device 0), created on first use and shared by
+// every calling thread, so a trace set is resident once (the reference's
+// db_handle is shared by concurrent readers).
 device& default_device();
+// The same device with its lock held: the drop-in functions below take it for
+// the whole call, so concurrent callers serialise on the GPU context.
+struct device_lease {
+  std::unique_lock<std::mutex> lock;
+  device& dev;
+};
+device_lease acquire_device();
 
 // ingest::ingest_traces (ingest.hpp:105-108, ingest.cpp:178-208).  `jobs` is
 // accepted for signature compatibility and ignored.
@@ -79,8 +91,9 @@ ingest::slice_table ingest_profiles(const store::db_handle& h, std::vector<uint3
                                     const std::vector<uint16_t>& metric_ids, unsigned jobs);
 
 // itermodel::build_tri_model (itermodel.hpp:118-120, itermodel.cpp:242-360).
-// An automatic anchor is chosen by the reference's suggest_anchor on the first
-// requested trace exactly as the reference does (itermodel.cpp:253-255).
+// An automatic anchor is chosen on the device (psg_query with
+// PSG_ANCHOR_AUTO: suggest_anchor's entry walk, gap CV and covered-time pick
+// on the first requested trace, itermodel.cpp:45-109, 253-255).
 itermodel::tri_model build_tri_model(const store::db_handle& h,
                                      const std::vector<uint32_t>& profile_ids,
                                      itermodel::anchor_policy policy, unsigned jobs);

@@ -267,6 +267,21 @@ def ref_congestion_report(db: str, glob: str = "MPI_*", method: str = "dbscan", 
     return _take(p)
 
 
+def ref_localize(outliers, universe) -> dict:
+    """topology::localize_outliers (topology.cpp:54-92) as its JSON report;
+    raises RuntimeError with the reference's parse_error message on a bad name."""
+    o = [h.encode() for h in outliers]
+    u = [h.encode() for h in universe]
+    oa = (C.c_char_p * max(1, len(o)))(*o)
+    ua = (C.c_char_p * max(1, len(u)))(*u)
+    p = C.c_void_p()
+    lib = ref()
+    lib.refh_localize.argtypes = [C.POINTER(C.c_char_p), C.c_size_t, C.POINTER(C.c_char_p), C.c_size_t,
+                                  C.POINTER(C.c_void_p)]
+    _chk(lib.refh_localize(oa, len(o), ua, len(u), C.byref(p)))
+    return json.loads(_take(p))
+
+
 def ref_slices(db: str, pids, ctx_ids=None, metric_ids=None, jobs: int = 1) -> dict:
     """The reference's ingest_profiles (ingest.cpp:155-176) through oracle/_ref."""
     p = np.ascontiguousarray(pids, np.uint32)

@@ -238,7 +238,7 @@ class Context:
                                      _ptr(cv, C.c_double), _ptr(ok, C.c_int32)))
         return {"leaves": leaves, "savings": sav, "summary": summ, "cv": cv, "cv_ok": ok}
 
-    def outliers(self, n_nodes: int) -> dict:
+    def outliers(self, n_nodes: int, masks: bool = True) -> dict:
         info = self.info
         ns = len(self._sites)
         ratio = np.empty(ns, np.float64)
@@ -251,11 +251,22 @@ class Context:
         fm = np.empty(max(1, nr), np.uint64)
         check(self.lib.psg_get_outliers(self.h, _ptr(ratio, C.c_double), _ptr(mean, C.c_double),
                                         _ptr(z, C.c_double), _ptr(sel, C.c_uint32),
-                                        _ptr(rows, C.c_uint32), _ptr(cm, C.c_uint64),
-                                        _ptr(fm, C.c_uint64)))
-        return {"site_ratio": ratio, "node_mean": mean, "node_z": z,
-                "selected": sel[: info["n_outliers"]], "racks": rows[:nr],
-                "chassis_mask": cm[:nr], "full_mask": fm[:nr]}
+                                        _ptr(rows, C.c_uint32),
+                                        _ptr(cm, C.c_uint64) if masks else None,
+                                        _ptr(fm, C.c_uint64) if masks else None))
+        out = {"site_ratio": ratio, "node_mean": mean, "node_z": z,
+               "selected": sel[: info["n_outliers"]], "racks": rows[:nr]}
+        if masks:
+            out["chassis_mask"], out["full_mask"] = cm[:nr], fm[:nr]
+        return out
+
+    def topology(self) -> np.ndarray:
+        """localize_outliers rows [rack, chassis, outlier nodes, fully affected]."""
+        n = C.c_uint32(0)
+        check(self.lib.psg_get_topology(self.h, C.byref(n), None))
+        rows = np.empty((max(1, n.value), 4), np.uint32)
+        check(self.lib.psg_get_topology(self.h, C.byref(n), _ptr(rows, C.c_uint32)))
+        return rows[: n.value]
 
     # ---- profile records (profile.db) -----------------------------------
     def load_profiles(self, records, rec_off, pids, ranks, node_of_profile=None):

@@ -195,6 +195,13 @@ struct psg_context {
   // nodes / topology
   uint32_t n_nodes = 0;
   std::vector<uint32_t> h_node_of_trace, h_rack_ids;  // rack id per rack index
+  // chassis ids of each rack's universe nodes, ascending: the device works on
+  // a rack's chassis slot (position in this list), so any chassis id works as
+  // long as a rack has at most 64 distinct chassis
+  std::vector<std::vector<uint32_t>> h_rack_chassis;
+  // set when a hostname of the node universe is not a Slingshot name: queries
+  // that need the topology raise it as PS_E_PARSE (topology.cpp:14-46)
+  std::string topo_error;
   dbuf<uint32_t> d_node_of_trace, d_node_rack_idx, d_node_chassis, d_uni_cnt;
 
   // anchor subtree (cached per anchor)
@@ -248,6 +255,7 @@ struct psg_context {
   std::vector<uint32_t> sites;
   dbuf<uint32_t> d_sites, d_worst, d_order, d_nsel, d_rack_nodes;
   dbuf<unsigned long long> site_acc, node_acc, rack_mask, rack_full;
+  dbuf<uint32_t> rack_cnt;  // [n_racks][64] outlier nodes per (rack, chassis slot)
   dbuf<double> site_ratio, node_mean, node_z;
 
   // profile records (profile.db; psg_profiles.cu)
@@ -618,9 +626,15 @@ static constexpr uint64_t kOneWarpMinEvents = PSG_ONE_WARP_MIN_EVENTS;
 
 // itermodel::suggest_anchor on the trace with the smallest profile id over all
 // ranks (build_tri_model uses pids.front(), itermodel.cpp:253-255): its owner
-// runs the device pass, every rank receives the result.
+// runs the device pass, every rank receives the result.  Both exchanges are
+// MIN all-reduces whose "nothing from me" sentinel sits below 2^63 (a host
+// reducer may reinterpret uint64 as int64); the owner's own failure travels
+// as a value between the anchors and the sentinel, so every rank fails with
+// the owner's status instead of waiting in a collective the owner never joins.
 uint32_t auto_anchor(psg_context* c) {
-  uint64_t mine = ~0ull;
+  constexpr uint64_t kAbsent = 0x7FFFFFFFFFFFFFFFull;  // this rank has nothing to say
+  constexpr uint64_t kErrBase = 1ull << 40;            // kErrBase | ps_status: the owner failed
+  uint64_t mine = kAbsent;
   uint32_t t_min = 0;
   for (uint32_t t = 0; t < c->n_traces; ++t)
     if (c->h_pid[t] < mine) {
@@ -628,32 +642,45 @@ uint32_t auto_anchor(psg_context* c) {
       t_min = t;
     }
   unsigned long long* d = c->summary.ensure(4);
-  uint64_t g = mine;
-  if (c->multi()) {
-    PSG_CUDA(cudaMemcpyAsync(d, &g, 8, cudaMemcpyHostToDevice, c->stream));
+  auto min_over_ranks = [&](uint64_t v) {
+    if (!c->multi()) return v;
+    PSG_CUDA(cudaMemcpyAsync(d, &v, 8, cudaMemcpyHostToDevice, c->stream));
     c->allreduce(reinterpret_cast<unsigned long long*>(d), 1, ncclUint64, ncclMin);
-    PSG_CUDA(cudaMemcpyAsync(&g, d, 8, cudaMemcpyDeviceToHost, c->stream));
+    PSG_CUDA(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
-  }
-  if (g == ~0ull) fail(PS_E_INVALID_ARGUMENT, "no traces loaded");
-  uint64_t anchor = ~0ull;
+    return v;
+  };
+  const uint64_t g = min_over_ranks(mine);
+  if (g == kAbsent) fail(PS_E_INVALID_ARGUMENT, "no traces loaded");
+  uint64_t anchor = kAbsent;
+  std::string owner_msg;
   if (g == mine) {
-    const uint64_t b = c->h_off[t_min], n = c->h_off[t_min + 1] - b;
-    const uint32_t a = launch_suggest_anchor(c->d_ts.p + b, c->d_ctx.p + b, n, c->h_tend[t_min],
-                                             c->d_parent.p, c->d_cct_pre.p, c->d_cct_size.p,
-                                             c->n_ctx, 3, 0.2, c->stream);
-    // kNone (no periodic context) travels as a valid "minimum" too
-    anchor = a;
+    try {
+      const uint64_t b = c->h_off[t_min], n = c->h_off[t_min + 1] - b;
+      // kNone (0xFFFFFFFF: no periodic context) travels as a valid "minimum" too
+      anchor = launch_suggest_anchor(c->d_ts.p + b, c->d_ctx.p + b, n, c->h_tend[t_min], c->d_parent.p,
+                                     c->d_cct_pre.p, c->d_cct_size.p, c->n_ctx, 3, 0.2, c->stream);
+    } catch (const failure& f) {
+      if (!c->multi()) throw;
+      anchor = kErrBase | static_cast<uint64_t>(f.status);
+      owner_msg = f.what();
+    }
   }
-  if (c->multi()) {
-    PSG_CUDA(cudaMemcpyAsync(d, &anchor, 8, cudaMemcpyHostToDevice, c->stream));
-    c->allreduce(reinterpret_cast<unsigned long long*>(d), 1, ncclUint64, ncclMin);
-    PSG_CUDA(cudaMemcpyAsync(&anchor, d, 8, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-  }
+  anchor = min_over_ranks(anchor);
+  if (anchor >= kErrBase && anchor < kAbsent)
+    fail(static_cast<ps_status>(anchor - kErrBase),
+         owner_msg.empty() ? "suggest_anchor failed on the rank owning the first trace" : owner_msg);
   if (anchor >= 0xFFFFFFFFull)  // itermodel.cpp:106-107
     fail(PS_E_NO_PERIODICITY, "no context shows periodic entries");
   return static_cast<uint32_t>(anchor);
+}
+
+// Whether some wide shape (>= 2 warps) fits the 227 KB of shared memory.
+bool fits_wide(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table_bytes) {
+  uint32_t w = PSG_WMAX;
+  while (w > 1 && static_cast<uint64_t>(n_traces) < 2ull * 148 * w) w /= 2;
+  while (w > 1 && table_bytes + w * per_warp_bytes > 227u * 1024) w /= 2;
+  return w > 1 || table_bytes + per_warp_bytes <= 227u * 1024;
 }
 
 uint32_t choose_warps(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table_bytes) {
@@ -672,30 +699,56 @@ uint32_t choose_warps(uint32_t n_traces, uint32_t per_warp_bytes, uint32_t table
 // The node universe shared by the trace and profile paths: n_nodes, and when
 // given, each node's rack and chassis (topology.cpp:54-92 universe counts).
 static void set_node_tables(psg_context* c, uint32_t n_nodes, const uint32_t* node_rack,
-                     const uint32_t* node_chassis) {
+                            const uint32_t* node_chassis) {
   c->n_nodes = n_nodes;
-  {
-    c->h_rack_ids.clear();
-    if (node_rack && node_chassis) {
-      std::set<uint32_t> racks(node_rack, node_rack + n_nodes);
-      c->h_rack_ids.assign(racks.begin(), racks.end());
-      std::vector<uint32_t> ridx(n_nodes), uni(c->h_rack_ids.size() * 64, 0);
-      for (uint32_t i = 0; i < n_nodes; ++i) {
-        ridx[i] = static_cast<uint32_t>(
-            std::lower_bound(c->h_rack_ids.begin(), c->h_rack_ids.end(), node_rack[i]) -
-            c->h_rack_ids.begin());
-        require(node_chassis[i] < 64, "chassis ids >= 64 are not supported");
-        uni[ridx[i] * 64 + node_chassis[i]] += 1;
-      }
-      PSG_CUDA(cudaMemcpyAsync(c->d_node_rack_idx.ensure(n_nodes), ridx.data(), 4ull * n_nodes,
-                               cudaMemcpyHostToDevice, c->stream));
-      PSG_CUDA(cudaMemcpyAsync(c->d_node_chassis.ensure(n_nodes), node_chassis, 4ull * n_nodes,
-                               cudaMemcpyHostToDevice, c->stream));
-      PSG_CUDA(cudaMemcpyAsync(c->d_uni_cnt.ensure(uni.size()), uni.data(), 4ull * uni.size(),
-                               cudaMemcpyHostToDevice, c->stream));
+  c->h_rack_ids.clear();
+  c->h_rack_chassis.clear();
+  if (node_rack && node_chassis) {
+    std::set<uint32_t> racks(node_rack, node_rack + n_nodes);
+    c->h_rack_ids.assign(racks.begin(), racks.end());
+    const size_t nr = c->h_rack_ids.size();
+    std::vector<std::set<uint32_t>> ch(nr);
+    std::vector<uint32_t> ridx(n_nodes), slot(n_nodes), uni(nr * 64, 0);
+    for (uint32_t i = 0; i < n_nodes; ++i) {
+      ridx[i] = static_cast<uint32_t>(
+          std::lower_bound(c->h_rack_ids.begin(), c->h_rack_ids.end(), node_rack[i]) -
+          c->h_rack_ids.begin());
+      ch[ridx[i]].insert(node_chassis[i]);
     }
+    c->h_rack_chassis.resize(nr);
+    for (size_t r = 0; r < nr; ++r) {
+      require(ch[r].size() <= 64, "a rack with more than 64 distinct chassis is not supported");
+      c->h_rack_chassis[r].assign(ch[r].begin(), ch[r].end());
+    }
+    for (uint32_t i = 0; i < n_nodes; ++i) {
+      const auto& v = c->h_rack_chassis[ridx[i]];
+      slot[i] = static_cast<uint32_t>(std::lower_bound(v.begin(), v.end(), node_chassis[i]) - v.begin());
+      uni[ridx[i] * 64 + slot[i]] += 1;
+    }
+    PSG_CUDA(cudaMemcpyAsync(c->d_node_rack_idx.ensure(n_nodes), ridx.data(), 4ull * n_nodes,
+                             cudaMemcpyHostToDevice, c->stream));
+    PSG_CUDA(cudaMemcpyAsync(c->d_node_chassis.ensure(n_nodes), slot.data(), 4ull * n_nodes,
+                             cudaMemcpyHostToDevice, c->stream));
+    PSG_CUDA(cudaMemcpyAsync(c->d_uni_cnt.ensure(uni.size()), uni.data(), 4ull * uni.size(),
+                             cudaMemcpyHostToDevice, c->stream));
   }
   c->sync();
+}
+
+// Rack / chassis of a database's node universe (hostnames in sorted order,
+// node_correlate's order).  A name that is not x<r>c<c>s<s>b<b>n<n> leaves the
+// nodes without topology and records the reference's parse_error message for
+// the first such name, which topology queries then raise (localize_outliers
+// parses the whole universe, topology.cpp:54-63).
+static void set_db_nodes(psg_context* c, const std::vector<std::string>& host_list) {
+  std::vector<uint32_t> rack(host_list.size()), chassis(host_list.size());
+  std::string err;
+  for (size_t i = 0; i < host_list.size() && err.empty(); ++i)
+    err = store::node_name_error(host_list[i], &rack[i], &chassis[i]);
+  const bool topo = err.empty() && !host_list.empty();
+  set_node_tables(c, static_cast<uint32_t>(host_list.size()), topo ? rack.data() : nullptr,
+                  topo ? chassis.data() : nullptr);
+  c->topo_error = err;
 }
 
 extern "C" {
@@ -851,6 +904,7 @@ ps_status psg_set_nodes(psg_context* c, const uint32_t* node_of_trace, uint32_t 
     PSG_CUDA(cudaMemcpyAsync(c->d_node_of_trace.ensure(c->n_traces + 1), node_of_trace,
                              4ull * c->n_traces, cudaMemcpyHostToDevice, c->stream));
     set_node_tables(c, n_nodes, node_rack, node_chassis);
+    c->topo_error.clear();
     c->sync();
   });
 }
@@ -973,17 +1027,12 @@ ps_status psg_load_profile_db(psg_context* c, const char* dir) {
     std::set<std::string> hosts;
     for (const auto& [r, h] : rank_host) hosts.insert(*h);
     std::vector<std::string> host_list(hosts.begin(), hosts.end());
-    std::vector<uint32_t> node_of(n, 0), rack(host_list.size()), chassis(host_list.size());
+    std::vector<uint32_t> node_of(n, 0);
     for (uint32_t i = 0; i < n; ++i)
       if (rank[i] >= 0)
         node_of[i] = static_cast<uint32_t>(std::lower_bound(host_list.begin(), host_list.end(),
                                                             *rank_host[rank[i]]) - host_list.begin());
-    bool topo = !host_list.empty();
-    for (size_t i = 0; i < host_list.size() && topo; ++i)
-      topo = store::parse_node_name(host_list[i], &rack[i], &chassis[i]) && chassis[i] < 64;
-    if (!host_list.empty())
-      set_node_tables(c, static_cast<uint32_t>(host_list.size()), topo ? rack.data() : nullptr,
-                      topo ? chassis.data() : nullptr);
+    if (!host_list.empty()) set_db_nodes(c, host_list);
     load_profiles_impl(c, body, off.data(), pid.data(), rank.data(),
                        host_list.empty() ? nullptr : node_of.data(), n);
   });
@@ -1065,6 +1114,7 @@ ps_status psg_profile_outliers(psg_context* c, uint16_t metric, const uint32_t* 
     ensure_device(c);
     if (c->n_rank_prof == 0) fail(PS_E_INSUFFICIENT_DATA, "balance_ratio of empty vector (no rank profiles loaded)");
     require(c->have_prof_nodes, "profile outliers need the profile -> node mapping (psg_load_profile_db or node_of_profile)");
+    if (!c->topo_error.empty()) fail(PS_E_PARSE, c->topo_error);
     invalidate_results(c);
     std::memset(info, 0, sizeof(*info));
     cudaStream_t s = c->stream;
@@ -1081,7 +1131,8 @@ ps_status psg_profile_outliers(psg_context* c, uint16_t metric, const uint32_t* 
     const uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
     if (nr)
       launch_topology(c->d_order.p, c->d_nsel.p, c->d_node_rack_idx.p, c->d_node_chassis.p, c->d_uni_cnt.p,
-                      nr, c->d_rack_nodes.ensure(nr), c->rack_mask.ensure(nr), c->rack_full.ensure(nr), s);
+                      nr, c->d_rack_nodes.ensure(nr), c->rack_mask.ensure(nr), c->rack_full.ensure(nr),
+                      c->rack_cnt.ensure(64ull * nr), s);
     PSG_CUDA(cudaEventRecord(c->ev[3], s));
     c->sync();
     c->have_outliers = true;
@@ -1173,17 +1224,15 @@ ps_status psg_load_trace_db(psg_context* c, const char* dir, const uint32_t* pid
       hosts.insert(h);
     }
     std::vector<std::string> host_list(hosts.begin(), hosts.end());
-    std::vector<uint32_t> node_of(sel.size()), rack(host_list.size()), chassis(host_list.size());
+    std::vector<uint32_t> node_of(sel.size());
     for (size_t i = 0; i < sel.size(); ++i)
       node_of[i] = static_cast<uint32_t>(
           std::lower_bound(host_list.begin(), host_list.end(), host_of_trace[i]) - host_list.begin());
-    bool topo = !host_list.empty();
-    for (size_t i = 0; i < host_list.size() && topo; ++i)
-      topo = store::parse_node_name(host_list[i], &rack[i], &chassis[i]) && chassis[i] < 64;
     if (!sel.empty()) {
-      ps_status st = psg_set_nodes(c, node_of.data(), static_cast<uint32_t>(host_list.size()),
-                                   topo ? rack.data() : nullptr, topo ? chassis.data() : nullptr);
-      if (st != PS_OK) fail(st, t_last_error);
+      c->h_node_of_trace = node_of;
+      PSG_CUDA(cudaMemcpyAsync(c->d_node_of_trace.ensure(c->n_traces + 1), node_of.data(),
+                               4ull * c->n_traces, cudaMemcpyHostToDevice, c->stream));
+      set_db_nodes(c, host_list);
     }
   });
 }
@@ -1449,6 +1498,10 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       if (!std::strcmp(e, "one")) one = true;
       if (!std::strcmp(e, "wide")) one = false;
     }
+    // the wide shape's CTA tables (and 16 carve-outs) may not fit where one
+    // warp's carve-out alone does: fall back to one-warp CTAs (a decision that
+    // depends only on the tree and the anchor, so every rank takes the same one)
+    if (!one && !fits_wide(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false))) one = true;
     uint32_t W = one ? choose_warps(1, L.bytes, 0) : choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false));
     if (one) W = 1;
     p.one_warp = one ? 1u : 0u;
@@ -1500,6 +1553,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     if (do_out) {
       require(q->site_ctx && q->n_sites > 0, "outliers need at least one candidate site ctx");
       require(c->n_nodes > 0, "outliers need the rank -> node mapping (psg_set_nodes)");
+      if (!c->topo_error.empty()) fail(PS_E_PARSE, c->topo_error);
       for (uint32_t i = 0; i < q->n_sites; ++i)
         require(q->site_ctx[i] < c->n_ctx, "site ctx out of range");
       c->sites.assign(q->site_ctx, q->site_ctx + q->n_sites);
@@ -1538,7 +1592,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       if (nr) {
         launch_topology(c->d_order.p, c->d_nsel.p, c->d_node_rack_idx.p, c->d_node_chassis.p,
                         c->d_uni_cnt.p, nr, c->d_rack_nodes.ensure(nr), c->rack_mask.ensure(nr),
-                        c->rack_full.ensure(nr), s);
+                        c->rack_full.ensure(nr), c->rack_cnt.ensure(64ull * nr), s);
       }
       c->have_outliers = true;
     }
@@ -1730,6 +1784,20 @@ ps_status psg_get_outliers(psg_context* c, double* site_ratio, double* node_mean
       PSG_CUDA(cudaMemcpy(rn.data(), c->d_rack_nodes.p, 4ull * nr, cudaMemcpyDeviceToHost));
       PSG_CUDA(cudaMemcpy(m.data(), c->rack_mask.p, 8ull * nr, cudaMemcpyDeviceToHost));
       PSG_CUDA(cudaMemcpy(fm.data(), c->rack_full.p, 8ull * nr, cudaMemcpyDeviceToHost));
+      // device masks are over chassis slots (position in the rack's chassis
+      // list); report them over chassis ids, which needs ids < 64
+      auto by_id = [&](uint32_t r, uint64_t slots) {
+        uint64_t out = 0;
+        for (uint32_t i = 0; i < 64; ++i)
+          if ((slots >> i) & 1) {
+            const uint32_t id = c->h_rack_chassis[r][i];
+            if (id >= 64)
+              fail(PS_E_INVALID_ARGUMENT,
+                   "chassis id " + std::to_string(id) + " >= 64 has no mask bit; use psg_get_topology");
+            out |= 1ull << id;
+          }
+        return out;
+      };
       size_t j = 0;
       for (uint32_t r = 0; r < nr; ++r) {
         if (!rn[r]) continue;
@@ -1738,11 +1806,38 @@ ps_status psg_get_outliers(psg_context* c, double* site_ratio, double* node_mean
           rack_rows[3 * j + 1] = rn[r];
           rack_rows[3 * j + 2] = static_cast<uint32_t>(__builtin_popcountll(m[r]));
         }
-        if (chassis_mask) chassis_mask[j] = m[r];
-        if (full_mask) full_mask[j] = fm[r];
+        if (chassis_mask) chassis_mask[j] = by_id(r, m[r]);
+        if (full_mask) full_mask[j] = by_id(r, fm[r]);
         ++j;
       }
     }
+  });
+}
+
+ps_status psg_get_topology(psg_context* c, uint32_t* n_rows, uint32_t* rows) {
+  if (!c || !n_rows) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_outliers) fail(PS_E_INVALID_ARGUMENT, "no outlier result (run psg_query with PSG_Q_OUTLIERS)");
+    ensure_device(c);
+    const uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
+    std::vector<uint32_t> cnt(64ull * nr);
+    if (nr) PSG_CUDA(cudaMemcpy(cnt.data(), c->rack_cnt.p, 4ull * cnt.size(), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> uni(64ull * nr);
+    if (nr) PSG_CUDA(cudaMemcpy(uni.data(), c->d_uni_cnt.p, 4ull * uni.size(), cudaMemcpyDeviceToHost));
+    uint32_t j = 0;
+    for (uint32_t r = 0; r < nr; ++r)
+      for (uint32_t i = 0; i < c->h_rack_chassis[r].size(); ++i) {
+        const uint32_t x = cnt[64ull * r + i];
+        if (!x) continue;
+        if (rows) {
+          rows[4ull * j] = c->h_rack_ids[r];
+          rows[4ull * j + 1] = c->h_rack_chassis[r][i];
+          rows[4ull * j + 2] = x;
+          rows[4ull * j + 3] = x == uni[64ull * r + i] ? 1u : 0u;
+        }
+        ++j;
+      }
+    *n_rows = j;
   });
 }
 

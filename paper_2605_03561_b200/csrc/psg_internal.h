@@ -312,6 +312,6 @@ void launch_profile_outliers(const profile_view& pv, const uint32_t* rank_slot, 
 void launch_topology(const uint32_t* selected, const uint32_t* n_sel, const uint32_t* node_rack_idx,
                      const uint32_t* node_chassis, const uint32_t* uni_cnt, uint32_t n_racks,
                      uint32_t* rack_nodes, unsigned long long* rack_mask,
-                     unsigned long long* rack_full, cudaStream_t s);
+                     unsigned long long* rack_full, uint32_t* rack_cnt, cudaStream_t s);
 
 }  // namespace psg

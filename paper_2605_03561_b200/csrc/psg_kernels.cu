@@ -387,6 +387,11 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
                         uint32_t* tpos, uint64_t* block_off, uint64_t* iter_off, uint64_t* kept_bo,
                         unsigned long long* summary, void* scratch, size_t scratch_bytes,
                         cudaStream_t s) {
+  unsigned long long init[5] = {0ull, 0xFFFFFFFFull, 0ull, 0ull, 0ull};
+  // an empty shard still reports its (empty) summary: no kept traces, the
+  // "no minimum" sentinel, no cells (a rank may hold no traces)
+  PSG_CUDA(cudaMemcpyAsync(summary, init, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  PSG_CUDA(cudaMemcpyAsync(summary + 4, init + 4, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   if (n == 0) return;
   uint64_t* kept = static_cast<uint64_t*>(scratch);
   uint64_t* cells = kept + (n + 1);
@@ -394,9 +399,6 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
   uint64_t* iters = tpos64 + (n + 1);
   void* temp = iters + (n + 1);
   size_t temp_bytes = scratch_bytes - 4ull * (n + 1) * sizeof(uint64_t);
-  unsigned long long init[5] = {0ull, 0xFFFFFFFFull, 0ull, 0ull, 0ull};
-  PSG_CUDA(cudaMemcpyAsync(summary, init, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-  PSG_CUDA(cudaMemcpyAsync(summary + 4, init + 4, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   k_layout_prep<<<(n + 255) / 256, 256, 0, s>>>(iter_count, n, nn, nnp, kept, cells, iters, summary);
   count_launch();
   PSG_CUDA(cudaGetLastError());
@@ -754,16 +756,17 @@ void launch_node_select(const unsigned long long* node_acc, uint32_t n_nodes, ui
 __global__ void k_topology(const uint32_t* selected, const uint32_t* n_sel, const uint32_t* rack_idx,
                            const uint32_t* chassis, const uint32_t* uni_cnt, uint32_t n_racks,
                            uint32_t* rack_nodes, unsigned long long* rack_mask,
-                           unsigned long long* rack_full) {
+                           unsigned long long* rack_full, uint32_t* rack_cnt) {
   extern __shared__ uint32_t cnt[];  // [n_racks][64]
   for (uint32_t i = threadIdx.x; i < n_racks * 64; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   const uint32_t ns = *n_sel;
   for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
     uint32_t nd = selected[i];
-    atomicAdd(&cnt[rack_idx[nd] * 64 + min(chassis[nd], 63u)], 1u);
+    atomicAdd(&cnt[rack_idx[nd] * 64 + min(chassis[nd], 63u)], 1u);  // chassis slot < 64
   }
   __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n_racks * 64; i += blockDim.x) rack_cnt[i] = cnt[i];
   for (uint32_t r = threadIdx.x; r < n_racks; r += blockDim.x) {
     uint32_t nodes = 0;
     u64 m = 0, f = 0;
@@ -784,7 +787,7 @@ __global__ void k_topology(const uint32_t* selected, const uint32_t* n_sel, cons
 void launch_topology(const uint32_t* selected, const uint32_t* n_sel, const uint32_t* node_rack_idx,
                      const uint32_t* node_chassis, const uint32_t* uni_cnt, uint32_t n_racks,
                      uint32_t* rack_nodes, unsigned long long* rack_mask,
-                     unsigned long long* rack_full, cudaStream_t s) {
+                     unsigned long long* rack_full, uint32_t* rack_cnt, cudaStream_t s) {
   if (n_racks == 0) return;
   size_t sm = sizeof(uint32_t) * n_racks * 64;
   if (sm > 200 * 1024) fail(PS_E_INVALID_ARGUMENT, "too many racks for the topology kernel");
@@ -792,7 +795,7 @@ void launch_topology(const uint32_t* selected, const uint32_t* n_sel, const uint
     PSG_CUDA(cudaFuncSetAttribute(k_topology, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sm)));
   k_topology<<<1, 512, sm, s>>>(selected, n_sel, node_rack_idx, node_chassis, uni_cnt, n_racks,
-                                rack_nodes, rack_mask, rack_full);
+                                rack_nodes, rack_mask, rack_full, rack_cnt);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }

@@ -40,6 +40,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <mutex>
 
 #include "psg_internal.h"
 
@@ -1401,12 +1402,20 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
 
 template <bool WIN, bool CUBE, bool EXACT, bool ONE>
 void launch_shape(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
-  static int configured_bytes = 0;
-  if (static_cast<int>(smem_bytes) > configured_bytes) {
-    PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT, ONE>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_bytes)));
-    configured_bytes = static_cast<int>(smem_bytes);
+  // the dynamic shared-memory opt-in is a per-device function attribute: track
+  // it per device (one process may drive several GPUs) under a lock
+  static std::mutex mu;
+  static int configured_bytes[64] = {};
+  int dev = 0;
+  PSG_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 64 || static_cast<int>(smem_bytes) > configured_bytes[dev]) {
+      PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT, ONE>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem_bytes)));
+      if (dev < 64) configured_bytes[dev] = static_cast<int>(smem_bytes);
+    }
   }
   const unsigned blocks = (p.tr.n + p.warps - 1) / p.warps;
   k_trace_query<WIN, CUBE, EXACT, ONE><<<blocks, p.warps * 32, smem_bytes, s>>>(p);

@@ -199,21 +199,32 @@ void open_profile_db(const std::string& dir, profile_db& db) {
   }
 }
 
-bool parse_node_name(const std::string& name, uint32_t* rack, uint32_t* chassis) {
+std::string node_name_error(const std::string& name, uint32_t* rack, uint32_t* chassis) {
+  // topology.cpp:14-46: the same checks in the same order, the same messages
   const char tags[5] = {'x', 'c', 's', 'b', 'n'};
   uint32_t v[5];
   size_t pos = 0;
   for (int f = 0; f < 5; ++f) {
-    if (pos >= name.size() || name[pos] != tags[f]) return false;
+    if (pos >= name.size() || name[pos] != tags[f])
+      return "node name parse error at byte " + std::to_string(pos) + ": expected '" +
+             std::string(1, tags[f]) + "' in \"" + name + "\"";
     ++pos;
     auto [p, ec] = std::from_chars(name.data() + pos, name.data() + name.size(), v[f]);
-    if (ec != std::errc() || p == name.data() + pos) return false;
+    if (ec != std::errc() || p == name.data() + pos)
+      return "node name parse error at byte " + std::to_string(pos) +
+             ": expected decimal integer in \"" + name + "\"";
     pos = static_cast<size_t>(p - name.data());
   }
-  if (pos != name.size()) return false;
-  *rack = v[0];
-  *chassis = v[1];
-  return true;
+  if (pos != name.size())
+    return "node name parse error at byte " + std::to_string(pos) + ": trailing characters in \"" +
+           name + "\"";
+  if (rack) *rack = v[0];
+  if (chassis) *chassis = v[1];
+  return std::string();
+}
+
+bool parse_node_name(const std::string& name, uint32_t* rack, uint32_t* chassis) {
+  return node_name_error(name, rack, chassis).empty();
 }
 
 }  // namespace psg::store

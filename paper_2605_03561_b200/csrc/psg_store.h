@@ -90,5 +90,8 @@ void open_profile_db(const std::string& dir, profile_db& out);
 
 // x<rack>c<chassis>s<slot>b<blade>n<node>, strict decimal (topology.cpp:33-46).
 bool parse_node_name(const std::string& name, uint32_t* rack, uint32_t* chassis);
+// The same parse; "" on success, else topology::parse_node_name's parse_error
+// message for the first violation (topology.cpp:14-46).
+std::string node_name_error(const std::string& name, uint32_t* rack, uint32_t* chassis);
 
 }  // namespace psg::store

@@ -42,7 +42,8 @@ def node_aligned_ranges(node_of_trace, world: int, weights=None) -> list[tuple[i
 def torch_reducer(group=None):
     """A host reducer over a torch.distributed process group: reduces a
     uint64/float64 numpy array in place (uint64 travels as int64: sums wrap
-    identically and max/min agree for values < 2^63, which ns and counts are)."""
+    identically; min/max flip the sign bit around the exchange so that they
+    compare in unsigned order for every value)."""
     import torch
     import torch.distributed as dist
 
@@ -50,8 +51,16 @@ def torch_reducer(group=None):
 
     def reduce(arr: np.ndarray, op: str) -> None:
         if arr.dtype == np.uint64:
+            # min / max in unsigned order: flip the sign bit so that the signed
+            # int64 comparison orders like uint64 (sums wrap identically)
+            flip = op in ("min", "max")
+            if flip:
+                arr ^= np.uint64(1 << 63)
             t = torch.from_numpy(arr.view(np.int64))
-        else:
-            t = torch.from_numpy(arr)
+            dist.all_reduce(t, op=ops[op], group=group)  # in place: t shares arr's memory
+            if flip:
+                arr ^= np.uint64(1 << 63)
+            return
+        t = torch.from_numpy(arr)
         dist.all_reduce(t, op=ops[op], group=group)  # in place: t shares arr's memory
     return reduce

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <functional>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "core/diagnostics.hpp"
@@ -258,6 +259,44 @@ void check_diagnostics(const db& d, const std::string& tag, uint32_t anchor, dou
   });
 }
 
+// The automatic anchor (itermodel.cpp:253-255): suggest_anchor on the first
+// requested trace.  The drop-in picks it on the device; the reference's result
+// (or the errc it raises) must come back.
+void check_auto_anchor(const db& d, const std::string& tag, std::vector<uint32_t> ids = {}) {
+  run(tag + ": auto anchor (device suggest_anchor) == reference", [&] {
+    const auto pids = ids.empty() ? d.ids() : ids;
+    auto pol = itermodel::anchor_policy::auto_detect();
+    itermodel::tri_model want;
+    const errc e = raised([&] { want = itermodel::build_tri_model(*d.h, pids, pol, 1); });
+    if (e != errc::ok) {
+      const errc g = raised([&] { gpu::build_tri_model(*d.h, pids, pol, 1); });
+      expect(g == e, "errc " + std::string(errc_name(g)) + " != reference " + errc_name(e));
+      return;
+    }
+    same_model(want, gpu::build_tri_model(*d.h, pids, pol, 1));
+  });
+}
+
+// No context enters periodically: suggest_anchor raises no_periodicity.
+store::database_image aperiodic_image() {
+  store::database_image img;
+  img.meta.metrics.push_back({0, store::metric_scope::inclusive, "cputime", "s"});
+  for (uint32_t c = 0; c < 4; ++c)
+    img.meta.contexts.push_back({c, c == 0 ? store::k_no_parent : c - 1, store::ctx_kind::function,
+                                 "c" + std::to_string(c)});
+  for (uint32_t t = 0; t < 3; ++t) {
+    img.meta.profiles.push_back({t + 1, static_cast<int32_t>(t), 0, "x1000c0s0b0n0", 0});
+    img.records.emplace_back();
+    store::trace_data td;
+    td.profile_id = t + 1;
+    // each context entered once, then the root: no context has 3 entries
+    td.events = {{0, 0}, {10, 1}, {25, 2}, {70, 3}, {200, 0}};
+    td.t_end_ns = 300;
+    img.traces.push_back(std::move(td));
+  }
+  return img;
+}
+
 }  // namespace
 
 int main() {
@@ -267,10 +306,22 @@ int main() {
     check_everything(d, "small_iter", {0, 1, 2});
     check_diagnostics(d, "small_iter", 1, 10.0);
     check_profiles(d, "small_iter");
-    run("small_iter: auto anchor == reference (itermodel.cpp:253-255)", [&] {
-      auto pol = itermodel::anchor_policy::auto_detect();
-      same_model(itermodel::build_tri_model(*d.h, d.ids(), pol, 1),
-                 gpu::build_tri_model(*d.h, d.ids(), pol, 1));
+    check_auto_anchor(d, "small_iter");
+    check_auto_anchor(d, "small_iter (subset, first = last trace)", {d.ids().back()});
+    run("small_iter: concurrent callers share one device (4 threads)", [&] {
+      auto want = itermodel::build_tri_model(*d.h, d.ids(), itermodel::anchor_policy::explicit_ctx(1), 1);
+      std::vector<std::thread> th;
+      std::vector<int> ok(4, 0);
+      for (int i = 0; i < 4; ++i)
+        th.emplace_back([&, i] {
+          try {
+            auto got = gpu::build_tri_model(*d.h, d.ids(), itermodel::anchor_policy::explicit_ctx(1), 1);
+            ok[i] = got.incl_ns == want.incl_ns && got.iter_counts == want.iter_counts;
+          } catch (...) {
+          }
+        });
+      for (auto& t : th) t.join();
+      for (int v : ok) expect(v == 1, "thread result");
     });
     run("small_iter: boundaries == generator truth", [&] {
       auto m = gpu::build_tri_model(*d.h, d.ids(), itermodel::anchor_policy::explicit_ctx(truth.anchor_ctx), 1);
@@ -296,12 +347,37 @@ int main() {
     auto [image, truth] = synthgen::generate_iterative_scenario(testutil::gamess_like_config());
     db d(image);
     check_everything(d, "gamess_like", {1});
+    check_auto_anchor(d, "gamess_like");
     check_diagnostics(d, "gamess_like", truth.anchor_ctx, 87.0);
   }
   for (uint64_t seed = 1; seed <= 6; ++seed) {
     db d(random_image(seed));
     check_everything(d, "random_" + std::to_string(seed), {0, 1, static_cast<uint32_t>(d.h->meta().contexts.size() - 1)});
+    check_auto_anchor(d, "random_" + std::to_string(seed));
   }
+  {
+    db d(aperiodic_image());
+    check_auto_anchor(d, "aperiodic");
+    run("aperiodic: auto anchor raises no_periodicity", [&] {
+      expect(raised([&] { gpu::build_tri_model(*d.h, d.ids(), itermodel::anchor_policy::auto_detect(), 1); }) ==
+                 errc::no_periodicity,
+             "errc");
+    });
+  }
+  run("a database rewritten in place is reloaded (resident-trace cache keyed by file identity)", [&] {
+    scratch_dir dir{"dropin_rewrite"};
+    for (uint64_t seed : {11, 12, 13}) {
+      store::write_database(random_image(seed), dir.path());
+      auto h = store::db_handle::open(dir.path());
+      std::vector<uint32_t> ids;
+      for (const auto& e : h.trace_index()) ids.push_back(e.profile_id);
+      uint64_t T = 0;
+      for (const auto& e : h.trace_index()) T = std::max(T, e.t_end_ns);
+      auto a = ingest::ingest_traces(h, ids, T / 4, 3 * T / 4, 1);
+      auto b = gpu::ingest_traces(h, ids, T / 4, 3 * T / 4, 1);
+      expect(a.events == b.events && a.carry_in == b.carry_in, "seed " + std::to_string(seed));
+    }
+  });
   std::printf("%s: %d failure(s)\n", g_failures ? "FAILED" : "OK", g_failures);
   return g_failures;
 }

@@ -15,24 +15,24 @@ import torch.distributed as dist
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_2605_03561_b200 import Q_ALL, Context, scenarios  # noqa: E402
+from paper_2605_03561_b200 import ANCHOR_AUTO, Q_ALL, Context, scenarios  # noqa: E402
 from paper_2605_03561_b200 import dist as pdist  # noqa: E402
 
 N_TRACES, N_PER_NODE, SITES = 40, 4, [2, 3, 4]
 
 
-def run(ctx: Context, lo: int, hi: int, T: int) -> dict:
+def run(ctx: Context, lo: int, hi: int, T: int, anchor: int = 1) -> dict:
     node_of = np.arange(lo, hi) // N_PER_NODE
     n_nodes = N_TRACES // N_PER_NODE
     node = np.arange(n_nodes)
     ctx.set_nodes(node_of, n_nodes, 4000 + node // 4, node % 4)
-    info = ctx.query(Q_ALL, t0=T // 4, t1=3 * T // 4, anchor=1, sites=SITES, top_k=4, z_min=-1e300)
+    info = ctx.query(Q_ALL, t0=T // 4, t1=3 * T // 4, anchor=anchor, sites=SITES, top_k=4, z_min=-1e300)
     out = {f"w_{k}": v for k, v in ctx.window().items()}
     out.update({f"c_{k}": v for k, v in ctx.cube().items()})
     out.update({f"s_{k}": v for k, v in ctx.stats(1.0).items()})
     out.update({f"o_{k}": v for k, v in ctx.outliers(n_nodes).items()})
     out["info"] = np.array([info["n_kept"], info["n_kept_global"], info["min_iterations"],
-                            info["worst_site"], info["n_outliers"]], np.int64)
+                            info["worst_site"], info["n_outliers"], info["anchor"]], np.int64)
     return out
 
 
@@ -92,18 +92,25 @@ def main(out_dir: str, mode: str = "gen") -> None:
         dist.barrier()
         dist.destroy_process_group()
         return
+    # "auto": PSG_ANCHOR_AUTO, the owner of the smallest profile id runs
+    # suggest_anchor and every rank receives it; "auto_empty": the same with
+    # the last rank holding no traces
+    anchor = ANCHOR_AUTO if mode.startswith("auto") else 1
     cfg = scenarios.iterative(N_TRACES, 9, n_kernels=6, seed=3, jitter=0.25)
     T = 0
     with Context(0) as single:  # to learn T (and, on rank 0, the reference run)
         single.generate_iterative(cfg)
         T = int(single.shard()["t_max"])
         if rank == 0:
-            np.savez(os.path.join(out_dir, "single.npz"), **run(single, 0, N_TRACES, T))
-    lo, hi = pdist.shard_range(N_TRACES, world, rank)
+            np.savez(os.path.join(out_dir, "single.npz"), **run(single, 0, N_TRACES, T, anchor))
+    if mode == "auto_empty":
+        lo, hi = pdist.shard_range(N_TRACES, world - 1, rank) if rank < world - 1 else (N_TRACES, N_TRACES)
+    else:
+        lo, hi = pdist.shard_range(N_TRACES, world, rank)
     with Context(0) as ctx:
         ctx.comm_init_host(world, rank, pdist.torch_reducer())
         ctx.generate_iterative(cfg, lo, hi)
-        res = run(ctx, lo, hi, T)
+        res = run(ctx, lo, hi, T, anchor)
         res["range"] = np.array([lo, hi], np.int64)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **res)
     dist.barrier()

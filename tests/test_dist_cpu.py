@@ -48,7 +48,9 @@ def _worker(rank, world, port, result_q):
     red = pdist.torch_reducer()
     out = {}
     # 1. the reducer
-    a = np.array([rank + 1, 10 * rank, 2**40 + rank], np.uint64)
+    # the last column straddles 2^63: rank 0 sends ~0 (a "nothing" sentinel
+    # in unsigned order), rank 1 sends 5 -- min / max must compare unsigned
+    a = np.array([rank + 1, 10 * rank, 2**40 + rank, 2**64 - 1 if rank == 0 else 5], np.uint64)
     b, c = a.copy(), a.copy()
     red(a, "sum")
     red(b, "max")
@@ -118,7 +120,8 @@ def test_gloo_two_ranks_merge_equals_single_process():
         p.join(timeout=60)
         assert p.exitcode == 0
     a, b, c, f = res[0]["reducer"]
-    assert a == [3, 10, 2 * 2**40 + 1] and b == [2, 10, 2**40 + 1] and c == [1, 0, 2**40]
+    assert a == [3, 10, 2 * 2**40 + 1, 4] and b == [2, 10, 2**40 + 1, 2**64 - 1]
+    assert c == [1, 0, 2**40, 5]
     assert f == [1.5]
     # the merged sufficient statistics equal the oracle over all traces
     with np.load(os.path.join(GOLDEN, "gamess_like.npz")) as z:

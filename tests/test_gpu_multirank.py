@@ -18,7 +18,8 @@ from tests.helpers import ROOT, assert_rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world,mode", [(2, "gen"), (3, "gen"), (2, "dup"), (3, "dup")])
+@pytest.mark.parametrize("world,mode", [(2, "gen"), (3, "gen"), (2, "dup"), (3, "dup"), (2, "auto"),
+                                        (3, "auto_empty")])
 def test_sharded_query_equals_single_context(tmp_path, world, mode):
     """mode "dup": one rank's traces make the optimistic pass 1 miss; the
     verdict is all-reduced, so every rank re-runs both passes exactly."""
@@ -39,6 +40,7 @@ def test_sharded_query_equals_single_context(tmp_path, world, mode):
     for x in ranks:
         assert x["info"][1] == one["info"][1] and x["info"][2] == one["info"][2]  # kept, K
         assert x["info"][3] == one["info"][3] and x["info"][4] == one["info"][4]  # worst site, n out
+        assert x["info"][5] == one["info"][5]  # anchor (the suggested one under PSG_ANCHOR_AUTO)
         assert np.array_equal(x["s_leaves"], one["s_leaves"])
         assert_rel(x["s_savings"], one["s_savings"], 1e-9, "savings")
         assert_rel(x["s_summary"], one["s_summary"], 1e-9, "summary")
