@@ -125,6 +125,9 @@ ps_status psg_get_traces(psg_context* ctx, uint64_t* ts, uint32_t* ctx_ids, uint
 /* Writes the loaded traces back as a packed trace.db body (12-byte AoS,
  * n_events * 12 bytes) into host memory (the inverse of K1). */
 ps_status psg_export_aos(psg_context* ctx, void* body);
+/* The same for the loaded traces [t_lo, t_hi) only (their events back to
+ * back: (event_off[t_hi] - event_off[t_lo]) * 12 bytes). */
+ps_status psg_export_aos_range(psg_context* ctx, uint32_t t_lo, uint32_t t_hi, void* body);
 /* Process-wide number of psg kernel launches so far (CUB library kernels
  * are not counted). */
 uint64_t psg_kernel_launches(void);
@@ -213,6 +216,14 @@ ps_status psg_get_carry(psg_context* ctx, uint8_t* has, uint64_t* ts, uint32_t* 
 ps_status psg_get_cube(psg_context* ctx, uint32_t* node_ids, uint32_t* iter_counts,
                        uint64_t* block_offset, int64_t* incl, int64_t* excl,
                        int64_t* gap_incl, int64_t* gap_excl);
+/* The same dense layout for the loaded traces [t_lo, t_hi) only (the kept
+ * ones, in load order, relative to the range): *n_cells and *n_kept are set
+ * first (any output pointer may be NULL, e.g. to size the arrays), then
+ * incl / excl [*n_cells] and gap rows [*n_kept][n_nodes].  Cells are widened
+ * to int64 on the device; no host buffer of the whole cube is needed. */
+ps_status psg_get_cube_range(psg_context* ctx, uint32_t t_lo, uint32_t t_hi, uint64_t* n_cells,
+                             uint32_t* n_kept, int64_t* incl, int64_t* excl, int64_t* gap_incl,
+                             int64_t* gap_excl);
 /* savings_report / iteration_cv_report per subtree leaf (diagnostics.cpp:100-158):
  * leaves[n_leaves]; savings rows [n_leaves][4] = avg_mean_s, avg_max_s,
  * savings_per_iter_s, total_reduction_s; summary[4] = n_iterations,

@@ -226,6 +226,22 @@ class Context:
         return {"node_ids": node_ids, "iter_counts": ic, "block_offset": bo, "incl": incl,
                 "excl": excl, "gap_incl": gi, "gap_excl": ge}
 
+    def cube_range(self, t_lo: int, t_hi: int) -> dict:
+        """The dense cube of loaded traces [t_lo, t_hi) (kept ones, in load
+        order): incl / excl cells and gap rows, widened on the device."""
+        nn = self.info["n_nodes"]
+        cells, kept = C.c_uint64(), C.c_uint32()
+        check(self.lib.psg_get_cube_range(self.h, t_lo, t_hi, C.byref(cells), C.byref(kept),
+                                          None, None, None, None))
+        incl = np.empty(cells.value, np.int64)
+        excl = np.empty(cells.value, np.int64)
+        gi = np.empty(kept.value * nn, np.int64)
+        ge = np.empty(kept.value * nn, np.int64)
+        check(self.lib.psg_get_cube_range(self.h, t_lo, t_hi, C.byref(cells), C.byref(kept),
+                                          _ptr(incl, C.c_int64), _ptr(excl, C.c_int64),
+                                          _ptr(gi, C.c_int64), _ptr(ge, C.c_int64)))
+        return {"incl": incl, "excl": excl, "gap_incl": gi, "gap_excl": ge, "n_kept": kept.value}
+
     def stats(self, total_time_s: float) -> dict:
         nl = self.info["n_leaves"]
         leaves = np.empty(nl, np.uint32)
@@ -313,9 +329,23 @@ class Context:
         """Writes the loaded traces as packed trace.db bytes to host address body_addr."""
         check(self.lib.psg_export_aos(self.h, C.c_void_p(body_addr)))
 
+    def export_aos_range(self, t_lo: int, t_hi: int) -> np.ndarray:
+        """Traces [t_lo, t_hi) as packed trace.db bytes (uint8 array)."""
+        idx = self.index()
+        n = int(idx["off"][t_hi] - idx["off"][t_lo])
+        body = np.empty(max(1, n * 12), np.uint8)
+        check(self.lib.psg_export_aos_range(self.h, t_lo, t_hi, C.c_void_p(body.ctypes.data)))
+        return body[: n * 12]
+
     @staticmethod
     def kernel_launches() -> int:
         return int(load().psg_kernel_launches())
+
+    def window_row_count(self, t0: int, t1: int) -> int:
+        """Rows of ingest_traces' window (psg_window_rows' size query only)."""
+        n = C.c_uint64()
+        check(self.lib.psg_window_rows(self.h, t0, t1, C.byref(n), None, None, None))
+        return n.value
 
     def window_rows(self, t0: int, t1: int) -> dict:
         n = C.c_uint64()

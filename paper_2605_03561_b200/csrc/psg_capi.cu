@@ -244,6 +244,7 @@ struct psg_context {
   bool cube32 = false;   // 32-bit cells (every stored iteration spans < 2^32 ns)
   dbuf<unsigned long long> summary;
   dbuf<uint8_t> scratch;
+  dbuf<uint64_t> dense_stage;  // int64 cells of the dense copy-out (k_cube_dense)
   dbuf<unsigned long long> x_acc;  // x_sum [K nn] | x_max [K nn] | x_sq [3 K nn]
   dbuf<double> within_cv, node_out;
   dbuf<uint8_t> within_ok;
@@ -1662,6 +1663,58 @@ ps_status psg_get_carry(psg_context* c, uint8_t* has, uint64_t* ts, uint32_t* ct
   });
 }
 
+namespace {
+// Dense int64 cells of the kept traces [t_lo, t_hi) into host arrays (dense
+// position relative to the range's first kept row): widened on the device
+// (k_cube_dense) in chunks of whole traces through a staging buffer, then one
+// D2H copy per chunk and column.  ic = host iteration counts of all traces.
+void cube_dense_to_host(psg_context* c, const std::vector<uint32_t>& ic, uint32_t t_lo, uint32_t t_hi,
+                        int64_t* incl, int64_t* excl) {
+  if (!incl && !excl) return;
+  if (excl && !c->have_excl)
+    fail(PS_E_INVALID_ARGUMENT, "the excl cube was not stored (PSG_Q_NO_CUBE_STORE)");
+  const uint64_t nn = c->nn;
+  constexpr uint64_t kChunkCells = 1ull << 27;  // 1 GiB of int64 per column per chunk
+  uint64_t row0 = 0;  // dense rows of the range before trace t
+  uint32_t t = t_lo;
+  const uint32_t nnp = row_stride(c->nn);
+  const uint32_t m = static_cast<uint32_t>(c->internal_pos.size());
+  while (t < t_hi) {
+    // whole traces up to the chunk size (at least one)
+    uint32_t e = t;
+    uint64_t rows = 0;
+    while (e < t_hi && (e == t || (rows + ic[e]) * nn <= kChunkCells)) rows += ic[e++];
+    if (rows == 0) {
+      t = e;
+      continue;
+    }
+    uint64_t dense_row0 = 0;  // iter_off of trace t on the device
+    PSG_CUDA(cudaMemcpyAsync(&dense_row0, c->iter_off.p + t, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    const uint64_t cells = rows * nn;
+    int64_t* di = reinterpret_cast<int64_t*>(c->dense_stage.ensure((incl ? cells : 0) + (excl ? cells : 0)));
+    int64_t* de = incl ? di + cells : di;
+    launch_cube_dense(c->cube_incl.p, c->cube32, c->cube_xint.p, c->iter_count.p, c->block_off.p,
+                      c->iter_off.p, c->d_node_tab.p, c->nn, nnp, m, t, e, dense_row0, incl ? di : nullptr,
+                      excl ? de : nullptr, c->stream);
+    if (incl)
+      PSG_CUDA(cudaMemcpyAsync(incl + row0 * nn, di, 8 * cells, cudaMemcpyDeviceToHost, c->stream));
+    if (excl)
+      PSG_CUDA(cudaMemcpyAsync(excl + row0 * nn, de, 8 * cells, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    row0 += rows;
+    t = e;
+  }
+}
+
+std::vector<uint32_t> host_iter_counts(psg_context* c) {
+  std::vector<uint32_t> ic(c->n_traces);
+  if (c->n_traces)
+    PSG_CUDA(cudaMemcpy(ic.data(), c->iter_count.p, 4ull * c->n_traces, cudaMemcpyDeviceToHost));
+  return ic;
+}
+}  // namespace
+
 ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts,
                        uint64_t* block_offset, int64_t* incl, int64_t* excl, int64_t* gap_incl,
                        int64_t* gap_excl) {
@@ -1670,9 +1723,7 @@ ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts
     if (!c->have_cube) fail(PS_E_INVALID_ARGUMENT, "no cube result (run psg_query with PSG_Q_CUBE)");
     ensure_device(c);
     if (node_ids) std::copy(c->node_ids.begin(), c->node_ids.end(), node_ids);
-    std::vector<uint32_t> ic(c->n_traces);
-    if (c->n_traces)
-      PSG_CUDA(cudaMemcpy(ic.data(), c->iter_count.p, 4ull * c->n_traces, cudaMemcpyDeviceToHost));
+    const std::vector<uint32_t> ic = host_iter_counts(c);
     if (iter_counts) std::copy(ic.begin(), ic.end(), iter_counts);
     if (block_offset) {  // dense cell offsets of the kept traces (itermodel.hpp:97-101)
       uint64_t off = 0;
@@ -1683,48 +1734,39 @@ ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts
           off += static_cast<uint64_t>(ic[t]) * c->nn;
         }
     }
-    if (excl && !c->have_excl)
+    if (c->n_cells) cube_dense_to_host(c, ic, 0, c->n_traces, incl, excl);
+    else if (excl && !c->have_excl)
       fail(PS_E_INVALID_ARGUMENT, "the excl cube was not stored (PSG_Q_NO_CUBE_STORE)");
-    if ((incl || excl) && c->n_cells) {
-      // storage -> the reference's dense int64 layout: rows of stride row_stride(nn)
-      // (pad column dropped), trace blocks padded to 4 cells, 32- or 64-bit cells
-      const size_t cb = c->cube32 ? 4 : 8;
-      std::vector<uint8_t> raw(c->n_store * cb);
-      PSG_CUDA(cudaMemcpy(raw.data(), c->cube_incl.p, raw.size(), cudaMemcpyDeviceToHost));
-      int64_t* dst = incl ? incl : excl;
-      const uint32_t nn = c->nn, nnp = row_stride(nn);
-      uint64_t so = 0, d = 0;
-      for (uint32_t t = 0; t < c->n_traces; ++t) {
-        if (ic[t] == 0) continue;
-        for (uint32_t k = 0; k < ic[t]; ++k)
-          for (uint32_t n = 0; n < nn; ++n, ++d) {
-            const uint64_t i = so + static_cast<uint64_t>(k) * nnp + n;
-            if (c->cube32) {
-              uint32_t v;
-              std::memcpy(&v, raw.data() + 4 * i, 4);
-              dst[d] = static_cast<int64_t>(v);
-            } else {
-              std::memcpy(&dst[d], raw.data() + 8 * i, 8);
-            }
-          }
-        so += (static_cast<uint64_t>(ic[t]) * nnp + 3) & ~3ull;
-      }
-      if (excl) {
-        // a leaf's excl equals its incl; internal nodes come from the
-        // [iteration][internal node] table
-        if (incl) std::memcpy(excl, incl, 8 * c->n_cells);
-        const size_t rows = c->n_cells / c->nn, m = c->internal_pos.size();
-        if (m) {
-          std::vector<int64_t> xi(rows * m);
-          PSG_CUDA(cudaMemcpy(xi.data(), c->cube_xint.p, 8 * rows * m, cudaMemcpyDeviceToHost));
-          for (size_t r = 0; r < rows; ++r)
-            for (size_t q = 0; q < m; ++q) excl[r * c->nn + c->internal_pos[q]] = xi[r * m + q];
-        }
-      }
-    }
     const size_t g = static_cast<size_t>(c->n_kept) * c->nn;
     if (gap_incl && g) PSG_CUDA(cudaMemcpy(gap_incl, c->gap_incl.p, 8 * g, cudaMemcpyDeviceToHost));
     if (gap_excl && g) PSG_CUDA(cudaMemcpy(gap_excl, c->gap_excl.p, 8 * g, cudaMemcpyDeviceToHost));
+  });
+}
+
+ps_status psg_get_cube_range(psg_context* c, uint32_t t_lo, uint32_t t_hi, uint64_t* n_cells,
+                             uint32_t* n_kept, int64_t* incl, int64_t* excl, int64_t* gap_incl,
+                             int64_t* gap_excl) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_cube) fail(PS_E_INVALID_ARGUMENT, "no cube result (run psg_query with PSG_Q_CUBE)");
+    require(t_lo <= t_hi && t_hi <= c->n_traces, "bad trace range");
+    ensure_device(c);
+    const std::vector<uint32_t> ic = host_iter_counts(c);
+    uint64_t rows = 0;
+    uint32_t kept_before = 0, kept = 0;
+    for (uint32_t t = 0; t < t_hi; ++t) {
+      if (t < t_lo) kept_before += ic[t] > 0;
+      else {
+        rows += ic[t];
+        kept += ic[t] > 0;
+      }
+    }
+    if (n_cells) *n_cells = rows * c->nn;
+    if (n_kept) *n_kept = kept;
+    if (rows) cube_dense_to_host(c, ic, t_lo, t_hi, incl, excl);
+    const size_t g = static_cast<size_t>(kept) * c->nn, g0 = static_cast<size_t>(kept_before) * c->nn;
+    if (gap_incl && g) PSG_CUDA(cudaMemcpy(gap_incl, c->gap_incl.p + g0, 8 * g, cudaMemcpyDeviceToHost));
+    if (gap_excl && g) PSG_CUDA(cudaMemcpy(gap_excl, c->gap_excl.p + g0, 8 * g, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -1842,6 +1884,29 @@ ps_status psg_get_topology(psg_context* c, uint32_t* n_rows, uint32_t* rows) {
 }
 
 uint64_t psg_kernel_launches(void) { return kernel_launches(); }
+
+ps_status psg_export_aos_range(psg_context* c, uint32_t t_lo, uint32_t t_hi, void* body) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    require(t_lo <= t_hi && t_hi <= c->n_traces, "bad trace range");
+    ensure_device(c);
+    const uint64_t e0 = c->h_off[t_lo], e1 = c->h_off[t_hi];
+    require(e1 == e0 || body != nullptr, "body is required");
+    const uint64_t chunk_ev = 4ull << 24;
+    uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, chunk_ev * 12 + 64));
+    // K1's inverse works on groups of 4 events from a 16-byte aligned start:
+    // export from the aligned-down event and skip the head on the copy
+    for (uint64_t done = e0; done < e1;) {
+      const uint64_t a = done & ~3ull;
+      const uint64_t ev = std::min(chunk_ev, e1 - a);
+      launch_soa_to_aos(c->d_ts.p + a, c->d_ctx.p + a, ev, stage, c->stream);
+      PSG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(body) + (done - e0) * 12, stage + (done - a) * 12,
+                               (a + ev - done) * 12, cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      done = a + ev;
+    }
+  });
+}
 
 ps_status psg_export_aos(psg_context* c, void* body) {
   if (!c || (!body && c->n_events)) return PS_E_INVALID_ARGUMENT;

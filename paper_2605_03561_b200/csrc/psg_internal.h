@@ -268,6 +268,12 @@ void launch_iter_spans(const uint64_t* cap_off, const uint64_t* bts, const uint3
                        cudaStream_t s);
 size_t cube_layout_scratch_bytes(uint32_t n);
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s);
+// Dense int64 incl / excl cells (the reference layout) of the kept traces in
+// [t_lo, t_hi), relative to dense row dense_row0 (= iter_off[t_lo]).
+void launch_cube_dense(const void* incl, bool cube32, const uint64_t* xint, const uint32_t* iter_count,
+                       const uint64_t* block_off, const uint64_t* iter_off, const int4* node_tab,
+                       uint32_t nn, uint32_t nnp, uint32_t m, uint32_t t_lo, uint32_t t_hi,
+                       uint64_t dense_row0, int64_t* out_incl, int64_t* out_excl, cudaStream_t s);
 void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, uint32_t n_kept,
                         uint32_t nn, uint32_t nnp, uint32_t K, unsigned long long* x_sum,
                         unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s);

@@ -124,6 +124,49 @@ void launch_soa_to_aos(const uint64_t* ts, const uint32_t* ctx, uint64_t n_event
   PSG_CUDA(cudaGetLastError());
 }
 
+// Dense int64 copy-out of the stored cube (itermodel.hpp:97-101): one CTA per
+// loaded trace of [t_lo, t_lo + gridDim.x); a kept trace's iterations x nodes
+// go to dense cell (iter_off[t] - dense_row0) * nn + k * nn + n, widened from
+// the 32- or 64-bit storage cells (rows of stride nnp); excl is the leaf's
+// incl, or the internal node's entry of the compact [row][m] excl table.
+__global__ void k_cube_dense(const void* __restrict__ incl, uint32_t cube32,
+                             const uint64_t* __restrict__ xint, const uint32_t* __restrict__ iter_count,
+                             const uint64_t* __restrict__ block_off, const uint64_t* __restrict__ iter_off,
+                             const int4* __restrict__ node_tab, uint32_t nn, uint32_t nnp, uint32_t m,
+                             uint32_t t_lo, uint64_t dense_row0, int64_t* __restrict__ out_incl,
+                             int64_t* __restrict__ out_excl) {
+  const uint32_t t = t_lo + blockIdx.x;
+  const uint32_t it = iter_count[t];
+  if (it == 0) return;
+  const uint64_t bo = block_off[t], row0 = iter_off[t];
+  const uint64_t cells = static_cast<uint64_t>(it) * nn;
+  int64_t* oi = out_incl ? out_incl + (row0 - dense_row0) * nn : nullptr;
+  int64_t* oe = out_excl ? out_excl + (row0 - dense_row0) * nn : nullptr;
+  for (uint64_t i = threadIdx.x; i < cells; i += blockDim.x) {
+    const uint64_t k = i / nn;
+    const uint32_t n = static_cast<uint32_t>(i - k * nn);
+    const uint64_t src = bo + k * nnp + n;
+    const int64_t v = cube32 ? static_cast<int64_t>(__ldg(static_cast<const uint32_t*>(incl) + src))
+                             : static_cast<int64_t>(ldg_u64(static_cast<const uint64_t*>(incl) + src));
+    if (oi) oi[i] = v;
+    if (oe) {
+      const int z = node_tab[n].z;
+      oe[i] = z ? static_cast<int64_t>(ldg_u64(xint + (row0 + k) * m + (z - 1))) : v;
+    }
+  }
+}
+
+void launch_cube_dense(const void* incl, bool cube32, const uint64_t* xint, const uint32_t* iter_count,
+                       const uint64_t* block_off, const uint64_t* iter_off, const int4* node_tab,
+                       uint32_t nn, uint32_t nnp, uint32_t m, uint32_t t_lo, uint32_t t_hi,
+                       uint64_t dense_row0, int64_t* out_incl, int64_t* out_excl, cudaStream_t s) {
+  if (t_hi <= t_lo || nn == 0) return;
+  k_cube_dense<<<t_hi - t_lo, 256, 0, s>>>(incl, cube32 ? 1u : 0u, xint, iter_count, block_off, iter_off,
+                                           node_tab, nn, nnp, m, t_lo, dense_row0, out_incl, out_excl);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
 // K1v: one warp per trace checks the invariants validate_database reports.
 __global__ void k_validate(trace_view tr, uint32_t n_ctx, const uint64_t* t_begin,
                            unsigned long long* bad, unsigned long long* first_bad) {
