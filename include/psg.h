@@ -224,6 +224,14 @@ ps_status psg_get_cube(psg_context* ctx, uint32_t* node_ids, uint32_t* iter_coun
 ps_status psg_get_cube_range(psg_context* ctx, uint32_t t_lo, uint32_t t_hi, uint64_t* n_cells,
                              uint32_t* n_kept, int64_t* incl, int64_t* excl, int64_t* gap_incl,
                              int64_t* gap_excl);
+/* detect_iterations' boundaries (itermodel.cpp:111-143) of loaded trace
+ * `trace` after a PSG_Q_CUBE query: *n boundary timestamps (strictly
+ * increasing; the last may equal t_end, an empty interval the cube drops).
+ * ts = NULL sizes. */
+ps_status psg_get_boundaries(psg_context* ctx, uint32_t trace, uint32_t* n, uint64_t* ts);
+/* topology::parse_node_name (topology.cpp:14-46): rack and chassis of an
+ * x<r>c<c>s<s>b<b>n<n> hostname, else PS_E_PARSE with the reference's message. */
+ps_status psg_node_name(const char* name, uint32_t* rack, uint32_t* chassis);
 /* savings_report / iteration_cv_report per subtree leaf (diagnostics.cpp:100-158):
  * leaves[n_leaves]; savings rows [n_leaves][4] = avg_mean_s, avg_max_s,
  * savings_per_iter_s, total_reduction_s; summary[4] = n_iterations,
@@ -288,6 +296,32 @@ ps_status psg_slice(psg_context* ctx, const uint32_t* pids, uint32_t n_pids, con
  * ms_total) and psg_get_outliers. */
 ps_status psg_profile_outliers(psg_context* ctx, uint16_t metric, const uint32_t* site_ctx,
                                uint32_t n_sites, uint32_t top_k, double z_min, psg_query_info* info);
+
+/* ---- device buffers and small diagnostics (the binding's hot-path
+ * signatures) ------------------------------------------- */
+/* Device memory on the context's device (e.g. frame columns uploaded by a
+ * host caller); psg_copy is cudaMemcpy in any direction, synchronous. */
+ps_status psg_dev_alloc(psg_context* ctx, uint64_t bytes, void** out);
+void psg_dev_free(psg_context* ctx, void* p);
+ps_status psg_copy(psg_context* ctx, void* dst, const void* src, uint64_t bytes);
+/* what = 0: diagnostics::balance_ratio, (Σ/n)/max or 1.0 when max == 0;
+ * what = 1: cv_percent, 100 * population std / mean (diagnostics.cpp:10-31).
+ * values: host or device f64.  Empty input is PS_E_INVALID_ARGUMENT
+ * (empty_input); a zero mean is PS_E_INSUFFICIENT_DATA (undefined_cv). */
+ps_status psg_vector_stats(psg_context* ctx, const double* values, uint64_t n, uint32_t what,
+                           double* result);
+/* node_correlate's sums (diagnostics.cpp:378-403): per node the mean of its
+ * values summed in input order (bit-identical to the reference's fold) and
+ * the count; node_of[i] < n_nodes.  Host or device values; host outputs. */
+ps_status psg_node_means(psg_context* ctx, const double* values, const uint32_t* node_of, uint64_t n,
+                         uint32_t n_nodes, double* mean, uint32_t* count);
+/* localize_outliers' counts (topology.cpp:54-92): nodes [0, n_universe) are
+ * the universe, further nodes are outliers outside it; outliers[] are node
+ * indices (distinct).  Rows as psg_get_topology: [rack, chassis, outlier
+ * nodes, fully affected] ascending; call with rows = NULL for *n_rows. */
+ps_status psg_localize(psg_context* ctx, const uint32_t* node_rack, const uint32_t* node_chassis,
+                       uint32_t n_nodes, uint32_t n_universe, const uint32_t* outliers, uint32_t n_out,
+                       uint32_t* n_rows, uint32_t* rows);
 
 /* ---- frame operators (frame.hpp) ------------------
  * The reference's columnar engine for numeric columns on the device, with its

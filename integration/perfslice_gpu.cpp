@@ -10,10 +10,17 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <set>
+#include <span>
+#include <tuple>
+#include <type_traits>
+#include <variant>
 #include <string>
 
 #include "core/common.hpp"
+#include "core/topology.hpp"
 #include "psg.h"
 
 namespace perfslice::gpu {
@@ -51,6 +58,7 @@ void check(ps_status s) {
   // reference condition where the C++ caller can tell them apart
   if (s == PS_E_INVALID_ARGUMENT && msg.find("trace has no events") != std::string::npos)
     e = errc::empty_input;  // suggest_anchor on an empty trace (itermodel.cpp:48)
+  if (s == PS_E_PARSE) raise(e, msg);  // the reference's own parse message, verbatim
   raise(e, "psg: " + msg);
 }
 
@@ -190,6 +198,414 @@ ingest::slice_table ingest_profiles(const store::db_handle& h, std::vector<uint3
     check(psg_slice(d.ctx(), profile_ids.data(), np, cx, ncx, mt, nmt, &n, out.profile_id.data(),
                     out.ctx_id.data(), out.metric_id.data(), out.value.data()));
   return out;
+}
+
+ingest::slice_table read_slices(const store::db_handle& h,
+                                const std::vector<ingest::slice_request>& requests, unsigned /*jobs*/) {
+  ingest::slice_table out;
+  if (requests.empty()) return out;
+  device_lease lease = acquire_device();
+  device& d = lease.dev;
+  d.bind_profiles(h);
+  // requests with identical (ctx, metric) filters go to the device together;
+  // each profile appears at most once per filter pair (query.cpp:322-334)
+  using key = std::tuple<bool, std::vector<uint32_t>, bool, std::vector<uint16_t>>;
+  std::map<key, std::vector<size_t>> groups;
+  for (size_t i = 0; i < requests.size(); ++i) {
+    const auto& r = requests[i];
+    groups[key{r.ctxs.all, r.ctxs.ids, r.metrics.all, r.metrics.ids}].push_back(i);
+  }
+  struct part {
+    size_t begin = 0, end = 0;  // rows of this request in its group's table
+    const ingest::slice_table* rows = nullptr;
+  };
+  std::vector<part> parts(requests.size());
+  std::vector<ingest::slice_table> tables;
+  tables.reserve(groups.size());
+  static const uint32_t k_no_ctx = 0;
+  static const uint16_t k_no_metric = 0;
+  for (const auto& [k, idx] : groups) {
+    const auto& [ctx_all, ctx_ids, m_all, m_ids] = k;
+    std::vector<uint32_t> pids;
+    for (size_t i : idx) pids.push_back(requests[i].profile_id);
+    // an explicit empty filter keeps nothing (non-null pointer, zero ids)
+    const uint32_t* cx = ctx_all ? nullptr : (ctx_ids.empty() ? &k_no_ctx : ctx_ids.data());
+    const uint16_t* mt = m_all ? nullptr : (m_ids.empty() ? &k_no_metric : m_ids.data());
+    const uint32_t ncx = static_cast<uint32_t>(ctx_ids.size()), nmt = static_cast<uint32_t>(m_ids.size());
+    const uint32_t np = static_cast<uint32_t>(pids.size());
+    uint64_t n = 0;
+    check(psg_slice(d.ctx(), pids.data(), np, cx, ncx, mt, nmt, &n, nullptr, nullptr, nullptr, nullptr));
+    ingest::slice_table t;
+    t.profile_id.resize(n);
+    t.ctx_id.resize(n);
+    t.metric_id.resize(n);
+    t.value.resize(n);
+    if (n)
+      check(psg_slice(d.ctx(), pids.data(), np, cx, ncx, mt, nmt, &n, t.profile_id.data(), t.ctx_id.data(),
+                      t.metric_id.data(), t.value.data()));
+    tables.push_back(std::move(t));
+    const ingest::slice_table& tb = tables.back();
+    // the device returns profiles ascending, each one's records contiguous
+    for (size_t i : idx) {
+      const uint32_t pid = requests[i].profile_id;
+      auto lo = std::lower_bound(tb.profile_id.begin(), tb.profile_id.end(), pid);
+      auto hi = std::upper_bound(lo, tb.profile_id.end(), pid);
+      parts[i] = part{static_cast<size_t>(lo - tb.profile_id.begin()),
+                      static_cast<size_t>(hi - tb.profile_id.begin()), &tb};
+    }
+  }
+  // ingest.cpp:122-153: request slots back to back in request order
+  size_t total = 0;
+  for (const auto& pt : parts) total += pt.end - pt.begin;
+  out.profile_id.reserve(total);
+  out.ctx_id.reserve(total);
+  out.metric_id.reserve(total);
+  out.value.reserve(total);
+  for (const auto& pt : parts)
+    for (size_t j = pt.begin; j < pt.end; ++j)
+      out.append(pt.rows->profile_id[j], pt.rows->ctx_id[j], pt.rows->metric_id[j], pt.rows->value[j]);
+  return out;
+}
+
+// ---- frame operators over a host frame::table --------------------------
+
+namespace {
+
+// Device allocation on the shared context, freed on scope exit.
+struct dev_buf {
+  psg_context* ctx = nullptr;
+  void* p = nullptr;
+  dev_buf(psg_context* c, uint64_t bytes) : ctx(c) { check(psg_dev_alloc(c, bytes, &p)); }
+  ~dev_buf() { psg_dev_free(ctx, p); }
+  dev_buf(const dev_buf&) = delete;
+  dev_buf& operator=(const dev_buf&) = delete;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+uint32_t psg_dtype(const frame::column& c) {
+  switch (c.type()) {
+    case frame::dtype::i64: return PSG_I64;
+    case frame::dtype::u64: return PSG_U64;
+    case frame::dtype::f64: return PSG_F64;
+    case frame::dtype::str: break;
+  }
+  raise(errc::type_mismatch, "gpu frame: column " + c.name() + " is a string column (host only)");
+}
+
+const void* host_data(const frame::column& c) {
+  switch (c.type()) {
+    case frame::dtype::i64: return c.i64s().data();
+    case frame::dtype::u64: return c.u64s().data();
+    case frame::dtype::f64: return c.f64s().data();
+    case frame::dtype::str: break;
+  }
+  return nullptr;
+}
+
+std::unique_ptr<dev_buf> upload(psg_context* ctx, const frame::column& c) {
+  psg_dtype(c);
+  auto b = std::make_unique<dev_buf>(ctx, 8ull * c.size() + 8);
+  check(psg_copy(ctx, b->p, host_data(c), 8ull * c.size()));
+  return b;
+}
+
+frame::column host_gather(const frame::column& c, const std::vector<uint64_t>& idx) {
+  auto pick = [&](const auto& v) {
+    std::remove_cvref_t<decltype(v)> out;
+    out.reserve(idx.size());
+    for (uint64_t i : idx) out.push_back(v[i]);
+    return out;
+  };
+  switch (c.type()) {
+    case frame::dtype::i64: return frame::column::of_i64(c.name(), pick(c.i64s()));
+    case frame::dtype::u64: return frame::column::of_u64(c.name(), pick(c.u64s()));
+    case frame::dtype::f64: return frame::column::of_f64(c.name(), pick(c.f64s()));
+    case frame::dtype::str: return frame::column::of_str(c.name(), pick(c.strs()));
+  }
+  return c;
+}
+
+}  // namespace
+
+frame::table group_aggregate(const frame::table& t, const std::vector<std::string>& keys,
+                             const std::vector<frame::agg_spec>& aggs, frame::backend /*b*/) {
+  std::vector<const frame::column*> kc;
+  for (const auto& k : keys) kc.push_back(&t.col(k));  // no_such_column like the reference
+  if (kc.empty()) raise(errc::invalid_argument, "at least one key column is required");
+  for (const auto& a : aggs) {
+    const frame::column& c = t.col(a.column);
+    if (c.type() == frame::dtype::str)  // require_numeric (frame.cpp:295-297)
+      raise(errc::type_mismatch, "column " + a.column + " is not numeric");
+  }
+  const uint64_t n = t.n_rows();
+  device_lease lease = acquire_device();
+  psg_context* ctx = lease.dev.ctx();
+  std::vector<std::unique_ptr<dev_buf>> kd;
+  std::vector<psg_col> cols;
+  for (const auto* c : kc) {
+    kd.push_back(upload(ctx, *c));
+    cols.push_back(psg_col{psg_dtype(*c), kd.back()->p});
+  }
+  dev_buf perm(ctx, 8 * n + 8), starts(ctx, 8 * n + 8);
+  uint64_t ng = 0;
+  check(psg_frame_group(ctx, cols.data(), static_cast<uint32_t>(cols.size()), n, perm.as<uint64_t>(),
+                        starts.as<uint64_t>(), &ng));
+  std::vector<uint64_t> hp(n), hs(ng);
+  check(psg_copy(ctx, hp.data(), perm.p, 8 * n));
+  check(psg_copy(ctx, hs.data(), starts.p, 8 * ng));
+  std::vector<uint64_t> heads(ng);
+  for (uint64_t g = 0; g < ng; ++g) heads[g] = hp[hs[g]];
+  frame::table out;
+  for (const auto* c : kc) out.add(host_gather(*c, heads));
+  for (const auto& a : aggs) {
+    const frame::column& src = t.col(a.column);
+    auto sd = upload(ctx, src);
+    dev_buf res(ctx, 8 * ng + 8);
+    check(psg_frame_group_agg(ctx, psg_col{psg_dtype(src), sd->p}, perm.as<uint64_t>(), starts.as<uint64_t>(),
+                              ng, n, static_cast<uint32_t>(a.fn == frame::agg_fn::sum     ? PSG_AGG_SUM
+                                                           : a.fn == frame::agg_fn::min   ? PSG_AGG_MIN
+                                                           : a.fn == frame::agg_fn::max   ? PSG_AGG_MAX
+                                                           : a.fn == frame::agg_fn::mean  ? PSG_AGG_MEAN
+                                                                                          : PSG_AGG_COUNT),
+                              res.p));
+    const std::string name = a.column + "_" + frame::agg_fn_name(a.fn);
+    if (a.fn == frame::agg_fn::count) {
+      std::vector<uint64_t> v(ng);
+      check(psg_copy(ctx, v.data(), res.p, 8 * ng));
+      out.add(frame::column::of_u64(name, std::move(v)));
+    } else if (a.fn == frame::agg_fn::mean || src.type() == frame::dtype::f64) {
+      std::vector<double> v(ng);
+      check(psg_copy(ctx, v.data(), res.p, 8 * ng));
+      out.add(frame::column::of_f64(name, std::move(v)));
+    } else if (src.type() == frame::dtype::i64) {
+      std::vector<int64_t> v(ng);
+      check(psg_copy(ctx, v.data(), res.p, 8 * ng));
+      out.add(frame::column::of_i64(name, std::move(v)));
+    } else {
+      std::vector<uint64_t> v(ng);
+      check(psg_copy(ctx, v.data(), res.p, 8 * ng));
+      out.add(frame::column::of_u64(name, std::move(v)));
+    }
+  }
+  return out;
+}
+
+frame::table filter(const frame::table& t, const std::string& column, frame::cmp_op op,
+                    const frame::literal& lit, frame::backend /*b*/) {
+  const frame::column& c = t.col(column);
+  if (static_cast<size_t>(c.type()) != lit.index())  // frame.cpp:427-429
+    raise(errc::type_mismatch, "literal type does not match column " + column);
+  const uint64_t n = t.n_rows();
+  device_lease lease = acquire_device();
+  psg_context* ctx = lease.dev.ctx();
+  auto cd = upload(ctx, c);
+  dev_buf idx(ctx, 8 * n + 8);
+  uint64_t m = 0;
+  const void* litp = std::visit([](const auto& v) -> const void* { return &v; }, lit);
+  check(psg_frame_filter(ctx, psg_col{psg_dtype(c), cd->p}, static_cast<uint32_t>(op), litp, n,
+                         idx.as<uint64_t>(), &m));
+  std::vector<uint64_t> sel(m);
+  check(psg_copy(ctx, sel.data(), idx.p, 8 * m));
+  frame::table out;
+  for (const auto& col : t.columns()) out.add(host_gather(col, sel));
+  return out;
+}
+
+// ---- single-trace iteration model (itermodel.cpp:111-183) ----------------
+
+namespace {
+
+// A second device context for span inputs (one trace given as events), so the
+// shared device keeps its resident trace set.
+struct span_device {
+  std::mutex mu;
+  std::unique_ptr<device> dev;
+};
+span_device& span_dev() {
+  static span_device s;
+  return s;
+}
+
+void load_span(psg_context* ctx, std::span<const store::trace_event> events, uint64_t t_end,
+               const store::meta_data& cct) {
+  std::vector<uint32_t> parent(cct.contexts.size());
+  for (size_t i = 0; i < parent.size(); ++i) parent[i] = cct.contexts[i].parent;
+  check(psg_set_cct(ctx, parent.data(), static_cast<uint32_t>(parent.size())));
+  std::vector<uint8_t> body(events.size() * store::k_event_size);
+  for (size_t i = 0; i < events.size(); ++i) {
+    std::memcpy(body.data() + 12 * i, &events[i].timestamp_ns, 8);
+    std::memcpy(body.data() + 12 * i + 8, &events[i].ctx_id, 4);
+  }
+  const uint64_t off[2] = {0, events.size()};
+  const uint32_t pid = 0;
+  check(psg_load_traces_aos(ctx, body.data(), events.size(), off, &pid, &t_end, 1));
+}
+
+}  // namespace
+
+std::vector<itermodel::interval> detect_iterations(std::span<const store::trace_event> events,
+                                                   uint64_t t_end_ns, const store::meta_data& cct,
+                                                   uint32_t anchor) {
+  if (anchor >= cct.contexts.size())  // itermodel.cpp:114-116
+    raise(errc::not_found, "anchor ctx " + std::to_string(anchor) + " not in tree");
+  for (const auto& e : events)
+    if (e.ctx_id >= cct.contexts.size())
+      raise(errc::dangling_context, "trace event ctx " + std::to_string(e.ctx_id) + " not in tree");
+  span_device& sd = span_dev();
+  std::lock_guard<std::mutex> lk(sd.mu);
+  if (!sd.dev) sd.dev = std::make_unique<device>(0);
+  psg_context* ctx = sd.dev->ctx();
+  load_span(ctx, events, std::max(t_end_ns, events.empty() ? t_end_ns : events.back().timestamp_ns), cct);
+  psg_query_spec q{};
+  q.flags = PSG_Q_CUBE | PSG_Q_NO_CUBE_STORE;
+  q.anchor_ctx = anchor;
+  psg_query_info info{};
+  check(psg_query(ctx, &q, &info));
+  uint32_t nb = 0;
+  check(psg_get_boundaries(ctx, 0, &nb, nullptr));
+  if (nb == 0) raise(errc::no_iterations, "anchor never entered in trace");
+  std::vector<uint64_t> b(nb);
+  check(psg_get_boundaries(ctx, 0, &nb, b.data()));
+  std::vector<itermodel::interval> out;
+  for (uint32_t k = 0; k < nb; ++k) {
+    const uint64_t t1 = k + 1 < nb ? b[k + 1] : t_end_ns;
+    if (b[k] < t1) out.push_back({b[k], t1});
+  }
+  if (out.empty()) raise(errc::no_iterations, "all detected iterations are empty");
+  return out;
+}
+
+itermodel::interval_profile rematerialize(std::span<const store::trace_event> events,
+                                          std::optional<store::trace_event> carry_in,
+                                          itermodel::interval iv, const store::meta_data& cct) {
+  if (iv.t0_ns >= iv.t1_ns) raise(errc::invalid_argument, "interval must have positive length");
+  // the carry-in event prepended to the span: the window query integrates
+  // [carry.ts, first.ts) and every event to its successor or t1, clipped to
+  // [t0, t1) -- rematerialize's segments (itermodel.cpp:168-176)
+  std::vector<store::trace_event> ev;
+  ev.reserve(events.size() + 1);
+  if (carry_in) ev.push_back(*carry_in);
+  ev.insert(ev.end(), events.begin(), events.end());
+  for (const auto& e : ev)
+    if (e.ctx_id >= cct.contexts.size())
+      raise(errc::dangling_context, "trace event ctx " + std::to_string(e.ctx_id) + " not in tree");
+  const size_t n_ctx = cct.contexts.size();
+  itermodel::interval_profile out;
+  if (ev.empty()) return out;
+  span_device& sd = span_dev();
+  std::lock_guard<std::mutex> lk(sd.mu);
+  if (!sd.dev) sd.dev = std::make_unique<device>(0);
+  psg_context* ctx = sd.dev->ctx();
+  load_span(ctx, ev, std::max(ev.back().timestamp_ns, iv.t1_ns), cct);
+  psg_query_spec q{};
+  q.flags = PSG_Q_WINDOW;
+  q.t0_ns = iv.t0_ns;
+  q.t1_ns = iv.t1_ns;
+  psg_query_info info{};
+  check(psg_query(ctx, &q, &info));
+  std::vector<int64_t> incl(n_ctx), excl(n_ctx);
+  check(psg_get_window(ctx, nullptr, nullptr, nullptr, nullptr, nullptr, excl.data(), incl.data()));
+  for (uint32_t c = 0; c < n_ctx; ++c)
+    if (incl[c] != 0 || excl[c] != 0) out.push_back({c, incl[c], excl[c]});
+  return out;
+}
+
+// ---- diagnostics and topology -------------------------------------------
+
+double balance_ratio(std::span<const double> values) {
+  if (values.empty()) raise(errc::empty_input, "balance_ratio of empty vector");
+  device_lease lease = acquire_device();
+  double r = 0.0;
+  check(psg_vector_stats(lease.dev.ctx(), values.data(), values.size(), 0, &r));
+  return r;
+}
+
+double cv_percent(std::span<const double> values) {
+  if (values.empty()) raise(errc::empty_input, "cv of empty vector");
+  device_lease lease = acquire_device();
+  double r = 0.0;
+  const ps_status st = psg_vector_stats(lease.dev.ctx(), values.data(), values.size(), 1, &r);
+  if (st == PS_E_INSUFFICIENT_DATA) raise(errc::undefined_cv, "cv undefined for zero mean");
+  check(st);
+  return r;
+}
+
+std::vector<diagnostics::node_stat> node_correlate(
+    const std::vector<std::pair<int32_t, double>>& rank_values, const store::meta_data& meta) {
+  // rank -> hostname from the first profile with that rank; hosts in string
+  // order (diagnostics.cpp:381-398): host bookkeeping stays on the host
+  std::map<int32_t, const std::string*> rank_host;
+  for (const auto& p : meta.profiles)
+    if (p.rank >= 0 && rank_host.find(p.rank) == rank_host.end()) rank_host[p.rank] = &p.hostname;
+  std::map<std::string, uint32_t> host_id;
+  std::vector<const std::string*> host_of(rank_values.size());
+  for (size_t i = 0; i < rank_values.size(); ++i) {
+    auto it = rank_host.find(rank_values[i].first);
+    if (it == rank_host.end())
+      raise(errc::not_found, "rank " + std::to_string(rank_values[i].first) + " has no profile descriptor");
+    host_of[i] = it->second;
+    host_id.emplace(*it->second, 0);
+  }
+  uint32_t k = 0;
+  for (auto& [h, id] : host_id) id = k++;
+  std::vector<uint32_t> node(rank_values.size());
+  std::vector<double> vals(rank_values.size());
+  for (size_t i = 0; i < rank_values.size(); ++i) {
+    node[i] = host_id[*host_of[i]];
+    vals[i] = rank_values[i].second;
+  }
+  std::vector<double> mean(host_id.size());
+  std::vector<uint32_t> count(host_id.size());
+  device_lease lease = acquire_device();
+  check(psg_node_means(lease.dev.ctx(), vals.data(), node.data(), vals.size(),
+                       static_cast<uint32_t>(host_id.size()), mean.data(), count.data()));
+  std::vector<diagnostics::node_stat> out;
+  for (const auto& [h, id] : host_id) out.push_back({h, mean[id], count[id]});
+  return out;
+}
+
+topology::congestion_report localize_outliers(const std::vector<std::string>& outliers,
+                                              const std::vector<std::string>& universe) {
+  // parse_error on the first bad name, universe first (topology.cpp:58-69)
+  std::vector<std::string> names = universe;
+  std::set<std::string> outlier_set(outliers.begin(), outliers.end());
+  std::map<std::string, uint32_t> idx;
+  for (size_t i = 0; i < universe.size(); ++i) idx.emplace(universe[i], static_cast<uint32_t>(i));
+  for (const auto& o : outlier_set)
+    if (!idx.count(o)) {
+      idx.emplace(o, static_cast<uint32_t>(names.size()));
+      names.push_back(o);
+    }
+  std::vector<uint32_t> rack(names.size()), chassis(names.size());
+  for (size_t i = 0; i < universe.size(); ++i)  // raises parse_error
+    check(psg_node_name(universe[i].c_str(), &rack[i], &chassis[i]));
+  for (const auto& o : outlier_set) check(psg_node_name(o.c_str(), &rack[idx[o]], &chassis[idx[o]]));
+  std::vector<uint32_t> sel;
+  for (const auto& o : outlier_set) sel.push_back(idx[o]);
+  device_lease lease = acquire_device();
+  uint32_t nr = 0;
+  check(psg_localize(lease.dev.ctx(), rack.data(), chassis.data(), static_cast<uint32_t>(names.size()),
+                     static_cast<uint32_t>(universe.size()), sel.data(), static_cast<uint32_t>(sel.size()),
+                     &nr, nullptr));
+  std::vector<uint32_t> rows(4ull * nr + 4);
+  check(psg_localize(lease.dev.ctx(), rack.data(), chassis.data(), static_cast<uint32_t>(names.size()),
+                     static_cast<uint32_t>(universe.size()), sel.data(), static_cast<uint32_t>(sel.size()),
+                     &nr, rows.data()));
+  topology::congestion_report rep;
+  rep.outlier_count = outlier_set.size();
+  for (uint32_t j = 0; j < nr; ++j) {
+    const uint32_t r = rows[4 * j], c = rows[4 * j + 1], cnt = rows[4 * j + 2], full = rows[4 * j + 3];
+    if (rep.racks.empty() || rep.racks.back().rack != r) {
+      rep.racks.emplace_back();
+      rep.racks.back().rack = r;
+    }
+    auto& e = rep.racks.back();
+    e.affected_nodes += cnt;
+    e.affected_chassis.push_back(c);
+    if (full) e.fully_affected_chassis.push_back(c);
+  }
+  return rep;
 }
 
 namespace {

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <string>
 #include <optional>
+#include <span>
 #include <vector>
 
 #include "core/diagnostics.hpp"
@@ -26,6 +27,7 @@
 #include "core/ingest.hpp"
 #include "core/itermodel.hpp"
 #include "core/store.hpp"
+#include "core/topology.hpp"
 
 struct psg_context;
 
@@ -89,6 +91,51 @@ frame::table window_aggregate(const store::db_handle& h, std::vector<uint32_t> p
 ingest::slice_table ingest_profiles(const store::db_handle& h, std::vector<uint32_t> profile_ids,
                                     const ingest::keep_set& keep,
                                     const std::vector<uint16_t>& metric_ids, unsigned jobs);
+
+// ingest::read_slices (ingest.hpp:77-80, ingest.cpp:122-153): the session's
+// cache-miss reads (query.cpp:337-338) on the device; requests with the same
+// (ctx, metric) filters share one psg_slice, and the rows come back in
+// request order exactly as the reference assembles them.
+ingest::slice_table read_slices(const store::db_handle& h,
+                                const std::vector<ingest::slice_request>& requests, unsigned jobs);
+
+// frame::group_aggregate / frame::filter (frame.hpp:100-113, frame.cpp:
+// 290-470) over a host table: the key / predicate / aggregate columns go to
+// the device (psg_frame_group, _group_agg, _filter: the reference's fold
+// order and NaN rules, bit for bit); the rows are gathered back on the host.
+// Numeric columns only on the device: a string key, predicate or aggregate
+// column raises type_mismatch (string columns in other positions are
+// gathered).  The backend argument is accepted and ignored.
+frame::table group_aggregate(const frame::table& t, const std::vector<std::string>& keys,
+                             const std::vector<frame::agg_spec>& aggs, frame::backend b);
+frame::table filter(const frame::table& t, const std::string& column, frame::cmp_op op,
+                    const frame::literal& lit, frame::backend b);
+
+// itermodel::detect_iterations / rematerialize (itermodel.hpp:54-64,
+// itermodel.cpp:111-183) on one trace given as events: the fused query's
+// boundary pass and window integration on a second device context (the
+// shared one keeps its resident traces).  Events must be timestamp-ordered
+// (a trace.db invariant; PS_E_FORMAT -> format_error otherwise).
+std::vector<itermodel::interval> detect_iterations(std::span<const store::trace_event> events,
+                                                   uint64_t t_end_ns, const store::meta_data& cct,
+                                                   uint32_t anchor);
+itermodel::interval_profile rematerialize(std::span<const store::trace_event> events,
+                                          std::optional<store::trace_event> carry_in,
+                                          itermodel::interval iv, const store::meta_data& cct);
+
+// diagnostics::balance_ratio / cv_percent (diagnostics.hpp:23-26): device
+// tree sums (within 1e-9 of the reference's sequential fold).
+double balance_ratio(std::span<const double> values);
+double cv_percent(std::span<const double> values);
+// diagnostics::node_correlate (diagnostics.hpp:128-130): hostname
+// bookkeeping on the host, per-host sums on the device in input order (bit
+// for bit the reference's fold).
+std::vector<diagnostics::node_stat> node_correlate(
+    const std::vector<std::pair<int32_t, double>>& rank_values, const store::meta_data& meta);
+// topology::localize_outliers (topology.hpp:52-53): names parsed by
+// psg_node_name (parse_error, the reference's message), counts on the device.
+topology::congestion_report localize_outliers(const std::vector<std::string>& outliers,
+                                              const std::vector<std::string>& universe);
 
 // itermodel::build_tri_model (itermodel.hpp:118-120, itermodel.cpp:242-360).
 // An automatic anchor is chosen on the device (psg_query with

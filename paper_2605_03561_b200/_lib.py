@@ -112,6 +112,14 @@ _SIGS = {
     "psg_get_stats": (C.c_int, [P, C.c_double, U32P, F64P, F64P, F64P, I32P]),
     "psg_get_outliers": (C.c_int, [P, F64P, F64P, F64P, U32P, U32P, U64P, U64P]),
     "psg_get_topology": (C.c_int, [P, U32P, U32P]),
+    "psg_get_boundaries": (C.c_int, [P, C.c_uint32, U32P, U64P]),
+    "psg_node_name": (C.c_int, [C.c_char_p, U32P, U32P]),
+    "psg_dev_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "psg_dev_free": (None, [P, C.c_void_p]),
+    "psg_copy": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "psg_vector_stats": (C.c_int, [P, F64P, C.c_uint64, C.c_uint32, F64P]),
+    "psg_node_means": (C.c_int, [P, F64P, U32P, C.c_uint64, C.c_uint32, F64P, U32P]),
+    "psg_localize": (C.c_int, [P, U32P, U32P, C.c_uint32, C.c_uint32, U32P, C.c_uint32, U32P, U32P]),
     "psg_get_cube_range": (C.c_int, [P, C.c_uint32, C.c_uint32, U64P, U32P, I64P, I64P, I64P, I64P]),
     "psg_export_aos_range": (C.c_int, [P, C.c_uint32, C.c_uint32, C.c_void_p]),
     "psg_window_rows": (C.c_int, [P, C.c_uint64, C.c_uint64, U64P, U32P, U64P, U32P]),

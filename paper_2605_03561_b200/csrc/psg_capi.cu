@@ -1743,6 +1743,35 @@ ps_status psg_get_cube(psg_context* c, uint32_t* node_ids, uint32_t* iter_counts
   });
 }
 
+ps_status psg_get_boundaries(psg_context* c, uint32_t trace, uint32_t* n, uint64_t* ts) {
+  if (!c || !n) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_cube) fail(PS_E_INVALID_ARGUMENT, "no cube result (run psg_query with PSG_Q_CUBE)");
+    require(trace < c->n_traces, "trace index out of range");
+    ensure_device(c);
+    uint32_t nb = 0, it = 0;
+    uint64_t off = 0;
+    PSG_CUDA(cudaMemcpy(&nb, c->d_nbounds.p + trace, 4, cudaMemcpyDeviceToHost));
+    PSG_CUDA(cudaMemcpy(&it, c->iter_count.p + trace, 4, cudaMemcpyDeviceToHost));
+    PSG_CUDA(cudaMemcpy(&off, c->d_cap_off.p + trace, 8, cudaMemcpyDeviceToHost));
+    *n = nb;
+    if (!ts || !nb) return;
+    if (it == 0) {  // one boundary, at t_end (the empty last interval dropped)
+      ts[0] = c->h_tend[trace];
+      return;
+    }
+    PSG_CUDA(cudaMemcpy(ts, c->d_bts.p + off, 8ull * nb, cudaMemcpyDeviceToHost));
+  });
+}
+
+ps_status psg_node_name(const char* name, uint32_t* rack, uint32_t* chassis) {
+  if (!name) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    const std::string err = store::node_name_error(name, rack, chassis);
+    if (!err.empty()) fail(PS_E_PARSE, err);
+  });
+}
+
 ps_status psg_get_cube_range(psg_context* c, uint32_t t_lo, uint32_t t_hi, uint64_t* n_cells,
                              uint32_t* n_kept, int64_t* incl, int64_t* excl, int64_t* gap_incl,
                              int64_t* gap_excl) {

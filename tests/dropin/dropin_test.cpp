@@ -21,6 +21,7 @@
 #include "core/itermodel.hpp"
 #include "core/store.hpp"
 #include "core/synthgen.hpp"
+#include "core/topology.hpp"
 #include "core/util.hpp"
 #include "helpers.hpp"
 #include "perfslice_gpu.hpp"
@@ -277,6 +278,139 @@ void check_auto_anchor(const db& d, const std::string& tag, std::vector<uint32_t
   });
 }
 
+// frame::group_aggregate / filter over a host table built from the window
+// rows (the composition's own input) plus a string and an f64 column.
+void check_frame(const db& d, const std::string& tag) {
+  run(tag + ": frame group_aggregate / filter == reference (host table)", [&] {
+    const auto ids = d.ids();
+    const uint64_t T = d.t_max();
+    auto ing = ingest::ingest_traces(*d.h, ids, T / 5, 4 * T / 5, 1);
+    const auto& ev = ing.events;
+    const size_t n = ev.size();
+    std::vector<uint64_t> pid(n), ctx(n);
+    std::vector<int64_t> dur(n);
+    std::vector<double> durf(n);
+    std::vector<std::string> tag_col(n);
+    for (size_t i = 0; i < n; ++i) {
+      pid[i] = ev.profile_id[i];
+      ctx[i] = ev.ctx_id[i];
+      const uint64_t next = (i + 1 < n && ev.profile_id[i + 1] == ev.profile_id[i]) ? ev.timestamp_ns[i + 1] : 4 * T / 5;
+      dur[i] = static_cast<int64_t>(next - ev.timestamp_ns[i]);
+      durf[i] = static_cast<double>(dur[i]) / 1e9;
+      tag_col[i] = "r" + std::to_string(i % 7);
+    }
+    frame::table t;
+    t.add(frame::column::of_u64("profile_id", pid));
+    t.add(frame::column::of_u64("ctx_id", ctx));
+    t.add(frame::column::of_i64("dur_ns", dur));
+    t.add(frame::column::of_f64("dur_s", durf));
+    t.add(frame::column::of_str("tag", tag_col));
+    const std::vector<frame::agg_spec> aggs = {
+        {"dur_ns", frame::agg_fn::sum}, {"dur_ns", frame::agg_fn::min},  {"dur_ns", frame::agg_fn::max},
+        {"dur_ns", frame::agg_fn::mean}, {"dur_ns", frame::agg_fn::count}, {"dur_s", frame::agg_fn::sum},
+        {"dur_s", frame::agg_fn::min},  {"dur_s", frame::agg_fn::max},   {"dur_s", frame::agg_fn::mean}};
+    for (const std::vector<std::string>& keys :
+         {std::vector<std::string>{"profile_id", "ctx_id"}, std::vector<std::string>{"ctx_id"},
+          std::vector<std::string>{"dur_s", "profile_id"}})
+      expect(frame::group_aggregate(t, keys, aggs, frame::backend::seq()) ==
+                 gpu::group_aggregate(t, keys, aggs, frame::backend::seq()),
+             "group_aggregate keys " + keys.front());
+    for (auto op : {frame::cmp_op::lt, frame::cmp_op::le, frame::cmp_op::eq, frame::cmp_op::ge, frame::cmp_op::gt,
+                    frame::cmp_op::ne}) {
+      expect(frame::filter(t, "dur_ns", op, frame::literal{int64_t{1000}}, frame::backend::seq()) ==
+                 gpu::filter(t, "dur_ns", op, frame::literal{int64_t{1000}}, frame::backend::seq()),
+             "filter i64");
+      expect(frame::filter(t, "ctx_id", op, frame::literal{uint64_t{3}}, frame::backend::seq()) ==
+                 gpu::filter(t, "ctx_id", op, frame::literal{uint64_t{3}}, frame::backend::seq()),
+             "filter u64");
+      expect(frame::filter(t, "dur_s", op, frame::literal{1e-3}, frame::backend::seq()) ==
+                 gpu::filter(t, "dur_s", op, frame::literal{1e-3}, frame::backend::seq()),
+             "filter f64");
+    }
+    expect(raised([&] { gpu::filter(t, "dur_ns", frame::cmp_op::lt, frame::literal{1.0}, frame::backend::seq()); }) ==
+               errc::type_mismatch,
+           "literal type mismatch");
+    expect(raised([&] { gpu::group_aggregate(t, {"tag"}, aggs, frame::backend::seq()); }) == errc::type_mismatch,
+           "string key");
+    expect(raised([&] { gpu::group_aggregate(t, {"nope"}, aggs, frame::backend::seq()); }) ==
+               raised([&] { frame::group_aggregate(t, {"nope"}, aggs, frame::backend::seq()); }),
+           "missing column");
+  });
+}
+
+// detect_iterations / rematerialize on single traces given as events.
+void check_span_itermodel(const db& d, const std::string& tag, std::vector<uint32_t> anchors) {
+  run(tag + ": detect_iterations / rematerialize (span inputs) == reference", [&] {
+    const auto& meta = d.h->meta();
+    const uint64_t T = d.t_max();
+    for (uint32_t pid : d.ids()) {
+      auto [events, t_end] = d.h->read_trace_full(pid);
+      for (uint32_t a : anchors) {
+        std::vector<itermodel::interval> want;
+        const errc e = raised([&] { want = itermodel::detect_iterations(events, t_end, meta, a); });
+        std::vector<itermodel::interval> got;
+        const errc g = raised([&] { got = gpu::detect_iterations(events, t_end, meta, a); });
+        expect(e == g, "detect_iterations errc, trace " + std::to_string(pid));
+        if (e == errc::ok) expect(want == got, "intervals, trace " + std::to_string(pid));
+      }
+      for (auto [t0, t1] : std::vector<std::pair<uint64_t, uint64_t>>{{T / 4, 3 * T / 4}, {0, T + 1}, {T / 3, T / 3 + 5}}) {
+        auto w = d.h->read_trace_window(pid, t0, t1);
+        const itermodel::interval iv{t0, t1};
+        expect(itermodel::rematerialize(w.events, w.carry_in, iv, meta) ==
+                   gpu::rematerialize(w.events, w.carry_in, iv, meta),
+               "rematerialize, trace " + std::to_string(pid));
+      }
+    }
+  });
+}
+
+void check_small_diagnostics() {
+  run("balance_ratio / cv_percent / node_correlate / localize_outliers == reference", [&] {
+    util::xorshift64s rng(99);
+    for (size_t n : {1, 2, 7, 1000, 100000}) {
+      std::vector<double> v(n);
+      for (auto& x : v) x = rng.next_unit() * 3.0;
+      expect_rel(gpu::balance_ratio(v), diagnostics::balance_ratio(v), "balance_ratio n=" + std::to_string(n));
+      expect_rel(gpu::cv_percent(v), diagnostics::cv_percent(v), "cv n=" + std::to_string(n), 1e-9, 1e-12);
+    }
+    std::vector<double> zeros(5, 0.0), empty;
+    expect(gpu::balance_ratio(zeros) == 1.0, "all-zero ratio");
+    expect(raised([&] { gpu::cv_percent(zeros); }) == errc::undefined_cv, "zero-mean cv");
+    expect(raised([&] { gpu::balance_ratio(empty); }) == errc::empty_input, "empty ratio");
+    expect(raised([&] { gpu::cv_percent(empty); }) == errc::empty_input, "empty cv");
+    // node_correlate on the aurora-like layout (10 ranks per node)
+    auto [img, truth] = synthgen::generate_congestion_scenario(testutil::aurora_like_config(42));
+    std::vector<std::pair<int32_t, double>> rv;
+    for (const auto& p : img.meta.profiles)
+      if (p.rank >= 0) rv.push_back({p.rank, rng.next_unit()});
+    auto a = diagnostics::node_correlate(rv, img.meta), b = gpu::node_correlate(rv, img.meta);
+    expect(a.size() == b.size(), "node count");
+    for (size_t i = 0; i < a.size(); ++i)
+      expect(a[i].hostname == b[i].hostname && a[i].mean_value == b[i].mean_value &&
+                 a[i].rank_count == b[i].rank_count,
+             "node " + a[i].hostname);
+    rv.push_back({1 << 30, 1.0});
+    expect(raised([&] { gpu::node_correlate(rv, img.meta); }) == errc::not_found, "unknown rank");
+    // localize_outliers: the truth outliers, an outlier outside the universe,
+    // duplicates, chassis ids >= 64, and parse errors
+    std::vector<std::string> outl = truth.outlier_hostnames, uni = truth.node_hostnames;
+    outl.push_back(outl.front());
+    outl.push_back("x9000c70s0b0n0");
+    uni.push_back("x9000c70s1b0n1");
+    uni.push_back("x9001c4096s0b0n0");
+    outl.push_back("x9001c4096s0b0n0");
+    expect(topology::localize_outliers(outl, uni) == gpu::localize_outliers(outl, uni), "localize");
+    for (const std::string bad : {"nid0001", "x1c2s3b4", "x1c2s3b4n5z", "x1cXs0b0n0"}) {
+      auto u2 = uni;
+      u2.push_back(bad);
+      std::string want_msg, got_msg;
+      try { topology::localize_outliers(outl, u2); } catch (const error& e) { want_msg = e.what(); }
+      try { gpu::localize_outliers(outl, u2); } catch (const error& e) { got_msg = e.what(); }
+      expect(!want_msg.empty() && want_msg == got_msg, "parse error message for " + bad + ": " + got_msg);
+    }
+  });
+}
+
 // No context enters periodically: suggest_anchor raises no_periodicity.
 store::database_image aperiodic_image() {
   store::database_image img;
@@ -307,6 +441,8 @@ int main() {
     check_diagnostics(d, "small_iter", 1, 10.0);
     check_profiles(d, "small_iter");
     check_auto_anchor(d, "small_iter");
+    check_frame(d, "small_iter");
+    check_span_itermodel(d, "small_iter", {0, 1, 2, 3});
     check_auto_anchor(d, "small_iter (subset, first = last trace)", {d.ids().back()});
     run("small_iter: concurrent callers share one device (4 threads)", [&] {
       auto want = itermodel::build_tri_model(*d.h, d.ids(), itermodel::anchor_policy::explicit_ctx(1), 1);
@@ -354,6 +490,8 @@ int main() {
     db d(random_image(seed));
     check_everything(d, "random_" + std::to_string(seed), {0, 1, static_cast<uint32_t>(d.h->meta().contexts.size() - 1)});
     check_auto_anchor(d, "random_" + std::to_string(seed));
+    check_frame(d, "random_" + std::to_string(seed));
+    check_span_itermodel(d, "random_" + std::to_string(seed), {0, 1, static_cast<uint32_t>(d.h->meta().contexts.size() - 1)});
   }
   {
     db d(aperiodic_image());
@@ -364,6 +502,7 @@ int main() {
              "errc");
     });
   }
+  check_small_diagnostics();
   run("a database rewritten in place is reloaded (resident-trace cache keyed by file identity)", [&] {
     scratch_dir dir{"dropin_rewrite"};
     for (uint64_t seed : {11, 12, 13}) {
