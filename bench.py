@@ -175,7 +175,12 @@ def main():
     torch.cuda.set_stream(stream)
 
     n = args.traces
-    lo, hi = rank * n // world, (rank + 1) * n // world
+    # shards: contiguous rank ranges balanced by events with edges on node
+    # boundaries (100 ranks per node), so node means stay shard-local
+    # (every trace of this workload has the same length)
+    from paper_2605_03561_b200 import dist as pdist
+    lo, hi = pdist.node_aligned_ranges(np.arange(n) // 100, world,
+                                       np.full(n, args.iters * 67, np.float64))[rank]
     ctx = Context(local, stream=stream.cuda_stream)
     if world > 1:
         uid = [Context.comm_unique_id() if rank == 0 else None]

@@ -196,6 +196,9 @@ typedef struct psg_query_info {
    * < 2^32 ns, else 8) and total bytes incl. the per-row pad column */
   uint32_t cube_cell_bytes;
   uint64_t cube_store_bytes;
+  /* host round trips (stream synchronisations) the query made: 1 once an
+   * earlier query on the same traces has sized the device buffers */
+  uint32_t host_syncs;
 } psg_query_info;
 
 ps_status psg_query(psg_context* ctx, const psg_query_spec* spec, psg_query_info* info);

@@ -74,6 +74,7 @@ class QueryInfo(C.Structure):
         ("n_outliers", C.c_uint32), ("n_racks", C.c_uint32),
         ("ms_total", C.c_float), ("ms_main", C.c_float), ("ms_bounds", C.c_float),
         ("cube_cell_bytes", C.c_uint32), ("cube_store_bytes", C.c_uint64),
+        ("host_syncs", C.c_uint32),
     ]
 
 

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -186,6 +187,10 @@ struct psg_context {
   std::vector<uint32_t> h_pid;
   dbuf<uint64_t> d_off, d_ts, d_tend;
   dbuf<uint32_t> d_ctx, d_pid;
+  // narrow mirror of d_ctx when every ctx < 256 (pass 1 reads 1 B/event
+  // instead of 4); built on load when HBM allows, else pass 1 reads d_ctx
+  dbuf<uint8_t> d_ctx8;
+  bool ctx8_valid = false;
   dbuf<uint8_t> d_stage;
   uint8_t* pinned[3] = {nullptr, nullptr, nullptr};  // pageable-source staging ring
   cudaEvent_t pinned_ev[3] = {nullptr, nullptr, nullptr};
@@ -300,8 +305,20 @@ struct psg_context {
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
+  // query status block (QS_*), and what the speculative path needs: buffers
+  // sized by an earlier query on these traces, the K its statistics planes
+  // are laid out for, the global rank count
+  dbuf<unsigned long long> qstat;
+  bool spec_ready = false;
+  uint32_t k_plane = 0;
+  uint64_t ranks_global_cache = 0;
+  uint64_t n_syncs = 0;  // stream synchronisations (psg_query_info::host_syncs)
+
   trace_view view() const { return {d_off.p, d_ts.p, d_ctx.p, d_tend.p, n_traces}; }
-  void sync() { PSG_CUDA(cudaStreamSynchronize(stream)); }
+  void sync() {
+    ++n_syncs;
+    PSG_CUDA(cudaStreamSynchronize(stream));
+  }
 
   // Summary exchange between ranks: NCCL on device buffers, or a host
   // callback (psg_comm_init_host) on a staged host copy.
@@ -364,6 +381,8 @@ void invalidate_results(psg_context* c) {
   c->have_window = c->have_carry = c->have_cube = c->have_stats = c->have_outliers = false;
 }
 
+void build_ctx8(psg_context* c);
+
 void set_cct_impl(psg_context* c, const uint32_t* parent, uint32_t n_ctx) {
   require(parent != nullptr && n_ctx > 0, "parent array and n_ctx > 0 are required");
   if (parent[0] != store::k_no_parent) fail(PS_E_FORMAT, "ctx 0: root must have no parent");
@@ -383,6 +402,27 @@ void set_cct_impl(psg_context* c, const uint32_t* parent, uint32_t n_ctx) {
   c->cached_anchor = -1;
   invalidate_results(c);
   c->sync();
+  build_ctx8(c);  // the mirror holds preorder positions of this tree
+}
+
+// The narrow ctx mirror (validated ctx < n_ctx <= 256): 1 B/event more HBM,
+// built only when at least half the event bytes stay free afterwards (room
+// for the cube, ~1/3 of the event bytes with 32-bit cells); PSG_NO_CTX8=1
+// turns it off (A/B).
+void build_ctx8(psg_context* c) {
+  c->ctx8_valid = false;
+  const char* off = std::getenv("PSG_NO_CTX8");
+  if ((off && *off == '1') || c->n_ctx > 256 || c->n_events == 0) return;
+  const uint64_t need = c->n_events + 2 * kEventPad;
+  if (c->d_ctx8.n < need) {
+    size_t free_b = 0, total_b = 0;
+    PSG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    c->d_ctx8.release();
+    if (free_b < need || free_b - need < 6 * c->n_events) return;
+    c->d_ctx8.ensure(need);
+  }
+  launch_ctx8(c->d_ctx.p, c->n_events, c->d_cct_pre.p, c->n_ctx, c->d_ctx8.p, c->stream);
+  c->ctx8_valid = true;
 }
 
 // Uploads the trace index and validates the SoA already in d_ts/d_ctx.
@@ -410,6 +450,8 @@ void finish_load(psg_context* c) {
                              8ull * c->n_traces, cudaMemcpyHostToDevice, c->stream));
     tb = c->d_tbegin.p;
   }
+  c->spec_ready = false;  // the first query on these traces sizes the buffers
+  c->ranks_global_cache = 0;
   launch_validate(c->view(), c->n_ctx, tb, flags, flags + 1, c->stream);
   unsigned long long out[2];
   PSG_CUDA(cudaMemcpyAsync(out, flags, sizeof(out), cudaMemcpyDeviceToHost, c->stream));
@@ -418,6 +460,7 @@ void finish_load(psg_context* c) {
     fail(PS_E_FORMAT, std::to_string(out[0]) + " trace(s) violate the format (first: trace " +
                           std::to_string(c->h_pid[out[1]]) +
                           "): non-decreasing timestamps, ctx < n_ctx and t_end >= last event are required");
+  build_ctx8(c);
   invalidate_results(c);
 }
 
@@ -840,6 +883,8 @@ ps_status psg_comm_init(psg_context* c, int nranks, int rank, const uint8_t id[1
     if (c->comm) nccl().comm_destroy(c->comm);
     c->comm = nullptr;
     c->host_fn = nullptr;
+    c->spec_ready = false;
+    c->ranks_global_cache = 0;
     c->nranks = nranks;
     c->rank = rank;
     if (nranks == 1) return;
@@ -856,6 +901,8 @@ ps_status psg_comm_init_host(psg_context* c, int nranks, int rank, psg_allreduce
     require(nranks >= 1 && rank >= 0 && rank < nranks, "bad nranks/rank");
     if (c->comm) nccl().comm_destroy(c->comm);
     c->comm = nullptr;
+    c->spec_ready = false;
+    c->ranks_global_cache = 0;
     c->nranks = nranks;
     c->rank = rank;
     c->host_fn = fn;
@@ -1338,6 +1385,22 @@ ps_status psg_get_traces(psg_context* c, uint64_t* ts, uint32_t* ctx_ids, uint64
 }
 
 // ---------------------------------------------------------------------------
+// Traces over all ranks (the balance ratios' denominator): one exchange per
+// load, cached.
+uint64_t ranks_global(psg_context* c) {
+  if (!c->multi()) return c->n_traces;
+  if (c->ranks_global_cache == 0) {
+    unsigned long long* d = c->summary.ensure(8);
+    unsigned long long hn = c->n_traces;
+    PSG_CUDA(cudaMemcpyAsync(d, &hn, 8, cudaMemcpyHostToDevice, c->stream));
+    c->allreduce(d, 1, ncclUint64, ncclSum);
+    PSG_CUDA(cudaMemcpyAsync(&hn, d, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    c->ranks_global_cache = hn;
+  }
+  return c->ranks_global_cache;
+}
+
 ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* info) {
   if (!c || !q || !info) return PS_E_INVALID_ARGUMENT;
   return guarded([&] {
@@ -1354,12 +1417,15 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     if (c->n_ctx == 0) fail(PS_E_INVALID_ARGUMENT, "no calling-context tree loaded");
     invalidate_results(c);
     std::memset(info, 0, sizeof(*info));
+    const uint64_t syncs0 = c->n_syncs;
     const uint32_t n = c->n_traces;
     cudaStream_t s = c->stream;
     PSG_CUDA(cudaEventRecord(c->ev[0], s));
 
     query_params p{};
     p.tr = c->view();
+    p.t_base = 0;
+    p.t_stop = n;
     p.n_ctx = c->n_ctx;
     p.G = PSG_G;
     if (do_window) {
@@ -1387,19 +1453,33 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     info->anchor = do_cube ? anchor : 0;
     bool exact_bounds = c->exact_hint || (f & PSG_Q_EXACT_BOUNDS) != 0;
     const bool force64 = (f & PSG_Q_CUBE64) != 0;
-    for (;;) {  // optimistic pass 1 / 32-bit cells, verified by pass 2 (re-run on a miss)
+    // The status block carries every count a later kernel needs (K, kept
+    // traces) and every verdict (pass-1 overflow, optimistic pass 1, buffer
+    // capacities).  A speculative query (buffers sized by an earlier query on
+    // these traces, optimistic pass 1) runs all its kernels back to back and
+    // reads the block once at the end; any miss re-runs the query with the
+    // host sizing each step (the first query after a load always does).
+    unsigned long long* qs = c->qstat.ensure(QS_WORDS);
+    unsigned long long hq[QS_WORDS] = {};
+    const char* nospec = std::getenv("PSG_NO_SPEC");
+    bool spec = c->spec_ready && !(nospec && *nospec == '1');
+    uint32_t k_cap = 0;  // K the statistics accumulators are laid out for
+    for (;;) {
+    const bool sp = spec && do_cube && !exact_bounds;
+    PSG_CUDA(cudaMemsetAsync(qs, 0, QS_WORDS * sizeof(unsigned long long), s));
     if (do_cube) {
       compute_subtree(c, anchor);
       nn = c->nn;
       uint32_t* ic = c->iter_count.ensure(n + 1);
       // pass 1: iteration boundaries (re-run with exact region bounds on overflow)
-      unsigned long long* sum = c->summary.ensure(8);
-      unsigned long long h[8];
       PSG_CUDA(cudaEventRecord(c->ev[4], s));
       for (;;) {
         if (!c->caps_valid) build_caps(c);
         bound_params bp{};
         bp.tr = c->view();
+        bp.ctx8 = c->ctx8_valid ? c->d_ctx8.p : nullptr;
+        bp.sub_lo = static_cast<uint32_t>(c->cct_po.pre[anchor]);
+        bp.sub_size = static_cast<uint32_t>(c->cct_po.size[anchor]);
         bp.contains = c->d_contains.p;
         bp.words = c->contains_words;
         bp.cap_off = c->d_cap_off.p;
@@ -1407,42 +1487,46 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
         bp.bts = c->d_bts.p;
         bp.n_bounds = c->d_nbounds.ensure(n + 1);
         bp.iter_count = ic;
-        bp.overflow = sum + 3;
-        PSG_CUDA(cudaMemsetAsync(sum + 3, 0, 8, s));
+        bp.overflow = qs + QS_OVERFLOW;
         launch_bounds(bp, exact_bounds, s);
-        PSG_CUDA(cudaMemcpyAsync(&h[3], sum + 3, 8, cudaMemcpyDeviceToHost, s));
+        if (sp) break;  // checked at the end
+        PSG_CUDA(cudaMemcpyAsync(&hq[QS_OVERFLOW], qs + QS_OVERFLOW, 8, cudaMemcpyDeviceToHost, s));
         c->sync();
-        if (h[3] == 0 || c->cap_div <= 2) break;
+        if (hq[QS_OVERFLOW] == 0 || c->cap_div <= 2) break;
         c->cap_div = 2;
         c->caps_valid = false;
+        PSG_CUDA(cudaMemsetAsync(qs + QS_OVERFLOW, 0, 8, s));
       }
       PSG_CUDA(cudaEventRecord(c->ev[5], s));
       const size_t sb = cube_layout_scratch_bytes(n);
       launch_cube_layout(ic, n, nn, row_stride(nn), c->tpos.ensure(n + 1), c->block_off.ensure(n + 1),
-                         c->iter_off.ensure(n + 1), c->kept_bo.ensure(n + 1), sum,
+                         c->iter_off.ensure(n + 1), c->kept_bo.ensure(n + 1), qs,
                          c->scratch.ensure(sb), sb, s);
-      PSG_CUDA(cudaMemsetAsync(sum + 5, 0, 16, s));  // [5] longest iteration, [6] pass-2 verdict
-      if (exact_bounds) launch_iter_spans(c->d_cap_off.p, c->d_bts.p, ic, c->d_tend.p, n, sum + 5, s);
-      PSG_CUDA(cudaMemcpyAsync(h, sum, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-      c->sync();
-      c->n_kept = static_cast<uint32_t>(h[0]);
-      c->n_cells = h[2];
-      c->n_store = h[4];
-      // 32-bit cells: exact spans from pass 1, or optimistic (verified by pass 2)
-      c->cube32 = !force64 && (!exact_bounds || h[5] < (1ull << 32));
-      unsigned long long g[2] = {h[1], h[0]};  // min iterations, kept count
+      if (exact_bounds) launch_iter_spans(c->d_cap_off.p, c->d_bts.p, ic, c->d_tend.p, n, qs + QS_SPAN, s);
+      // global {kept, min iterations}: K for every kernel that follows
+      PSG_CUDA(cudaMemcpyAsync(qs + QS_KEPT_G, qs + QS_KEPT, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, s));
+      static_assert(QS_MIN_IT_G == QS_KEPT_G + 1 && QS_MIN_IT == QS_KEPT + 1, "status layout");
       if (c->multi()) {
-        unsigned long long* d = c->summary.p;  // reuse as staging
-        PSG_CUDA(cudaMemcpyAsync(d, g, sizeof(g), cudaMemcpyHostToDevice, s));
         c->group_begin();
-        c->allreduce(d, 1, ncclUint64, ncclMin);
-        c->allreduce(d + 1, 1, ncclUint64, ncclSum);
+        c->allreduce(qs + QS_KEPT_G, 1, ncclUint64, ncclSum);
+        c->allreduce(qs + QS_MIN_IT_G, 1, ncclUint64, ncclMin);
         c->group_end();
-        PSG_CUDA(cudaMemcpyAsync(g, d, sizeof(g), cudaMemcpyDeviceToHost, s));
-        c->sync();
       }
-      c->K = g[1] > 0 ? static_cast<uint32_t>(g[0]) : 0;
-      c->n_kept_global = static_cast<uint32_t>(g[1]);
+      const uint32_t m = static_cast<uint32_t>(c->internal_pos.size());
+      if (!sp) {
+        PSG_CUDA(cudaMemcpyAsync(hq, qs, sizeof(hq), cudaMemcpyDeviceToHost, s));
+        c->sync();
+        // 32-bit cells: exact spans from pass 1, or optimistic (verified by pass 2)
+        c->cube32 = !force64 && (!exact_bounds || hq[QS_SPAN] < (1ull << 32));
+        // buffers sized exactly (grow-only: later queries run speculatively in them)
+        c->cube_incl.ensure((hq[QS_STORE] * (c->cube32 ? 4 : 8) + 7) / 8 + 2);
+        if (store_cube) c->cube_xint.ensure((nn ? hq[QS_CELLS] / nn : 0) * m + 1);
+        k_cap = qs_K(hq);
+      } else {
+        c->cube32 = !force64;
+        k_cap = (do_stats && nn) ? static_cast<uint32_t>(c->x_acc.n / (5ull * nn)) : 0u;
+      }
       p.do_cube = 1;
       p.store_cube = store_cube ? 1 : 0;
       p.sub_pre = c->d_sub_pre.p;
@@ -1457,27 +1541,31 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       p.tpos = c->tpos.p;
       p.block_off = c->block_off.p;
       p.iter_off = c->iter_off.p;
-      p.K = c->K;
+      p.qs = qs;
+      p.cap_miss = sp ? qs + QS_CAP_MISS : nullptr;
       // incl is always materialised (the cross-rank statistics stream it);
       // PSG_Q_NO_CUBE_STORE drops the excl half
-      p.cube_incl = c->cube_incl.ensure((c->n_store * (c->cube32 ? 4 : 8) + 7) / 8 + 2);
+      p.cube_incl = c->cube_incl.ensure(1);
+      p.cube_cap = c->cube_incl.n * 8 / (c->cube32 ? 4 : 8);
       p.cube32 = c->cube32 ? 1 : 0;
       p.exact_bounds = exact_bounds ? 1 : 0;
-      p.m = static_cast<uint32_t>(c->internal_pos.size());
-      if (store_cube) p.cube_xint = c->cube_xint.ensure((nn ? c->n_cells / nn : 0) * p.m + 1);
+      p.m = m;
+      if (store_cube) p.cube_xint = c->cube_xint.ensure(1);
+      p.xint_cap = store_cube ? c->cube_xint.n : 0;
       c->have_excl = store_cube;
-      p.gap_incl = c->gap_incl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
-      p.gap_excl = c->gap_excl.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
-      if (do_stats && c->K > 0) {
-        const size_t plane = static_cast<size_t>(c->K) * nn;
+      // per kept trace rows: sized for every trace (the kept count is known on the device)
+      p.gap_incl = c->gap_incl.ensure(static_cast<size_t>(n) * nn + 1);
+      p.gap_excl = c->gap_excl.ensure(static_cast<size_t>(n) * nn + 1);
+      if (do_stats && k_cap > 0) {
+        const size_t plane = static_cast<size_t>(k_cap) * nn;
         unsigned long long* x = c->x_acc.ensure(5 * plane);
         PSG_CUDA(cudaMemsetAsync(x, 0, 5 * plane * sizeof(unsigned long long), s));
         p.do_stats = 1;
         p.x_sum = x;
         p.x_max = x + plane;
         p.x_sq = x + 2 * plane;
-        p.within_cv = c->within_cv.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
-        p.within_ok = c->within_ok.ensure(static_cast<size_t>(c->n_kept) * nn + 1);
+        p.within_cv = c->within_cv.ensure(static_cast<size_t>(n) * nn + 1);
+        p.within_ok = c->within_ok.ensure(static_cast<size_t>(n) * nn + 1);
       }
     }
     // launch geometry
@@ -1516,28 +1604,27 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     if (do_cube && !exact_bounds) {
       // the optimistic pass 1 (and its 32-bit cells) against the boundary
       // timestamps pass 2 recorded; a miss re-runs both passes exactly
-      unsigned long long* v = c->summary.p + 6;
+      unsigned long long* v = qs + QS_VERIFY;
       launch_verify_bounds(c->view(), c->d_cap_off.p, c->d_bts.p, c->d_nbounds.p, c->iter_count.p, v, s);
-      if (c->multi()) c->allreduce(v, 1, ncclUint64, ncclMax);  // every rank re-runs together
-      unsigned long long hv = 0;
-      PSG_CUDA(cudaMemcpyAsync(&hv, v, 8, cudaMemcpyDeviceToHost, s));
-      c->sync();
-      if (hv) {  // duplicate boundary timestamps, or an iteration >= 2^32 ns
-        exact_bounds = c->exact_hint = true;
-        continue;
+      if (!sp) {
+        if (c->multi()) c->allreduce(v, 1, ncclUint64, ncclMax);  // every rank re-runs together
+        PSG_CUDA(cudaMemcpyAsync(&hq[QS_VERIFY], v, 8, cudaMemcpyDeviceToHost, s));
+        c->sync();
+        if (hq[QS_VERIFY]) {  // duplicate boundary timestamps, or an iteration >= 2^32 ns
+          exact_bounds = c->exact_hint = true;
+          continue;
+        }
       }
     }
-    break;
-    }
 
-    if (do_stats && c->K > 0) {
-      const size_t plane = static_cast<size_t>(c->K) * nn;
-      launch_cross_stats(c->cube_incl.p, c->cube32, c->kept_bo.p, c->n_kept, nn, row_stride(nn), c->K, c->x_acc.p,
-                         c->x_acc.p + plane, c->x_acc.p + 2 * plane, s);
+    if (do_stats && k_cap > 0) {
+      const size_t plane = static_cast<size_t>(k_cap) * nn;
+      launch_cross_stats(c->cube_incl.p, c->cube32, c->kept_bo.p, n, nn, row_stride(nn), k_cap, c->x_acc.p,
+                         c->x_acc.p + plane, c->x_acc.p + 2 * plane, qs, s);
       double* no = c->node_out.ensure(static_cast<size_t>(nn) * (10 + 2 * 148) + 1);  // + tile partials
       // within-rank partial sums per node, then cross-GPU sums of everything
-      launch_stats_finalize(nullptr, nullptr, nullptr, c->K, nn, c->n_kept_global, c->within_cv.p,
-                            c->within_ok.p, c->n_kept, no, s);
+      launch_stats_finalize(nullptr, nullptr, nullptr, k_cap, k_cap, nn, n, c->within_cv.p,
+                            c->within_ok.p, n, no, qs, s);
       if (c->multi()) {
         c->group_begin();
         c->allreduce(c->x_acc.p, plane, ncclUint64, ncclSum);
@@ -1546,9 +1633,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
         c->allreduce(no + static_cast<size_t>(nn) * 8, 2 * nn, ncclFloat64, ncclSum);
         c->group_end();
       }
-      launch_stats_finalize(c->x_acc.p, c->x_acc.p + plane, c->x_acc.p + 2 * plane, c->K, nn,
-                            c->n_kept_global, nullptr, nullptr, c->n_kept, no, s);
-      c->have_stats = true;
+      launch_stats_finalize(c->x_acc.p, c->x_acc.p + plane, c->x_acc.p + 2 * plane, k_cap, k_cap, nn,
+                            n, nullptr, nullptr, n, no, qs, s);
     }
 
     if (do_out) {
@@ -1566,21 +1652,13 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       PSG_CUDA(cudaMemsetAsync(na, 0, 16ull * c->n_nodes, s));
       launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
                       sa, na, c->d_worst.ensure(2), c->site_ratio.ensure(ns), 0, s);
-      uint64_t ranks_global = n;
       if (c->multi()) {
         c->group_begin();
         c->allreduce(sa, ns, ncclUint64, ncclSum);
         c->allreduce(sa + ns, ns, ncclUint64, ncclMax);
         c->group_end();
-        unsigned long long* d = c->summary.p;
-        unsigned long long hn = n;
-        PSG_CUDA(cudaMemcpyAsync(d, &hn, 8, cudaMemcpyHostToDevice, s));
-        c->allreduce(d, 1, ncclUint64, ncclSum);
-        PSG_CUDA(cudaMemcpyAsync(&hn, d, 8, cudaMemcpyDeviceToHost, s));
-        c->sync();
-        ranks_global = hn;
       }
-      launch_outliers(c->w_incl.p, static_cast<uint32_t>(ranks_global), c->n_ctx, c->d_sites.p, ns,
+      launch_outliers(c->w_incl.p, static_cast<uint32_t>(ranks_global(c)), c->n_ctx, c->d_sites.p, ns,
                       c->d_node_of_trace.p, c->n_nodes, sa, na, c->d_worst.p, c->site_ratio.p, 1, s);
       launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
                       sa, na, c->d_worst.p, c->site_ratio.p, 2, s);
@@ -1595,10 +1673,53 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
                         c->d_uni_cnt.p, nr, c->d_rack_nodes.ensure(nr), c->rack_mask.ensure(nr),
                         c->rack_full.ensure(nr), c->rack_cnt.ensure(64ull * nr), s);
       }
-      c->have_outliers = true;
+      launch_outlier_summary(c->d_worst.p, c->d_nsel.p, c->site_ratio.p, nr ? c->d_rack_nodes.p : nullptr,
+                             nr, qs, s);
+    }
+    if (sp && do_stats) launch_qs_check_k(qs, k_cap, s);  // K beyond the accumulator planes
+    if (sp && c->multi()) {  // every rank re-runs together
+      c->group_begin();
+      c->allreduce(qs + QS_OVERFLOW, 1, ncclUint64, ncclMax);
+      c->allreduce(qs + QS_VERIFY, 1, ncclUint64, ncclMax);
+      c->allreduce(qs + QS_CAP_MISS, 1, ncclUint64, ncclMax);
+      c->group_end();
     }
     PSG_CUDA(cudaEventRecord(c->ev[3], s));
+    // the query's one host round trip: the status block
+    PSG_CUDA(cudaMemcpyAsync(hq, qs, sizeof(hq), cudaMemcpyDeviceToHost, s));
     c->sync();
+    if (const char* tq = std::getenv("PSG_TRACE_QUERY"); tq && *tq == '1')
+      std::fprintf(stderr, "psg_query: spec=%d exact=%d overflow=%llu verify=%llu cap_miss=%llu K=%u k_cap=%u syncs=%llu\n",
+                   sp ? 1 : 0, exact_bounds ? 1 : 0, hq[QS_OVERFLOW], hq[QS_VERIFY], hq[QS_CAP_MISS],
+                   qs_K(hq), k_cap, static_cast<unsigned long long>(c->n_syncs - syncs0));
+    if (sp && (hq[QS_OVERFLOW] || hq[QS_VERIFY] || hq[QS_CAP_MISS])) {
+      // a miss: re-run with the host sizing every step (and, for the
+      // optimistic pass 1's verdict, in the exact mode)
+      if (hq[QS_OVERFLOW]) {
+        c->cap_div = 2;
+        c->caps_valid = false;
+      }
+      // the verdict on the optimistic pass 1 only counts for a run whose
+      // regions and buffers held (clamped regions make pass 2's boundary
+      // record meaningless); the re-run verifies again
+      if (hq[QS_VERIFY] && !hq[QS_OVERFLOW] && !hq[QS_CAP_MISS]) exact_bounds = c->exact_hint = true;
+      spec = false;
+      continue;
+    }
+    break;
+    }
+
+    if (do_cube) {
+      c->n_kept = static_cast<uint32_t>(hq[QS_KEPT]);
+      c->n_cells = hq[QS_CELLS];
+      c->n_store = hq[QS_STORE];
+      c->K = qs_K(hq);
+      c->n_kept_global = static_cast<uint32_t>(hq[QS_KEPT_G]);
+      c->k_plane = k_cap;
+      c->spec_ready = true;
+    }
+    if (do_stats && c->K > 0) c->have_stats = true;
+    if (do_out) c->have_outliers = true;
 
     // info
     if (do_window) c->have_window = c->have_carry = true;
@@ -1614,21 +1735,15 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     info->n_leaves = do_cube ? static_cast<uint32_t>(c->leaves.size()) : 0;
     info->n_internal = do_cube ? static_cast<uint32_t>(c->internal_pos.size()) : 0;
     if (do_out) {
-      uint32_t w[2];
-      PSG_CUDA(cudaMemcpy(w, c->d_worst.p, 4, cudaMemcpyDeviceToHost));
-      PSG_CUDA(cudaMemcpy(&info->n_outliers, c->d_nsel.p, 4, cudaMemcpyDeviceToHost));
-      info->worst_site = c->sites[w[0]];
-      PSG_CUDA(cudaMemcpy(&info->worst_ratio, c->site_ratio.p + w[0], 8, cudaMemcpyDeviceToHost));
-      uint32_t nr = static_cast<uint32_t>(c->h_rack_ids.size());
-      if (nr) {
-        std::vector<uint32_t> rn(nr);
-        PSG_CUDA(cudaMemcpy(rn.data(), c->d_rack_nodes.p, 4ull * nr, cudaMemcpyDeviceToHost));
-        for (uint32_t x : rn) info->n_racks += x > 0;
-      }
+      info->worst_site = c->sites[hq[QS_WORST]];
+      info->n_outliers = static_cast<uint32_t>(hq[QS_NSEL]);
+      std::memcpy(&info->worst_ratio, &hq[QS_WORST_RATIO], sizeof(double));
+      info->n_racks = static_cast<uint32_t>(hq[QS_RACKS]);
     }
     PSG_CUDA(cudaEventElapsedTime(&info->ms_total, c->ev[0], c->ev[3]));
     PSG_CUDA(cudaEventElapsedTime(&info->ms_main, c->ev[1], c->ev[2]));
     if (do_cube) PSG_CUDA(cudaEventElapsedTime(&info->ms_bounds, c->ev[4], c->ev[5]));
+    info->host_syncs = static_cast<uint32_t>(c->n_syncs - syncs0);
   });
 }
 

@@ -76,9 +76,40 @@ struct profile_view {
   uint32_t n;
 };
 
+// The query's device-side status block (u64 words).  The layout kernels,
+// pass 1, pass 2 and the verification write it; the statistics kernels read
+// K and the kept counts from it, so a query needs no host round trip between
+// its kernels: the host reads the block once, at the end (psg_capi.cu).
+enum : uint32_t {
+  QS_KEPT = 0,       // kept traces (this rank)
+  QS_MIN_IT = 1,     // min iterations over kept traces (this rank; ~0 when none)
+  QS_CELLS = 2,      // logical cube cells (Σ iters * nn)
+  QS_OVERFLOW = 3,   // pass-1 traces whose boundaries did not fit their region
+  QS_STORE = 4,      // storage cells of the cube
+  QS_SPAN = 5,       // longest stored iteration (exact pass 1)
+  QS_VERIFY = 6,     // verdict on the optimistic pass 1 (bits; k_verify_bounds)
+  QS_CAP_MISS = 7,   // the speculative capacities did not hold (bits: 1 cube, 2 excl, 4 K)
+  QS_KEPT_G = 8,     // kept traces over all ranks
+  QS_MIN_IT_G = 9,   // min iterations over all ranks' kept traces
+  QS_WORST = 10,     // outliers: worst site index
+  QS_NSEL = 11,      // outliers: selected nodes
+  QS_WORST_RATIO = 12,  // outliers: the worst site's ratio (f64 bits)
+  QS_RACKS = 13,     // outliers: racks holding a selected node
+  QS_WORDS = 16
+};
+// K = the global min iterations over kept traces (0 when none: diagnostics.cpp:101)
+__host__ __device__ inline uint32_t qs_K(const unsigned long long* qs) {
+  return qs[QS_KEPT_G] ? static_cast<uint32_t>(qs[QS_MIN_IT_G]) : 0u;
+}
+
 // Pass 1 (k_bounds): iteration boundaries per trace (itermodel.cpp:111-143).
 struct bound_params {
   trace_view tr;
+  // narrow mirror of tr.ctx (every ctx < 256), or null: 1 B/event holding the
+  // ctx's preorder position in the whole CCT, so the anchor subtree is the
+  // byte range [sub_lo, sub_lo + sub_size) and membership is a SIMD compare
+  const uint8_t* ctx8;
+  uint32_t sub_lo, sub_size;
   const uint32_t* contains;  // [ceil(n_ctx/32)] bit c set iff ctx c is in the anchor subtree
   uint32_t words;
   const uint64_t* cap_off;   // [n+1] offsets of the per-trace boundary regions in bidx
@@ -191,7 +222,11 @@ struct query_params {
   const uint32_t* tpos;        // [n] position among kept traces
   const uint64_t* block_off;   // [n] storage cell offset of the trace's first row (kept traces)
   const uint64_t* iter_off;    // [n] iterations stored before the trace (kept traces)
-  uint32_t K;                  // global min iterations over kept traces (0: none)
+  uint32_t K;                  // global min iterations over kept traces (0: none) ...
+  const unsigned long long* qs;  // ... or, when set, qs_K(qs) of the device status block
+  unsigned long long* cap_miss;  // speculative capacities: QS_CAP_MISS word (or null)
+  uint64_t cube_cap;             // storage cells the cube buffer holds
+  uint64_t xint_cap;             // entries the compact excl buffer holds
   // The cube is stored compactly: incl in rows of stride nnp (nn + 1 rounded
   // up to even: pad columns), each trace's block padded to 16 bytes, as 32-bit cells when every
   // stored iteration spans < 2^32 ns (cube32) else 64-bit; excl only for the m
@@ -211,6 +246,7 @@ struct query_params {
   warp_smem_layout L;  // per-warp shared-memory carve-out (computed on the host)
   uint32_t cta_bytes;  // cta_table_bytes(n_ctx, nn, warps), computed on the host
   uint32_t one_warp;   // CTA shape: one warp per CTA (long traces) or up to 16
+  uint32_t t_base, t_stop;  // this launch's traces [t_base, t_stop) (a part of tr.n)
 };
 
 // CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]
@@ -234,6 +270,10 @@ void launch_soa_to_aos(const uint64_t* ts, const uint32_t* ctx, uint64_t n_event
 
 void launch_aos_to_soa(const uint8_t* body, uint64_t n_events, uint64_t* ts, uint32_t* ctx,
                        cudaStream_t s);
+// Narrow mirror of the ctx words (every ctx < 256): out[i] = pre[ctx[i]] (the
+// ctx's preorder position in the CCT), n events.
+void launch_ctx8(const uint32_t* ctx, uint64_t n, const int32_t* pre, uint32_t n_ctx, uint8_t* out,
+                 cudaStream_t s);
 void launch_validate(const trace_view& tr, uint32_t n_ctx, const uint64_t* t_begin,
                      unsigned long long* bad, unsigned long long* first_bad, cudaStream_t s);
 void launch_gen_iterative(const uint64_t* jump_mats, uint64_t seed, uint32_t n_ranks,
@@ -274,13 +314,34 @@ void launch_cube_dense(const void* incl, bool cube32, const uint64_t* xint, cons
                        const uint64_t* block_off, const uint64_t* iter_off, const int4* node_tab,
                        uint32_t nn, uint32_t nnp, uint32_t m, uint32_t t_lo, uint32_t t_hi,
                        uint64_t dense_row0, int64_t* out_incl, int64_t* out_excl, cudaStream_t s);
+// Cross-rank sums over k < K, n_kept kept traces; with qs set, K and n_kept
+// come from the status block and the arguments are capacities (K_cap sets the
+// accumulator plane stride K_cap * nn); a set QS_CAP_MISS word skips the work.
+// part: with tpos set, only the kept traces of loaded traces [ta, tb) (kept
+// positions tpos[ta] .. tpos[tb], tpos[n] = QS_KEPT), in CTAs of `threads`.
+struct cross_part {
+  const uint32_t* tpos = nullptr;
+  uint32_t ta = 0, tb = 0, n = 0;
+  uint32_t threads = 512;
+};
 void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, uint32_t n_kept,
                         uint32_t nn, uint32_t nnp, uint32_t K, unsigned long long* x_sum,
-                        unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s);
+                        unsigned long long* x_max, unsigned long long* x_sq,
+                        const unsigned long long* qs, cudaStream_t s, const cross_part& part = {});
+// plane_k: the K of the accumulator layout (x_sq limbs at plane_k * nn strides);
+// with qs set, K / n_kept (global) / n_kept_local come from the status block.
 void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,
-                           const unsigned long long* x_sq, uint32_t K, uint32_t nn,
+                           const unsigned long long* x_sq, uint32_t K, uint32_t plane_k, uint32_t nn,
                            uint32_t n_kept, const double* within_cv, const uint8_t* within_ok,
-                           uint32_t n_kept_local, double* node_out /*[nn][8]*/, cudaStream_t s);
+                           uint32_t n_kept_local, double* node_out /*[nn][8]*/,
+                           const unsigned long long* qs, cudaStream_t s);
+// QS_CAP_MISS |= 4 when the query's K exceeds k_cap (the statistics planes).
+void launch_qs_check_k(unsigned long long* qs, uint32_t k_cap, cudaStream_t s);
+// The end-of-query summary of the outlier step into the status block
+// (QS_WORST, QS_NSEL, QS_WORST_RATIO, QS_RACKS).
+void launch_outlier_summary(const uint32_t* worst, const uint32_t* n_sel, const double* site_ratio,
+                            const uint32_t* rack_nodes, uint32_t n_racks, unsigned long long* qs,
+                            cudaStream_t s);
 void launch_window_bounds(const trace_view& tr, uint64_t t0, uint64_t t1, uint64_t* cnt,
                           uint8_t* c_has, uint64_t* c_ts, uint32_t* c_ctx, cudaStream_t s);
 void launch_window_copy(const trace_view& tr, const uint32_t* pid, uint64_t t0,

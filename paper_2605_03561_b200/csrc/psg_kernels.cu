@@ -196,6 +196,49 @@ void launch_validate(const trace_view& tr, uint32_t n_ctx, const uint64_t* t_beg
   PSG_CUDA(cudaGetLastError());
 }
 
+// K1n: the narrow ctx mirror pass 1 reads (1 B/event instead of 4): 16 ctx
+// words (four 16-byte loads) -> 16 bytes (one 16-byte store) per thread, each
+// ctx replaced by its preorder position in the CCT (any subtree is then one
+// contiguous byte range).
+__global__ void __launch_bounds__(256) k_ctx8(const uint32_t* __restrict__ ctx, uint64_t n,
+                                              const int32_t* __restrict__ pre, uint32_t n_ctx,
+                                              uint8_t* __restrict__ out) {
+  __shared__ uint32_t s_pre[256];
+  s_pre[threadIdx.x] = threadIdx.x < n_ctx ? static_cast<uint32_t>(pre[threadIdx.x]) : 0u;
+  __syncthreads();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 16;
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; i < n;
+       i += stride) {
+    if (i + 16 <= n) {
+      const uint4* src = reinterpret_cast<const uint4*>(ctx + i);
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = __ldg(src + q);
+        w[q] = s_pre[v.x & 255u] | (s_pre[v.y & 255u] << 8) | (s_pre[v.z & 255u] << 16) |
+               (s_pre[v.w & 255u] << 24);
+      }
+      *reinterpret_cast<uint4*>(out + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      for (uint64_t j = i; j < n; ++j) out[j] = static_cast<uint8_t>(s_pre[ctx[j] & 255u]);
+    }
+  }
+}
+
+void launch_ctx8(const uint32_t* ctx, uint64_t n, const int32_t* pre, uint32_t n_ctx, uint8_t* out,
+                 cudaStream_t s) {
+  if (n == 0) return;
+  if (n_ctx > 256) fail(PS_E_INTERNAL, "ctx8 mirror needs n_ctx <= 256");
+  int dev = 0, sms = 148;
+  PSG_CUDA(cudaGetDevice(&dev));
+  PSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const uint64_t need = (n + 16 * 256 - 1) / (16 * 256);
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(need, static_cast<uint64_t>(sms) * 8));
+  k_ctx8<<<g, 256, 0, s>>>(ctx, n, pre, n_ctx, out);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
 // ===========================================================================
 // K0: device replay of synthgen::generate_iterative_scenario.  The reference
 // draws one xorshift64* value per (rank, iteration, kernel) from a single
@@ -463,8 +506,10 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
 __global__ void __launch_bounds__(256) k_within_partial(const double* within_cv,
                                                         const uint8_t* within_ok, uint32_t n_kept,
                                                         uint32_t nn, uint32_t per_tile,
-                                                        double* part /*[tiles][2][nn]*/) {
+                                                        double* part /*[tiles][2][nn]*/,
+                                                        const unsigned long long* qs) {
   __shared__ double s_sum[256], s_bad[256];
+  if (qs) n_kept = min(n_kept, static_cast<uint32_t>(qs[QS_KEPT]));
   const uint32_t ne = min(nn, blockDim.x), S = blockDim.x / ne;
   const uint32_t j = threadIdx.x / ne, nl = threadIdx.x % ne;
   const uint32_t t0 = blockIdx.x * per_tile, t1 = min(n_kept, t0 + per_tile);
@@ -511,11 +556,18 @@ __global__ void k_within_finish(const double* part, uint32_t tiles, uint32_t nn,
 __global__ void __launch_bounds__(256) k_stats_finalize(const unsigned long long* x_sum,
                                                         const unsigned long long* x_max,
                                                         const unsigned long long* x_sq, uint32_t K,
-                                                        uint32_t nn, uint32_t n_kept,
+                                                        uint32_t plane_k, uint32_t nn, uint32_t n_kept,
                                                         const double* within_sum,
-                                                        const double* within_bad, double* out) {
+                                                        const double* within_bad, double* out,
+                                                        const unsigned long long* qs) {
   const uint32_t n = blockIdx.x;
-  const size_t plane = static_cast<size_t>(K) * nn;
+  const size_t plane = static_cast<size_t>(plane_k) * nn;
+  if (qs) {
+    if (qs[QS_CAP_MISS]) return;  // the query re-runs
+    K = qs_K(qs);
+    n_kept = static_cast<uint32_t>(qs[QS_KEPT_G]);
+  }
+  if (K == 0) return;
   double m = 0.0, mx_s = 0.0, across = 0.0, bad = 0.0;
   for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) {
     const size_t cell = static_cast<size_t>(k) * nn + n;
@@ -553,9 +605,10 @@ __global__ void __launch_bounds__(256) k_stats_finalize(const unsigned long long
 }
 
 void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,
-                           const unsigned long long* x_sq, uint32_t K, uint32_t nn,
+                           const unsigned long long* x_sq, uint32_t K, uint32_t plane_k, uint32_t nn,
                            uint32_t n_kept, const double* within_cv, const uint8_t* within_ok,
-                           uint32_t n_kept_local, double* node_out, cudaStream_t s) {
+                           uint32_t n_kept_local, double* node_out, const unsigned long long* qs,
+                           cudaStream_t s) {
   // node_out layout: [nn][8] result rows, then [nn] within sums, [nn] bad counts
   double* wsum = node_out + static_cast<size_t>(nn) * 8;
   double* wbad = wsum + nn;
@@ -564,16 +617,48 @@ void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long 
     const uint32_t tiles = std::max(1u, std::min(148u, (n_kept_local + 63) / 64));
     const uint32_t per_tile = (std::max(1u, n_kept_local) + tiles - 1) / tiles;
     double* part = wbad + nn;
-    k_within_partial<<<tiles, 256, 0, s>>>(within_cv, within_ok, n_kept_local, nn, per_tile, part);
+    k_within_partial<<<tiles, 256, 0, s>>>(within_cv, within_ok, n_kept_local, nn, per_tile, part, qs);
     k_within_finish<<<(nn + 127) / 128, 128, 0, s>>>(part, tiles, nn, wsum, wbad);
     count_launch(2);
     PSG_CUDA(cudaGetLastError());
   }
   if (x_sum) {
-    k_stats_finalize<<<nn, 256, 0, s>>>(x_sum, x_max, x_sq, K, nn, n_kept, wsum, wbad, node_out);
+    k_stats_finalize<<<nn, 256, 0, s>>>(x_sum, x_max, x_sq, K, plane_k, nn, n_kept, wsum, wbad, node_out, qs);
     count_launch();
     PSG_CUDA(cudaGetLastError());
   }
+}
+
+__global__ void k_qs_check_k(unsigned long long* qs, uint32_t k_cap) {
+  if (qs_K(qs) > k_cap) qs[QS_CAP_MISS] |= 4ull;
+}
+
+void launch_qs_check_k(unsigned long long* qs, uint32_t k_cap, cudaStream_t s) {
+  k_qs_check_k<<<1, 1, 0, s>>>(qs, k_cap);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
+__global__ void k_outlier_summary(const uint32_t* worst, const uint32_t* n_sel, const double* site_ratio,
+                                  const uint32_t* rack_nodes, uint32_t n_racks, unsigned long long* qs) {
+  uint32_t racks = 0;
+  for (uint32_t r = threadIdx.x; r < n_racks; r += blockDim.x) racks += rack_nodes[r] > 0 ? 1u : 0u;
+  for (int d = 16; d > 0; d >>= 1) racks += __shfl_xor_sync(FULL, racks, d);
+  if (threadIdx.x == 0) {
+    const uint32_t w = worst[0];
+    qs[QS_WORST] = w;
+    qs[QS_NSEL] = n_sel[0];
+    qs[QS_WORST_RATIO] = static_cast<unsigned long long>(__double_as_longlong(site_ratio[w]));
+    qs[QS_RACKS] = racks;
+  }
+}
+
+void launch_outlier_summary(const uint32_t* worst, const uint32_t* n_sel, const double* site_ratio,
+                            const uint32_t* rack_nodes, uint32_t n_racks, unsigned long long* qs,
+                            cudaStream_t s) {
+  k_outlier_summary<<<1, 32, 0, s>>>(worst, n_sel, site_ratio, rack_nodes, n_racks, qs);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
 }
 
 // ===========================================================================

@@ -218,8 +218,27 @@ __device__ __forceinline__ void warp_prefix(const u64* src, u64* dst, uint32_t n
 // exact unless two candidates share a timestamp; pass 2 reads every
 // boundary's timestamp from its own stream, flags that case, and the host
 // re-runs both passes with EXACT = true.
-template <bool SMALL, bool EXACT>  // SMALL: <= 128 contexts, membership bits live in registers
+// C8: the ctx words come from the narrow mirror (1 B/event): a lane owns a run
+// of 32 events (one 32-byte load), block steps of 1024 events start on
+// multiples of 32 events.  Otherwise a lane owns RB events of u32 ctx words.
+template <bool C8> struct bounds_geom {
+  static constexpr int R = C8 ? 32 : RB;        // events per lane per block step
+  static constexpr int STEP = 32 * R;
+  static constexpr u64 ALIGN = C8 ? 31 : 7;     // block steps start on multiples of ALIGN + 1
+  static constexpr int NV = C8 ? 2 : RB / 4;    // uint4 registers per lane per block step
+};
+
+// lanes' bits [lo, hi) of a 32-bit run mask (0 <= lo, hi <= 32)
+__device__ __forceinline__ uint32_t run_mask(int lo, int hi) {
+  const uint32_t h = hi >= 32 ? FULL : ((1u << hi) - 1u);
+  const uint32_t l = lo >= 32 ? FULL : ((1u << lo) - 1u);
+  return h & ~l;
+}
+
+template <bool SMALL, bool EXACT, bool C8>  // SMALL: <= 128 contexts, membership bits live in registers
 __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
+  typedef bounds_geom<C8> GM;
+  constexpr int RR = GM::R, STEP = GM::STEP, NV = GM::NV;
   extern __shared__ uint32_t s_bits[];
   for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) s_bits[i] = p.contains[i];
   auto word = [&](uint32_t w) -> u64 { return w < p.words ? static_cast<u64>(p.contains[w]) : 0ull; };
@@ -231,6 +250,8 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
   if (t >= p.tr.n) return;
   const u64 b = p.tr.off[t], e = p.tr.off[t + 1];
   const u64 cap = p.cap_off[t + 1] - p.cap_off[t];
+  const uint32_t lo4 = p.sub_lo * 0x01010101u, sz4 = p.sub_size * 0x01010101u;
+  const bool sub_all = p.sub_size >= 256;
 #define BTS(i) ldg64(p.tr.ts + (i))
   uint32_t* out = p.bidx + p.cap_off[t];
   uint64_t* out_ts = p.bts + p.cap_off[t];
@@ -240,61 +261,71 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
   u64 nb = 0, last_b = 0;
   // software pipeline: the next block step's ctx words are loaded into
   // registers while this one is processed (the arrays carry one block step of
-  // slack past the last event)
-  // block steps start on multiples of 8 events: each lane's 16 ctx words are
-  // two 32-byte aligned LDG.256 (whole sectors per instruction)
+  // slack past the last event).  Every load is one 32-byte aligned LDG.256
+  // (whole sectors per instruction).
   static_assert(RB % 8 == 0, "RB must be a multiple of 8");
-  uint4 nxt[RB / 4];
-  {
-    const uint32_t* src = p.tr.ctx + (b & ~7ull) + static_cast<u64>(lane) * RB;
+  uint4 nxt[NV];
+  auto load = [&](u64 r) {
+    if (C8) {
+      ldg256x(reinterpret_cast<const uint32_t*>(p.ctx8 + r), nxt[0], nxt[1]);
+    } else {
 #pragma unroll
-    for (int q = 0; q < RB / 8; ++q) ldg256x(src + 8 * q, nxt[2 * q], nxt[2 * q + 1]);
-  }
-  for (u64 s = b & ~7ull; s < e; s += STEP_B) {
-    const u64 r0 = s + static_cast<u64>(lane) * RB;
+      for (int q = 0; q < NV / 2; ++q) ldg256x(p.tr.ctx + r + 8 * q, nxt[2 * q], nxt[2 * q + 1]);
+    }
+  };
+  load((b & ~GM::ALIGN) + static_cast<u64>(lane) * RR);
+  for (u64 s = b & ~GM::ALIGN; s < e; s += STEP) {
+    const u64 r0 = s + static_cast<u64>(lane) * RR;
 #ifndef PSG_NO_BOUNDS_PREFETCH
 #ifndef PSG_B_PF_DIST
 #define PSG_B_PF_DIST 0  // block steps of L2 prefetch run-ahead in pass 1 (0: none;
                          // with the 256-bit loads it no longer pays: 3.07 vs 3.04 ms)
 #endif
-    if (PSG_B_PF_DIST > 0 && lane == 0 && s + (PSG_B_PF_DIST + 1) * STEP_B <= e)
-      prefetch_l2(p.tr.ctx + s + PSG_B_PF_DIST * STEP_B, 4 * STEP_B);
+    if (!C8 && PSG_B_PF_DIST > 0 && lane == 0 && s + (PSG_B_PF_DIST + 1) * STEP <= e)
+      prefetch_l2(p.tr.ctx + s + PSG_B_PF_DIST * STEP, 4 * STEP);
 #endif
-    uint32_t cx[RB];
+    uint32_t w[4 * NV];  // this step's ctx words (C8: 4 ctx bytes per word)
 #pragma unroll
-    for (int q = 0; q < RB / 4; ++q) {
-      cx[4 * q] = nxt[q].x;
-      cx[4 * q + 1] = nxt[q].y;
-      cx[4 * q + 2] = nxt[q].z;
-      cx[4 * q + 3] = nxt[q].w;
+    for (int q = 0; q < NV; ++q) {
+      w[4 * q] = nxt[q].x;
+      w[4 * q + 1] = nxt[q].y;
+      w[4 * q + 2] = nxt[q].z;
+      w[4 * q + 3] = nxt[q].w;
     }
-    if (s + STEP_B < e) {
-      const uint32_t* src = p.tr.ctx + r0 + STEP_B;
-#pragma unroll
-      for (int q = 0; q < RB / 8; ++q) ldg256x(src + 8 * q, nxt[2 * q], nxt[2 * q + 1]);
-    }
-    // events of this trace in the lane's run: local indices [lo, hi) of [0, RB)
+    if (s + STEP < e) load(r0 + STEP);
+    // events of this trace in the lane's run: local indices [lo, hi) of [0, RR)
     const int64_t lo64 = static_cast<int64_t>(b) - static_cast<int64_t>(r0);
     const int64_t hi64 = static_cast<int64_t>(e) - static_cast<int64_t>(r0);
-    const int lo = lo64 < 0 ? 0 : static_cast<int>(lo64 > RB ? RB : lo64);
-    const int hi = hi64 < 0 ? 0 : static_cast<int>(hi64 > RB ? RB : hi64);
-    const uint32_t real = (hi >= 32 ? FULL : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+    const int lo = lo64 < 0 ? 0 : static_cast<int>(lo64 > RR ? RR : lo64);
+    const int hi = hi64 < 0 ? 0 : static_cast<int>(hi64 > RR ? RR : hi64);
+    const uint32_t real = run_mask(lo, hi);
     uint32_t inm = 0;
+    if (C8) {
+      // preorder bytes: in the subtree iff (b - lo) mod 256 < size, four
+      // events per SIMD compare; the four 0xff/0 bytes fold into a nibble
+      // (bit k of byte k, summed into the top byte by one multiply)
 #pragma unroll
-    for (int j = 0; j < RB; ++j) {
-      const uint32_t c = cx[j];
-      uint32_t in;
-      if (SMALL)  // ctx < 128 on real events
-        in = static_cast<uint32_t>((c & 64 ? bits_hi : bits_lo) >> (c & 63)) & 1u;
-      else
-        in = (s_bits[min(c, p.words * 32 - 1) >> 5] >> (c & 31)) & 1u;
-      inm |= in << j;
+      for (int q = 0; q < RR / 4; ++q) {
+        const uint32_t m = sub_all ? FULL : __vcmpltu4(__vsub4(w[q], lo4), sz4);
+        inm |= (((m & 0x08040201u) * 0x01010101u) >> 24) << (4 * q);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < RR; ++j) {
+        const uint32_t c = w[j];
+        uint32_t in;
+        if (SMALL)  // ctx < 128 on real events
+          in = static_cast<uint32_t>((c & 64 ? bits_hi : bits_lo) >> (c & 63)) & 1u;
+        else
+          in = (s_bits[min(c, p.words * 32 - 1) >> 5] >> (c & 31)) & 1u;
+        inm |= in << j;
+      }
     }
     inm &= real;
-    uint32_t up = __shfl_up_sync(FULL, inm >> (RB - 1), 1);
+    uint32_t up = __shfl_up_sync(FULL, inm >> (RR - 1), 1);
     if (lane == 0) up = prev_in;
     const uint32_t candm = inm & ~((inm << 1) | (up & 1u));
-    prev_in = __shfl_sync(FULL, (inm >> (RB - 1)) & 1u, 31);
+    prev_in = __shfl_sync(FULL, (inm >> (RR - 1)) & 1u, 31);
     const unsigned any = __ballot_sync(FULL, candm != 0);
     if (!any) continue;
     if (!EXACT) {  // every candidate is a boundary (verified by pass 2)
@@ -359,9 +390,13 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
   if (lane == 0) {
     uint32_t it = static_cast<uint32_t>(nb);
     if (nb > 0 && last_b >= p.tr.t_end[t]) it -= 1;  // empty last interval dropped
+    if (nb > cap) {  // the query re-runs with larger regions; until then every
+      atomicAdd(p.overflow, 1ull);  // reader stays inside this trace's region
+      nb = cap;
+      it = static_cast<uint32_t>(cap);
+    }
     p.n_bounds[t] = static_cast<uint32_t>(nb);
     p.iter_count[t] = it;
-    if (nb > cap) atomicAdd(p.overflow, 1ull);
   }
 }
 #undef BTS
@@ -369,16 +404,21 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
 void launch_bounds(const bound_params& p, bool exact, cudaStream_t s) {
   if (p.tr.n == 0) return;
   const unsigned g = (p.tr.n + 7) / 8, sm = 4u * p.words;
-  if (p.words <= 4) {
+  if (p.ctx8) {  // membership from the preorder bytes: no bit tables
     if (exact)
-      k_bounds<true, true><<<g, 256, sm, s>>>(p);
+      k_bounds<true, true, true><<<g, 256, sm, s>>>(p);
     else
-      k_bounds<true, false><<<g, 256, sm, s>>>(p);
+      k_bounds<true, false, true><<<g, 256, sm, s>>>(p);
+  } else if (p.words <= 4) {
+    if (exact)
+      k_bounds<true, true, false><<<g, 256, sm, s>>>(p);
+    else
+      k_bounds<true, false, false><<<g, 256, sm, s>>>(p);
   } else {
     if (exact)
-      k_bounds<false, true><<<g, 256, sm, s>>>(p);
+      k_bounds<false, true, false><<<g, 256, sm, s>>>(p);
     else
-      k_bounds<false, false><<<g, 256, sm, s>>>(p);
+      k_bounds<false, false, false><<<g, 256, sm, s>>>(p);
   }
   count_launch();
   PSG_CUDA(cudaGetLastError());
@@ -922,8 +962,10 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   }
   if (lane == 0) T.carry[0] = T.carry[1] = T.carry[2] = 0;
 
-  const uint32_t t = blockIdx.x * W + warp;
-  const bool active = t < p.tr.n;
+  const uint32_t t = p.t_base + blockIdx.x * W + warp;
+  bool active = t < p.t_stop;
+  // K from the device status block (no host round trip between the passes)
+  const uint32_t Kq = p.qs ? qs_K(p.qs) : p.K;
   if (WIN && active) {
     T.gminb = reinterpret_cast<unsigned long long*>(p.w_min) + static_cast<size_t>(t) * n_ctx;
     T.gmaxb = reinterpret_cast<unsigned long long*>(p.w_max) + static_cast<size_t>(t) * n_ctx;
@@ -932,15 +974,26 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       T.gmaxb[c] = 0ull;
     }
   }
+  uint32_t iters = (CUBE && active) ? p.iter_count[t] : 0;
+  const uint32_t tp = iters > 0 ? p.tpos[t] : 0;
+  const u64 bo = iters > 0 ? p.block_off[t] : 0;
+  const u64 ib = iters > 0 ? p.iter_off[t] : 0;  // iterations stored before this trace
+  if (p.cap_miss && iters > 0) {
+    // speculative capacities (sized by an earlier query): a trace whose block
+    // does not fit flags the query, which re-runs with exact sizes
+    const bool over_c = bo + ((static_cast<u64>(iters) * nnp + 3) & ~3ull) > p.cube_cap;
+    const bool over_x = p.store_cube && (ib + iters) * p.m > p.xint_cap;
+    if (over_c || over_x) {
+      if (lane == 0) atomicOr(p.cap_miss, over_c ? 1ull : 2ull);
+      active = false;
+      iters = 0;
+    }
+  }
   const u64 b = active ? p.tr.off[t] : 0, e = active ? p.tr.off[t + 1] : 0;
   const u64 n_t = e - b;
   const u64 tend = active ? p.tr.t_end[t] : 0;
-  const uint32_t iters = (CUBE && active) ? p.iter_count[t] : 0;
   const uint32_t nbd = (CUBE && active) ? p.n_bounds[t] : 0;
   const bool kept = iters > 0;
-  const uint32_t tp = kept ? p.tpos[t] : 0;
-  const u64 bo = kept ? p.block_off[t] : 0;
-  const u64 ib = kept ? p.iter_off[t] : 0;  // iterations stored before this trace
   const u64 region = (CUBE && active) ? p.cap_off[t] : 0;
   const uint32_t* bt = p.bidx + region;
   const uint64_t* btt = p.bts + region;
@@ -1235,7 +1288,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
     const uint32_t k_lo = kb;
     const uint32_t k_hi = min(kb + G, iters);
     const uint32_t n_iter_rows = k_hi > k_lo ? k_hi - k_lo : 0;
-    const uint32_t kcap = (CUBE && p.do_stats && kb < p.K) ? min(n_iter_rows, p.K - kb) : 0;
+    const uint32_t kcap = (CUBE && p.do_stats && kb < Kq) ? min(n_iter_rows, Kq - kb) : 0;
     if (CUBE && kept) {
       const uint32_t s0 = kb & (R2 - 1);  // the chunk's rows are slots [s0, s0 + G)
       uint32_t* rhw = cwide ? rhi : nullptr;  // high words (all zero in narrow chunks)
@@ -1387,11 +1440,11 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       p.c_ctx[t] = c_has ? c_ctx : 0;
     }
   }
-  if (CUBE && p.do_stats && kept && p.K > 0) {
+  if (CUBE && p.do_stats && kept && Kq > 0) {
     for (uint32_t n = lane; n < nn; n += 32) {
       const u64 sx = wsx[n];
       const u128 sq = (static_cast<u128>(wsqhi[n]) << 64) | wsqlo[n];
-      const u128 num = static_cast<u128>(p.K) * sq - static_cast<u128>(sx) * sx;
+      const u128 num = static_cast<u128>(Kq) * sq - static_cast<u128>(sx) * sx;
       const bool ok = sx > 0;
       p.within_cv[static_cast<size_t>(tp) * nn + n] =
           ok ? 100.0 * sqrt(u128_to_double(num)) / static_cast<double>(sx) : 0.0;
@@ -1417,7 +1470,7 @@ void launch_shape(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
       if (dev < 64) configured_bytes[dev] = static_cast<int>(smem_bytes);
     }
   }
-  const unsigned blocks = (p.tr.n + p.warps - 1) / p.warps;
+  const unsigned blocks = (p.t_stop - p.t_base + p.warps - 1) / p.warps;
   k_trace_query<WIN, CUBE, EXACT, ONE><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
 }
 
@@ -1435,7 +1488,10 @@ void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) 
 }  // namespace
 
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
-  if (p.tr.n == 0) return;
+  if (p.t_stop <= p.t_base || p.t_stop > p.tr.n) {
+    if (p.t_stop > p.tr.n) fail(PS_E_INTERNAL, "trace range past the loaded traces");
+    return;
+  }
   if (p.G != GC) fail(PS_E_INTERNAL, "chunk size mismatch between host and kernel (PSG_G)");
   const bool exact = p.do_cube && p.exact_bounds;
   if (p.do_window && p.do_cube)
@@ -1499,16 +1555,30 @@ __global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__
                                                         uint32_t K, uint32_t kt, uint32_t per_tile,
                                                         unsigned long long* x_sum,
                                                         unsigned long long* x_max,
-                                                        unsigned long long* x_sq) {
+                                                        unsigned long long* x_sq,
+                                                        const unsigned long long* qs,
+                                                        const uint32_t* tpos, uint32_t ta,
+                                                        uint32_t tb, uint32_t n_tr) {
   // The tile's trace block offsets are staged in shared memory in batches and
   // read as broadcasts; U independent pair loads are in flight per thread.
   constexpr int U = sizeof(CELL) == 4 ? PSG_X_U : 8;
   constexpr uint32_t TB = 512;
   __shared__ u64 s_bo[TB];
-  const uint32_t k0 = blockIdx.x * kt;
-  const uint32_t kc = min(kt, K - k0);
-  const uint32_t t_lo = blockIdx.y * per_tile, t_hi = min(n_kept, t_lo + per_tile);
+  // K (the accumulator plane's stride) and n_kept are capacities when the
+  // status block is given: the actual values come from it
   const size_t plane = static_cast<size_t>(K) * nn;
+  if (qs) {
+    if (qs[QS_CAP_MISS]) return;  // the query re-runs
+    K = min(K, qs_K(qs));
+    n_kept = min(n_kept, static_cast<uint32_t>(qs[QS_KEPT]));
+  }
+  const uint32_t k0 = blockIdx.x * kt;
+  if (k0 >= K) return;
+  const uint32_t kc = min(kt, K - k0);
+  // a part: the kept traces among loaded traces [ta, tb)
+  const uint32_t ka = tpos ? (ta < n_tr ? tpos[ta] : n_kept) : 0u;
+  const uint32_t kb = tpos ? (tb < n_tr ? tpos[tb] : n_kept) : n_kept;
+  const uint32_t t_lo = ka + blockIdx.y * per_tile, t_hi = min(kb, t_lo + per_tile);
   const uint32_t hp = nnp / 2;  // pairs per row
   const uint32_t npairs = kc * hp;
   for (uint32_t pr0 = 0; pr0 < npairs; pr0 += blockDim.x) {
@@ -1600,9 +1670,12 @@ __global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__
 
 void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, uint32_t n_kept,
                         uint32_t nn, uint32_t nnp, uint32_t K, unsigned long long* x_sum,
-                        unsigned long long* x_max, unsigned long long* x_sq, cudaStream_t s) {
+                        unsigned long long* x_max, unsigned long long* x_sq,
+                        const unsigned long long* qs, cudaStream_t s, const cross_part& part) {
+  if (part.tpos) n_kept = part.tb - part.ta;  // the part's traces bound its kept ones
   if (n_kept == 0 || K == 0 || nn == 0) return;
-  const uint32_t kt = nnp >= 1024 ? 1u : 1024u / nnp;  // ~512 pairs per CTA
+  const uint32_t th = part.threads;
+  const uint32_t kt = nnp >= 2 * th ? 1u : 2 * th / nnp;  // ~th pairs per CTA
   const uint32_t gx = (K + kt - 1) / kt;  // iteration tiles
   // trace ranges: the CTA count fills whole waves of the resident slots as
   // closely as possible (a last wave of a few CTAs would leave the GPU idle
@@ -1611,9 +1684,9 @@ void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, 
   PSG_CUDA(cudaGetDevice(&dev));
   PSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (cube32)
-    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cross_stats<uint32_t>, 512, 0));
+    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cross_stats<uint32_t>, th, 0));
   else
-    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cross_stats<unsigned long long>, 512, 0));
+    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cross_stats<unsigned long long>, th, 0));
   const uint32_t slots = static_cast<uint32_t>(std::max(1, sms * std::max(1, per_sm)));
   const uint32_t gy_cap = std::max(1u, (n_kept + 63) / 64);  // >= 64 traces per CTA
   uint32_t gy = 1, per_tile = n_kept;
@@ -1630,14 +1703,16 @@ void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, 
       per_tile = pt;
     }
   }
+  const uint32_t nk_arg = part.tpos ? 0xFFFFFFFFu : n_kept;  // parts: the kept total comes from qs
   if (cube32)
-    k_cross_stats<uint32_t><<<dim3(gx, gy), 512, 0, s>>>(static_cast<const uint32_t*>(incl), kept_bo,
-                                                         n_kept, nn, nnp, K, kt, per_tile, x_sum,
-                                                         x_max, x_sq);
+    k_cross_stats<uint32_t><<<dim3(gx, gy), th, 0, s>>>(static_cast<const uint32_t*>(incl), kept_bo,
+                                                        nk_arg, nn, nnp, K, kt, per_tile, x_sum,
+                                                        x_max, x_sq, qs, part.tpos, part.ta, part.tb,
+                                                        part.n);
   else
-    k_cross_stats<unsigned long long><<<dim3(gx, gy), 512, 0, s>>>(
-        static_cast<const unsigned long long*>(incl), kept_bo, n_kept, nn, nnp, K, kt, per_tile,
-        x_sum, x_max, x_sq);
+    k_cross_stats<unsigned long long><<<dim3(gx, gy), th, 0, s>>>(
+        static_cast<const unsigned long long*>(incl), kept_bo, nk_arg, nn, nnp, K, kt, per_tile,
+        x_sum, x_max, x_sq, qs, part.tpos, part.ta, part.tb, part.n);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
