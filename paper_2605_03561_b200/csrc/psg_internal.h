@@ -142,15 +142,18 @@ struct bound_params {
 enum : uint32_t { WT_CNT = 0, WT_LO = 1, WT_MIN = 2, WT_MAX = 3, WT_PPO = 4, WT_NBIG = 5,
                   WT_ACC = 6 /* lo, hi words */, WT_STRIDE = 9 };
 // First word of ctx c's record.  Lanes hold runs of 8 consecutive events, so
-// in an iterative trace the lanes of one iteration touch contexts 8 apart;
-// with a stride of 9 words those share a bank every 4 lanes (3-way conflicts
-// measured).  Leaving one record slot free after every 8 contexts makes
-// contexts 8 apart 81 words apart: 17 banks, distinct for all 32 lanes.
+// in an iterative trace the lanes of one instruction touch contexts 8 apart
+// (mod the iteration's length): with a stride of 9 words alone those share a
+// bank every 4 lanes.  Skipping one record slot after every 8 contexts
+// (PSG_WT_SWIZZLE 1) or every 32 (2) spreads them: a bank-conflict model of
+// configs[1] (67 contexts per iteration) gives 2.97 / 2.21 / 2.00 shared
+// wavefronts per record access for 0 / 1 / 2, and k_trace_query measured
+// 18.36 / 17.60 / 17.40 ms (profiles/r2g_ab_wt_swizzle.txt).
 #ifndef PSG_WT_SWIZZLE
-#define PSG_WT_SWIZZLE 1
+#define PSG_WT_SWIZZLE 2
 #endif
 __host__ __device__ inline uint32_t wt_word(uint32_t c) {
-  return WT_STRIDE * (PSG_WT_SWIZZLE ? c + (c >> 3) : c);
+  return WT_STRIDE * (PSG_WT_SWIZZLE == 2 ? c + (c >> 5) : PSG_WT_SWIZZLE ? c + (c >> 3) : c);
 }
 
 // Cube row stride in cells: nn + 1 rounded up to even (pad columns).
@@ -184,7 +187,7 @@ struct warp_smem_layout {
     off_pref = take(8u * (nn + 1));  // generic rows and the gap row
     off_bwin = take(4u * (2 * G + 2));
     off_bts = take(8u * (2 * G + 2));
-    off_wtab = take(4u * WT_STRIDE * (n_ctx + n_ctx / 8 + 1));
+    off_wtab = take(4u * WT_STRIDE * (n_ctx + (PSG_WT_SWIZZLE == 2 ? n_ctx / 32 : n_ctx / 8) + 1));
     off_wsx = take(8u * nn);
     off_wsqlo = take(8u * nn);
     off_wsqhi = take(8u * nn);

@@ -284,6 +284,13 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
     if (!C8 && PSG_B_PF_DIST > 0 && lane == 0 && s + (PSG_B_PF_DIST + 1) * STEP <= e)
       prefetch_l2(p.tr.ctx + s + PSG_B_PF_DIST * STEP, 4 * STEP);
 #endif
+#ifndef PSG_B8_PF_DIST
+#define PSG_B8_PF_DIST 0  // C8: block steps of TMA L2 prefetch run-ahead (measured: 2, 3, 6 all slower;
+                          // 1.33 vs 1.23 ms at configs[1])
+#endif
+    if (C8 && PSG_B8_PF_DIST > 0)
+      prefetch_l2_lane0(p.ctx8 + s + PSG_B8_PF_DIST * STEP, STEP,
+                        lane == 0 && s + (PSG_B8_PF_DIST + 1) * STEP <= e);
     uint32_t w[4 * NV];  // this step's ctx words (C8: 4 ctx bytes per word)
 #pragma unroll
     for (int q = 0; q < NV; ++q) {

@@ -26,7 +26,18 @@ def run(ctx: Context, lo: int, hi: int, T: int, anchor: int = 1) -> dict:
     n_nodes = N_TRACES // N_PER_NODE
     node = np.arange(n_nodes)
     ctx.set_nodes(node_of, n_nodes, 4000 + node // 4, node % 4)
-    info = ctx.query(Q_ALL, t0=T // 4, t1=3 * T // 4, anchor=anchor, sites=SITES, top_k=4, z_min=-1e300)
+    # twice: the second query runs speculatively (one host round trip, its
+    # collectives in a different order) and must give the same results
+    first = None
+    for rep in range(2):
+        info = ctx.query(Q_ALL, t0=T // 4, t1=3 * T // 4, anchor=anchor, sites=SITES, top_k=4, z_min=-1e300)
+        got = {f"w_{k}": v for k, v in ctx.window().items()}
+        got.update({f"c_{k}": v for k, v in ctx.cube().items()})
+        if rep == 0:
+            first = got
+    for k, v in first.items():
+        if v is not None:
+            assert np.array_equal(v, got[k]), f"speculative re-run differs: {k}"
     out = {f"w_{k}": v for k, v in ctx.window().items()}
     out.update({f"c_{k}": v for k, v in ctx.cube().items()})
     out.update({f"s_{k}": v for k, v in ctx.stats(1.0).items()})
@@ -76,6 +87,28 @@ def load_dup(ctx: Context, lo: int, hi: int) -> None:
 def main(out_dir: str, mode: str = "gen") -> None:
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
+    if mode == "nccl":
+        # one GPU per rank, the summaries over NCCL on device buffers
+        # (psg_comm_init: the unique id travels over the gloo group)
+        dev = int(os.environ.get("LOCAL_RANK", rank))
+        cfg = scenarios.iterative(N_TRACES, 9, n_kernels=6, seed=3, jitter=0.25)
+        with Context(dev) as single:
+            single.generate_iterative(cfg)
+            T = int(single.shard()["t_max"])
+            if rank == 0:
+                np.savez(os.path.join(out_dir, "single.npz"), **run(single, 0, N_TRACES, T))
+        lo, hi = pdist.shard_range(N_TRACES, world, rank)
+        uid = [Context.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        with Context(dev) as ctx:
+            ctx.comm_init(world, rank, uid[0])
+            ctx.generate_iterative(cfg, lo, hi)
+            res = run(ctx, lo, hi, T)
+            res["range"] = np.array([lo, hi], np.int64)
+            np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **res)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if mode == "dup":
         with Context(0) as single:
             load_dup(single, 0, N_TRACES)

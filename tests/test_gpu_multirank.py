@@ -18,11 +18,23 @@ from tests.helpers import ROOT, assert_rel
 pytestmark = pytest.mark.gpu
 
 
+def _gpus() -> int:
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
 @pytest.mark.parametrize("world,mode", [(2, "gen"), (3, "gen"), (2, "dup"), (3, "dup"), (2, "auto"),
-                                        (3, "auto_empty")])
+                                        (3, "auto_empty"), (2, "nccl"), (8, "nccl")])
 def test_sharded_query_equals_single_context(tmp_path, world, mode):
     """mode "dup": one rank's traces make the optimistic pass 1 miss; the
-    verdict is all-reduced, so every rank re-runs both passes exactly."""
+    verdict is all-reduced, so every rank re-runs both passes exactly.
+    mode "nccl": one GPU per rank and the data-plane collectives on NCCL
+    (psg_comm_init); runs where the box has that many GPUs."""
+    if mode == "nccl" and _gpus() < world:
+        pytest.skip(f"NCCL data plane needs {world} GPUs (this box has {_gpus()})")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
            f"--nproc-per-node={world}", os.path.join(ROOT, "tests", "mp_shard_worker.py"),
            str(tmp_path), mode]
