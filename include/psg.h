@@ -147,6 +147,10 @@ enum {
   PSG_Q_EXACT_BOUNDS = 1u << 11, /* run pass 1 in its exact mode (boundary timestamps loaded
                                     and deduplicated there) instead of the optimistic one
                                     verified by pass 2 */
+  PSG_Q_SPARSE = 1u << 12,       /* window as sparse (trace, ctx) rows (psg_get_window_groups /
+                                    psg_get_remat_rows) instead of dense [trace][ctx]; taken
+                                    anyway when the tree is too large for the fused kernel's
+                                    per-warp window records or the dense result for HBM */
   PSG_Q_ALL = PSG_Q_WINDOW | PSG_Q_CUBE | PSG_Q_STATS | PSG_Q_OUTLIERS
 };
 
@@ -199,6 +203,10 @@ typedef struct psg_query_info {
   /* host round trips (stream synchronisations) the query made: 1 once an
    * earlier query on the same traces has sized the device buffers */
   uint32_t host_syncs;
+  /* the window's layout: 1 = sparse rows (PSG_Q_SPARSE or a large tree), and
+   * the rematerialize rows (incl or excl nonzero) it holds */
+  uint32_t window_sparse;
+  uint64_t n_remat_rows;
 } psg_query_info;
 
 ps_status psg_query(psg_context* ctx, const psg_query_spec* spec, psg_query_info* info);
@@ -210,6 +218,16 @@ ps_status psg_query(psg_context* ctx, const psg_query_spec* spec, psg_query_info
  * segment (itermodel::rematerialize over [t0,t1)). */
 ps_status psg_get_window(psg_context* ctx, uint64_t* count, int64_t* sum, int64_t* min,
                          int64_t* max, double* mean, int64_t* excl, int64_t* incl);
+/* The window as sparse rows sorted by (trace, ctx), for either layout:
+ * group_aggregate over the window rows keyed by (pid, ctx) (frame.cpp:290-408)
+ * — *n rows with count > 0: loaded-trace index, ctx, count, sum / min / max of
+ * the clipped row durations (ns), mean; and itermodel::rematerialize over
+ * [t0, t1) per trace (itermodel.cpp:145-183) — *n rows with incl or excl
+ * nonzero.  Call with NULL arrays to size. */
+ps_status psg_get_window_groups(psg_context* ctx, uint64_t* n, uint32_t* trace, uint32_t* ctx_ids,
+                                uint64_t* count, int64_t* sum, int64_t* min, int64_t* max, double* mean);
+ps_status psg_get_remat_rows(psg_context* ctx, uint64_t* n, uint32_t* trace, uint32_t* ctx_ids,
+                             int64_t* incl, int64_t* excl);
 /* Per trace carry-in (store.cpp:667-670): has (0/1), ts, ctx. */
 ps_status psg_get_carry(psg_context* ctx, uint8_t* has, uint64_t* ts, uint32_t* ctx_ids);
 /* tri_model (itermodel.hpp:78-116): node_ids[n_nodes], per loaded trace

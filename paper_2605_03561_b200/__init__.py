@@ -14,11 +14,11 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import (ANCHOR_AUTO, PsgError, Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_CUBE64, Q_EXACT_BOUNDS, Q_NO_CUBE_STORE, Q_OUTLIERS, Q_STATS, Q_WINDOW,
+from ._lib import (ANCHOR_AUTO, PsgError, Q_ALL, Q_CLAMP_TEND, Q_CUBE, Q_CUBE64, Q_EXACT_BOUNDS, Q_NO_CUBE_STORE, Q_OUTLIERS, Q_SPARSE, Q_STATS, Q_WINDOW,
                    check, load)
 from . import scenarios
 
-__all__ = ["ANCHOR_AUTO", "Context", "PsgError", "Q_ALL", "Q_CLAMP_TEND", "Q_CUBE", "Q_CUBE64", "Q_EXACT_BOUNDS", "Q_NO_CUBE_STORE", "Q_OUTLIERS", "Q_STATS",
+__all__ = ["ANCHOR_AUTO", "Context", "PsgError", "Q_ALL", "Q_CLAMP_TEND", "Q_CUBE", "Q_CUBE64", "Q_EXACT_BOUNDS", "Q_NO_CUBE_STORE", "Q_OUTLIERS", "Q_SPARSE", "Q_STATS",
            "Q_WINDOW", "load", "scenarios"]
 
 
@@ -197,6 +197,34 @@ class Context:
             _ptr(out["min"], C.c_int64), _ptr(out["max"], C.c_int64),
             _ptr(out["mean"], C.c_double), _ptr(out["excl"], C.c_int64),
             _ptr(out["incl"], C.c_int64)))
+        return out
+
+    def window_groups(self) -> dict:
+        """group_aggregate rows of the window (count > 0), sorted by (trace, ctx)."""
+        n = C.c_uint64(0)
+        check(self.lib.psg_get_window_groups(self.h, C.byref(n), None, None, None, None, None, None, None))
+        m = n.value
+        out = {"trace": np.empty(m, np.uint32), "ctx": np.empty(m, np.uint32), "count": np.empty(m, np.uint64),
+               "sum": np.empty(m, np.int64), "min": np.empty(m, np.int64), "max": np.empty(m, np.int64),
+               "mean": np.empty(m, np.float64)}
+        if m:
+            check(self.lib.psg_get_window_groups(
+                self.h, C.byref(n), _ptr(out["trace"], C.c_uint32), _ptr(out["ctx"], C.c_uint32),
+                _ptr(out["count"], C.c_uint64), _ptr(out["sum"], C.c_int64), _ptr(out["min"], C.c_int64),
+                _ptr(out["max"], C.c_int64), _ptr(out["mean"], C.c_double)))
+        return out
+
+    def remat_rows(self) -> dict:
+        """rematerialize rows of the window (incl or excl nonzero), sorted by (trace, ctx)."""
+        n = C.c_uint64(0)
+        check(self.lib.psg_get_remat_rows(self.h, C.byref(n), None, None, None, None))
+        m = n.value
+        out = {"trace": np.empty(m, np.uint32), "ctx": np.empty(m, np.uint32), "incl": np.empty(m, np.int64),
+               "excl": np.empty(m, np.int64)}
+        if m:
+            check(self.lib.psg_get_remat_rows(self.h, C.byref(n), _ptr(out["trace"], C.c_uint32),
+                                              _ptr(out["ctx"], C.c_uint32), _ptr(out["incl"], C.c_int64),
+                                              _ptr(out["excl"], C.c_int64)))
         return out
 
     def carry(self) -> dict:

@@ -26,6 +26,7 @@ Q_NO_CUBE_STORE = 1 << 8
 Q_CLAMP_TEND = 1 << 9
 Q_CUBE64 = 1 << 10
 Q_EXACT_BOUNDS = 1 << 11
+Q_SPARSE = 1 << 12
 Q_ALL = Q_WINDOW | Q_CUBE | Q_STATS | Q_OUTLIERS
 ANCHOR_AUTO = 0xFFFFFFFF
 
@@ -74,7 +75,7 @@ class QueryInfo(C.Structure):
         ("n_outliers", C.c_uint32), ("n_racks", C.c_uint32),
         ("ms_total", C.c_float), ("ms_main", C.c_float), ("ms_bounds", C.c_float),
         ("cube_cell_bytes", C.c_uint32), ("cube_store_bytes", C.c_uint64),
-        ("host_syncs", C.c_uint32),
+        ("host_syncs", C.c_uint32), ("window_sparse", C.c_uint32), ("n_remat_rows", C.c_uint64),
     ]
 
 
@@ -109,6 +110,8 @@ _SIGS = {
     "psg_query": (C.c_int, [P, C.POINTER(QuerySpec), C.POINTER(QueryInfo)]),
     "psg_get_window": (C.c_int, [P, U64P, I64P, I64P, I64P, F64P, I64P, I64P]),
     "psg_get_carry": (C.c_int, [P, U8P, U64P, U32P]),
+    "psg_get_window_groups": (C.c_int, [P, U64P, U32P, U32P, U64P, I64P, I64P, I64P, F64P]),
+    "psg_get_remat_rows": (C.c_int, [P, U64P, U32P, U32P, I64P, I64P]),
     "psg_get_cube": (C.c_int, [P, U32P, U32P, U64P, I64P, I64P, I64P, I64P]),
     "psg_get_stats": (C.c_int, [P, C.c_double, U32P, F64P, F64P, F64P, I32P]),
     "psg_get_outliers": (C.c_int, [P, F64P, F64P, F64P, U32P, U32P, U64P, U64P]),

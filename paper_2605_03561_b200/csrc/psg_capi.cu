@@ -305,6 +305,15 @@ struct psg_context {
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
+  // the sparse window (psg_sparse.cu): the last query's rows when it took the
+  // sparse layout, or the copy-out of a dense window (sp_valid)
+  sparse_result sp;
+  bool sp_valid = false, window_sparse = false;
+  dbuf<uint32_t> d_depth;  // [n_ctx] ancestors per ctx (set_cct)
+  dbuf<uint32_t> d_ppo_g;  // [n_ctx] cube column byte offsets of the current anchor (compute_subtree)
+  dbuf<uint64_t> site_vals;  // [n][n_sites] site incl of a sparse window (outliers)
+  dbuf<uint32_t> d_site_iota;
+
   // query status block (QS_*), and what the speculative path needs: buffers
   // sized by an earlier query on these traces, the K its statistics planes
   // are laid out for, the global rank count
@@ -379,6 +388,7 @@ void build_caps(psg_context* c) {
 
 void invalidate_results(psg_context* c) {
   c->have_window = c->have_carry = c->have_cube = c->have_stats = c->have_outliers = false;
+  c->sp_valid = false;
 }
 
 void build_ctx8(psg_context* c);
@@ -399,6 +409,10 @@ void set_cct_impl(psg_context* c, const uint32_t* parent, uint32_t n_ctx) {
                            cudaMemcpyHostToDevice, c->stream));
   PSG_CUDA(cudaMemcpyAsync(c->d_parent.ensure(n_ctx), parent, 4ull * n_ctx,
                            cudaMemcpyHostToDevice, c->stream));
+  std::vector<uint32_t> depth(n_ctx, 0);  // parents precede their children
+  for (uint32_t i = 1; i < n_ctx; ++i) depth[i] = depth[parent[i]] + 1;
+  PSG_CUDA(cudaMemcpyAsync(c->d_depth.ensure(n_ctx), depth.data(), 4ull * n_ctx, cudaMemcpyHostToDevice,
+                           c->stream));
   c->cached_anchor = -1;
   invalidate_results(c);
   c->sync();
@@ -649,6 +663,10 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
   c->h_sub_pre = npos;
   PSG_CUDA(cudaMemcpyAsync(c->d_sub_pre.ensure(c->n_ctx), npos.data(), 4ull * c->n_ctx,
                            cudaMemcpyHostToDevice, c->stream));
+  std::vector<uint32_t> ppo(c->n_ctx);  // the global column table (large trees: no window records)
+  for (uint32_t id = 0; id < c->n_ctx; ++id) ppo[id] = 4u * (npos[id] >= 0 ? static_cast<uint32_t>(npos[id]) : c->nn);
+  PSG_CUDA(cudaMemcpyAsync(c->d_ppo_g.ensure(c->n_ctx), ppo.data(), 4ull * c->n_ctx, cudaMemcpyHostToDevice,
+                           c->stream));
   PSG_CUDA(cudaMemcpyAsync(c->d_node_tab.ensure(c->nn), tab.data(), sizeof(int4) * c->nn,
                            cudaMemcpyHostToDevice, c->stream));
   PSG_CUDA(cudaMemcpyAsync(c->d_contains.ensure(c->contains_words), bits.data(),
@@ -1428,7 +1446,46 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     p.t_stop = n;
     p.n_ctx = c->n_ctx;
     p.G = PSG_G;
-    if (do_window) {
+    uint32_t anchor = q->anchor_ctx;
+    if (do_cube && anchor == PSG_ANCHOR_AUTO) anchor = auto_anchor(c);
+    if (do_cube) compute_subtree(c, anchor);
+    // Window layout: the fused kernel keeps one record per ctx in each warp's
+    // shared memory and writes a dense [trace][ctx] result; a tree too large
+    // for either (or PSG_Q_SPARSE) takes the sparse path, and the cube then
+    // reads its column offsets from a global table when the records do not fit
+    const uint32_t nn0 = do_cube ? c->nn : 1u;
+    auto carve_out = [&](uint32_t n_ctx_tab) {
+      warp_smem_layout Lx;
+      Lx.init(n_ctx_tab, nn0, PSG_G, do_cube && (c->exact_hint || (f & PSG_Q_EXACT_BOUNDS)));
+      return Lx.bytes;
+    };
+    constexpr uint32_t kSmemCap = 227u * 1024;
+    const bool records_fit = carve_out(c->n_ctx) <= kSmemCap;
+    const uint64_t dense_bytes = 56ull * n * c->n_ctx;
+    const bool sparse = do_window && ((f & PSG_Q_SPARSE) || !records_fit || dense_bytes > (24ull << 30));
+    const bool global_cols = do_cube && !records_fit;
+    if (global_cols && carve_out(0) > kSmemCap)
+      fail(PS_E_INVALID_ARGUMENT, "anchor subtree too large for the fused kernel's cube rows");
+    c->window_sparse = sparse;
+    if (sparse) {
+      sparse_args a{};
+      a.tr = c->view();
+      a.n_ctx = c->n_ctx;
+      a.t0 = q->t0_ns;
+      a.t1 = q->t1_ns;
+      a.clamp_tend = (f & PSG_Q_CLAMP_TEND) ? 1 : 0;
+      a.parent = c->d_parent.p;
+      a.depth = c->d_depth.p;
+      a.row_budget = 1ull << 27;  // 128 Mi rows per batch: ~5 GB of sort scratch
+      if (const char* e = std::getenv("PSG_SPARSE_ROW_BUDGET")) a.row_budget = std::strtoull(e, nullptr, 10);
+      a.c_has = c->c_has.ensure(n + 1);
+      a.c_ts = c->c_ts.ensure(n + 1);
+      a.c_ctx = c->c_ctx.ensure(n + 1);
+      sparse_window(a, c->sp, s);
+      c->n_syncs += 3;  // the sparse path sizes its batches on the host
+      c->sp_valid = true;
+    }
+    if (do_window && !sparse) {
       const size_t cells = static_cast<size_t>(n) * c->n_ctx + 1;
       p.do_window = 1;
       p.clamp_tend = (f & PSG_Q_CLAMP_TEND) ? 1 : 0;
@@ -1448,8 +1505,6 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       p.cct_size = c->d_cct_size.p;
     }
     uint32_t nn = 0;
-    uint32_t anchor = q->anchor_ctx;
-    if (do_cube && anchor == PSG_ANCHOR_AUTO) anchor = auto_anchor(c);
     info->anchor = do_cube ? anchor : 0;
     bool exact_bounds = c->exact_hint || (f & PSG_Q_EXACT_BOUNDS) != 0;
     const bool force64 = (f & PSG_Q_CUBE64) != 0;
@@ -1570,7 +1625,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     }
     // launch geometry
     warp_smem_layout L;
-    L.init(c->n_ctx, nn, p.G, do_cube && exact_bounds);
+    L.init((global_cols || (!p.do_window && !p.do_cube)) ? 0u : c->n_ctx, nn, p.G, do_cube && exact_bounds);
+    p.ppo_g = global_cols ? c->d_ppo_g.p : nullptr;
     // CTA shape: one warp per CTA for long traces (17 resident per SM, no
     // CTA tail), 16-warp CTAs for short ones (their per-trace prologue and
     // epilogue run better in warps that start together); PSG_CTA_SHAPE=one|wide
@@ -1591,6 +1647,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     // warp's carve-out alone does: fall back to one-warp CTAs (a decision that
     // depends only on the tree and the anchor, so every rank takes the same one)
     if (!one && !fits_wide(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false))) one = true;
+    if (global_cols) one = true;
     uint32_t W = one ? choose_warps(1, L.bytes, 0) : choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false));
     if (one) W = 1;
     p.one_warp = one ? 1u : 0u;
@@ -1599,7 +1656,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     p.cta_bytes = cta_table_bytes(c->n_ctx, nn, W, one);
     uint32_t smem = p.cta_bytes + W * L.bytes;
     PSG_CUDA(cudaEventRecord(c->ev[1], s));
-    launch_trace_query(p, smem, s);
+    if (p.do_window || p.do_cube) launch_trace_query(p, smem, s);
     PSG_CUDA(cudaEventRecord(c->ev[2], s));
     if (do_cube && !exact_bounds) {
       // the optimistic pass 1 (and its 32-bit cells) against the boundary
@@ -1650,7 +1707,22 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       unsigned long long* na = c->node_acc.ensure(2 * c->n_nodes);
       PSG_CUDA(cudaMemsetAsync(sa, 0, 16ull * ns, s));
       PSG_CUDA(cudaMemsetAsync(na, 0, 16ull * c->n_nodes, s));
-      launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
+      // per-rank site values: the dense window's incl columns, or for a sparse
+      // window the sites' incl looked up in the remat rows ([n][ns], sites 0..ns-1)
+      const uint64_t* wv = c->w_incl.p;
+      uint32_t wstride = c->n_ctx;
+      const uint32_t* wsite = c->d_sites.p;
+      if (sparse) {
+        std::vector<uint32_t> iota(ns);
+        for (uint32_t i = 0; i < ns; ++i) iota[i] = i;
+        PSG_CUDA(cudaMemcpyAsync(c->d_site_iota.ensure(ns), iota.data(), 4ull * ns, cudaMemcpyHostToDevice, s));
+        sparse_site_values(c->sp, c->d_sites.p, ns, n, c->site_vals.ensure(static_cast<size_t>(n) * ns + 1), s);
+        c->sync();  // the host iota above
+        wv = c->site_vals.p;
+        wstride = ns;
+        wsite = c->d_site_iota.p;
+      }
+      launch_outliers(wv, n, wstride, wsite, ns, c->d_node_of_trace.p, c->n_nodes,
                       sa, na, c->d_worst.ensure(2), c->site_ratio.ensure(ns), 0, s);
       if (c->multi()) {
         c->group_begin();
@@ -1658,9 +1730,9 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
         c->allreduce(sa + ns, ns, ncclUint64, ncclMax);
         c->group_end();
       }
-      launch_outliers(c->w_incl.p, static_cast<uint32_t>(ranks_global(c)), c->n_ctx, c->d_sites.p, ns,
+      launch_outliers(wv, static_cast<uint32_t>(ranks_global(c)), wstride, wsite, ns,
                       c->d_node_of_trace.p, c->n_nodes, sa, na, c->d_worst.p, c->site_ratio.p, 1, s);
-      launch_outliers(c->w_incl.p, n, c->n_ctx, c->d_sites.p, ns, c->d_node_of_trace.p, c->n_nodes,
+      launch_outliers(wv, n, wstride, wsite, ns, c->d_node_of_trace.p, c->n_nodes,
                       sa, na, c->d_worst.p, c->site_ratio.p, 2, s);
       c->allreduce(na, 2ull * c->n_nodes, ncclUint64, ncclSum);
       const size_t ssb = node_select_scratch_bytes(c->n_nodes);
@@ -1744,6 +1816,63 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     PSG_CUDA(cudaEventElapsedTime(&info->ms_main, c->ev[1], c->ev[2]));
     if (do_cube) PSG_CUDA(cudaEventElapsedTime(&info->ms_bounds, c->ev[4], c->ev[5]));
     info->host_syncs = static_cast<uint32_t>(c->n_syncs - syncs0);
+    info->window_sparse = sparse ? 1u : 0u;
+    if (sparse) {
+      info->n_window_rows = c->sp.n_rows;
+      info->n_window_groups = c->sp.n_groups;
+      info->n_remat_rows = c->sp.n_remat;
+    }
+  });
+}
+
+namespace {
+// the window as sparse rows: the sparse query's own, or the dense result compacted once
+void ensure_sparse_rows(psg_context* c) {
+  if (!c->have_window) fail(PS_E_INVALID_ARGUMENT, "no window result (run psg_query with PSG_Q_WINDOW)");
+  ensure_device(c);
+  if (c->sp_valid) return;
+  dense_window w{c->w_cnt.p, c->w_sum.p, c->w_min.p, c->w_max.p, c->w_mean.p, c->w_incl.p, c->w_excl.p};
+  dense_to_sparse(w, c->n_traces, c->n_ctx, c->sp, c->stream);
+  c->sp_valid = true;
+}
+}  // namespace
+
+ps_status psg_get_window_groups(psg_context* c, uint64_t* n, uint32_t* trace, uint32_t* ctx_ids,
+                                uint64_t* count, int64_t* sum, int64_t* mn, int64_t* mx, double* mean) {
+  if (!c || !n) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_sparse_rows(c);
+    const sparse_result& r = c->sp;
+    *n = r.n_groups;
+    const size_t m = r.n_groups;
+    auto cp = [&](void* dst, const void* src, size_t b) {
+      if (dst && b) PSG_CUDA(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost));
+    };
+    cp(trace, r.g_trace.p, 4 * m);
+    cp(ctx_ids, r.g_ctx.p, 4 * m);
+    cp(count, r.g_cnt.p, 8 * m);
+    cp(sum, r.g_sum.p, 8 * m);
+    cp(mn, r.g_min.p, 8 * m);
+    cp(mx, r.g_max.p, 8 * m);
+    cp(mean, r.g_mean.p, 8 * m);
+  });
+}
+
+ps_status psg_get_remat_rows(psg_context* c, uint64_t* n, uint32_t* trace, uint32_t* ctx_ids, int64_t* incl,
+                             int64_t* excl) {
+  if (!c || !n) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    ensure_sparse_rows(c);
+    const sparse_result& r = c->sp;
+    *n = r.n_remat;
+    const size_t m = r.n_remat;
+    auto cp = [&](void* dst, const void* src, size_t b) {
+      if (dst && b) PSG_CUDA(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost));
+    };
+    cp(trace, r.r_trace.p, 4 * m);
+    cp(ctx_ids, r.r_ctx.p, 4 * m);
+    cp(incl, r.r_incl.p, 8 * m);
+    cp(excl, r.r_excl.p, 8 * m);
   });
 }
 
@@ -1752,6 +1881,10 @@ ps_status psg_get_window(psg_context* c, uint64_t* count, int64_t* sum, int64_t*
   if (!c) return PS_E_INVALID_ARGUMENT;
   return guarded([&] {
     if (!c->have_window) fail(PS_E_INVALID_ARGUMENT, "no window result (run psg_query with PSG_Q_WINDOW)");
+    if (c->window_sparse)
+      fail(PS_E_INVALID_ARGUMENT,
+           "the window is sparse (PSG_Q_SPARSE or a large calling-context tree): use psg_get_window_groups / "
+           "psg_get_remat_rows");
     ensure_device(c);
     const size_t cells = static_cast<size_t>(c->n_traces) * c->n_ctx;
     auto cp = [&](void* dst, const void* src, size_t b) {

@@ -250,6 +250,8 @@ struct query_params {
   uint32_t cta_bytes;  // cta_table_bytes(n_ctx, nn, warps), computed on the host
   uint32_t one_warp;   // CTA shape: one warp per CTA (long traces) or up to 16
   uint32_t t_base, t_stop;  // this launch's traces [t_base, t_stop) (a part of tr.n)
+  const uint32_t* ppo_g;    // [n_ctx] cube column byte offsets (4 * node position, pad 4 * nn),
+                            // or null: they live in the per-warp window records
 };
 
 // CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]
@@ -261,6 +263,51 @@ __host__ __device__ inline uint32_t cta_table_bytes(uint32_t n_ctx, uint32_t nn,
   uint32_t b = 16u * nn + 4u * n_ctx * 3 + 4u * warps;
   return (b + 15u) & ~15u;
 }
+
+// ---- the sparse window path (psg_sparse.cu): large calling-context trees --
+struct sparse_args {
+  trace_view tr;
+  uint32_t n_ctx;
+  uint64_t t0, t1;
+  uint32_t clamp_tend;
+  const uint32_t* parent;  // [n_ctx] (0xFFFFFFFF for the root)
+  const uint32_t* depth;   // [n_ctx] ancestors of each ctx
+  uint64_t row_budget;     // window rows per batch of traces (scratch bound)
+  uint8_t* c_has;          // [n] carry-in outputs
+  uint64_t* c_ts;
+  uint32_t* c_ctx;
+};
+struct sparse_result {
+  uint64_t n_rows = 0, n_groups = 0, n_remat = 0;
+  // group_aggregate rows, sorted by (trace, ctx)
+  dbuf<uint32_t> g_trace, g_ctx;
+  dbuf<uint64_t> g_cnt;
+  dbuf<int64_t> g_sum, g_min, g_max;
+  dbuf<double> g_mean;
+  // rematerialize rows (incl or excl nonzero), sorted by (trace, ctx)
+  dbuf<uint32_t> r_trace, r_ctx;
+  dbuf<int64_t> r_incl, r_excl;
+};
+void sparse_window(const sparse_args& a, sparse_result& r, cudaStream_t s);
+struct sparse_result_view {
+  uint32_t *g_trace, *g_ctx;
+  uint64_t* g_cnt;
+  int64_t *g_sum, *g_min, *g_max;
+  double* g_mean;
+  uint32_t *r_trace, *r_ctx;
+  int64_t *r_incl, *r_excl;
+};
+struct dense_window {
+  const uint64_t *cnt, *sum, *mn, *mx;
+  const double* mean;
+  const uint64_t *incl, *excl;
+};
+// the dense [trace][ctx] window result as sparse rows (count > 0 groups;
+// incl or excl nonzero remat rows)
+void dense_to_sparse(const dense_window& w, uint32_t n_traces, uint32_t n_ctx, sparse_result& r, cudaStream_t s);
+// [n_traces][n_sites] incl of each site ctx (0 when the trace has no row for it)
+void sparse_site_values(const sparse_result& r, const uint32_t* site, uint32_t n_sites, uint32_t n_traces,
+                        uint64_t* out, cudaStream_t s);
 
 // ---- launchers (psg_kernels.cu) ------------------------------------------
 

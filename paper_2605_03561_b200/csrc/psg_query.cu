@@ -900,9 +900,14 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
 // smaller, which the instruction cache notices).
 // ONE: one warp per CTA (else up to 16).
 // (the optimistic cube-only one-warp instantiation spills at 96 registers: 16 CTAs per SM, 128)
-template <bool WIN, bool CUBE, bool EXACT, bool ONE>
+// GT: the cube's column offsets come from a global per-ctx table (p.ppo_g)
+// instead of the per-warp window records (cube-only queries over calling-
+// context trees too large for the records; the window then takes the sparse
+// path, psg_sparse.cu).
+template <bool WIN, bool CUBE, bool EXACT, bool ONE, bool GT = false>
 __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !EXACT) ? 16 : PSG_ONE_MINB) : PSG_WIDE_MINB)
     k_trace_query(query_params p) {
+  static_assert(!GT || (!WIN && ONE), "global column tables: cube-only, one-warp CTAs");
   extern __shared__ __align__(16) uint8_t smem[];
   // one-warp CTAs: the trace index and everything derived from it are
   // uniform across the CTA, so they live in uniform registers
@@ -959,7 +964,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       for (uint32_t j = lane; j < (R2 + 1) * nnp; j += 32) rhi[j] = 0;
     for (uint32_t j = lane; j < nn; j += 32) wsx[j] = wsqlo[j] = wsqhi[j] = 0;
   }
-  for (uint32_t c = lane; c < n_ctx; c += 32) {
+  for (uint32_t c = lane; c < (GT ? 0u : n_ctx); c += 32) {
     uint32_t* r = T.wt + wt_word(c);
     r[WT_CNT] = r[WT_LO] = r[WT_MAX] = r[WT_NBIG] = 0u;
     r[WT_MIN] = 0xFFFFFFFFu;
@@ -1249,7 +1254,8 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           uint32_t ppo[RM];
 #pragma unroll
           for (int j = 0; j < RM; ++j)
-            ppo[j] = *reinterpret_cast<const uint32_t*>(smem + wt_off + 4u * (wt_word(cv[j]) + WT_PPO));
+            ppo[j] = GT ? __ldg(p.ppo_g + cv[j])
+                        : *reinterpret_cast<const uint32_t*>(smem + wt_off + 4u * (wt_word(cv[j]) + WT_PPO));
           if (wm == WIN_FULL)
             run_fast<WIN_FULL>(tv, cv, smem, wt_off, bpos, rb0, rb1, ppo);
           else
@@ -1460,7 +1466,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   }
 }
 
-template <bool WIN, bool CUBE, bool EXACT, bool ONE>
+template <bool WIN, bool CUBE, bool EXACT, bool ONE, bool GT = false>
 void launch_shape(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
   // the dynamic shared-memory opt-in is a per-device function attribute: track
   // it per device (one process may drive several GPUs) under a lock
@@ -1471,14 +1477,14 @@ void launch_shape(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 64 || static_cast<int>(smem_bytes) > configured_bytes[dev]) {
-      PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT, ONE>,
+      PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT, ONE, GT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem_bytes)));
       if (dev < 64) configured_bytes[dev] = static_cast<int>(smem_bytes);
     }
   }
   const unsigned blocks = (p.t_stop - p.t_base + p.warps - 1) / p.warps;
-  k_trace_query<WIN, CUBE, EXACT, ONE><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
+  k_trace_query<WIN, CUBE, EXACT, ONE, GT><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
 }
 
 template <bool WIN, bool CUBE, bool EXACT>
@@ -1501,7 +1507,12 @@ void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t
   }
   if (p.G != GC) fail(PS_E_INTERNAL, "chunk size mismatch between host and kernel (PSG_G)");
   const bool exact = p.do_cube && p.exact_bounds;
-  if (p.do_window && p.do_cube)
+  if (p.ppo_g) {  // cube only, global column table (large calling-context trees)
+    if (p.do_window || !p.do_cube || !p.one_warp || p.warps != 1)
+      fail(PS_E_INTERNAL, "global column tables need a cube-only query on one-warp CTAs");
+    exact ? launch_shape<false, true, true, true, true>(p, smem_bytes, s)
+          : launch_shape<false, true, false, true, true>(p, smem_bytes, s);
+  } else if (p.do_window && p.do_cube)
     exact ? launch_variant<true, true, true>(p, smem_bytes, s) : launch_variant<true, true, false>(p, smem_bytes, s);
   else if (p.do_window)
     launch_variant<true, false, false>(p, smem_bytes, s);
