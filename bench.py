@@ -98,13 +98,16 @@ def measured_peak() -> tuple[float, str]:
         return 6650.0, "fallback"
 
 
-def ncu_traffic(per_event_key: str = "main_dram_bytes_per_event"):
-    """Per-event DRAM bytes of the fused kernel from the committed ncu summary."""
+def ncu_kernels() -> dict:
+    """Per-event DRAM bytes (read + write) of the query's big kernels, from the
+    committed ncu capture at configs[1] (profiles/ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
-        return float(json.load(open(p))[per_event_key])
+        d = json.load(open(p))
+        return {k: (v["dram_bytes_read"] + v["dram_bytes_write"]) / d["events"]
+                for k, v in d["kernels"].items()} | {"_source": d["round"]}
     except Exception:
-        return None
+        return {}
 
 
 # ---------------------------------------------------------------------------
@@ -248,22 +251,32 @@ def main():
     main_s = statistics.mean(main_ms) / 1000.0
     peak, peak_kind = measured_peak()
     achieved = alg_bytes / main_s / 1e9
-    per_ev = ncu_traffic()
+    ncu = ncu_kernels()
+    per_ev = ncu.get("k_trace_query")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_kind": peak_kind,
+                # ncu dram__bytes_read + _write of this kernel at this config
+                # (one launch, profiles/ncu_summary.json), scaled to this shard
                 "traffic": per_ev * events_local if per_ev else None,
+                "traffic_source": ncu.get("_source"),
                 "kernel": "k_trace_query", "alg_bytes_per_launch": alg_bytes,
                 "cube_cell_bytes": info["cube_cell_bytes"],
                 "kernel_ms": main_s * 1000.0, "kernel_share_of_step": main_s * 1000.0 / (ms / args.steps),
                 "pass1_k_bounds_ms": statistics.mean(bounds_ms),
                 "frac_of_nominal_8tbs": achieved / 8000.0}
-    # the whole query step against the same peak: pass 1 reads the ctx words
-    # (4 B per event), pass 2 its algorithmic bytes, k_cross_stats re-reads the
-    # stored cube (k < K; all iterations here)
-    step_bytes = 4 * events_local + alg_bytes + info["cube_store_bytes"]
+    # the whole query step: its algorithmic bytes are the
+    # events read ONCE plus every output written once -- the same bytes as
+    # k_trace_query's (the statistics and outlier outputs are < 1 MB).  The
+    # DRAM traffic adds what the step re-reads: pass 1's 1-byte ctx mirror
+    # (k_bounds) and the stored cube (k_cross_stats); wasted_traffic_ratio =
+    # measured DRAM bytes of the three kernels / algorithmic bytes.
     step_s = ms / args.steps / 1000.0
-    roofline["step"] = {"alg_bytes": step_bytes, "achieved": step_bytes / step_s / 1e9,
-                        "frac": step_bytes / step_s / 1e9 / peak}
+    dram = (sum(ncu[k] for k in ("k_bounds", "k_trace_query", "k_cross_stats")) * events_local
+            if all(k in ncu for k in ("k_bounds", "k_trace_query", "k_cross_stats")) else None)
+    roofline["step"] = {"alg_bytes": alg_bytes, "achieved": alg_bytes / step_s / 1e9,
+                        "frac": alg_bytes / step_s / 1e9 / peak,
+                        "dram_bytes": dram, "wasted_traffic_ratio": dram / alg_bytes if dram else None,
+                        "dram_frac": dram / step_s / 1e9 / peak if dram else None}
 
     # end to end through the public API: pinned host trace.db bytes -> HBM ->
     # query -> results back to host, every step.
@@ -278,6 +291,18 @@ def main():
         pin = {k: torch.empty(n_cells * 8, dtype=torch.uint8, pin_memory=True)
                for k, _ in Context.WINDOW_DTYPES}
         wout = {k: pin[k].numpy().view(dt).reshape(n_local, sh["n_ctx"]) for k, dt in Context.WINDOW_DTYPES}
+        # the cube (the query's largest output) comes back too, in its stored
+        # lossless form (32-bit incl cells + the internal nodes' excl), into
+        # pinned buffers sized from the warm-up query
+        cube_pin = None
+        try:
+            xrows = info["n_cells"] // max(1, nn) * info["n_internal"]
+            cube_pin = (torch.empty(info["cube_store_bytes"] + 16, dtype=torch.uint8, pin_memory=True),
+                        torch.empty(8 * xrows + 8, dtype=torch.uint8, pin_memory=True))
+            cube_np = (cube_pin[0].numpy().view(np.uint32 if info["cube_cell_bytes"] == 4 else np.uint64),
+                       cube_pin[1].numpy().view(np.int64))
+        except Exception as e:  # host RAM too small to pin it: say so in the line
+            cube_pin, cube_err = None, f"{type(e).__name__}: {e}"
         d2h = 0
         secs = []
         for i in range(args.e2e_steps + 1):
@@ -291,6 +316,7 @@ def main():
             st = ctx.stats(1.0)
             ou = ctx.outliers(n_nodes)
             cb = ctx.cube(with_cells=False)
+            cs = ctx.cube_stored(*cube_np) if cube_pin is not None else None
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
@@ -300,13 +326,17 @@ def main():
                 secs.append(float(tt.item()))
             d2h = (sum(a.nbytes for a in w.values()) + sum(a.nbytes for a in st.values())
                    + sum(a.nbytes for a in ou.values())
-                   + sum(a.nbytes for k, a in cb.items() if a is not None))
+                   + sum(a.nbytes for k, a in cb.items() if a is not None)
+                   + (cs["incl"].nbytes + cs["xint"].nbytes + cs["stored_off"].nbytes if cs else 0))
         e2e = {"value": total_events / statistics.mean(secs), "unit": "events/s",
                "h2d_bytes_per_step": int(events_local * 12 + 8 * (n_local + 1) + 12 * n_local),
                "d2h_bytes_per_step": int(d2h), "steps": len(secs),
                "s_per_step": statistics.mean(secs),
                "note": "pinned trace.db bytes -> psg_load_traces_aos -> psg_query -> window/"
-                       "stats/outliers/iteration counts copied back; the cube stays in HBM"}
+                       "stats/outliers/iteration counts and the cube (stored lossless form: "
+                       "32-bit incl cells + internal-node excl, psg_get_cube_stored) copied "
+                       "back into pinned host memory" if cube_pin is not None else
+                       "cube copy-out skipped: " + cube_err}
         del host
 
     cpu = None

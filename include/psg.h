@@ -237,6 +237,18 @@ ps_status psg_get_carry(psg_context* ctx, uint8_t* has, uint64_t* ts, uint32_t* 
 ps_status psg_get_cube(psg_context* ctx, uint32_t* node_ids, uint32_t* iter_counts,
                        uint64_t* block_offset, int64_t* incl, int64_t* excl,
                        int64_t* gap_incl, int64_t* gap_excl);
+/* The cube exactly as stored in HBM, copied without conversion (lossless;
+ * the fast copy-out for host consumers that read the compact form): the
+ * incl cells (*cell_bytes = 4 or 8) in rows of stride *row_stride (n_nodes + 1
+ * rounded up to even; column n_nodes is padding), each kept trace's
+ * iter_counts[t] rows starting at cell stored_off[t] (loaded-trace index;
+ * undefined for skipped traces), and the exclusive time of the anchor
+ * subtree's internal nodes [rows][n_internal] (rows in trace order; a leaf's
+ * excl is its incl) when the query stored it.  Sizes are set first; any
+ * output pointer may be NULL. */
+ps_status psg_get_cube_stored(psg_context* ctx, uint32_t* cell_bytes, uint32_t* row_stride,
+                              uint64_t* incl_bytes, void* incl, uint64_t* stored_off,
+                              uint64_t* xint_cells, int64_t* xint);
 /* The same dense layout for the loaded traces [t_lo, t_hi) only (the kept
  * ones, in load order, relative to the range): *n_cells and *n_kept are set
  * first (any output pointer may be NULL, e.g. to size the arrays), then

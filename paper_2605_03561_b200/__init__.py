@@ -270,6 +270,26 @@ class Context:
                                           _ptr(gi, C.c_int64), _ptr(ge, C.c_int64)))
         return {"incl": incl, "excl": excl, "gap_incl": gi, "gap_excl": ge, "n_kept": kept.value}
 
+    def cube_stored(self, incl_out: Optional[np.ndarray] = None,
+                    xint_out: Optional[np.ndarray] = None) -> dict:
+        """The cube as stored in HBM, copied without conversion: incl cells
+        (uint32 or uint64) in rows of `row_stride`, per-trace stored offsets,
+        and the internal nodes' excl.  Pass pinned arrays (e.g. torch
+        pin_memory buffers viewed through numpy) to copy at full PCIe rate."""
+        cb, st, nb, nx = C.c_uint32(), C.c_uint32(), C.c_uint64(), C.c_uint64()
+        check(self.lib.psg_get_cube_stored(self.h, C.byref(cb), C.byref(st), C.byref(nb), None, None,
+                                           C.byref(nx), None))
+        dt = np.uint32 if cb.value == 4 else np.uint64
+        incl = incl_out if incl_out is not None else np.empty(nb.value // cb.value, dt)
+        assert incl.nbytes >= nb.value, "incl_out too small"
+        xint = xint_out if xint_out is not None else np.empty(nx.value, np.int64)
+        off = np.empty(self.shard()["n_traces"], np.uint64)
+        check(self.lib.psg_get_cube_stored(self.h, None, None, None, C.c_void_p(incl.ctypes.data),
+                                           _ptr(off, C.c_uint64), None,
+                                           _ptr(xint, C.c_int64) if nx.value else None))
+        return {"incl": incl.view(dt)[: nb.value // cb.value], "xint": xint[: nx.value],
+                "stored_off": off, "row_stride": st.value, "cell_bytes": cb.value}
+
     def stats(self, total_time_s: float) -> dict:
         nl = self.info["n_leaves"]
         leaves = np.empty(nl, np.uint32)

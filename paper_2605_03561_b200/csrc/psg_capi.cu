@@ -2047,6 +2047,30 @@ ps_status psg_get_cube_range(psg_context* c, uint32_t t_lo, uint32_t t_hi, uint6
   });
 }
 
+ps_status psg_get_cube_stored(psg_context* c, uint32_t* cell_bytes, uint32_t* stride,
+                              uint64_t* incl_bytes, void* incl, uint64_t* stored_off,
+                              uint64_t* xint_cells, int64_t* xint) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (!c->have_cube) fail(PS_E_INVALID_ARGUMENT, "no cube result (run psg_query with PSG_Q_CUBE)");
+    ensure_device(c);
+    const uint64_t cb = c->cube32 ? 4 : 8, bytes = c->n_store * cb;
+    const uint64_t nx = c->have_excl && c->nn ? c->n_cells / c->nn * c->internal_pos.size() : 0;
+    if (cell_bytes) *cell_bytes = static_cast<uint32_t>(cb);
+    if (stride) *stride = row_stride(c->nn);
+    if (incl_bytes) *incl_bytes = bytes;
+    if (xint_cells) *xint_cells = nx;
+    if (xint && !c->have_excl && c->n_cells)
+      fail(PS_E_INVALID_ARGUMENT, "the excl cube was not stored (PSG_Q_NO_CUBE_STORE)");
+    // straight DMA of the device buffers (full PCIe rate into pinned memory)
+    if (incl && bytes) PSG_CUDA(cudaMemcpyAsync(incl, c->cube_incl.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (stored_off && c->n_traces)
+      PSG_CUDA(cudaMemcpyAsync(stored_off, c->block_off.p, 8ull * c->n_traces, cudaMemcpyDeviceToHost, c->stream));
+    if (xint && nx) PSG_CUDA(cudaMemcpyAsync(xint, c->cube_xint.p, 8 * nx, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  });
+}
+
 ps_status psg_get_stats(psg_context* c, double total_time_s, uint32_t* leaves, double* savings,
                         double* summary, double* cv, int32_t* cv_ok) {
   if (!c) return PS_E_INVALID_ARGUMENT;

@@ -44,6 +44,7 @@ def check_cube(ctx, tr, parent, anchor, stats=True):
         g = ctx.cube()
         for k in ("node_ids", "iter_counts", "block_offset", "incl", "excl", "gap_incl", "gap_excl"):
             assert np.array_equal(g[k], o[k]), f"cube {k} differs (anchor {anchor}, flags {extra})"
+        check_stored(ctx, g, parent)
         assert info["n_kept"] == kept
         if stats and kept > 0:
             s = ctx.stats(1.0)
@@ -151,6 +152,27 @@ def test_window_rows_match_ingest_traces(gpu_ctx_factory):
     with pytest.raises(PsgError) as e:
         ctx.window_rows(5, 4)
     assert e.value.name == "invalid_argument"
+
+
+def check_stored(ctx, g, parent):
+    """psg_get_cube_stored (the lossless compact copy-out) rebuilds the dense
+    cube: incl rows from the padded blocks, excl = incl for leaves and the
+    compact internal-node rows for the rest."""
+    st = ctx.cube_stored()
+    nn, ic = len(g["node_ids"]), g["iter_counts"]
+    ids = set(int(x) for x in g["node_ids"])
+    internal = [j for j, c in enumerate(g["node_ids"])
+                if any(int(parent[x]) == int(c) for x in ids if x != c and parent[x] != 0xFFFFFFFF)]
+    rows = []
+    for t in np.flatnonzero(ic):
+        o = int(st["stored_off"][t])
+        rows.append(st["incl"][o:o + int(ic[t]) * st["row_stride"]].reshape(-1, st["row_stride"])[:, :nn])
+    incl = np.concatenate(rows).astype(np.int64) if rows else np.zeros((0, nn), np.int64)
+    assert np.array_equal(incl.ravel(), g["incl"]), "stored incl"
+    excl = incl.copy()
+    if internal and len(incl):
+        excl[:, internal] = st["xint"].reshape(len(incl), len(internal))
+    assert np.array_equal(excl.ravel(), g["excl"]), "stored excl"
 
 
 def test_cube_matches_build_tri_model(gpu_ctx_factory):
