@@ -149,8 +149,11 @@ enum : uint32_t { WT_CNT = 0, WT_LO = 1, WT_MIN = 2, WT_MAX = 3, WT_PPO = 4, WT_
 // configs[1] (67 contexts per iteration) gives 2.97 / 2.21 / 2.00 shared
 // wavefronts per record access for 0 / 1 / 2, and k_trace_query measured
 // 18.36 / 17.60 / 17.40 ms (profiles/r2g_ab_wt_swizzle.txt).
+#ifndef PSG_IL
+#define PSG_IL 1
+#endif
 #ifndef PSG_WT_SWIZZLE
-#define PSG_WT_SWIZZLE 2
+#define PSG_WT_SWIZZLE (PSG_IL ? 0 : 2)
 #endif
 __host__ __device__ inline uint32_t wt_word(uint32_t c) {
   return WT_STRIDE * (PSG_WT_SWIZZLE == 2 ? c + (c >> 5) : PSG_WT_SWIZZLE ? c + (c >> 3) : c);

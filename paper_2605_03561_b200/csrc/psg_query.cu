@@ -182,6 +182,44 @@ __device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_ab
   if (lane == 31) nf = ldg64(tr.ts + s_abs + 32 * RM);
 }
 
+// Interleaved lane layout (PSG_IL, pass 2): lane l holds events l, l + 32,
+// ..., l + 32 (RM - 1) of a block step, so the 32 lanes of one instruction
+// hold 32 CONSECUTIVE events.  Consecutive events of a trace are mostly
+// distinct contexts (sequential ids in a call sequence), so their window
+// records and cube columns fall in distinct shared-memory banks; with runs of
+// RM consecutive events per lane the lanes of an instruction touched contexts
+// RM apart, which for an iteration of 67 contexts costs 2-3 wavefronts per
+// shared access (measured: conflict-free addressing takes k_trace_query from
+// 17.3 to 15.1 ms at configs[1], tools/ab_bench.sh).  Each load instruction
+// reads 32 consecutive timestamps (256 B) or ctx words (128 B): whole sectors.
+#ifndef PSG_IL
+#define PSG_IL 1
+#endif
+__device__ __forceinline__ void load_step_il(const trace_view& tr, u64 s_abs, int lane, u64 (&ts)[RM],
+                                             uint32_t (&cx)[RM], u64& nf) {
+  const unsigned long long* tp = reinterpret_cast<const unsigned long long*>(tr.ts + s_abs) + lane;
+  const unsigned int* cp = reinterpret_cast<const unsigned int*>(tr.ctx + s_abs) + lane;
+#pragma unroll
+  for (int j = 0; j < RM; ++j) ts[j] = __ldg(tp + 32 * j);
+#pragma unroll
+  for (int j = 0; j < RM; ++j) cx[j] = __ldg(cp + 32 * j);
+  if (lane == 31) nf = ldg64(tr.ts + s_abs + 32 * RM);
+}
+
+// Timestamp of the event after (lane, j) in the interleaved layout: lane + 1's
+// event j, lane 0's event j + 1 for lane 31, and the step's successor (tv[RM]
+// on lane 31) for the last one.  Warp-uniform call (a shuffle).
+__device__ __forceinline__ u64 next_ts_il(const u64 (&tv)[RM + 1], int j, int lane) {
+  const u64 src = (lane == 0 && j + 1 < RM) ? tv[j + 1] : tv[j];
+  const u64 x = __shfl_sync(FULL, src, (lane + 1) & 31);
+  return (lane == 31 && j == RM - 1) ? tv[RM] : x;
+}
+__device__ __forceinline__ uint32_t next_lo_il(const u64 (&tv)[RM + 1], int j, int lane) {
+  const uint32_t src = static_cast<uint32_t>((lane == 0 && j + 1 < RM) ? tv[j + 1] : tv[j]);
+  const uint32_t x = __shfl_sync(FULL, src, (lane + 1) & 31);
+  return (lane == 31 && j == RM - 1) ? static_cast<uint32_t>(tv[RM]) : x;
+}
+
 // 64-bit add into shared memory through two 32-bit words (lo, hi) with
 // native 32-bit atomics: the carry of the low word is added to the high word.
 __device__ __forceinline__ void sadd64(uint32_t* lo, uint32_t* hi, u64 v) {
@@ -662,6 +700,89 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
   }
 }
 
+// The general path in the interleaved layout: lane event j is li = lane + 32 j
+// of the block step; its successor comes from the neighbouring lane.  Between
+// two of a lane's events lie 32 events, so several boundaries may be crossed
+// (each recorded by the lane owning its event).
+template <bool WIN, bool CUBE, int WM, bool CWIDE, bool ALL>
+__device__ __forceinline__ void run_events_il(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM], int lane, const run_ctx& R, run_state& st,
+                                              const warp_tables& T) {
+#pragma unroll
+  for (int j = 0; j < RM; ++j) {
+    const int li = lane + 32 * j;
+    const bool valid =
+        ALL || static_cast<unsigned>(li - R.lo) < static_cast<unsigned>(R.hi - R.lo);
+    const u64 tsj = tv[j];
+    const u64 nts = next_ts_il(tv, j, lane);
+    const uint32_t cj = valid ? cv[j] : 0u;
+    if (CUBE) {
+      if (li >= st.nxt) {
+        do {
+          ++st.k;
+          ++st.cnt;
+          if (li == st.nxt && R.bts_out && static_cast<uint32_t>(st.k) < R.nbd) R.bts_out[st.k] = tsj;
+          st.nxt = st.cnt <= R.R2 ? local_of(R.bwin[st.cnt], R.base3) : INT_MAX;
+        } while (li >= st.nxt);
+        st.slot = st.k < 0 ? R.R2 : (static_cast<uint32_t>(st.k) & (R.R2 - 1));
+        st.rowb = st.slot * R.nnp;
+        st.cube_ok = st.k < R.iters;
+      }
+      const int pp = R.s_sub_pre[cj];
+      if (valid && pp >= 0 && st.cube_ok) {
+        const uint32_t idx = st.rowb + pp;
+        if (CWIDE) {
+          const u64 dc = ((!ALL && li == R.last_li) ? R.tend : nts) - tsj;
+          sadd64(R.rlo + idx, R.rhi + idx, dc);
+        } else {
+          const uint32_t dc = static_cast<uint32_t>((!ALL && li == R.last_li) ? R.tend : nts) -
+                              static_cast<uint32_t>(tsj);
+          atomicAdd(R.rlo + idx, dc);
+        }
+      }
+    }
+    if (WIN && WM == WIN_FULL) {
+      if (valid) win_row32(T, cj, static_cast<uint32_t>(nts) - static_cast<uint32_t>(tsj));
+    } else if (WIN && WM == WIN_PART) {
+      if (valid) {
+        if (tsj >= R.t0) {
+          if (tsj < R.t1w)
+            win_row32(T, cj, static_cast<uint32_t>(min(nts, R.t1w)) - static_cast<uint32_t>(tsj));
+        } else if (nts >= R.t0) {
+          carry_in(T, cj, tsj, min(nts, R.t1w), R.t0);
+        }
+      }
+    } else if (WIN && WM == WIN_WIDE) {
+      if (valid) {
+        const bool last = li == R.last_li;
+        const u64 e2 = last ? R.t1w : min(nts, R.t1w);
+        if (tsj >= R.t0) {
+          if (tsj < R.t1w) win_row64(T, cj, e2 - tsj);
+        } else if (last || nts >= R.t0) {
+          carry_in(T, cj, tsj, e2, R.t0);
+        }
+      }
+    }
+  }
+}
+
+template <bool WIN, bool CUBE, bool CWIDE>
+__device__ __forceinline__ void run_block_il(int wm, const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM], int lane, const run_ctx& R, run_state& st,
+                                             const warp_tables& T) {
+  const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
+  if (!CWIDE && all && wm == WIN_FULL)
+    run_events_il<WIN, CUBE, WIN_FULL, false, true>(tv, cv, lane, R, st, T);
+  else if (!CWIDE && all && wm == WIN_NONE)
+    run_events_il<WIN, CUBE, WIN_NONE, false, true>(tv, cv, lane, R, st, T);
+  else if (wm == WIN_FULL)
+    run_events_il<WIN, CUBE, WIN_FULL, CWIDE, false>(tv, cv, lane, R, st, T);
+  else if (wm == WIN_PART)
+    run_events_il<WIN, CUBE, WIN_PART, CWIDE, false>(tv, cv, lane, R, st, T);
+  else if (wm == WIN_WIDE)
+    run_events_il<WIN, CUBE, WIN_WIDE, CWIDE, false>(tv, cv, lane, R, st, T);
+  else
+    run_events_il<WIN, CUBE, WIN_NONE, CWIDE, false>(tv, cv, lane, R, st, T);
+}
+
 template <bool WIN, bool CUBE, bool CWIDE>
 __device__ __forceinline__ void run_block(int wm, const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
                                           const run_ctx& R, run_state& st, const warp_tables& T) {
@@ -745,6 +866,41 @@ __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t
   for (int j = 0; j < RM; ++j) {
     const uint32_t rb = j >= bpos ? rb_after : rb_before;
     atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + (PSG_X_CUBEADDR ? 4u * (threadIdx.x & 31) : ppo[j])), d[j]);
+  }
+}
+
+// Interior block step, fast path in the interleaved layout: every event of the
+// step is valid and none is the trace's last, the chunk is narrow, the window
+// class is FULL or NONE, and each group of 32 consecutive events (one j)
+// holds at most one iteration boundary.  fa / fb carry, per group, its
+// boundary's lane + 1 in 6-bit fields (0: none; groups 0-4 in fa, 5-7 in fb)
+// and ra is the ring row of the iteration before the step (>= 0): lanes below
+// the group's boundary add into row ra, the others into the next ring row
+// (uniform per group).  Contexts outside the anchor subtree add into the
+// rows' pad column (no branch).
+template <int WM, bool GT>
+__device__ __forceinline__ void run_fast_il(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM], int lane,
+                                            uint8_t* sm, uint32_t wt_off, const uint32_t* ppo_g,
+                                            uint32_t fa, uint32_t fb, uint32_t ra, uint32_t rows_off,
+                                            uint32_t rows_end, uint32_t row_bytes) {
+#pragma unroll
+  for (int j = 0; j < RM; ++j) {
+    const uint32_t field = j < 5 ? (fa >> (6 * j)) & 63u : (fb >> (6 * (j - 5))) & 63u;
+    const uint32_t bj = (field - 1u) & 63u;  // the boundary's lane; 63: none
+    uint32_t rn = ra + row_bytes;  // the next iteration's ring row
+    rn = rn == rows_end ? rows_off : rn;
+    const uint32_t d = next_lo_il(tv, j, lane) - static_cast<uint32_t>(tv[j]);
+    uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word(cv[j]));
+    if (WM == WIN_FULL && !PSG_X_NOWIN) {
+      atomicAdd(r + WT_CNT, 1u);
+      atomicAdd(r + WT_LO, d);
+      atomicMin(r + WT_MIN, d);
+      atomicMax(r + WT_MAX, d);
+    }
+    const uint32_t ppo = GT ? __ldg(ppo_g + cv[j]) : r[WT_PPO];
+    const uint32_t rb = static_cast<uint32_t>(lane) >= bj ? rn : ra;
+    atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + ppo), d);
+    ra = field ? rn : ra;
   }
 }
 
@@ -982,7 +1138,8 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
     r[WT_CNT] = r[WT_LO] = r[WT_MAX] = r[WT_NBIG] = 0u;
     r[WT_MIN] = 0xFFFFFFFFu;
     const int32_t sp = CUBE ? p.sub_pre[c] : -1;
-    r[WT_PPO] = 4u * (sp >= 0 ? static_cast<uint32_t>(sp) : nn);  // pad column nn
+    // contexts outside the anchor subtree: the rows' pad column nn
+    r[WT_PPO] = 4u * (sp >= 0 ? static_cast<uint32_t>(sp) : nn);
     T.set_acc(c, 0ull);
   }
   if (lane == 0) T.carry[0] = T.carry[1] = T.carry[2] = 0;
@@ -1067,7 +1224,12 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   R.bts_out = kept ? bts_out : nullptr;
   R.nbd = nbd;
   __syncthreads();
-#if PSG_PIPE
+#if PSG_PIPE && PSG_IL
+  u64 pts[RM];
+  uint32_t pcx[RM];
+  u64 pnf = 0;
+  u64 pf_pos = ~0ull;
+#elif PSG_PIPE
   ulonglong2 pts[RM / 2];
   uint4 pcx[RM / 4];
   u64 pnf = 0;
@@ -1130,7 +1292,24 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       }
       u64 tv[RM + 1];
       uint32_t cv[RM];
-#if PSG_PIPE
+#if PSG_PIPE && PSG_IL
+      // software pipeline (interleaved layout): this block step's events were
+      // loaded while the previous one was processed; load the next one now
+      if (pf_pos != s_abs) load_step_il(p.tr, s_abs, lane, pts, pcx, pnf);
+#pragma unroll
+      for (int q = 0; q < RM; ++q) {
+        tv[q] = pts[q];
+        cv[q] = pcx[q];
+      }
+      tv[RM] = pnf;  // lane 31: the event after the step
+      {
+        const bool more = lim < n_t && (PSG_PIPE_CROSS || lim < E1);
+        const u64 nxt = (b + lim) & ~static_cast<u64>(SOFF);
+        const u64 lp = more ? nxt : s_abs;
+        pf_pos = more ? nxt : ~0ull;
+        load_step_il(p.tr, lp, lane, pts, pcx, pnf);
+      }
+#elif PSG_PIPE
       // software pipeline: this block step's events were loaded into registers
       // while the previous one was processed; load the next one now
       if (pf_pos != s_abs) {
@@ -1202,6 +1381,17 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         if (all) {
           first = __shfl_sync(FULL, tv[0], 0);
           after = __shfl_sync(FULL, tv[RM], 31);
+        } else if (PSG_IL) {
+          // event i sits in lane i % 32, register i / 32; lo <= SOFF < 32
+          u64 a = tv[0];
+          {
+            const int hx = R.hi >> 5;
+#pragma unroll
+            for (int q = 1; q < RM; ++q)
+              if (hx == q) a = tv[q];
+          }
+          first = __shfl_sync(FULL, tv[0], R.lo);
+          after = R.hi >= STEP_M ? __shfl_sync(FULL, tv[RM], 31) : __shfl_sync(FULL, a, R.hi & 31);
         } else {
           u64 f = tv[0];  // lo <= SOFF < RM: lane 0 owns the first valid event
 #pragma unroll
@@ -1242,6 +1432,40 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       }
 
       bool done = false;
+#if PSG_IL
+      if (CUBE && kept && all && !cwide && (wm == WIN_FULL || wm == WIN_NONE)) {
+        // boundaries of this block step: lane j <= 2G holds boundary kb + j;
+        // fast path: at most one per group of 32 events, and every iteration
+        // of the step is stored
+        const uint32_t base32 = static_cast<uint32_t>(base);  // >= 0 here (lo == 0)
+        const uint32_t rel = mybw - base32;
+        const bool inb = mybw >= base32 && rel < static_cast<uint32_t>(STEP_M);
+        const uint32_t g = rel >> 5;
+        const uint32_t H = __reduce_or_sync(FULL, inb ? 1u << g : 0u);
+        const unsigned inm = __ballot_sync(FULL, inb);
+        const uint32_t nb0 = __popc(__ballot_sync(FULL, mybw < base32));
+        const int k0 = static_cast<int>(kb) - 1 + static_cast<int>(nb0);
+        if (__popc(H) == __popc(inm) && kb + nb0 + __popc(inm) <= iters && k0 >= 0) {
+          const uint32_t f = (rel & 31u) + 1u;
+          const uint32_t fa = __reduce_or_sync(FULL, (inb && g < 5) ? f << (6 * g) : 0u);
+          const uint32_t fb = __reduce_or_sync(FULL, (inb && g >= 5) ? f << (6 * (g - 5)) : 0u);
+          // the boundaries' timestamps (optimistic pass 1): loaded now by the
+          // lanes holding them, stored after the step's reductions
+          const bool rec = bts_out && inb && kb + static_cast<uint32_t>(lane) < nbd;
+          const u64 bval = rec ? ldg64(p.tr.ts + b + mybw) : 0ull;
+          const uint32_t ra = rows_off + (static_cast<uint32_t>(k0) & (R2 - 1)) * row_bytes;
+          const uint32_t rows_end = rows_off + R2 * row_bytes;
+          if (wm == WIN_FULL)
+            run_fast_il<WIN_FULL, GT>(tv, cv, lane, smem, wt_off, p.ppo_g, fa, fb, ra, rows_off, rows_end,
+                                      row_bytes);
+          else
+            run_fast_il<WIN_NONE, GT>(tv, cv, lane, smem, wt_off, p.ppo_g, fa, fb, ra, rows_off, rows_end,
+                                      row_bytes);
+          if (rec) bts_out[kb + lane] = bval;
+          done = true;
+        }
+      }
+#else
       if (CUBE && kept && all && !cwide && (wm == WIN_FULL || wm == WIN_NONE)) {
         // boundaries of this block step: lane j <= 2G holds boundary kb + j;
         // H marks the lanes whose run holds one (fast path: at most one per
@@ -1277,6 +1501,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           done = true;
         }
       }
+#endif
       if (!done) {
         run_state st;
         st.k = -1;
@@ -1288,7 +1513,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         if (CUBE) {
           // iteration of this lane's first event: boundaries of the window at or before it
           uint32_t cnt = 0;
-          const uint32_t lp3 = R.base3 + static_cast<uint32_t>(R.lb);
+          const uint32_t lp3 = R.base3 + static_cast<uint32_t>(PSG_IL ? lane : R.lb);
           for (uint32_t j = 0; j <= R2; ++j) cnt += bwin[j] <= lp3 ? 1u : 0u;
           st.cnt = cnt;
           // a boundary on the lane's first event is counted here, not crossed
@@ -1301,10 +1526,17 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           st.rowb = st.slot * nnp;
           st.cube_ok = st.k < R.iters;
         }
+#if PSG_IL
+        if (cwide)
+          run_block_il<WIN, CUBE, true>(wm, tv, cv, lane, R, st, T);
+        else
+          run_block_il<WIN, CUBE, false>(wm, tv, cv, lane, R, st, T);
+#else
         if (cwide)
           run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
         else
           run_block<WIN, CUBE, false>(wm, tv, cv, R, st, T);
+#endif
       }
       pos = lim;
     }
