@@ -318,6 +318,13 @@ struct psg_context {
   // sized by an earlier query on these traces, the K its statistics planes
   // are laid out for, the global rank count
   dbuf<unsigned long long> qstat;
+  // work units of pass 2 (intra-trace split of long traces), planned from the
+  // loaded traces' event counts; units_key = the plan's (traces, events, unit size)
+  dbuf<uint4> d_units;
+  dbuf<uint32_t> d_split;
+  uint32_t n_units = 0, n_split = 0;
+  uint64_t units_key = 0;
+  dbuf<unsigned long long> wacc;
   bool spec_ready = false;
   uint32_t k_plane = 0;
   uint64_t ranks_global_cache = 0;
@@ -465,6 +472,7 @@ void finish_load(psg_context* c) {
     tb = c->d_tbegin.p;
   }
   c->spec_ready = false;  // the first query on these traces sizes the buffers
+  c->units_key = 0;
   c->ranks_global_cache = 0;
   launch_validate(c->view(), c->n_ctx, tb, flags, flags + 1, c->stream);
   unsigned long long out[2];
@@ -682,6 +690,10 @@ void compute_subtree(psg_context* c, uint32_t anchor) {
 #define PSG_ONE_WARP_MIN_EVENTS 40000  // average events per trace from which one-warp CTAs are used (measured crossover 33.5k-50k)
 #endif
 static constexpr uint64_t kOneWarpMinEvents = PSG_ONE_WARP_MIN_EVENTS;
+#ifndef PSG_UNIT_MIN
+#define PSG_UNIT_MIN 16384  // events: the smallest work unit of a split trace
+#endif
+static constexpr uint64_t kUnitMinEvents = PSG_UNIT_MIN;
 #ifndef PSG_G
 #define PSG_G 8  // iterations per chunk of k_trace_query (power of two, <= 15)
 #endif
@@ -1419,6 +1431,49 @@ uint64_t ranks_global(psg_context* c) {
   return c->ranks_global_cache;
 }
 
+namespace {
+// Work units for pass 2 (SURVEY.md §5 "long-context": the reference runs one
+// thread per trace, itermodel.cpp:276).  U = the events one resident warp
+// gets when the work is spread evenly (events / resident warps, at least
+// PSG_UNIT_MIN).  A trace longer than 2U would outlast the rest of the query
+// on its one warp: it is split into ceil(n_t / U) units of equal event ranges
+// (pass 2 snaps them to chunk starts).  Evenly sized traces are never split
+// (configs[1], C3: measured slower split, tools/c3_units.py — a split trace
+// merges its window and within-rank sums with atomics).  PSG_UNIT_EVENTS
+// overrides U and splits every trace longer than it (tests).
+void plan_units(psg_context* c, uint64_t slots) {
+  uint64_t U = std::max<uint64_t>(kUnitMinEvents, c->n_events / std::max<uint64_t>(1, slots));
+  uint64_t thresh = 2 * U;
+  if (const char* e = std::getenv("PSG_UNIT_EVENTS")) thresh = U = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+  const uint64_t key = (static_cast<uint64_t>(c->n_traces) * 1000003ull) ^ (c->n_events * 7919ull) ^ (U << 40) ^ (thresh << 20) ^ 1ull;
+  if (key == c->units_key) return;
+  std::vector<uint4> units;
+  std::vector<uint32_t> split;
+  bool any = false;
+  for (uint32_t t = 0; t < c->n_traces && !any; ++t) any = c->h_off[t + 1] - c->h_off[t] > thresh;
+  if (any) {
+    units.reserve(c->n_traces);
+    for (uint32_t t = 0; t < c->n_traces; ++t) {
+      const uint64_t n_t = c->h_off[t + 1] - c->h_off[t];
+      const uint64_t u = n_t > thresh ? (n_t + U - 1) / U : 1;
+      if (u > 1) split.push_back(t);
+      for (uint64_t i = 0; i < u; ++i)
+        units.push_back(make_uint4(t, static_cast<uint32_t>(n_t * i / u), static_cast<uint32_t>(n_t * (i + 1) / u),
+                                   u > 1 ? 1u : 0u));
+    }
+    if (units.size() >= (1ull << 31)) fail(PS_E_INVALID_ARGUMENT, "too many work units");
+    PSG_CUDA(cudaMemcpyAsync(c->d_units.ensure(units.size()), units.data(), sizeof(uint4) * units.size(),
+                             cudaMemcpyHostToDevice, c->stream));
+    PSG_CUDA(cudaMemcpyAsync(c->d_split.ensure(split.size() + 1), split.data(), 4 * split.size(),
+                             cudaMemcpyHostToDevice, c->stream));
+    c->sync();  // the host vectors go out of scope
+  }
+  c->n_units = static_cast<uint32_t>(units.size());
+  c->n_split = static_cast<uint32_t>(split.size());
+  c->units_key = key;
+}
+}  // namespace
+
 ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* info) {
   if (!c || !q || !info) return PS_E_INVALID_ARGUMENT;
   return guarded([&] {
@@ -1648,6 +1703,15 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     // depends only on the tree and the anchor, so every rank takes the same one)
     if (!one && !fits_wide(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false))) one = true;
     if (global_cols) one = true;
+    // work units: long traces split across warps (one-warp CTAs)
+    {
+      int dev = 0, sms = 148;
+      PSG_CUDA(cudaGetDevice(&dev));
+      PSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      plan_units(c, static_cast<uint64_t>(sms) * 16);
+    }
+    const bool units = c->n_split > 0;
+    if (units) one = true;
     uint32_t W = one ? choose_warps(1, L.bytes, 0) : choose_warps(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false));
     if (one) W = 1;
     p.one_warp = one ? 1u : 0u;
@@ -1656,7 +1720,14 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     p.cta_bytes = cta_table_bytes(c->n_ctx, nn, W, one);
     uint32_t smem = p.cta_bytes + W * L.bytes;
     PSG_CUDA(cudaEventRecord(c->ev[1], s));
+    if (units) {
+      p.units = c->d_units.p;
+      p.n_units = c->n_units;
+      p.wacc = (p.do_stats && nn) ? c->wacc.ensure(static_cast<size_t>(n) * nn * 3 + 1) : nullptr;
+      launch_split_init(p, c->d_split.p, c->n_split, s);
+    }
     if (p.do_window || p.do_cube) launch_trace_query(p, smem, s);
+    if (units) launch_split_finish(p, c->d_split.p, c->n_split, 0, s);
     PSG_CUDA(cudaEventRecord(c->ev[2], s));
     if (do_cube && !exact_bounds) {
       // the optimistic pass 1 (and its 32-bit cells) against the boundary

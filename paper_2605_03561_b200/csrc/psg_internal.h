@@ -255,6 +255,15 @@ struct query_params {
   uint32_t t_base, t_stop;  // this launch's traces [t_base, t_stop) (a part of tr.n)
   const uint32_t* ppo_g;    // [n_ctx] cube column byte offsets (4 * node position, pad 4 * nn),
                             // or null: they live in the per-warp window records
+  // Work units (intra-trace split): when set, warp i of the grid runs unit i =
+  // {trace, first event, end event, split} instead of trace t_base + i.  A
+  // split trace's units snap their event ranges to chunk starts (G-iteration
+  // boundaries) on the device, accumulate the window and the within-rank
+  // sums into global rows with atomics (rows prepared by k_split_init), and
+  // k_split_finish derives mean / min / within CV afterwards.
+  const uint4* units;
+  uint32_t n_units;
+  unsigned long long* wacc;  // [n][nn][3] within-rank Σx, Σx² lo, hi of split traces (by tpos)
 };
 
 // CTA-shared tables placed before the per-warp carve-outs: node_tab [nn]
@@ -361,6 +370,11 @@ void launch_iter_spans(const uint64_t* cap_off, const uint64_t* bts, const uint3
                        cudaStream_t s);
 size_t cube_layout_scratch_bytes(uint32_t n);
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s);
+// split traces (list of loaded-trace indices): prepare their global window rows
+// and within-rank accumulators before pass 2, finish them after
+void launch_split_init(const query_params& p, const uint32_t* split_traces, uint32_t n_split, cudaStream_t s);
+void launch_split_finish(const query_params& p, const uint32_t* split_traces, uint32_t n_split, uint32_t K,
+                         cudaStream_t s);
 // Dense int64 incl / excl cells (the reference layout) of the kept traces in
 // [t_lo, t_hi), relative to dense row dense_row0 (= iter_off[t_lo]).
 void launch_cube_dense(const void* incl, bool cube32, const uint64_t* xint, const uint32_t* iter_count,

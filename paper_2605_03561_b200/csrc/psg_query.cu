@@ -1063,6 +1063,32 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   __syncwarp();
 }
 
+// First chunk c in [0, n_chunks] whose start event is at or after e: chunk 0
+// starts at event 0, chunk c at boundary c * G (bt, strictly increasing), and
+// chunk n_chunks "starts" at n_t.  Two rounds of 32 sampled loads for up to
+// 1024 chunks (warp-uniform result).
+__device__ __forceinline__ uint32_t first_chunk_at(const uint32_t* bt, uint32_t n_chunks, u64 n_t, u64 e,
+                                                   int lane) {
+  if (e == 0) return 0;
+  if (e >= n_t) return n_chunks;
+  uint32_t lo = 1, hi = n_chunks;  // the answer lies in [lo, hi]; chunk hi starts at or after e
+  while (hi > lo) {
+    const uint32_t S = (hi - lo + 31) / 32;
+    const uint32_t c = lo + static_cast<uint32_t>(lane) * S;
+    const bool ge = c < hi && static_cast<u64>(__ldg(bt + static_cast<size_t>(c) * GC)) >= e;
+    const unsigned m = __ballot_sync(FULL, ge);
+    if (m) {
+      const uint32_t f = static_cast<uint32_t>(__ffs(m)) - 1u;
+      if (f == 0) return lo;
+      hi = lo + f * S;
+      lo = lo + (f - 1) * S + 1;
+    } else {
+      lo = lo + ((hi - lo + S - 1) / S - 1) * S + 1;
+    }
+  }
+  return lo;
+}
+
 // EXACT: pass 1 ran in the exact mode (p.exact_bounds): boundary timestamps
 // are known and chunks may need 64-bit cells.  The optimistic instantiation
 // runs 32-bit throughout and carries none of the 64-bit cell code (a third
@@ -1144,17 +1170,29 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   }
   if (lane == 0) T.carry[0] = T.carry[1] = T.carry[2] = 0;
 
-  const uint32_t t = p.t_base + blockIdx.x * W + warp;
+  uint32_t t = p.t_base + blockIdx.x * W + warp;
   bool active = t < p.t_stop;
+  u64 ue0 = 0, ue1 = ~0ull;  // this unit's event range (relative; snapped to chunk starts below)
+  bool split = false;
+  if (p.units) {
+    const uint32_t ui = blockIdx.x * W + warp;
+    active = ui < p.n_units;
+    const uint4 u = active ? p.units[ui] : make_uint4(0u, 0u, 0u, 0u);
+    t = u.x;
+    ue0 = u.y;
+    ue1 = u.z;
+    split = u.w != 0;
+  }
   // K from the device status block (no host round trip between the passes)
   const uint32_t Kq = p.qs ? qs_K(p.qs) : p.K;
   if (WIN && active) {
     T.gminb = reinterpret_cast<unsigned long long*>(p.w_min) + static_cast<size_t>(t) * n_ctx;
     T.gmaxb = reinterpret_cast<unsigned long long*>(p.w_max) + static_cast<size_t>(t) * n_ctx;
-    for (uint32_t c = lane; c < n_ctx; c += 32) {
-      T.gminb[c] = ~0ull;
-      T.gmaxb[c] = 0ull;
-    }
+    if (!split)  // split traces: k_split_init prepared the rows
+      for (uint32_t c = lane; c < n_ctx; c += 32) {
+        T.gminb[c] = ~0ull;
+        T.gmaxb[c] = 0ull;
+      }
   }
   uint32_t iters = (CUBE && active) ? p.iter_count[t] : 0;
   const uint32_t tp = iters > 0 ? p.tpos[t] : 0;
@@ -1182,6 +1220,28 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   // this lane's entry of the boundary windows of the next chunk (index and
   // timestamp) and of the one after (index): the timestamp load depends on
   // the index, so indices run one chunk further ahead
+  // a split trace's unit: chunks [c_lo, c_hi), events [pos0, end) (kept
+  // traces: the unit's nominal event range snapped to chunk starts; others:
+  // the range itself)
+  uint32_t c_lo = 0, c_stop = (iters + G - 1) / G;  // chunks [c_lo, c_stop)
+  u64 pos0 = 0, end = n_t;
+  if (split) {
+    if (CUBE && kept) {
+      const uint32_t n_chunks = (iters + G - 1) / G;
+      c_lo = first_chunk_at(bt, n_chunks, n_t, ue0, lane);
+      const uint32_t c_hi = first_chunk_at(bt, n_chunks, n_t, ue1, lane);
+      pos0 = c_lo == 0 ? 0ull : static_cast<u64>(__ldg(bt + c_lo * G));
+      end = c_hi >= n_chunks ? n_t : static_cast<u64>(__ldg(bt + c_hi * G));
+      c_stop = c_hi;
+      if (c_lo >= c_hi) active = false;  // no chunk starts in this unit's range
+    } else {
+      pos0 = min(ue0, n_t);
+      end = min(ue1, n_t);
+      if (pos0 >= end) active = false;
+    }
+    if (!active) return;  // nothing to do; no CTA barrier follows (one-warp CTAs)
+  }
+  const uint32_t kb0 = c_lo * G;
   uint32_t nx_idx = static_cast<uint32_t>(n_t), nn_idx = static_cast<uint32_t>(n_t);
   u64 nx_ts = tend;
   // Boundary timestamps come from pass 1 in its exact mode.  After the
@@ -1192,14 +1252,14 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   constexpr bool optimistic = !EXACT;  // == !p.exact_bounds (launch_variant)
   uint64_t* bts_out = optimistic ? p.bts + region : nullptr;
   if (CUBE && kept && lane <= static_cast<int>(2 * G)) {
-    const bool have = static_cast<uint32_t>(lane) < nbd;
-    nx_idx = have ? __ldg(bt + lane) : static_cast<uint32_t>(n_t);
-    nx_ts = (have && !optimistic) ? ldg64(btt + lane) : tend;
-    const bool have2 = static_cast<uint32_t>(lane) + G < nbd;
-    nn_idx = have2 ? __ldg(bt + G + lane) : static_cast<uint32_t>(n_t);
+    const bool have = kb0 + static_cast<uint32_t>(lane) < nbd;
+    nx_idx = have ? __ldg(bt + kb0 + lane) : static_cast<uint32_t>(n_t);
+    nx_ts = (have && !optimistic) ? ldg64(btt + kb0 + lane) : tend;
+    const bool have2 = kb0 + static_cast<uint32_t>(lane) + G < nbd;
+    nn_idx = have2 ? __ldg(bt + kb0 + G + lane) : static_cast<uint32_t>(n_t);
   }
   const u64 t0 = p.t0, t1w = (p.clamp_tend && tend < p.t1) ? tend : p.t1;
-  u64 pos = 0;    // next unprocessed event, relative to b
+  u64 pos = pos0;  // next unprocessed event, relative to b
   u64 wspan = 0;  // time span added to the 32-bit pending window sums since the last fold
   uint32_t mybw = 0xFFFFFFFFu;  // lane j <= 2G: relative event index of boundary kb + j
 
@@ -1236,9 +1296,9 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   u64 pf_pos = ~0ull;  // block start whose events sit in pts/pcx/pnf
 #endif
 
-  for (uint32_t c = 0;; ++c) {
+  for (uint32_t c = c_lo;; ++c) {
     const uint32_t kb = c * G;
-    u64 E1 = n_t, E2 = n_t;
+    u64 E1 = end, E2 = end;
     bool cwide = false;
     if (CUBE && kept) {
       // boundary window of this chunk (prefetched during the previous one)
@@ -1255,8 +1315,8 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       const bool have2 = lane <= static_cast<int>(R2) && k + G < nbd;
       nn_idx = have2 ? __ldg(bt + k + G) : static_cast<uint32_t>(n_t);
       __syncwarp();
-      E1 = bwin[G] - SOFF;
-      E2 = bwin[R2] - SOFF;
+      E1 = min(static_cast<u64>(bwin[G] - SOFF), end);
+      E2 = min(static_cast<u64>(bwin[R2] - SOFF), end);
       // iteration spans of the ring (and the gap in chunk 0) decide 32- vs
       // 64-bit cells (exact mode; the optimistic mode runs 32-bit throughout)
       if (EXACT) {
@@ -1656,7 +1716,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       }
       __syncwarp();
     }
-    if (pos >= n_t && static_cast<u64>(kb) + G >= iters) break;
+    if (pos >= end && c + 1 >= c_stop) break;
   }
 
   if (!active) return;
@@ -1678,7 +1738,33 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
     __threadfence();  // the big min/max atomics of all lanes, before the read-back
     __syncwarp();
     const size_t base = static_cast<size_t>(t) * n_ctx;
-    for (uint32_t c = lane; c < n_ctx; c += 32) {
+    if (split) {
+      // one unit of a split trace: merge into the rows k_split_init prepared
+      // (the min / max of durations >= 2^32 are already in them)
+      for (uint32_t c = lane; c < n_ctx; c += 32) {
+        const uint32_t* r = T.wt + wt_word(c);
+        const int pr = s_cct_pre[c], sz = s_cct_size[c];
+        const u64 cnt = r[WT_CNT], nbig = r[WT_NBIG];
+        unsigned long long* wc = reinterpret_cast<unsigned long long*>(p.w_cnt) + base + c;
+        if (cnt) {
+          atomicAdd(wc, cnt);
+          atomicAdd(reinterpret_cast<unsigned long long*>(p.w_sum) + base + c, T.acc(c) + r[WT_LO]);
+        }
+        if (cnt > nbig) {
+          atomicMin(reinterpret_cast<unsigned long long*>(p.w_min) + base + c, static_cast<u64>(r[WT_MIN]));
+          atomicMax(reinterpret_cast<unsigned long long*>(p.w_max) + base + c, static_cast<u64>(r[WT_MAX]));
+        }
+        const u64 ex = scan[pr + 1] - scan[pr], in = scan[pr + sz] - scan[pr];
+        if (ex) atomicAdd(reinterpret_cast<unsigned long long*>(p.w_excl) + base + c, ex);
+        if (in) atomicAdd(reinterpret_cast<unsigned long long*>(p.w_incl) + base + c, in);
+      }
+      if (lane == 0 && c_has) {  // the carry-in event lies in exactly one unit
+        p.c_has[t] = 1;
+        p.c_ts[t] = T.carry[0];
+        p.c_ctx[t] = c_ctx;
+      }
+    }
+    for (uint32_t c = lane; c < (split ? 0u : n_ctx); c += 32) {
       const uint32_t* r = T.wt + wt_word(c);
       const int pr = s_cct_pre[c], sz = s_cct_size[c];
       const u64 cnt = r[WT_CNT], nbig = r[WT_NBIG];
@@ -1692,13 +1778,27 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       p.w_excl[base + c] = scan[pr + 1] - scan[pr];
       p.w_incl[base + c] = scan[pr + sz] - scan[pr];
     }
-    if (lane == 0) {
+    if (lane == 0 && !split) {
       p.c_has[t] = c_has ? 1 : 0;
       p.c_ts[t] = c_has ? T.carry[0] : 0;
       p.c_ctx[t] = c_has ? c_ctx : 0;
     }
   }
-  if (CUBE && p.do_stats && kept && Kq > 0) {
+  if (CUBE && p.do_stats && kept && Kq > 0 && split) {
+    // a unit's within-rank sums into the trace's accumulators (128-bit Σx²:
+    // the low word's carry goes to the high word)
+    unsigned long long* a = p.wacc + static_cast<size_t>(tp) * nn * 3;
+    for (uint32_t n = lane; n < nn; n += 32) {
+      if (wsx[n]) atomicAdd(a + 3 * n, wsx[n]);
+      const u64 ql = wsqlo[n];
+      u64 qh = wsqhi[n];
+      if (ql) {
+        const u64 old = atomicAdd(a + 3 * n + 1, ql);
+        qh += old + ql < old ? 1ull : 0ull;
+      }
+      if (qh) atomicAdd(a + 3 * n + 2, qh);
+    }
+  } else if (CUBE && p.do_stats && kept && Kq > 0) {
     for (uint32_t n = lane; n < nn; n += 32) {
       const u64 sx = wsx[n];
       const u128 sq = (static_cast<u128>(wsqhi[n]) << 64) | wsqlo[n];
@@ -1728,7 +1828,8 @@ void launch_shape(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
       if (dev < 64) configured_bytes[dev] = static_cast<int>(smem_bytes);
     }
   }
-  const unsigned blocks = (p.t_stop - p.t_base + p.warps - 1) / p.warps;
+  const unsigned blocks = p.units ? (p.n_units + p.warps - 1) / p.warps
+                                  : (p.t_stop - p.t_base + p.warps - 1) / p.warps;
   k_trace_query<WIN, CUBE, EXACT, ONE, GT><<<blocks, p.warps * 32, smem_bytes, s>>>(p);
 }
 
@@ -1763,6 +1864,79 @@ void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t
     launch_variant<true, false, false>(p, smem_bytes, s);
   else
     exact ? launch_variant<false, true, true>(p, smem_bytes, s) : launch_variant<false, true, false>(p, smem_bytes, s);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
+// ---- split traces (work units) ----------------------------------------------
+// One warp per split trace: its global window rows start empty (min at ~0 for
+// the atomicMin merges), its carry-in absent, its within-rank accumulators 0.
+__global__ void k_split_init(query_params p, const uint32_t* split, uint32_t n_split) {
+  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n_split) return;
+  const uint32_t t = split[i];
+  if (p.do_window) {
+    const size_t base = static_cast<size_t>(t) * p.n_ctx;
+    for (uint32_t c = lane; c < p.n_ctx; c += 32) {
+      p.w_cnt[base + c] = p.w_sum[base + c] = p.w_max[base + c] = 0;
+      p.w_excl[base + c] = p.w_incl[base + c] = 0;
+      p.w_min[base + c] = ~0ull;
+    }
+    if (lane == 0) {
+      p.c_has[t] = 0;
+      p.c_ts[t] = 0;
+      p.c_ctx[t] = 0;
+    }
+  }
+  if (p.do_cube && p.do_stats && p.wacc && p.iter_count[t] > 0) {
+    unsigned long long* a = p.wacc + static_cast<size_t>(p.tpos[t]) * p.nn * 3;
+    for (uint32_t j = lane; j < 3 * p.nn; j += 32) a[j] = 0;
+  }
+}
+
+// After pass 2: a split trace's window mean and empty-group min, and its
+// within-rank CVs from the merged sums (the same formula as pass 2's epilogue).
+__global__ void k_split_finish(query_params p, const uint32_t* split, uint32_t n_split) {
+  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n_split) return;
+  const uint32_t t = split[i];
+  if (p.do_window) {
+    const size_t base = static_cast<size_t>(t) * p.n_ctx;
+    for (uint32_t c = lane; c < p.n_ctx; c += 32) {
+      const u64 cnt = p.w_cnt[base + c];
+      if (cnt == 0) p.w_min[base + c] = 0;
+      p.w_mean[base + c] = cnt ? static_cast<double>(p.w_sum[base + c]) / static_cast<double>(cnt) : 0.0;
+    }
+  }
+  const uint32_t Kq = p.qs ? qs_K(p.qs) : p.K;
+  if (p.do_cube && p.do_stats && p.wacc && p.iter_count[t] > 0 && Kq > 0) {
+    const uint32_t tp = p.tpos[t];
+    const unsigned long long* a = p.wacc + static_cast<size_t>(tp) * p.nn * 3;
+    for (uint32_t n = lane; n < p.nn; n += 32) {
+      const u64 sx = a[3 * n];
+      const u128 sq = (static_cast<u128>(a[3 * n + 2]) << 64) | a[3 * n + 1];
+      const u128 num = static_cast<u128>(Kq) * sq - static_cast<u128>(sx) * sx;
+      const bool ok = sx > 0;
+      p.within_cv[static_cast<size_t>(tp) * p.nn + n] =
+          ok ? 100.0 * sqrt(u128_to_double(num)) / static_cast<double>(sx) : 0.0;
+      p.within_ok[static_cast<size_t>(tp) * p.nn + n] = ok ? 1 : 0;
+    }
+  }
+}
+
+void launch_split_init(const query_params& p, const uint32_t* split, uint32_t n_split, cudaStream_t s) {
+  if (!n_split) return;
+  k_split_init<<<(n_split + 7) / 8, 256, 0, s>>>(p, split, n_split);
+  count_launch();
+  PSG_CUDA(cudaGetLastError());
+}
+
+void launch_split_finish(const query_params& p, const uint32_t* split, uint32_t n_split, uint32_t,
+                         cudaStream_t s) {
+  if (!n_split) return;
+  k_split_finish<<<(n_split + 7) / 8, 256, 0, s>>>(p, split, n_split);
   count_launch();
   PSG_CUDA(cudaGetLastError());
 }
