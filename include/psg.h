@@ -249,6 +249,13 @@ ps_status psg_get_cube(psg_context* ctx, uint32_t* node_ids, uint32_t* iter_coun
 ps_status psg_get_cube_stored(psg_context* ctx, uint32_t* cell_bytes, uint32_t* row_stride,
                               uint64_t* incl_bytes, void* incl, uint64_t* stored_off,
                               uint64_t* xint_cells, int64_t* xint);
+/* The same copy, enqueued on the context's copy-out stream and returned at
+ * once (pinned destinations): it overlaps whatever the host does next, e.g.
+ * loading the next batch of traces (the H2D and D2H directions run on
+ * separate copy engines).  The next psg_query waits for it on the device;
+ * psg_wait_copies blocks the host until the data has landed. */
+ps_status psg_get_cube_stored_async(psg_context* ctx, void* incl, uint64_t* stored_off, int64_t* xint);
+ps_status psg_wait_copies(psg_context* ctx);
 /* The same dense layout for the loaded traces [t_lo, t_hi) only (the kept
  * ones, in load order, relative to the range): *n_cells and *n_kept are set
  * first (any output pointer may be NULL, e.g. to size the arrays), then

@@ -271,11 +271,14 @@ class Context:
         return {"incl": incl, "excl": excl, "gap_incl": gi, "gap_excl": ge, "n_kept": kept.value}
 
     def cube_stored(self, incl_out: Optional[np.ndarray] = None,
-                    xint_out: Optional[np.ndarray] = None) -> dict:
+                    xint_out: Optional[np.ndarray] = None, wait: bool = True,
+                    off_out: Optional[np.ndarray] = None) -> dict:
         """The cube as stored in HBM, copied without conversion: incl cells
         (uint32 or uint64) in rows of `row_stride`, per-trace stored offsets,
         and the internal nodes' excl.  Pass pinned arrays (e.g. torch
-        pin_memory buffers viewed through numpy) to copy at full PCIe rate."""
+        pin_memory buffers viewed through numpy) to copy at full PCIe rate;
+        wait=False returns at once (the arrays fill in the background until
+        wait_copies() or the next query)."""
         cb, st, nb, nx = C.c_uint32(), C.c_uint32(), C.c_uint64(), C.c_uint64()
         check(self.lib.psg_get_cube_stored(self.h, C.byref(cb), C.byref(st), C.byref(nb), None, None,
                                            C.byref(nx), None))
@@ -283,12 +286,20 @@ class Context:
         incl = incl_out if incl_out is not None else np.empty(nb.value // cb.value, dt)
         assert incl.nbytes >= nb.value, "incl_out too small"
         xint = xint_out if xint_out is not None else np.empty(nx.value, np.int64)
-        off = np.empty(self.shard()["n_traces"], np.uint64)
-        check(self.lib.psg_get_cube_stored(self.h, None, None, None, C.c_void_p(incl.ctypes.data),
-                                           _ptr(off, C.c_uint64), None,
-                                           _ptr(xint, C.c_int64) if nx.value else None))
+        off = off_out if off_out is not None else np.empty(self.shard()["n_traces"], np.uint64)
+        if wait:
+            check(self.lib.psg_get_cube_stored(self.h, None, None, None, C.c_void_p(incl.ctypes.data),
+                                               _ptr(off, C.c_uint64), None,
+                                               _ptr(xint, C.c_int64) if nx.value else None))
+        else:
+            check(self.lib.psg_get_cube_stored_async(self.h, C.c_void_p(incl.ctypes.data), _ptr(off, C.c_uint64),
+                                                     _ptr(xint, C.c_int64) if nx.value else None))
         return {"incl": incl.view(dt)[: nb.value // cb.value], "xint": xint[: nx.value],
                 "stored_off": off, "row_stride": st.value, "cell_bytes": cb.value}
+
+    def wait_copies(self):
+        """Block until an asynchronous copy-out (cube_stored(wait=False)) landed."""
+        check(self.lib.psg_wait_copies(self.h))
 
     def stats(self, total_time_s: float) -> dict:
         nl = self.info["n_leaves"]

@@ -125,6 +125,8 @@ _SIGS = {
     "psg_node_means": (C.c_int, [P, F64P, U32P, C.c_uint64, C.c_uint32, F64P, U32P]),
     "psg_localize": (C.c_int, [P, U32P, U32P, C.c_uint32, C.c_uint32, U32P, C.c_uint32, U32P, U32P]),
     "psg_get_cube_stored": (C.c_int, [P, U32P, U32P, U64P, C.c_void_p, U64P, U64P, I64P]),
+    "psg_get_cube_stored_async": (C.c_int, [P, C.c_void_p, U64P, I64P]),
+    "psg_wait_copies": (C.c_int, [P]),
     "psg_get_cube_range": (C.c_int, [P, C.c_uint32, C.c_uint32, U64P, U32P, I64P, I64P, I64P, I64P]),
     "psg_export_aos_range": (C.c_int, [P, C.c_uint32, C.c_uint32, C.c_void_p]),
     "psg_window_rows": (C.c_int, [P, C.c_uint64, C.c_uint64, U64P, U32P, U64P, U32P]),

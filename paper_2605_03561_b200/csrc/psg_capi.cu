@@ -325,6 +325,15 @@ struct psg_context {
   uint32_t n_units = 0, n_split = 0;
   uint64_t units_key = 0;
   dbuf<unsigned long long> wacc;
+  // asynchronous copy-out (psg_get_cube_stored_async): its own stream, so the
+  // D2H of one query's cube overlaps the H2D of the next query's traces
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t d2h_ready = nullptr, d2h_done = nullptr;
+  bool d2h_pending = false;
+  void wait_copies() {
+    if (d2h_pending) PSG_CUDA(cudaEventSynchronize(d2h_done));
+    d2h_pending = false;
+  }
   bool spec_ready = false;
   uint32_t k_plane = 0;
   uint64_t ranks_global_cache = 0;
@@ -884,6 +893,12 @@ void psg_close(psg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->d2h_stream) {
+    cudaStreamSynchronize(ctx->d2h_stream);
+    cudaStreamDestroy(ctx->d2h_stream);
+    cudaEventDestroy(ctx->d2h_ready);
+    cudaEventDestroy(ctx->d2h_done);
+  }
   delete ctx;
 }
 
@@ -1193,6 +1208,9 @@ ps_status psg_profile_outliers(psg_context* c, uint16_t metric, const uint32_t* 
     if (c->n_rank_prof == 0) fail(PS_E_INSUFFICIENT_DATA, "balance_ratio of empty vector (no rank profiles loaded)");
     require(c->have_prof_nodes, "profile outliers need the profile -> node mapping (psg_load_profile_db or node_of_profile)");
     if (!c->topo_error.empty()) fail(PS_E_PARSE, c->topo_error);
+    // an asynchronous copy-out of the previous result may still read the
+    // buffers this query rewrites: the stream waits for it (no host block)
+    if (c->d2h_pending) PSG_CUDA(cudaStreamWaitEvent(c->stream, c->d2h_done, 0));
     invalidate_results(c);
     std::memset(info, 0, sizeof(*info));
     cudaStream_t s = c->stream;
@@ -1488,6 +1506,9 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     if (do_window && q->t0_ns > q->t1_ns)
       fail(PS_E_INVALID_ARGUMENT, "trace window start after end");
     if (c->n_ctx == 0) fail(PS_E_INVALID_ARGUMENT, "no calling-context tree loaded");
+    // an asynchronous copy-out of the previous result may still read the
+    // buffers this query rewrites: the stream waits for it (no host block)
+    if (c->d2h_pending) PSG_CUDA(cudaStreamWaitEvent(c->stream, c->d2h_done, 0));
     invalidate_results(c);
     std::memset(info, 0, sizeof(*info));
     const uint64_t syncs0 = c->n_syncs;
@@ -2118,9 +2139,9 @@ ps_status psg_get_cube_range(psg_context* c, uint32_t t_lo, uint32_t t_hi, uint6
   });
 }
 
-ps_status psg_get_cube_stored(psg_context* c, uint32_t* cell_bytes, uint32_t* stride,
-                              uint64_t* incl_bytes, void* incl, uint64_t* stored_off,
-                              uint64_t* xint_cells, int64_t* xint) {
+namespace {
+ps_status get_cube_stored(psg_context* c, uint32_t* cell_bytes, uint32_t* stride, uint64_t* incl_bytes,
+                          void* incl, uint64_t* stored_off, uint64_t* xint_cells, int64_t* xint, bool async) {
   if (!c) return PS_E_INVALID_ARGUMENT;
   return guarded([&] {
     if (!c->have_cube) fail(PS_E_INVALID_ARGUMENT, "no cube result (run psg_query with PSG_Q_CUBE)");
@@ -2134,12 +2155,45 @@ ps_status psg_get_cube_stored(psg_context* c, uint32_t* cell_bytes, uint32_t* st
     if (xint && !c->have_excl && c->n_cells)
       fail(PS_E_INVALID_ARGUMENT, "the excl cube was not stored (PSG_Q_NO_CUBE_STORE)");
     // straight DMA of the device buffers (full PCIe rate into pinned memory)
-    if (incl && bytes) PSG_CUDA(cudaMemcpyAsync(incl, c->cube_incl.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    cudaStream_t st = c->stream;
+    if (async) {
+      if (!c->d2h_stream) {
+        PSG_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+        PSG_CUDA(cudaEventCreateWithFlags(&c->d2h_ready, cudaEventDisableTiming));
+        PSG_CUDA(cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming));
+      }
+      c->wait_copies();  // one copy-out in flight at a time
+      PSG_CUDA(cudaEventRecord(c->d2h_ready, c->stream));
+      PSG_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->d2h_ready, 0));
+      st = c->d2h_stream;
+    }
+    if (incl && bytes) PSG_CUDA(cudaMemcpyAsync(incl, c->cube_incl.p, bytes, cudaMemcpyDeviceToHost, st));
     if (stored_off && c->n_traces)
-      PSG_CUDA(cudaMemcpyAsync(stored_off, c->block_off.p, 8ull * c->n_traces, cudaMemcpyDeviceToHost, c->stream));
-    if (xint && nx) PSG_CUDA(cudaMemcpyAsync(xint, c->cube_xint.p, 8 * nx, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
+      PSG_CUDA(cudaMemcpyAsync(stored_off, c->block_off.p, 8ull * c->n_traces, cudaMemcpyDeviceToHost, st));
+    if (xint && nx) PSG_CUDA(cudaMemcpyAsync(xint, c->cube_xint.p, 8 * nx, cudaMemcpyDeviceToHost, st));
+    if (async) {
+      PSG_CUDA(cudaEventRecord(c->d2h_done, st));
+      c->d2h_pending = true;
+    } else {
+      c->sync();
+    }
   });
+}
+}  // namespace
+
+ps_status psg_get_cube_stored(psg_context* c, uint32_t* cell_bytes, uint32_t* stride,
+                              uint64_t* incl_bytes, void* incl, uint64_t* stored_off,
+                              uint64_t* xint_cells, int64_t* xint) {
+  return get_cube_stored(c, cell_bytes, stride, incl_bytes, incl, stored_off, xint_cells, xint, false);
+}
+
+ps_status psg_get_cube_stored_async(psg_context* c, void* incl, uint64_t* stored_off, int64_t* xint) {
+  return get_cube_stored(c, nullptr, nullptr, nullptr, incl, stored_off, nullptr, xint, true);
+}
+
+ps_status psg_wait_copies(psg_context* c) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] { c->wait_copies(); });
 }
 
 ps_status psg_get_stats(psg_context* c, double total_time_s, uint32_t* leaves, double* savings,

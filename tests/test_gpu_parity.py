@@ -173,6 +173,11 @@ def check_stored(ctx, g, parent):
     if internal and len(incl):
         excl[:, internal] = st["xint"].reshape(len(incl), len(internal))
     assert np.array_equal(excl.ravel(), g["excl"]), "stored excl"
+    # the asynchronous copy-out lands the same bytes
+    a = ctx.cube_stored(np.zeros_like(st["incl"]), np.zeros_like(st["xint"]), wait=False)
+    ctx.wait_copies()
+    for k in ("incl", "xint", "stored_off"):
+        assert np.array_equal(a[k], st[k]), f"async stored {k}"
 
 
 def test_cube_matches_build_tri_model(gpu_ctx_factory):
