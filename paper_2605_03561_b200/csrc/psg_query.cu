@@ -195,6 +195,26 @@ __device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_ab
 #ifndef PSG_IL
 #define PSG_IL 1
 #endif
+// Rotating register pipeline (interleaved layout): as soon as event j of the
+// current block step is consumed, its registers receive event j of the next
+// step, so the loads of step s + 1 are in flight during step s without a
+// second register set or the copy between them.
+#ifndef PSG_ROT
+#define PSG_ROT 1
+#endif
+// the rotating pipeline's source: this lane's events of the step at lp
+struct rot_src {
+  const unsigned long long* ts;  // tr.ts + lp + lane
+  const unsigned int* ctx;       // tr.ctx + lp + lane
+};
+__device__ __forceinline__ void rot_load(const rot_src& r, int j, u64 (&tv)[RM + 1], uint32_t (&cv)[RM]) {
+  tv[j] = __ldg(r.ts + 32 * j);
+  cv[j] = __ldg(r.ctx + 32 * j);
+}
+// lane 31 also loads the event after the step once j = RM - 1 is consumed
+__device__ __forceinline__ void rot_tail(const rot_src& r, int lane, u64 (&tv)[RM + 1]) {
+  if (lane == 31) tv[RM] = __ldg(r.ts + 32 * RM - 31);
+}
 __device__ __forceinline__ void load_step_il(const trace_view& tr, u64 s_abs, int lane, u64 (&ts)[RM],
                                              uint32_t (&cx)[RM], u64& nf) {
   const unsigned long long* tp = reinterpret_cast<const unsigned long long*>(tr.ts + s_abs) + lane;
@@ -705,8 +725,9 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
 // two of a lane's events lie 32 events, so several boundaries may be crossed
 // (each recorded by the lane owning its event).
 template <bool WIN, bool CUBE, int WM, bool CWIDE, bool ALL>
-__device__ __forceinline__ void run_events_il(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM], int lane, const run_ctx& R, run_state& st,
-                                              const warp_tables& T) {
+__device__ __forceinline__ void run_events_il(u64 (&tv)[RM + 1], uint32_t (&cv)[RM], int lane,
+                                              const run_ctx& R, run_state& st,
+                                              const warp_tables& T, const rot_src& rs) {
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
     const int li = lane + 32 * j;
@@ -762,25 +783,28 @@ __device__ __forceinline__ void run_events_il(const u64 (&tv)[RM + 1], const uin
         }
       }
     }
+    if (PSG_ROT) rot_load(rs, j, tv, cv);
   }
+  if (PSG_ROT) rot_tail(rs, lane, tv);
 }
 
 template <bool WIN, bool CUBE, bool CWIDE>
-__device__ __forceinline__ void run_block_il(int wm, const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM], int lane, const run_ctx& R, run_state& st,
-                                             const warp_tables& T) {
+__device__ __forceinline__ void run_block_il(int wm, u64 (&tv)[RM + 1], uint32_t (&cv)[RM], int lane,
+                                             const run_ctx& R, run_state& st,
+                                             const warp_tables& T, const rot_src& rs) {
   const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
   if (!CWIDE && all && wm == WIN_FULL)
-    run_events_il<WIN, CUBE, WIN_FULL, false, true>(tv, cv, lane, R, st, T);
+    run_events_il<WIN, CUBE, WIN_FULL, false, true>(tv, cv, lane, R, st, T, rs);
   else if (!CWIDE && all && wm == WIN_NONE)
-    run_events_il<WIN, CUBE, WIN_NONE, false, true>(tv, cv, lane, R, st, T);
+    run_events_il<WIN, CUBE, WIN_NONE, false, true>(tv, cv, lane, R, st, T, rs);
   else if (wm == WIN_FULL)
-    run_events_il<WIN, CUBE, WIN_FULL, CWIDE, false>(tv, cv, lane, R, st, T);
+    run_events_il<WIN, CUBE, WIN_FULL, CWIDE, false>(tv, cv, lane, R, st, T, rs);
   else if (wm == WIN_PART)
-    run_events_il<WIN, CUBE, WIN_PART, CWIDE, false>(tv, cv, lane, R, st, T);
+    run_events_il<WIN, CUBE, WIN_PART, CWIDE, false>(tv, cv, lane, R, st, T, rs);
   else if (wm == WIN_WIDE)
-    run_events_il<WIN, CUBE, WIN_WIDE, CWIDE, false>(tv, cv, lane, R, st, T);
+    run_events_il<WIN, CUBE, WIN_WIDE, CWIDE, false>(tv, cv, lane, R, st, T, rs);
   else
-    run_events_il<WIN, CUBE, WIN_NONE, CWIDE, false>(tv, cv, lane, R, st, T);
+    run_events_il<WIN, CUBE, WIN_NONE, CWIDE, false>(tv, cv, lane, R, st, T, rs);
 }
 
 template <bool WIN, bool CUBE, bool CWIDE>
@@ -879,10 +903,10 @@ __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t
 // (uniform per group).  Contexts outside the anchor subtree add into the
 // rows' pad column (no branch).
 template <int WM, bool GT>
-__device__ __forceinline__ void run_fast_il(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM], int lane,
+__device__ __forceinline__ void run_fast_il(u64 (&tv)[RM + 1], uint32_t (&cv)[RM], int lane,
                                             uint8_t* sm, uint32_t wt_off, const uint32_t* ppo_g,
                                             uint32_t fa, uint32_t fb, uint32_t ra, uint32_t rows_off,
-                                            uint32_t rows_end, uint32_t row_bytes) {
+                                            uint32_t rows_end, uint32_t row_bytes, const rot_src& rs) {
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
     const uint32_t field = j < 5 ? (fa >> (6 * j)) & 63u : (fb >> (6 * (j - 5))) & 63u;
@@ -901,7 +925,9 @@ __device__ __forceinline__ void run_fast_il(const u64 (&tv)[RM + 1], const uint3
     const uint32_t rb = static_cast<uint32_t>(lane) >= bj ? rn : ra;
     atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + ppo), d);
     ra = field ? rn : ra;
+    if (PSG_ROT) rot_load(rs, j, tv, cv);
   }
+  if (PSG_ROT) rot_tail(rs, lane, tv);
 }
 
 // Flush of a full narrow chunk (G rows, every cell < 2^32) when the anchor is
@@ -1284,7 +1310,11 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   R.bts_out = kept ? bts_out : nullptr;
   R.nbd = nbd;
   __syncthreads();
-#if PSG_PIPE && PSG_IL
+#if PSG_IL && PSG_ROT
+  u64 tv[RM + 1];  // the block step loaded ahead (rotating pipeline)
+  uint32_t cv[RM];
+  u64 pf_pos = ~0ull;
+#elif PSG_PIPE && PSG_IL
   u64 pts[RM];
   uint32_t pcx[RM];
   u64 pnf = 0;
@@ -1350,9 +1380,31 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         prefetch_l2_lane0(p.tr.ts + s_abs + PSG_Q_PF_DIST * STEP_M, 8 * STEP_M, pf);
         prefetch_l2_lane0(p.tr.ctx + s_abs + PSG_Q_PF_DIST * STEP_M, 4 * STEP_M, pf);
       }
+#if PSG_IL && PSG_ROT
+      rot_src rs;
+      {
+        if (pf_pos != s_abs) {  // first step (or the pipeline did not run ahead): load now
+          u64 nf = 0;
+          u64 t8[RM];
+          load_step_il(p.tr, s_abs, lane, t8, cv, nf);
+#pragma unroll
+          for (int q = 0; q < RM; ++q) tv[q] = t8[q];
+          tv[RM] = nf;
+        }
+        const bool more = lim < n_t && (PSG_PIPE_CROSS || lim < E1);
+        const u64 nxt = (b + lim) & ~static_cast<u64>(SOFF);
+        const u64 lp = more ? nxt : s_abs;
+        pf_pos = more ? nxt : ~0ull;
+        rs.ts = reinterpret_cast<const unsigned long long*>(p.tr.ts + lp) + lane;
+        rs.ctx = reinterpret_cast<const unsigned int*>(p.tr.ctx + lp) + lane;
+      }
+#else
       u64 tv[RM + 1];
       uint32_t cv[RM];
-#if PSG_PIPE && PSG_IL
+      rot_src rs{};
+#endif
+#if PSG_IL && PSG_ROT
+#elif PSG_PIPE && PSG_IL
       // software pipeline (interleaved layout): this block step's events were
       // loaded while the previous one was processed; load the next one now
       if (pf_pos != s_abs) load_step_il(p.tr, s_abs, lane, pts, pcx, pnf);
@@ -1517,10 +1569,10 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           const uint32_t rows_end = rows_off + R2 * row_bytes;
           if (wm == WIN_FULL)
             run_fast_il<WIN_FULL, GT>(tv, cv, lane, smem, wt_off, p.ppo_g, fa, fb, ra, rows_off, rows_end,
-                                      row_bytes);
+                                      row_bytes, rs);
           else
             run_fast_il<WIN_NONE, GT>(tv, cv, lane, smem, wt_off, p.ppo_g, fa, fb, ra, rows_off, rows_end,
-                                      row_bytes);
+                                      row_bytes, rs);
           if (rec) bts_out[kb + lane] = bval;
           done = true;
         }
@@ -1588,9 +1640,9 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         }
 #if PSG_IL
         if (cwide)
-          run_block_il<WIN, CUBE, true>(wm, tv, cv, lane, R, st, T);
+          run_block_il<WIN, CUBE, true>(wm, tv, cv, lane, R, st, T, rs);
         else
-          run_block_il<WIN, CUBE, false>(wm, tv, cv, lane, R, st, T);
+          run_block_il<WIN, CUBE, false>(wm, tv, cv, lane, R, st, T, rs);
 #else
         if (cwide)
           run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
