@@ -53,19 +53,6 @@ constexpr unsigned long long kSpan32 = 1ull << 32;
 typedef unsigned long long u64;
 typedef unsigned __int128 u128;
 
-// A/B experiment hooks (wrong results; never on in a product build)
-#ifndef PSG_X_NOWIN
-#define PSG_X_NOWIN 0
-#endif
-#ifndef PSG_X_WINADDR
-#define PSG_X_WINADDR 0
-#endif
-#ifndef PSG_X_CUBEADDR
-#define PSG_X_CUBEADDR 0
-#endif
-#ifndef PSG_X_NOSTATS
-#define PSG_X_NOSTATS 0
-#endif
 // Tuning knobs (compile-time; tools/variants.sh builds alternatives for A/B runs).
 #ifndef PSG_RM
 #define PSG_RM 8
@@ -876,10 +863,10 @@ __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t
   for (int j = 0; j < RM; ++j) d[j] = static_cast<uint32_t>(tv[j + 1]) - static_cast<uint32_t>(tv[j]);
   // the window reductions first (they need no column offset): the column
   // loads' latency is hidden behind them
-  if (WM == WIN_FULL && !PSG_X_NOWIN) {
+  if (WM == WIN_FULL) {
 #pragma unroll
     for (int j = 0; j < RM; ++j) {
-      uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word(PSG_X_WINADDR ? (threadIdx.x & 31) + 32 * (j & 1) : cv[j]));
+      uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word(cv[j]));
       atomicAdd(r + WT_CNT, 1u);
       atomicAdd(r + WT_LO, d[j]);
       atomicMin(r + WT_MIN, d[j]);
@@ -889,7 +876,7 @@ __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
     const uint32_t rb = j >= bpos ? rb_after : rb_before;
-    atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + (PSG_X_CUBEADDR ? 4u * (threadIdx.x & 31) : ppo[j])), d[j]);
+    atomicAdd(reinterpret_cast<uint32_t*>(sm + rb + ppo[j]), d[j]);
   }
 }
 
@@ -915,7 +902,7 @@ __device__ __forceinline__ void run_fast_il(u64 (&tv)[RM + 1], uint32_t (&cv)[RM
     rn = rn == rows_end ? rows_off : rn;
     const uint32_t d = next_lo_il(tv, j, lane) - static_cast<uint32_t>(tv[j]);
     uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word(cv[j]));
-    if (WM == WIN_FULL && !PSG_X_NOWIN) {
+    if (WM == WIN_FULL) {
       atomicAdd(r + WT_CNT, 1u);
       atomicAdd(r + WT_LO, d);
       atomicMin(r + WT_MIN, d);
@@ -1664,7 +1651,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       uint32_t* rhw = cwide ? rhi : nullptr;  // high words (all zero in narrow chunks)
       const u64 ob = bo + static_cast<u64>(kb) * nnp;  // storage cell of the chunk's first row
       if (root_only && !cwide && n_iter_rows == G && (kcap == 0 || kcap == G)) {
-        if (kcap && !PSG_X_NOSTATS)
+        if (kcap)
           flush_fast<true>(p, rlo + s0 * nnp, nn, nnp, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
         else
           flush_fast<false>(p, rlo + s0 * nnp, nn, nnp, ob, ib + kb, wsx, wsqlo, wsqhi, lane);
