@@ -149,14 +149,17 @@ enum : uint32_t { WT_CNT = 0, WT_LO = 1, WT_MIN = 2, WT_MAX = 3, WT_PPO = 4, WT_
 // configs[1] (67 contexts per iteration) gives 2.97 / 2.21 / 2.00 shared
 // wavefronts per record access for 0 / 1 / 2, and k_trace_query measured
 // 18.36 / 17.60 / 17.40 ms (profiles/r2g_ab_wt_swizzle.txt).
-#ifndef PSG_IL
-#define PSG_IL 1
-#endif
-#ifndef PSG_WT_SWIZZLE
-#define PSG_WT_SWIZZLE (PSG_IL ? 0 : 2)
-#endif
-__host__ __device__ inline uint32_t wt_word(uint32_t c) {
-  return WT_STRIDE * (PSG_WT_SWIZZLE == 2 ? c + (c >> 5) : PSG_WT_SWIZZLE ? c + (c >> 3) : c);
+// IL = the interleaved lane layout (one-warp CTAs: the lanes of an
+// instruction hold consecutive events, so consecutive contexts, which the odd
+// stride alone puts in distinct banks); the run layout (wide CTAs) skips one
+// record slot every 32 contexts instead (model: 2.00 instead of 2.97
+// wavefronts per access at configs[1]; measured 17.40 vs 18.36 ms, r2g).
+template <bool IL>
+__host__ __device__ inline uint32_t wt_word_l(uint32_t c) {
+  return WT_STRIDE * (IL ? c : c + (c >> 5));
+}
+__host__ __device__ inline uint32_t wt_word(uint32_t c, bool il) {
+  return il ? wt_word_l<true>(c) : wt_word_l<false>(c);
 }
 
 // Cube row stride in cells: nn + 1 rounded up to even (pad columns).
@@ -190,7 +193,7 @@ struct warp_smem_layout {
     off_pref = take(8u * (nn + 1));  // generic rows and the gap row
     off_bwin = take(4u * (2 * G + 2));
     off_bts = take(8u * (2 * G + 2));
-    off_wtab = take(4u * WT_STRIDE * (n_ctx + (PSG_WT_SWIZZLE == 2 ? n_ctx / 32 : n_ctx / 8) + 1));
+    off_wtab = take(4u * WT_STRIDE * (n_ctx + n_ctx / 32 + 1));
     off_wsx = take(8u * nn);
     off_wsqlo = take(8u * nn);
     off_wsqhi = take(8u * nn);

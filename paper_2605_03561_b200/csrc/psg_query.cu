@@ -169,7 +169,7 @@ __device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_ab
   if (lane == 31) nf = ldg64(tr.ts + s_abs + 32 * RM);
 }
 
-// Interleaved lane layout (PSG_IL, pass 2): lane l holds events l, l + 32,
+// Interleaved lane layout (pass 2, one-warp CTAs): lane l holds events l, l + 32,
 // ..., l + 32 (RM - 1) of a block step, so the 32 lanes of one instruction
 // hold 32 CONSECUTIVE events.  Consecutive events of a trace are mostly
 // distinct contexts (sequential ids in a call sequence), so their window
@@ -179,16 +179,14 @@ __device__ __forceinline__ void load_step(const trace_view& tr, u64 r0, u64 s_ab
 // shared access (measured: conflict-free addressing takes k_trace_query from
 // 17.3 to 15.1 ms at configs[1], tools/ab_bench.sh).  Each load instruction
 // reads 32 consecutive timestamps (256 B) or ctx words (128 B): whole sectors.
-#ifndef PSG_IL
-#define PSG_IL 1
+#ifndef PSG_PIPE_UNCOND
+#define PSG_PIPE_UNCOND 1  // run layout: always load the next step (no branch)
 #endif
 // Rotating register pipeline (interleaved layout): as soon as event j of the
 // current block step is consumed, its registers receive event j of the next
 // step, so the loads of step s + 1 are in flight during step s without a
 // second register set or the copy between them.
-#ifndef PSG_ROT
 #define PSG_ROT 1
-#endif
 // the rotating pipeline's source: this lane's events of the step at lp
 struct rot_src {
   const unsigned long long* ts;  // tr.ts + lp + lane
@@ -550,15 +548,16 @@ namespace {
 enum : int { WIN_NONE = 0, WIN_FULL = 1, WIN_PART = 2, WIN_WIDE = 3 };
 
 struct warp_tables {
+  bool il;       // the records' slot map (wt_word): interleaved or run lane layout
   uint32_t* wt;  // n_ctx records of WT_STRIDE words (psg_internal.h)
   unsigned long long *gminb, *gmaxb;  // the trace's global w_min / w_max rows (durations >= 2^32)
   u64* carry;
   __device__ __forceinline__ u64 acc(uint32_t c) const {
-    const uint32_t* r = wt + wt_word(c) + WT_ACC;
+    const uint32_t* r = wt + wt_word(c, il) + WT_ACC;
     return static_cast<u64>(r[0]) | (static_cast<u64>(r[1]) << 32);
   }
   __device__ __forceinline__ void set_acc(uint32_t c, u64 v) const {
-    uint32_t* r = wt + wt_word(c) + WT_ACC;
+    uint32_t* r = wt + wt_word(c, il) + WT_ACC;
     r[0] = static_cast<uint32_t>(v);
     r[1] = static_cast<uint32_t>(v >> 32);
   }
@@ -567,7 +566,7 @@ struct warp_tables {
 // One window row of duration d for ctx c (frame::group_aggregate's
 // count/sum/min/max fold, order-free in integers).
 __device__ __forceinline__ void win_row32(const warp_tables& T, uint32_t c, uint32_t d) {
-  uint32_t* r = T.wt + wt_word(c);
+  uint32_t* r = T.wt + wt_word(c, T.il);
   atomicAdd(r + WT_CNT, 1u);
   atomicAdd(r + WT_LO, d);
   atomicMin(r + WT_MIN, d);
@@ -575,7 +574,7 @@ __device__ __forceinline__ void win_row32(const warp_tables& T, uint32_t c, uint
 }
 
 __device__ __forceinline__ void win_row64(const warp_tables& T, uint32_t c, u64 d) {
-  uint32_t* r = T.wt + wt_word(c);
+  uint32_t* r = T.wt + wt_word(c, T.il);
   atomicAdd(r + WT_CNT, 1u);
   sadd64(r + WT_ACC, r + WT_ACC + 1, d);
   if (d >> 32) {
@@ -866,7 +865,7 @@ __device__ __forceinline__ void run_fast(const u64 (&tv)[RM + 1], const uint32_t
   if (WM == WIN_FULL) {
 #pragma unroll
     for (int j = 0; j < RM; ++j) {
-      uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word(cv[j]));
+      uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word_l<false>(cv[j]));
       atomicAdd(r + WT_CNT, 1u);
       atomicAdd(r + WT_LO, d[j]);
       atomicMin(r + WT_MIN, d[j]);
@@ -901,7 +900,7 @@ __device__ __forceinline__ void run_fast_il(u64 (&tv)[RM + 1], uint32_t (&cv)[RM
     uint32_t rn = ra + row_bytes;  // the next iteration's ring row
     rn = rn == rows_end ? rows_off : rn;
     const uint32_t d = next_lo_il(tv, j, lane) - static_cast<uint32_t>(tv[j]);
-    uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word(cv[j]));
+    uint32_t* r = reinterpret_cast<uint32_t*>(sm + wt_off + 4u * wt_word_l<true>(cv[j]));
     if (WM == WIN_FULL) {
       atomicAdd(r + WT_CNT, 1u);
       atomicAdd(r + WT_LO, d);
@@ -1116,6 +1115,10 @@ template <bool WIN, bool CUBE, bool EXACT, bool ONE, bool GT = false>
 __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !EXACT) ? 16 : PSG_ONE_MINB) : PSG_WIDE_MINB)
     k_trace_query(query_params p) {
   static_assert(!GT || (!WIN && ONE), "global column tables: cube-only, one-warp CTAs");
+  // lane layout: interleaved for one-warp CTAs (long traces; bank-conflict
+  // free shared accesses), runs of RM events for wide CTAs (short traces: the
+  // interleaved layout measured 19 % slower there, C5 at 100k traces)
+  constexpr bool IL = ONE;
   extern __shared__ __align__(16) uint8_t smem[];
   // one-warp CTAs: the trace index and everything derived from it are
   // uniform across the CTA, so they live in uniform registers
@@ -1151,6 +1154,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   u64* wsqlo = reinterpret_cast<u64*>(wb + L.off_wsqlo);
   u64* wsqhi = reinterpret_cast<u64*>(wb + L.off_wsqhi);
   warp_tables T;
+  T.il = IL;
   T.wt = reinterpret_cast<uint32_t*>(wb + L.off_wtab);
   T.carry = reinterpret_cast<u64*>(wb + L.off_carry);
   // byte offsets from smem for the fast path
@@ -1173,7 +1177,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
     for (uint32_t j = lane; j < nn; j += 32) wsx[j] = wsqlo[j] = wsqhi[j] = 0;
   }
   for (uint32_t c = lane; c < (GT ? 0u : n_ctx); c += 32) {
-    uint32_t* r = T.wt + wt_word(c);
+    uint32_t* r = T.wt + wt_word(c, IL);
     r[WT_CNT] = r[WT_LO] = r[WT_MAX] = r[WT_NBIG] = 0u;
     r[WT_MIN] = 0xFFFFFFFFu;
     const int32_t sp = CUBE ? p.sub_pre[c] : -1;
@@ -1297,21 +1301,15 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   R.bts_out = kept ? bts_out : nullptr;
   R.nbd = nbd;
   __syncthreads();
-#if PSG_IL && PSG_ROT
-  u64 tv[RM + 1];  // the block step loaded ahead (rotating pipeline)
+  // register pipelines of the two lane layouts: the interleaved one (one-warp
+  // CTAs) rotates the step registers (tv / cv hold the step loaded ahead); the
+  // run layout (wide CTAs) loads the next step into a second register set
+  u64 tv[RM + 1];
   uint32_t cv[RM];
-  u64 pf_pos = ~0ull;
-#elif PSG_PIPE && PSG_IL
-  u64 pts[RM];
-  uint32_t pcx[RM];
-  u64 pnf = 0;
-  u64 pf_pos = ~0ull;
-#elif PSG_PIPE
+  u64 pf_pos = ~0ull;  // block start whose events sit in the pipeline registers
   ulonglong2 pts[RM / 2];
   uint4 pcx[RM / 4];
   u64 pnf = 0;
-  u64 pf_pos = ~0ull;  // block start whose events sit in pts/pcx/pnf
-#endif
 
   for (uint32_t c = c_lo;; ++c) {
     const uint32_t kb = c * G;
@@ -1367,8 +1365,8 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         prefetch_l2_lane0(p.tr.ts + s_abs + PSG_Q_PF_DIST * STEP_M, 8 * STEP_M, pf);
         prefetch_l2_lane0(p.tr.ctx + s_abs + PSG_Q_PF_DIST * STEP_M, 4 * STEP_M, pf);
       }
-#if PSG_IL && PSG_ROT
-      rot_src rs;
+      rot_src rs{};
+      if constexpr (IL) {
       {
         if (pf_pos != s_abs) {  // first step (or the pipeline did not run ahead): load now
           u64 nf = 0;
@@ -1385,30 +1383,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         rs.ts = reinterpret_cast<const unsigned long long*>(p.tr.ts + lp) + lane;
         rs.ctx = reinterpret_cast<const unsigned int*>(p.tr.ctx + lp) + lane;
       }
-#else
-      u64 tv[RM + 1];
-      uint32_t cv[RM];
-      rot_src rs{};
-#endif
-#if PSG_IL && PSG_ROT
-#elif PSG_PIPE && PSG_IL
-      // software pipeline (interleaved layout): this block step's events were
-      // loaded while the previous one was processed; load the next one now
-      if (pf_pos != s_abs) load_step_il(p.tr, s_abs, lane, pts, pcx, pnf);
-#pragma unroll
-      for (int q = 0; q < RM; ++q) {
-        tv[q] = pts[q];
-        cv[q] = pcx[q];
-      }
-      tv[RM] = pnf;  // lane 31: the event after the step
-      {
-        const bool more = lim < n_t && (PSG_PIPE_CROSS || lim < E1);
-        const u64 nxt = (b + lim) & ~static_cast<u64>(SOFF);
-        const u64 lp = more ? nxt : s_abs;
-        pf_pos = more ? nxt : ~0ull;
-        load_step_il(p.tr, lp, lane, pts, pcx, pnf);
-      }
-#elif PSG_PIPE
+      } else {
       // software pipeline: this block step's events were loaded into registers
       // while the previous one was processed; load the next one now
       if (pf_pos != s_abs) {
@@ -1431,9 +1406,6 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         if (lane == 31) nf = pnf;
         tv[RM] = nf;
       }
-#ifndef PSG_PIPE_UNCOND
-#define PSG_PIPE_UNCOND 1
-#endif
       if (PSG_PIPE_UNCOND) {
         // always load (this step again past the trace end: no branch, so the
         // loaded registers need no copies to join the paths)
@@ -1448,29 +1420,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       } else {
         pf_pos = ~0ull;
       }
-#else
-      {
-        const ulonglong2* tsrc = reinterpret_cast<const ulonglong2*>(p.tr.ts + r0);
-#pragma unroll
-        for (int q = 0; q < RM / 2; ++q) {
-          const ulonglong2 v = __ldg(tsrc + q);
-          tv[2 * q] = v.x;
-          tv[2 * q + 1] = v.y;
-        }
-        const uint4* csrc = reinterpret_cast<const uint4*>(p.tr.ctx + r0);
-#pragma unroll
-        for (int q = 0; q < RM / 4; ++q) {
-          const uint4 v = __ldg(csrc + q);
-          cv[4 * q] = v.x;
-          cv[4 * q + 1] = v.y;
-          cv[4 * q + 2] = v.z;
-          cv[4 * q + 3] = v.w;
-        }
-        u64 nf = __shfl_down_sync(FULL, tv[0], 1);
-        if (lane == 31) nf = ldg64(p.tr.ts + s_abs + STEP_M);
-        tv[RM] = nf;
       }
-#endif
       const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
 
       // window class of this block step (warp-uniform)
@@ -1480,7 +1430,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         if (all) {
           first = __shfl_sync(FULL, tv[0], 0);
           after = __shfl_sync(FULL, tv[RM], 31);
-        } else if (PSG_IL) {
+        } else if (IL) {
           // event i sits in lane i % 32, register i / 32; lo <= SOFF < 32
           u64 a = tv[0];
           {
@@ -1518,7 +1468,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           if (wspan + span >= kSpan32) {  // fold the pending 32-bit sums
             __syncwarp();
             for (uint32_t x = lane; x < n_ctx; x += 32) {
-              uint32_t* r = T.wt + wt_word(x);
+              uint32_t* r = T.wt + wt_word(x, IL);
               T.set_acc(x, T.acc(x) + r[WT_LO]);
               r[WT_LO] = 0;
             }
@@ -1531,7 +1481,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       }
 
       bool done = false;
-#if PSG_IL
+      if constexpr (IL) {
       if (CUBE && kept && all && !cwide && (wm == WIN_FULL || wm == WIN_NONE)) {
         // boundaries of this block step: lane j <= 2G holds boundary kb + j;
         // fast path: at most one per group of 32 events, and every iteration
@@ -1564,7 +1514,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           done = true;
         }
       }
-#else
+      } else {
       if (CUBE && kept && all && !cwide && (wm == WIN_FULL || wm == WIN_NONE)) {
         // boundaries of this block step: lane j <= 2G holds boundary kb + j;
         // H marks the lanes whose run holds one (fast path: at most one per
@@ -1591,7 +1541,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
 #pragma unroll
           for (int j = 0; j < RM; ++j)
             ppo[j] = GT ? __ldg(p.ppo_g + cv[j])
-                        : *reinterpret_cast<const uint32_t*>(smem + wt_off + 4u * (wt_word(cv[j]) + WT_PPO));
+                        : *reinterpret_cast<const uint32_t*>(smem + wt_off + 4u * (wt_word_l<false>(cv[j]) + WT_PPO));
           if (wm == WIN_FULL)
             run_fast<WIN_FULL>(tv, cv, smem, wt_off, bpos, rb0, rb1, ppo);
           else
@@ -1600,7 +1550,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           done = true;
         }
       }
-#endif
+      }
       if (!done) {
         run_state st;
         st.k = -1;
@@ -1612,7 +1562,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         if (CUBE) {
           // iteration of this lane's first event: boundaries of the window at or before it
           uint32_t cnt = 0;
-          const uint32_t lp3 = R.base3 + static_cast<uint32_t>(PSG_IL ? lane : R.lb);
+          const uint32_t lp3 = R.base3 + static_cast<uint32_t>(IL ? lane : R.lb);
           for (uint32_t j = 0; j <= R2; ++j) cnt += bwin[j] <= lp3 ? 1u : 0u;
           st.cnt = cnt;
           // a boundary on the lane's first event is counted here, not crossed
@@ -1625,17 +1575,17 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           st.rowb = st.slot * nnp;
           st.cube_ok = st.k < R.iters;
         }
-#if PSG_IL
+        if constexpr (IL) {
         if (cwide)
           run_block_il<WIN, CUBE, true>(wm, tv, cv, lane, R, st, T, rs);
         else
           run_block_il<WIN, CUBE, false>(wm, tv, cv, lane, R, st, T, rs);
-#else
+        } else {
         if (cwide)
           run_block<WIN, CUBE, true>(wm, tv, cv, R, st, T);
         else
           run_block<WIN, CUBE, false>(wm, tv, cv, R, st, T);
-#endif
+        }
       }
       pos = lim;
     }
@@ -1769,7 +1719,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
     const uint32_t c_ctx = static_cast<uint32_t>(T.carry[2]);
     const u64 c_d = T.carry[1];
     for (uint32_t c = lane; c < n_ctx; c += 32) {
-      const u64 sum = T.acc(c) + T.wt[wt_word(c) + WT_LO];
+      const u64 sum = T.acc(c) + T.wt[wt_word(c, IL) + WT_LO];
       tmp[s_cct_pre[c]] = sum + ((c_has && c == c_ctx) ? c_d : 0ull);
     }
     __syncwarp();
@@ -1781,7 +1731,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       // one unit of a split trace: merge into the rows k_split_init prepared
       // (the min / max of durations >= 2^32 are already in them)
       for (uint32_t c = lane; c < n_ctx; c += 32) {
-        const uint32_t* r = T.wt + wt_word(c);
+        const uint32_t* r = T.wt + wt_word(c, IL);
         const int pr = s_cct_pre[c], sz = s_cct_size[c];
         const u64 cnt = r[WT_CNT], nbig = r[WT_NBIG];
         unsigned long long* wc = reinterpret_cast<unsigned long long*>(p.w_cnt) + base + c;
@@ -1804,7 +1754,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       }
     }
     for (uint32_t c = lane; c < (split ? 0u : n_ctx); c += 32) {
-      const uint32_t* r = T.wt + wt_word(c);
+      const uint32_t* r = T.wt + wt_word(c, IL);
       const int pr = s_cct_pre[c], sz = s_cct_size[c];
       const u64 cnt = r[WT_CNT], nbig = r[WT_NBIG];
       const u64 sum = T.acc(c) + r[WT_LO];

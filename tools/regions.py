@@ -33,12 +33,14 @@ def find(s, start=0):
 
 
 marks = [("run_events (general path)", find("__device__ __forceinline__ void run_events")),
+         ("run_events_il (general path)", find("__device__ __forceinline__ void run_events_il")),
          ("run_block", find("__device__ __forceinline__ void run_block")),
          ("helpers", find("__device__ __forceinline__ u64 cell64")),
-         ("run_fast", find("__device__ __forceinline__ void run_fast")),
+         ("run_fast", find("__device__ __forceinline__ void run_fast(")),
+         ("run_fast_il", find("__device__ __forceinline__ void run_fast_il")),
          ("flush_fast", find("__device__ __forceinline__ void flush_fast")),
          ("prologue", find("k_trace_query(query_params p) {")),
-         ("chunk head", find("for (uint32_t c = 0;; ++c) {")),
+         ("chunk head", find("for (uint32_t c = c_lo;; ++c) {")),
          ("step: loads + window class", find("while (pos < E1) {")),
          ("step: fast-path setup", find("if (CUBE && kept && all && !cwide")),
          ("step: general setup", find("if (!done) {")),
