@@ -1740,6 +1740,8 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     p.L = L;
     p.cta_bytes = cta_table_bytes(c->n_ctx, nn, W, one);
     uint32_t smem = p.cta_bytes + W * L.bytes;
+    if (const char* e = std::getenv("PSG_ONE_MIN_SMEM"); e && one)  // A/B: cap resident CTAs per SM
+      smem = std::max<uint32_t>(smem, static_cast<uint32_t>(std::strtoul(e, nullptr, 10)));
     PSG_CUDA(cudaEventRecord(c->ev[1], s));
     if (units) {
       p.units = c->d_units.p;
