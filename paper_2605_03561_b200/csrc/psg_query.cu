@@ -1241,19 +1241,19 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   // traces: the unit's nominal event range snapped to chunk starts; others:
   // the range itself)
   uint32_t c_lo = 0, c_stop = (iters + G - 1) / G;  // chunks [c_lo, c_stop)
-  u64 pos0 = 0, end = n_t;
+  uint32_t pos0 = 0, end = static_cast<uint32_t>(n_t);  // relative event indices are 32-bit (finish_load)
   if (split) {
     if (CUBE && kept) {
       const uint32_t n_chunks = (iters + G - 1) / G;
       c_lo = first_chunk_at(bt, n_chunks, n_t, ue0, lane);
       const uint32_t c_hi = first_chunk_at(bt, n_chunks, n_t, ue1, lane);
-      pos0 = c_lo == 0 ? 0ull : static_cast<u64>(__ldg(bt + c_lo * G));
-      end = c_hi >= n_chunks ? n_t : static_cast<u64>(__ldg(bt + c_hi * G));
+      pos0 = c_lo == 0 ? 0u : __ldg(bt + c_lo * G);
+      end = c_hi >= n_chunks ? static_cast<uint32_t>(n_t) : __ldg(bt + c_hi * G);
       c_stop = c_hi;
       if (c_lo >= c_hi) active = false;  // no chunk starts in this unit's range
     } else {
-      pos0 = min(ue0, n_t);
-      end = min(ue1, n_t);
+      pos0 = static_cast<uint32_t>(min(ue0, n_t));
+      end = static_cast<uint32_t>(min(ue1, n_t));
       if (pos0 >= end) active = false;
     }
     if (!active) return;  // nothing to do; no CTA barrier follows (one-warp CTAs)
@@ -1276,7 +1276,11 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
     nn_idx = have2 ? __ldg(bt + kb0 + G + lane) : static_cast<uint32_t>(n_t);
   }
   const u64 t0 = p.t0, t1w = (p.clamp_tend && tend < p.t1) ? tend : p.t1;
-  u64 pos = pos0;  // next unprocessed event, relative to b
+  uint32_t pos = pos0;  // next unprocessed event, relative to b
+  // block steps start on multiples of SA events of the whole stream: relative
+  // to the aligned trace base b0 = b - d0 every step position is 32-bit
+  const u64 b0 = b & ~static_cast<u64>(SOFF);
+  const uint32_t d0 = static_cast<uint32_t>(b - b0), n32 = static_cast<uint32_t>(n_t);
   u64 wspan = 0;  // time span added to the 32-bit pending window sums since the last fold
   uint32_t mybw = 0xFFFFFFFFu;  // lane j <= 2G: relative event index of boundary kb + j
 
@@ -1313,7 +1317,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
 
   for (uint32_t c = c_lo;; ++c) {
     const uint32_t kb = c * G;
-    u64 E1 = end, E2 = end;
+    uint32_t E1 = end, E2 = end;
     bool cwide = false;
     if (CUBE && kept) {
       // boundary window of this chunk (prefetched during the previous one)
@@ -1330,8 +1334,8 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       const bool have2 = lane <= static_cast<int>(R2) && k + G < nbd;
       nn_idx = have2 ? __ldg(bt + k + G) : static_cast<uint32_t>(n_t);
       __syncwarp();
-      E1 = min(static_cast<u64>(bwin[G] - SOFF), end);
-      E2 = min(static_cast<u64>(bwin[R2] - SOFF), end);
+      E1 = min(bwin[G] - SOFF, end);
+      E2 = min(bwin[R2] - SOFF, end);
       // iteration spans of the ring (and the gap in chunk 0) decide 32- vs
       // 64-bit cells (exact mode; the optimistic mode runs 32-bit throughout)
       if (EXACT) {
@@ -1348,20 +1352,23 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
 
     // ---- phase 1: consume events [pos, E1), possibly running ahead to E2 ----
     while (pos < E1) {
-      const u64 s_abs = (b + pos) & ~static_cast<u64>(SOFF);
-      const int64_t base = static_cast<int64_t>(s_abs) - static_cast<int64_t>(b);  // >= -SOFF
-      const u64 lim = min(static_cast<u64>(base + STEP_M), E2);
-      R.base3 = static_cast<uint32_t>(base + SOFF);
-      R.lo = static_cast<int>(static_cast<int64_t>(pos) - base);
-      R.hi = static_cast<int>(static_cast<int64_t>(lim) - base);
-      const int64_t lr = static_cast<int64_t>(n_t) - 1 - base;
-      R.last_li = lr < STEP_M ? static_cast<int>(lr) : -1;
+      // step start sr (relative to b0); its base relative to b is sr - d0
+      // >= -SOFF, kept as base3 = base + SOFF >= 0 so all of it is unsigned
+      const uint32_t sr = (pos + d0) & ~static_cast<uint32_t>(SOFF);
+      const uint32_t base3 = sr - d0 + SOFF;
+      const uint32_t lim = min(base3 - SOFF + STEP_M, E2);
+      const u64 s_abs = b0 + sr;
+      R.base3 = base3;
+      R.lo = static_cast<int>(pos + SOFF - base3);
+      R.hi = static_cast<int>(lim + SOFF - base3);
+      const uint32_t lr = n32 + SOFF - 1 - base3;  // the trace's last event, local index
+      R.last_li = lr < static_cast<uint32_t>(STEP_M) ? static_cast<int>(lr) : -1;
       const u64 r0 = s_abs + static_cast<u64>(R.lb);
 #ifndef PSG_Q_PF_DIST
 #define PSG_Q_PF_DIST 3  // block steps of L2 prefetch run-ahead (0: none; 0 costs +18 %)
 #endif
       if (PSG_Q_PF_DIST > 0) {
-        const bool pf = lane == 0 && s_abs + (PSG_Q_PF_DIST + 1) * STEP_M <= e;
+        const bool pf = lane == 0 && static_cast<u64>(sr) + (PSG_Q_PF_DIST + 1) * STEP_M <= static_cast<u64>(n32) + d0;
         prefetch_l2_lane0(p.tr.ts + s_abs + PSG_Q_PF_DIST * STEP_M, 8 * STEP_M, pf);
         prefetch_l2_lane0(p.tr.ctx + s_abs + PSG_Q_PF_DIST * STEP_M, 4 * STEP_M, pf);
       }
@@ -1376,8 +1383,8 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           for (int q = 0; q < RM; ++q) tv[q] = t8[q];
           tv[RM] = nf;
         }
-        const bool more = lim < n_t && (PSG_PIPE_CROSS || lim < E1);
-        const u64 nxt = (b + lim) & ~static_cast<u64>(SOFF);
+        const bool more = lim < n32 && (PSG_PIPE_CROSS || lim < E1);
+        const u64 nxt = b0 + ((lim + d0) & ~static_cast<uint32_t>(SOFF));
         const u64 lp = more ? nxt : s_abs;
         pf_pos = more ? nxt : ~0ull;
         rs.ts = reinterpret_cast<const unsigned long long*>(p.tr.ts + lp) + lane;
@@ -1409,13 +1416,13 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
       if (PSG_PIPE_UNCOND) {
         // always load (this step again past the trace end: no branch, so the
         // loaded registers need no copies to join the paths)
-        const bool more = lim < n_t && (PSG_PIPE_CROSS || lim < E1);
-        const u64 nxt = (b + lim) & ~static_cast<u64>(SOFF);
+        const bool more = lim < n32 && (PSG_PIPE_CROSS || lim < E1);
+        const u64 nxt = b0 + ((lim + d0) & ~static_cast<uint32_t>(SOFF));
         const u64 lp = more ? nxt : s_abs;
         pf_pos = more ? nxt : ~0ull;
         load_step(p.tr, lp + static_cast<u64>(R.lb), lp, lane, pts, pcx, pnf);
-      } else if (lim < n_t && (PSG_PIPE_CROSS || lim < E1)) {
-        pf_pos = (b + lim) & ~static_cast<u64>(SOFF);
+      } else if (lim < n32 && (PSG_PIPE_CROSS || lim < E1)) {
+        pf_pos = b0 + ((lim + d0) & ~static_cast<uint32_t>(SOFF));
         load_step(p.tr, pf_pos + static_cast<u64>(R.lb), pf_pos, lane, pts, pcx, pnf);
       } else {
         pf_pos = ~0ull;
@@ -1486,7 +1493,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         // boundaries of this block step: lane j <= 2G holds boundary kb + j;
         // fast path: at most one per group of 32 events, and every iteration
         // of the step is stored
-        const uint32_t base32 = static_cast<uint32_t>(base);  // >= 0 here (lo == 0)
+        const uint32_t base32 = base3 - SOFF;  // >= 0 here (lo == 0)
         const uint32_t rel = mybw - base32;
         const bool inb = mybw >= base32 && rel < static_cast<uint32_t>(STEP_M);
         const uint32_t g = rel >> 5;
@@ -1519,7 +1526,7 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
         // boundaries of this block step: lane j <= 2G holds boundary kb + j;
         // H marks the lanes whose run holds one (fast path: at most one per
         // run, and every iteration of the step is stored)
-        const uint32_t base32 = static_cast<uint32_t>(base);  // >= 0 here (lo == 0)
+        const uint32_t base32 = base3 - SOFF;  // >= 0 here (lo == 0)
         const uint32_t rel = mybw - base32;
         const bool inb = mybw >= base32 && rel < static_cast<uint32_t>(STEP_M);
         const uint32_t H = __reduce_or_sync(FULL, inb ? 1u << (rel / RM) : 0u);
