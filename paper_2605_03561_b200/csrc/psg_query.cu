@@ -357,11 +357,15 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
     }
     if (s + STEP < e) load(r0 + STEP);
     // events of this trace in the lane's run: local indices [lo, hi) of [0, RR)
-    const int64_t lo64 = static_cast<int64_t>(b) - static_cast<int64_t>(r0);
-    const int64_t hi64 = static_cast<int64_t>(e) - static_cast<int64_t>(r0);
-    const int lo = lo64 < 0 ? 0 : static_cast<int>(lo64 > RR ? RR : lo64);
-    const int hi = hi64 < 0 ? 0 : static_cast<int>(hi64 > RR ? RR : hi64);
-    const uint32_t real = run_mask(lo, hi);
+    // (interior block steps, warp-uniform: all of them)
+    uint32_t real = FULL;
+    if (s < b || s + STEP > e) {
+      const int64_t lo64 = static_cast<int64_t>(b) - static_cast<int64_t>(r0);
+      const int64_t hi64 = static_cast<int64_t>(e) - static_cast<int64_t>(r0);
+      const int lo = lo64 < 0 ? 0 : static_cast<int>(lo64 > RR ? RR : lo64);
+      const int hi = hi64 < 0 ? 0 : static_cast<int>(hi64 > RR ? RR : hi64);
+      real = run_mask(lo, hi);
+    }
     uint32_t inm = 0;
     if (C8) {
       // preorder bytes: in the subtree iff (b - lo) mod 256 < size, four
