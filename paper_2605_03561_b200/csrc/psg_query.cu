@@ -355,7 +355,6 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
       w[4 * q + 2] = nxt[q].z;
       w[4 * q + 3] = nxt[q].w;
     }
-    if (s + STEP < e) load(r0 + STEP);
     // events of this trace in the lane's run: local indices [lo, hi) of [0, RR)
     // (interior block steps, warp-uniform: all of them)
     uint32_t real = FULL;
@@ -389,6 +388,9 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
       }
     }
     inm &= real;
+    // the next block step's words load into the registers this one's just
+    // left (no copy between register sets; in flight during the rest)
+    if (s + STEP < e) load(r0 + STEP);
     uint32_t up = __shfl_up_sync(FULL, inm >> (RR - 1), 1);
     if (lane == 0) up = prev_in;
     const uint32_t candm = inm & ~((inm << 1) | (up & 1u));
