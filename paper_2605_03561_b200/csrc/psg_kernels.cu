@@ -502,7 +502,8 @@ void launch_cube_layout(const uint32_t* iter_count, uint32_t n, uint32_t nn, uin
 // Stage 1: one CTA per tile of kept traces.  Threads cover (sub-row j, node
 // n) so that consecutive threads read consecutive cells of a trace's row
 // (coalesced); each thread sums its node over the tile's traces j, j + S, ...
-// in order, and sub-row partials are added in fixed order: deterministic.
+// eight at a time (eight independent loads in flight, then added in trace
+// order), and sub-row partials are added in fixed order: deterministic.
 __global__ void __launch_bounds__(256) k_within_partial(const double* within_cv,
                                                         const uint8_t* within_ok, uint32_t n_kept,
                                                         uint32_t nn, uint32_t per_tile,
@@ -516,11 +517,27 @@ __global__ void __launch_bounds__(256) k_within_partial(const double* within_cv,
   for (uint32_t nb = 0; nb < nn; nb += ne) {
     const uint32_t n = nb + nl;
     double sm = 0.0, bad = 0.0;
-    if (j < S && n < nn)
-      for (uint32_t t = t0 + j; t < t1; t += S) {
+    if (j < S && n < nn) {
+      uint32_t t = t0 + j;
+      for (; t + 7 * S < t1; t += 8 * S) {
+        double v[8];
+        uint8_t ok[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] = __ldg(within_cv + static_cast<size_t>(t + u * S) * nn + n);
+          ok[u] = __ldg(within_ok + static_cast<size_t>(t + u * S) * nn + n);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          sm += v[u];
+          bad += ok[u] ? 0.0 : 1.0;
+        }
+      }
+      for (; t < t1; t += S) {
         sm += within_cv[static_cast<size_t>(t) * nn + n];
         bad += within_ok[static_cast<size_t>(t) * nn + n] ? 0.0 : 1.0;
       }
+    }
     s_sum[threadIdx.x] = sm;
     s_bad[threadIdx.x] = bad;
     __syncthreads();
@@ -536,18 +553,27 @@ __global__ void __launch_bounds__(256) k_within_partial(const double* within_cv,
   }
 }
 
-// Stage 2: per node, the tile partials in tile order.
+// Stage 2: per node (one warp), the tile partials in a fixed order: lane l
+// sums tiles l, l + 32, ... in order, then a fixed butterfly.
 __global__ void k_within_finish(const double* part, uint32_t tiles, uint32_t nn, double* out_sum,
                                 double* out_bad) {
-  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (n >= nn) return;
   double sm = 0.0, bad = 0.0;
-  for (uint32_t b = 0; b < tiles; ++b) {
+  for (uint32_t b = lane; b < tiles; b += 32) {
     sm += part[(static_cast<size_t>(b) * 2) * nn + n];
     bad += part[(static_cast<size_t>(b) * 2 + 1) * nn + n];
   }
-  out_sum[n] = sm;
-  out_bad[n] = bad;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    sm += __shfl_xor_sync(0xFFFFFFFFu, sm, d);
+    bad += __shfl_xor_sync(0xFFFFFFFFu, bad, d);
+  }
+  if (lane == 0) {
+    out_sum[n] = sm;
+    out_bad[n] = bad;
+  }
 }
 
 // One CTA per node: the per-iteration terms are summed with a fixed-order
@@ -618,7 +644,7 @@ void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long 
     const uint32_t per_tile = (std::max(1u, n_kept_local) + tiles - 1) / tiles;
     double* part = wbad + nn;
     k_within_partial<<<tiles, 256, 0, s>>>(within_cv, within_ok, n_kept_local, nn, per_tile, part, qs);
-    k_within_finish<<<(nn + 127) / 128, 128, 0, s>>>(part, tiles, nn, wsum, wbad);
+    k_within_finish<<<(nn + 7) / 8, 256, 0, s>>>(part, tiles, nn, wsum, wbad);
     count_launch(2);
     PSG_CUDA(cudaGetLastError());
   }
@@ -748,15 +774,24 @@ __global__ void __launch_bounds__(256) k_site_acc(const uint64_t* w_incl, uint32
   }
 }
 
+// Balance ratio per site, then the worst (smallest ratio, first on ties:
+// workflows.cpp:478-495): one thread per site, a fixed-order argmin.
 __global__ void k_pick_worst(const unsigned long long* acc, uint32_t n_sites, uint32_t n_ranks,
                              uint32_t* worst, double* ratio) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __shared__ double s_r[1024];
+  for (uint32_t s = threadIdx.x; s < n_sites; s += blockDim.x) {
+    const double mx = static_cast<double>(acc[n_sites + s]) / 1e9;
+    const double sum = static_cast<double>(acc[s]) / 1e9;
+    const double r = mx == 0.0 ? 1.0 : sum / static_cast<double>(n_ranks) / mx;
+    ratio[s] = r;
+    if (s < 1024) s_r[s] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   uint32_t w = 0;
-  for (uint32_t s = 0; s < n_sites; ++s) {
-    double mx = static_cast<double>(acc[n_sites + s]) / 1e9;
-    double sum = static_cast<double>(acc[s]) / 1e9;
-    ratio[s] = mx == 0.0 ? 1.0 : sum / static_cast<double>(n_ranks) / mx;
-    if (ratio[s] < ratio[w]) w = s;
+  for (uint32_t s = 1; s < n_sites; ++s) {
+    const double r = s < 1024 ? s_r[s] : ratio[s];
+    if (r < (w < 1024 ? s_r[w] : ratio[w])) w = s;
   }
   *worst = w;
 }
@@ -784,7 +819,7 @@ void launch_outliers(const uint64_t* w_incl, uint32_t n_traces, uint32_t n_ctx,
       k_site_acc<<<dim3(gx, n_sites), 256, 0, s>>>(w_incl, n_traces, n_ctx, site_ctx, n_sites, site_acc);
     }
   } else if (phase == 1) {
-    k_pick_worst<<<1, 32, 0, s>>>(site_acc, n_sites, n_traces /* global rank count */, worst,
+    k_pick_worst<<<1, 256, 0, s>>>(site_acc, n_sites, n_traces /* global rank count */, worst,
                                   site_ratio);
   } else {
     if (n_traces)
