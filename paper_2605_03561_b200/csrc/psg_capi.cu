@@ -1772,7 +1772,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       const size_t plane = static_cast<size_t>(k_cap) * nn;
       launch_cross_stats(c->cube_incl.p, c->cube32, c->kept_bo.p, n, nn, row_stride(nn), k_cap, c->x_acc.p,
                          c->x_acc.p + plane, c->x_acc.p + 2 * plane, qs, s);
-      double* no = c->node_out.ensure(static_cast<size_t>(nn) * (10 + 2 * 148) + 1);  // + tile partials
+      double* no = c->node_out.ensure(static_cast<size_t>(nn) * (10 + 2 * kWithinTiles) + 1);  // + tile partials
       // within-rank partial sums per node, then cross-GPU sums of everything
       launch_stats_finalize(nullptr, nullptr, nullptr, k_cap, k_cap, nn, n, c->within_cv.p,
                             c->within_ok.p, n, no, qs, s);

@@ -400,6 +400,8 @@ void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, 
                         const unsigned long long* qs, cudaStream_t s, const cross_part& part = {});
 // plane_k: the K of the accumulator layout (x_sq limbs at plane_k * nn strides);
 // with qs set, K / n_kept (global) / n_kept_local come from the status block.
+// tiles of the within-CV mean's first stage (node_out holds their partials)
+constexpr uint32_t kWithinTiles = 592;
 void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,
                            const unsigned long long* x_sq, uint32_t K, uint32_t plane_k, uint32_t nn,
                            uint32_t n_kept, const double* within_cv, const uint8_t* within_ok,

@@ -640,7 +640,7 @@ void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long 
   double* wbad = wsum + nn;
   if (within_cv) {
     // tile partials live after the bad counts in node_out (sized by the caller)
-    const uint32_t tiles = std::max(1u, std::min(148u, (n_kept_local + 63) / 64));
+    const uint32_t tiles = std::max(1u, std::min(kWithinTiles, (n_kept_local + 31) / 32));
     const uint32_t per_tile = (std::max(1u, n_kept_local) + tiles - 1) / tiles;
     double* part = wbad + nn;
     k_within_partial<<<tiles, 256, 0, s>>>(within_cv, within_ok, n_kept_local, nn, per_tile, part, qs);
