@@ -16,7 +16,6 @@
 //                   reference's own fp64 arithmetic and order (gap_cv,
 //                   itermodel.cpp:27-41), and the candidate with the most
 //                   covered time (ties: the smallest id)
-#include <cub/cub.cuh>
 
 #include <cstdint>
 #include <vector>
@@ -150,10 +149,8 @@ uint32_t launch_suggest_anchor(const uint64_t* ts, const uint32_t* ctx, uint64_t
   count_launch();
   PSG_CUDA(cudaGetLastError());
   {  // entry offsets: exclusive scan of the per-event counts
-    size_t tb = 0;
-    PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ent_cnt, ent_off, static_cast<int>(n), s));
-    void* temp = sc.get<uint8_t>(tb);
-    PSG_CUDA(cub::DeviceScan::ExclusiveSum(temp, tb, ent_cnt, ent_off, static_cast<int>(n), s));
+    const size_t tb = exclusive_sum_scratch_bytes(n);
+    exclusive_sum_u64(ent_cnt, ent_off, n, sc.get<uint8_t>(tb), tb, s);
   }
   uint64_t last_off = 0, last_cnt = 0;
   PSG_CUDA(cudaMemcpyAsync(&last_off, ent_off + n - 1, 8, cudaMemcpyDeviceToHost, s));
@@ -169,12 +166,9 @@ uint32_t launch_suggest_anchor(const uint64_t* ts, const uint32_t* ctx, uint64_t
   PSG_CUDA(cudaGetLastError());
   int bits = 1;
   while ((1ull << bits) < n_ctx && bits < 32) ++bits;
-  size_t sb = 0;
-  PSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb, keys, keys2, vals, vals2,
-                                           static_cast<int>(total), 0, bits, s));
-  void* stemp = sc.get<uint8_t>(sb);
-  PSG_CUDA(cub::DeviceRadixSort::SortPairs(stemp, sb, keys, keys2, vals, vals2,
-                                           static_cast<int>(total), 0, bits, s));
+  // stable: each ctx's entries keep their event order
+  const size_t sb = sort_pairs_scratch_bytes<uint32_t, uint64_t>(total);
+  sort_pairs<uint32_t, uint64_t>(keys, keys2, vals, vals2, total, 0, bits, false, sc.get<uint8_t>(sb), sb, s);
   k_anchor_pick<<<1, 32, 0, s>>>(parent, n_ctx, ctx_cnt, excl, vals2, min_iters, cv_max, best);
   count_launch();
   PSG_CUDA(cudaGetLastError());

@@ -12,7 +12,6 @@
 //     fold the block sums left (frame.cpp:599-647): reduce_sum equals the last
 //     element of cumulative_sum bit for bit.
 // All column pointers are device pointers; results stay on the device.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -115,14 +114,14 @@ void argsort(const psg_col* keys, uint32_t n_keys, const uint8_t* ascending, uin
   u64* kin = sc.get<u64>(n);
   u64* kout = sc.get<u64>(n);
   uint64_t* pout = sc.get<uint64_t>(n);
-  size_t tb = 0;
-  PSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, perm, pout, static_cast<int64_t>(n), 0, 64, s));
+  const size_t tb = sort_pairs_scratch_bytes<uint64_t, uint64_t>(n);
   void* tmp = sc.get<uint8_t>(tb);
   for (uint32_t k = n_keys; k-- > 0;) {
     check_dtype(keys[k].dtype);
     k_gather_key<<<blocks(n), 256, 0, s>>>(keys[k].data, keys[k].dtype, ascending && !ascending[k], perm, n, kin);
     count_launch();
-    PSG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, perm, pout, static_cast<int64_t>(n), 0, 64, s));
+    sort_pairs<uint64_t, uint64_t>(reinterpret_cast<const uint64_t*>(kin), reinterpret_cast<uint64_t*>(kout),
+                                   perm, pout, n, 0, 64, false, tmp, tb, s);
     PSG_CUDA(cudaMemcpyAsync(perm, pout, 8 * n, cudaMemcpyDeviceToDevice, s));
   }
   PSG_CUDA(cudaGetLastError());
@@ -146,10 +145,8 @@ __global__ void k_scatter_starts(const uint64_t* flag, const uint64_t* pos, uint
 
 // exclusive scan of n u64 flags into pos; returns the total
 uint64_t scan_count(const uint64_t* flag, uint64_t n, uint64_t* pos, cudaStream_t s, scratch& sc) {
-  size_t tb = 0;
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, static_cast<int64_t>(n), s));
-  void* tmp = sc.get<uint8_t>(tb);
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, static_cast<int64_t>(n), s));
+  const size_t tb = exclusive_sum_scratch_bytes(n);
+  exclusive_sum_u64(flag, pos, n, sc.get<uint8_t>(tb), tb, s);
   uint64_t last_pos = 0, last_flag = 0;
   PSG_CUDA(cudaMemcpyAsync(&last_pos, pos + n - 1, 8, cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaMemcpyAsync(&last_flag, flag + n - 1, 8, cudaMemcpyDeviceToHost, s));

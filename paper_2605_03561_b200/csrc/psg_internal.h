@@ -400,6 +400,42 @@ void launch_cross_stats(const void* incl, bool cube32, const uint64_t* kept_bo, 
                         const unsigned long long* qs, cudaStream_t s, const cross_part& part = {});
 // plane_k: the K of the accumulator layout (x_sq limbs at plane_k * nn strides);
 // with qs set, K / n_kept (global) / n_kept_local come from the status block.
+#ifdef __CUDACC__
+// Fixed-order CTA reduction (warp butterflies, then the warps' results in
+// warp order; every thread receives the result): deterministic for a fixed
+// block size.  s_warp holds 32 values; the block is a multiple of 32 threads.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T* s_warp) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = op(v, __shfl_xor_sync(0xFFFFFFFFu, v, d));
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) s_warp[w] = v;
+  __syncthreads();
+  T r = s_warp[0];
+  for (int i = 1; i < nw; ++i) r = op(r, s_warp[i]);
+  __syncthreads();  // s_warp is free for the next reduction
+  return r;
+}
+struct op_add {
+  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
+};
+struct op_max {
+  template <typename T> __device__ __forceinline__ T operator()(T a, T b) const { return a > b ? a : b; }
+};
+
+#endif  // __CUDACC__
+
+// ---- device-wide primitives (psg_sort.cu, hand-written) -------------------
+size_t exclusive_sum_scratch_bytes(uint64_t n);
+void exclusive_sum_u64(const uint64_t* in, uint64_t* out, uint64_t n, void* scratch, size_t scratch_bytes,
+                       cudaStream_t s);
+template <typename K, typename V>
+size_t sort_pairs_scratch_bytes(uint64_t n);
+// stable LSD radix sort of (key, value) pairs over key bits [begin_bit, end_bit)
+template <typename K, typename V>
+void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n, int begin_bit, int end_bit, bool desc,
+                void* scratch, size_t scratch_bytes, cudaStream_t s);
+
 // tiles of the within-CV mean's first stage (node_out holds their partials)
 constexpr uint32_t kWithinTiles = 592;
 void launch_stats_finalize(const unsigned long long* x_sum, const unsigned long long* x_max,

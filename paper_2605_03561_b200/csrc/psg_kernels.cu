@@ -14,7 +14,6 @@
 // which is exact and order-free, so the GPU reproduces the reference's integer
 // outputs bit for bit regardless of thread order.  Floating-point outputs are
 // derived from exact integer sufficient statistics at the end.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -451,17 +450,11 @@ void launch_iter_spans(const uint64_t* cap_off, const uint64_t* bts, const uint3
   PSG_CUDA(cudaGetLastError());
 }
 
-size_t exclusive_scan_u64_scratch(uint32_t n) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint64_t*>(nullptr),
-                                static_cast<uint64_t*>(nullptr), static_cast<int>(n));
-  return bytes;
-}
+size_t exclusive_scan_u64_scratch(uint32_t n) { return exclusive_sum_scratch_bytes(n); }
 
 void launch_exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint32_t n, void* scratch,
                                size_t scratch_bytes, cudaStream_t s) {
-  if (n == 0) return;
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(scratch, scratch_bytes, in, out, static_cast<int>(n), s));
+  exclusive_sum_u64(in, out, n, scratch, scratch_bytes, s);
 }
 
 size_t cube_layout_scratch_bytes(uint32_t n) {
@@ -609,15 +602,11 @@ __global__ void __launch_bounds__(256) k_stats_finalize(const unsigned long long
       across += 100.0 * sqrt(u128_to_double(num)) / static_cast<double>(s);
     }
   }
-  typedef cub::BlockReduce<double, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const double avg_mean = BR(tmp).Sum(m) / static_cast<double>(K);
-  __syncthreads();
-  const double avg_max = BR(tmp).Sum(mx_s) / static_cast<double>(K);
-  __syncthreads();
-  const double acr = BR(tmp).Sum(across) / static_cast<double>(K);
-  __syncthreads();
-  const double nbad = BR(tmp).Sum(bad);
+  __shared__ double s_warp[32];
+  const double avg_mean = block_reduce(m, op_add(), s_warp) / static_cast<double>(K);
+  const double avg_max = block_reduce(mx_s, op_add(), s_warp) / static_cast<double>(K);
+  const double acr = block_reduce(across, op_add(), s_warp) / static_cast<double>(K);
+  const double nbad = block_reduce(bad, op_add(), s_warp);
   if (threadIdx.x != 0) return;
   double* o = out + static_cast<size_t>(n) * 8;
   o[0] = avg_mean;
@@ -763,11 +752,9 @@ __global__ void __launch_bounds__(256) k_site_acc(const uint64_t* w_incl, uint32
     sum += v;
     mx = max(mx, v);
   }
-  typedef cub::BlockReduce<u64, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  sum = BR(tmp).Sum(sum);
-  __syncthreads();
-  mx = BR(tmp).Reduce(mx, cub::Max());
+  __shared__ u64 s_warp[32];
+  sum = block_reduce(sum, op_add(), s_warp);
+  mx = block_reduce(mx, op_max(), s_warp);
   if (threadIdx.x == 0) {
     atomicAdd(acc + s, sum);
     atomicMax(acc + n_sites + s, mx);
@@ -886,12 +873,7 @@ __global__ void k_node_cut(const uint32_t* sorted_ids, const double* z, uint32_t
 }
 
 size_t node_select_scratch_bytes(uint32_t n_nodes) {
-  size_t temp_bytes = 0;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, static_cast<const uint64_t*>(nullptr),
-                                            static_cast<uint64_t*>(nullptr),
-                                            static_cast<const uint32_t*>(nullptr),
-                                            static_cast<uint32_t*>(nullptr), static_cast<int>(n_nodes),
-                                            0, 64);
+  const size_t temp_bytes = sort_pairs_scratch_bytes<uint64_t, uint32_t>(n_nodes);
   return sizeof(uint64_t) * n_nodes * 2 + sizeof(uint32_t) * (n_nodes + 8) + temp_bytes + 64;
 }
 
@@ -907,8 +889,7 @@ void launch_node_select(const unsigned long long* node_acc, uint32_t n_nodes, ui
   k_node_stats<<<1, 1024, 0, s>>>(node_acc, n_nodes, node_mean, node_z, k_in, ids_in);
   count_launch();
   PSG_CUDA(cudaGetLastError());
-  PSG_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, k_in, k_out, ids_in, order,
-                                                     static_cast<int>(n_nodes), 0, 64, s));
+  sort_pairs<uint64_t, uint32_t>(k_in, k_out, ids_in, order, n_nodes, 0, 64, true, temp, temp_bytes, s);
   k_node_cut<<<1, 1024, 0, s>>>(order, node_z, n_nodes, top_k, z_min, n_sel);
   count_launch();
   PSG_CUDA(cudaGetLastError());

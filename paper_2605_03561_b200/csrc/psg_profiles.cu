@@ -19,7 +19,6 @@
 //                          summed in rank order, / count
 // The z-score / top-k selection and the topology are the trace path's kernels
 // (psg_kernels.cu K7/K8) fed with these node means.
-#include <cub/cub.cuh>
 
 #include <cstdint>
 
@@ -166,14 +165,10 @@ __global__ void __launch_bounds__(256) k_site_ratio(const double* vals, uint32_t
     mx = have ? fmax(mx, v) : v;
     have = true;
   }
-  typedef cub::BlockReduce<double, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  __shared__ double s_sum;
-  const double tot = BR(tmp).Sum(sum);
-  if (threadIdx.x == 0) s_sum = tot;
-  __syncthreads();
+  __shared__ double s_warp[32];
+  const double s_sum = block_reduce(sum, op_add(), s_warp);
   // max over the ranks (ranks beyond n_ranks contribute nothing)
-  const double m = BR(tmp).Reduce(have ? mx : -1.0e308, cub::Max());
+  const double m = block_reduce(have ? mx : -1.0e308, op_max(), s_warp);
   if (threadIdx.x == 0)
     ratio[s] = (n_ranks == 0 || m == 0.0) ? 1.0 : s_sum / static_cast<double>(n_ranks) / m;
 }

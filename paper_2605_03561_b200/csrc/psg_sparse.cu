@@ -24,7 +24,6 @@
 //
 // Traces are processed in batches that bound the scratch; each batch appends
 // to the outputs.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdint>
@@ -247,9 +246,8 @@ uint64_t run_starts(const uint64_t* keys, uint64_t n, dbuf<uint64_t>& flag, dbuf
   flag.ensure(n);
   pos.ensure(n);
   k_sp_flags<<<blocks_for(n, 256), 256, 0, s>>>(keys, n, flag.p);
-  size_t sb = 0;
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, flag.p, pos.p, n, s));
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(scratch.ensure(sb), sb, flag.p, pos.p, n, s));
+  const size_t sb = exclusive_sum_scratch_bytes(n);
+  exclusive_sum_u64(flag.p, pos.p, n, scratch.ensure(sb), sb, s);
   uint64_t last[2];
   PSG_CUDA(cudaMemcpyAsync(&last[0], pos.p + n - 1, 8, cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaMemcpyAsync(&last[1], flag.p + n - 1, 8, cudaMemcpyDeviceToHost, s));
@@ -262,14 +260,13 @@ uint64_t run_starts(const uint64_t* keys, uint64_t n, dbuf<uint64_t>& flag, dbuf
   return runs;
 }
 
-void sort_pairs(dbuf<uint64_t>& k, dbuf<uint64_t>& v, dbuf<uint64_t>& k2, dbuf<uint64_t>& v2, uint64_t n,
+void sort_kv(dbuf<uint64_t>& k, dbuf<uint64_t>& v, dbuf<uint64_t>& k2, dbuf<uint64_t>& v2, uint64_t n,
                 int end_bit, dbuf<uint8_t>& scratch, cudaStream_t s) {
   if (n == 0) return;
   k2.ensure(n);
   v2.ensure(n);
-  size_t sb = 0;
-  PSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb, k.p, k2.p, v.p, v2.p, n, 0, end_bit, s));
-  PSG_CUDA(cub::DeviceRadixSort::SortPairs(scratch.ensure(sb), sb, k.p, k2.p, v.p, v2.p, n, 0, end_bit, s));
+  const size_t sb = sort_pairs_scratch_bytes<uint64_t, uint64_t>(n);
+  sort_pairs<uint64_t, uint64_t>(k.p, k2.p, v.p, v2.p, n, 0, end_bit, false, scratch.ensure(sb), sb, s);
   std::swap(k.p, k2.p);
   std::swap(k.n, k2.n);
   std::swap(v.p, v2.p);
@@ -331,7 +328,7 @@ void sparse_window(const sparse_args& a, sparse_result& r, cudaStream_t s) {
                                                               roff.p, key.p, val.p);
       count_launch(2);
       PSG_CUDA(cudaGetLastError());
-      sort_pairs(key, val, key2, val2, nr, tbits + cbits, scratch, s);
+      sort_kv(key, val, key2, val2, nr, tbits + cbits, scratch, s);
       ng = run_starts(key.p, nr, flag, pos, starts, scratch, s);
       grow_keep(r.g_trace, r.n_groups, r.n_groups + ng, s);
       grow_keep(r.g_ctx, r.n_groups, r.n_groups + ng, s);
@@ -353,9 +350,8 @@ void sparse_window(const sparse_args& a, sparse_result& r, cudaStream_t s) {
     k_sp_contrib_count<<<blocks_for(nc, 256), 256, 0, s>>>(r.g_ctx.p, r.g_sum.p, r.n_groups, ng, a.c_has, a.c_ctx,
                                                            cdur.p, t_lo, nb, a.depth, ccnt.p);
     PSG_CUDA(cudaMemsetAsync(ccnt.p + nc, 0, 8, s));
-    size_t sb = 0;
-    PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, ccnt.p, coff.p, nc + 1, s));
-    PSG_CUDA(cub::DeviceScan::ExclusiveSum(scratch.ensure(sb), sb, ccnt.p, coff.p, nc + 1, s));
+    const size_t sb = exclusive_sum_scratch_bytes(nc + 1);
+    exclusive_sum_u64(ccnt.p, coff.p, nc + 1, scratch.ensure(sb), sb, s);
     uint64_t ne = 0;
     PSG_CUDA(cudaMemcpyAsync(&ne, coff.p + nc, 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
@@ -368,7 +364,7 @@ void sparse_window(const sparse_args& a, sparse_result& r, cudaStream_t s) {
                                                            cbits, key.p, val.p);
       count_launch();
       PSG_CUDA(cudaGetLastError());
-      sort_pairs(key, val, key2, val2, ne, tbits + cbits, scratch, s);
+      sort_kv(key, val, key2, val2, ne, tbits + cbits, scratch, s);
       const uint64_t nrm = run_starts(key.p, ne, flag, pos, starts, scratch, s);
       grow_keep(r.r_trace, r.n_remat, r.n_remat + nrm, s);
       grow_keep(r.r_ctx, r.n_remat, r.n_remat + nrm, s);
@@ -438,10 +434,9 @@ void dense_to_sparse(const dense_window& w, uint32_t n_traces, uint32_t n_ctx, s
   count_launch();
   PSG_CUDA(cudaMemsetAsync(fg.p + cells, 0, 8, s));
   PSG_CUDA(cudaMemsetAsync(fr.p + cells, 0, 8, s));
-  size_t sb = 0;
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, fg.p, pg.p, cells + 1, s));
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(scratch.ensure(sb), sb, fg.p, pg.p, cells + 1, s));
-  PSG_CUDA(cub::DeviceScan::ExclusiveSum(scratch.p, sb, fr.p, pr.p, cells + 1, s));
+  const size_t sb = exclusive_sum_scratch_bytes(cells + 1);
+  exclusive_sum_u64(fg.p, pg.p, cells + 1, scratch.ensure(sb), sb, s);
+  exclusive_sum_u64(fr.p, pr.p, cells + 1, scratch.p, sb, s);
   uint64_t tot[2];
   PSG_CUDA(cudaMemcpyAsync(&tot[0], pg.p + cells, 8, cudaMemcpyDeviceToHost, s));
   PSG_CUDA(cudaMemcpyAsync(&tot[1], pr.p + cells, 8, cudaMemcpyDeviceToHost, s));

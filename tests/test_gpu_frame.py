@@ -51,6 +51,20 @@ def test_sort_and_filter(gpu_ctx_factory, n):
         assert np.array_equal(f.col("row").numpy(), want), (col, op, lit)
 
 
+@pytest.mark.parametrize("n", [2_000_003])
+def test_sort_large_multi_tile(gpu_ctx_factory, n):
+    """The hand-written radix sort (psg_sort.cu) across many tiles and all
+    eight digit passes: full-range int64 keys, few-valued keys with long runs
+    of ties (stability), descending order, and NaN / -0.0 doubles."""
+    ctx = gpu_ctx_factory()
+    a, b, c, v, w = inputs(7, n)
+    t = table(ctx, a=a, b=b, c=c, w=w, row=np.arange(n, dtype=np.uint64))
+    for keys, asc in ((["w"], None), (["c"], [False]), (["a", "w"], [True, False]), (["b", "c"], None)):
+        want = oracle.ref_frame_sort([{"a": a, "b": b, "c": c, "w": w}[k] for k in keys], asc)
+        s = frame.sort(t, keys, asc)
+        assert np.array_equal(s.col("row").numpy(), want), (keys, asc)
+
+
 @pytest.mark.parametrize("n", [1, 5000, 100_000])
 def test_group_aggregate(gpu_ctx_factory, n):
     ctx = gpu_ctx_factory()
