@@ -25,7 +25,10 @@ namespace psg {
 namespace {
 
 constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
-constexpr int kSortThreads = 256, kSortItems = 8, kSortTile = kSortThreads * kSortItems;
+#ifndef PSG_SORT_ITEMS
+#define PSG_SORT_ITEMS 8
+#endif
+constexpr int kSortThreads = 256, kSortItems = PSG_SORT_ITEMS, kSortTile = kSortThreads * kSortItems;
 constexpr int kSortWarps = kSortThreads / 32;
 
 __device__ __forceinline__ unsigned lanemask_lt_s() {
@@ -158,25 +161,32 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const K* keys, uint
 
 // Per tile: stable ranks (warp w owns items [w * 32 * kSortItems, ...) of the
 // tile, round r the 32 consecutive items r * 32 + lane of them: the order
-// (w, r, lane) is the input order), then the scatter.
+// (w, r, lane) is the input order), then the scatter through shared memory:
+// the tile is first placed in digit order locally, so that consecutive
+// threads write consecutive addresses of each digit's run (coalesced).
 template <typename K, typename V>
 __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* kin, K* kout, const V* vin, V* vout,
                                                                 uint64_t n, int shift, bool desc,
                                                                 const uint64_t* off, uint32_t n_tiles) {
   __shared__ uint32_t s_cnt[kSortWarps][256];
+  __shared__ uint32_t s_start[256];  // tile-local start of each digit
+  __shared__ uint32_t s_gdelta[256];  // global start - local start, per digit
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint64_t s_buf[kSortTile];  // keys, then values, in local digit order
+  __shared__ uint8_t s_dig[kSortTile];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&s_cnt[0][0])[i] = 0;
   __syncthreads();
-  const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kSortTile + static_cast<uint64_t>(w) * 32 * kSortItems;
+  const uint64_t tbase = static_cast<uint64_t>(blockIdx.x) * kSortTile;
+  const uint64_t wbase = tbase + static_cast<uint64_t>(w) * 32 * kSortItems;
+  const uint32_t tn = static_cast<uint32_t>(min(static_cast<uint64_t>(kSortTile), n - tbase));
   K key[kSortItems];
-  V val[kSortItems];
   uint32_t dig[kSortItems], rank[kSortItems];
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     const uint64_t j = wbase + static_cast<uint64_t>(r) * 32 + lane;
     const bool ok = j < n;
     key[r] = ok ? kin[j] : K(0);
-    val[r] = ok ? vin[j] : V(0);
     dig[r] = ok ? digit_of(key[r], shift, desc) : 256u + static_cast<uint32_t>(lane);
   }
 #pragma unroll
@@ -193,25 +203,43 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* kin, K*
     __syncwarp();
   }
   __syncthreads();
-  // per digit: the warps' counts -> their exclusive prefix (in place)
-  for (int d = threadIdx.x; d < 256; d += kSortThreads) {
-    uint32_t run = static_cast<uint32_t>(off[static_cast<uint64_t>(d) * n_tiles + blockIdx.x]);
+  // per digit: the warps' exclusive prefix within the digit, the digit's total
+  uint32_t tot = 0;
+  {
+    const int d = threadIdx.x;  // kSortThreads == 256 digits
 #pragma unroll
     for (int q = 0; q < kSortWarps; ++q) {
       const uint32_t c = s_cnt[q][d];
-      s_cnt[q][d] = run;
-      run += c;
+      s_cnt[q][d] = tot;
+      tot += c;
     }
   }
+  uint32_t all;
+  const uint32_t start = block_exclusive<uint32_t, kSortThreads>(tot, s_warp, &all);
+  s_start[threadIdx.x] = start;
+  s_gdelta[threadIdx.x] = static_cast<uint32_t>(off[static_cast<uint64_t>(threadIdx.x) * n_tiles + blockIdx.x]) - start;
   __syncthreads();
+  uint32_t lpos[kSortItems];
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     if (dig[r] < 256u) {
-      const uint32_t pos = s_cnt[w][dig[r]] + rank[r];
-      kout[pos] = key[r];
-      vout[pos] = val[r];
+      lpos[r] = s_start[dig[r]] + s_cnt[w][dig[r]] + rank[r];
+      s_buf[lpos[r]] = static_cast<uint64_t>(key[r]);
+      s_dig[lpos[r]] = static_cast<uint8_t>(dig[r]);
     }
   }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads)
+    kout[s_gdelta[s_dig[i]] + i] = static_cast<K>(s_buf[i]);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    const uint64_t j = wbase + static_cast<uint64_t>(r) * 32 + lane;
+    if (dig[r] < 256u) s_buf[lpos[r]] = static_cast<uint64_t>(vin[j]);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads)
+    vout[s_gdelta[s_dig[i]] + i] = static_cast<V>(s_buf[i]);
 }
 
 }  // namespace

@@ -46,7 +46,7 @@ for name, fl in (("window_sparse", Q_WINDOW), ("cube_global_cols", Q_CUBE)):
         info = c.query(fl, t0=T // 4, t1=3 * T // 4, anchor=anchor)
         wall.append(time.perf_counter() - t)
         ms.append(info["ms_total"])
-    res[name] = {"ms_device": statistics.mean(ms[2:]), "s_wall": statistics.mean(wall[2:]),
+    res[name] = {"ms_device": statistics.mean(ms[2:]), "s_wall": statistics.mean(wall[2:]), "ms_each": [round(x, 2) for x in ms],
                  "events_per_s_device": E / (statistics.mean(ms[2:]) / 1e3),
                  "events_per_s_wall": E / statistics.mean(wall[2:])}
     if fl == Q_WINDOW:
