@@ -1459,21 +1459,44 @@ namespace {
 // (configs[1], C3: measured slower split, tools/c3_units.py — a split trace
 // merges its window and within-rank sums with atomics).  PSG_UNIT_EVENTS
 // overrides U and splits every trace longer than it (tests).
-void plan_units(psg_context* c, uint64_t slots) {
+//
+// Tail fill (tail_fill: the query runs one-warp CTAs anyway): evenly sized
+// traces run in waves of `slots` warps; when the last wave would be at most
+// half full, its traces are split into k = slots / rem units each, so it lasts
+// 1 / k of a trace (C3: 8,192 traces on 2,368 slots = 3 waves + 1,088 traces:
+// 4 -> 3.5 trace times).
+void plan_units(psg_context* c, uint64_t slots, bool tail_fill) {
   uint64_t U = std::max<uint64_t>(kUnitMinEvents, c->n_events / std::max<uint64_t>(1, slots));
   uint64_t thresh = 2 * U;
-  if (const char* e = std::getenv("PSG_UNIT_EVENTS")) thresh = U = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
-  const uint64_t key = (static_cast<uint64_t>(c->n_traces) * 1000003ull) ^ (c->n_events * 7919ull) ^ (U << 40) ^ (thresh << 20) ^ 1ull;
+  const char* env = std::getenv("PSG_UNIT_EVENTS");
+  if (env) thresh = U = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
+  const uint64_t key = (static_cast<uint64_t>(c->n_traces) * 1000003ull) ^ (c->n_events * 7919ull) ^ (U << 40) ^
+                       (thresh << 20) ^ (slots << 4) ^ (tail_fill ? 2ull : 1ull);
   if (key == c->units_key) return;
   std::vector<uint4> units;
   std::vector<uint32_t> split;
   bool any = false;
-  for (uint32_t t = 0; t < c->n_traces && !any; ++t) any = c->h_off[t + 1] - c->h_off[t] > thresh;
-  if (any) {
+  uint64_t max_t = 0;
+  for (uint32_t t = 0; t < c->n_traces; ++t) {
+    const uint64_t n_t = c->h_off[t + 1] - c->h_off[t];
+    any = any || n_t > thresh;
+    max_t = std::max(max_t, n_t);
+  }
+  // tail fill: the last `rem` traces (the last CTAs launched) split k ways
+  uint32_t tail_from = c->n_traces, tail_k = 1;
+  if (!any && !env && tail_fill && slots && c->n_traces > slots && c->n_events &&
+      max_t * c->n_traces <= c->n_events + c->n_events / 4) {  // evenly sized: max <= 1.25 mean
+    const uint64_t rem = c->n_traces % slots;
+    if (rem && 2 * rem <= slots && max_t >= 2 * kUnitMinEvents) {
+      tail_k = static_cast<uint32_t>(std::min<uint64_t>(slots / rem, std::max<uint64_t>(1, max_t / kUnitMinEvents)));
+      if (tail_k >= 2) tail_from = c->n_traces - static_cast<uint32_t>(rem);
+    }
+  }
+  if (any || tail_from < c->n_traces) {
     units.reserve(c->n_traces);
     for (uint32_t t = 0; t < c->n_traces; ++t) {
       const uint64_t n_t = c->h_off[t + 1] - c->h_off[t];
-      const uint64_t u = n_t > thresh ? (n_t + U - 1) / U : 1;
+      const uint64_t u = t >= tail_from ? tail_k : n_t > thresh ? (n_t + U - 1) / U : 1;
       if (u > 1) split.push_back(t);
       for (uint64_t i = 0; i < u; ++i)
         units.push_back(make_uint4(t, static_cast<uint32_t>(n_t * i / u), static_cast<uint32_t>(n_t * (i + 1) / u),
@@ -1724,12 +1747,15 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     // depends only on the tree and the anchor, so every rank takes the same one)
     if (!one && !fits_wide(n, L.bytes, cta_table_bytes(c->n_ctx, nn, 16, false))) one = true;
     if (global_cols) one = true;
-    // work units: long traces split across warps (one-warp CTAs)
+    // work units: long traces split across warps (one-warp CTAs); the
+    // resident slots are those of the one-warp instantiation this query uses
     {
       int dev = 0, sms = 148;
       PSG_CUDA(cudaGetDevice(&dev));
       PSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      plan_units(c, static_cast<uint64_t>(sms) * 16);
+      const uint32_t per_sm = trace_query_one_warp_per_sm(p.do_window != 0, p.do_cube != 0,
+                                                          p.do_cube && exact_bounds, global_cols, L.bytes);
+      plan_units(c, static_cast<uint64_t>(sms) * std::max(1u, per_sm), one);
     }
     const bool units = c->n_split > 0;
     if (units) one = true;

@@ -373,6 +373,8 @@ void launch_iter_spans(const uint64_t* cap_off, const uint64_t* bts, const uint3
                        cudaStream_t s);
 size_t cube_layout_scratch_bytes(uint32_t n);
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s);
+// resident one-warp CTAs per SM of the pass-2 instantiation a query would use
+uint32_t trace_query_one_warp_per_sm(bool win, bool cube, bool exact, bool gt, uint32_t smem_bytes);
 // split traces (list of loaded-trace indices): prepare their global window rows
 // and within-rank accumulators before pass 2, finish them after
 void launch_split_init(const query_params& p, const uint32_t* split_traces, uint32_t n_split, cudaStream_t s);

@@ -1846,7 +1846,27 @@ void launch_variant(const query_params& p, uint32_t smem_bytes, cudaStream_t s) 
   }
 }
 
+template <bool WIN, bool CUBE, bool EXACT, bool GT>
+uint32_t one_warp_occupancy(uint32_t smem_bytes) {
+  int per_sm = 0;
+  PSG_CUDA(cudaFuncSetAttribute(k_trace_query<WIN, CUBE, EXACT, true, GT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes)));
+  PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace_query<WIN, CUBE, EXACT, true, GT>, 32,
+                                                         smem_bytes));
+  return static_cast<uint32_t>(per_sm);
+}
+
 }  // namespace
+
+uint32_t trace_query_one_warp_per_sm(bool win, bool cube, bool exact, bool gt, uint32_t smem_bytes) {
+  if (gt) return exact ? one_warp_occupancy<false, true, true, true>(smem_bytes)
+                       : one_warp_occupancy<false, true, false, true>(smem_bytes);
+  if (win && cube) return exact ? one_warp_occupancy<true, true, true, false>(smem_bytes)
+                                : one_warp_occupancy<true, true, false, false>(smem_bytes);
+  if (win) return one_warp_occupancy<true, false, false, false>(smem_bytes);
+  return exact ? one_warp_occupancy<false, true, true, false>(smem_bytes)
+               : one_warp_occupancy<false, true, false, false>(smem_bytes);
+}
 
 void launch_trace_query(const query_params& p, uint32_t smem_bytes, cudaStream_t s) {
   if (p.t_stop <= p.t_base || p.t_stop > p.tr.n) {
