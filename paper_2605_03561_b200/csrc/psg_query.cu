@@ -508,13 +508,25 @@ __global__ void k_verify_bounds(trace_view tr, const uint64_t* cap_off, const ui
   const uint64_t* bt = bts + cap_off[t];
   const u64 first = ldg64(tr.ts + tr.off[t]), tend = tr.t_end[t];
   bool dup = false, wide = false;
-  for (uint32_t j = lane; j < nbd; j += 32) {
-    const u64 tj = bt[j];
-    const u64 prev = j > 0 ? bt[j - 1] : first;
-    if (j > 0) dup |= tj == prev;
-    else wide |= tj - prev >= kSpan32;  // the gap row [first, b_0)
-    const u64 nx = j + 1 < nbd ? bt[j + 1] : tend;
-    if (j < it) wide |= nx - tj >= kSpan32;
+  // four rows of 32 boundaries per round: twelve independent loads in flight
+  // per lane (the kernel is latency-bound: one short trace region per warp)
+  for (uint32_t j0 = lane; j0 < nbd; j0 += 128) {
+    u64 tj[4], pv[4], nx[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t j = j0 + 32 * q;
+      tj[q] = j < nbd ? ldg64(bt + j) : 0;
+      pv[q] = (j < nbd && j > 0) ? ldg64(bt + j - 1) : first;
+      nx[q] = j + 1 < nbd ? ldg64(bt + j + 1) : tend;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t j = j0 + 32 * q;
+      if (j >= nbd) continue;
+      if (j > 0) dup |= tj[q] == pv[q];
+      else wide |= tj[q] - pv[q] >= kSpan32;  // the gap row [first, b_0)
+      if (j < it) wide |= nx[q] - tj[q] >= kSpan32;
+    }
   }
   const unsigned v = (__ballot_sync(FULL, dup) ? 1u : 0u) | (__ballot_sync(FULL, wide) ? 2u : 0u);
   if (v && lane == 0) atomicOr(verify, static_cast<unsigned long long>(v));
