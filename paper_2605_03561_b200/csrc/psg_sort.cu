@@ -10,7 +10,7 @@
 //                       a per-tile digit histogram, an exclusive scan of the
 //                       digit-major histogram (every tile's first slot per
 //                       digit), and a stable in-tile ranking by warp
-//                       (__match_any_sync per round of 32 keys, per-warp digit
+//                       (a ballot-based match per round of 32 keys, per-warp digit
 //                       counters, a prefix over warps) that scatters each key
 //                       to its digit's slot.  Descending order inverts the
 //                       digits.  Stable: ties keep their input order, which
@@ -129,6 +129,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint64_t* in,
   }
 }
 
+// Lanes of the warp holding the same 9-bit value (digit, or 256 + lane for an
+// empty slot): nine ballots, one per bit (a __match_any_sync equivalent that
+// every execution model, including compute-sanitizer's, treats alike).
+__device__ __forceinline__ unsigned match_digit(uint32_t v) {
+  unsigned peers = 0xFFFFFFFFu;
+#pragma unroll
+  for (int b = 0; b < 9; ++b) {
+    const bool bit = (v >> b) & 1u;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift, bool desc) {
   const uint32_t d = static_cast<uint32_t>(key >> shift) & 0xFFu;
@@ -191,7 +205,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* kin, K*
   }
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
-    const unsigned peers = __match_any_sync(0xFFFFFFFFu, dig[r]);
+    const unsigned peers = match_digit(dig[r]);
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
     if (lane == leader && dig[r] < 256u) {
@@ -240,6 +254,31 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* kin, K*
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads)
     vout[s_gdelta[s_dig[i]] + i] = static_cast<V>(s_buf[i]);
+}
+
+// Small inputs (n <= kSmallSort, e.g. the outlier order over nodes): one CTA
+// ranks every pair by counting (stable: equal keys keep their input order),
+// instead of the 5 launches per digit pass of the general path.
+constexpr uint32_t kSmallSort = 2048;
+template <typename K, typename V>
+__global__ void __launch_bounds__(1024) k_sort_small(const K* kin, K* kout, const V* vin, V* vout, uint32_t n,
+                                                     int begin_bit, int end_bit, bool desc) {
+  __shared__ K s_key[kSmallSort];
+  const int nb = end_bit - begin_bit;
+  const K mask = nb >= static_cast<int>(8 * sizeof(K)) ? ~K(0) : ((K(1) << nb) - K(1));
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s_key[i] = (kin[i] >> begin_bit) & mask;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const K ki = s_key[i];
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      const K kj = s_key[j];
+      const bool before = desc ? (kj > ki) : (kj < ki);
+      rank += (before || (kj == ki && j < i)) ? 1u : 0u;
+    }
+    kout[rank] = kin[i];
+    vout[rank] = vin[i];
+  }
 }
 
 }  // namespace
@@ -293,6 +332,12 @@ void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n, int be
   if (passes <= 0) {  // no key bits: the stable order is the input order
     PSG_CUDA(cudaMemcpyAsync(kout, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, s));
     PSG_CUDA(cudaMemcpyAsync(vout, vin, n * sizeof(V), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (n <= kSmallSort) {
+    k_sort_small<K, V><<<1, 1024, 0, s>>>(kin, kout, vin, vout, static_cast<uint32_t>(n), begin_bit, end_bit, desc);
+    count_launch();
+    PSG_CUDA(cudaGetLastError());
     return;
   }
   const K* ks = kin;
