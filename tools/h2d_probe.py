@@ -15,3 +15,15 @@ with torch.cuda.stream(s1): d[:half].copy_(h[:half], non_blocking=True)
 with torch.cuda.stream(s2): d[half:].copy_(h[half:], non_blocking=True)
 torch.cuda.synchronize(); dt = time.perf_counter() - t
 print("2 streams:", n / dt / 1e9, "GB/s")
+# duplex: H2D of one buffer while D2H of another (the e2e overlap)
+h2 = torch.empty(n // 2, dtype=torch.uint8, pin_memory=True)
+d2 = torch.empty(n // 2, dtype=torch.uint8, device="cuda")
+torch.cuda.synchronize(); t = time.perf_counter()
+with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
+with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize(); dt = time.perf_counter() - t
+print("duplex: H2D", n / dt / 1e9, "GB/s with D2H of", (n // 2) / 1e9, "GB")
+torch.cuda.synchronize(); t = time.perf_counter()
+h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize(); dt = time.perf_counter() - t
+print("D2H alone:", (n // 2) / dt / 1e9, "GB/s")
