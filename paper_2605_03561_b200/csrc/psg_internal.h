@@ -302,6 +302,12 @@ struct sparse_result {
   // rematerialize rows (incl or excl nonzero), sorted by (trace, ctx)
   dbuf<uint32_t> r_trace, r_ctx;
   dbuf<int64_t> r_incl, r_excl;
+  // the path's device workspace, kept across queries (grow-only): the sort
+  // and scan scratch alone is GBs, and allocating it per query stalled the
+  // stream for up to ~0.5 s (cudaMalloc / cudaFree of large buffers)
+  dbuf<uint64_t> w_rows, w_i0s, w_roff, w_cdur, w_key, w_val, w_key2, w_val2, w_flag, w_pos, w_starts, w_ccnt,
+      w_coff;
+  dbuf<uint8_t> w_scratch;
 };
 void sparse_window(const sparse_args& a, sparse_result& r, cudaStream_t s);
 struct sparse_result_view {

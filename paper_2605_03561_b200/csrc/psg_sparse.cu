@@ -286,8 +286,10 @@ void sparse_window(const sparse_args& a, sparse_result& r, cudaStream_t s) {
   const uint32_t n = tr.n;
   const int cbits = bits_for(a.n_ctx);
   r.n_groups = r.n_remat = 0;
-  dbuf<uint64_t> rows, i0s, roff, cdur, key, val, key2, val2, flag, pos, starts, ccnt, coff;
-  dbuf<uint8_t> scratch;
+  dbuf<uint64_t>&rows = r.w_rows, &i0s = r.w_i0s, &roff = r.w_roff, &cdur = r.w_cdur, &key = r.w_key,
+                &val = r.w_val, &key2 = r.w_key2, &val2 = r.w_val2, &flag = r.w_flag, &pos = r.w_pos,
+                &starts = r.w_starts, &ccnt = r.w_ccnt, &coff = r.w_coff;
+  dbuf<uint8_t>& scratch = r.w_scratch;
   rows.ensure(n + 1);
   i0s.ensure(n + 1);
   cdur.ensure(n + 1);
