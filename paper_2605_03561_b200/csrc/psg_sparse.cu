@@ -426,8 +426,9 @@ void dense_to_sparse(const dense_window& w, uint32_t n_traces, uint32_t n_ctx, s
   const uint64_t cells = static_cast<uint64_t>(n_traces) * n_ctx;
   r.n_groups = r.n_remat = 0;
   if (cells == 0) return;
-  dbuf<uint64_t> fg, pg, fr, pr;
-  dbuf<uint8_t> scratch;
+  // the workspace of the sparse path, reused (grow-only)
+  dbuf<uint64_t>&fg = r.w_flag, &pg = r.w_pos, &fr = r.w_key, &pr = r.w_val;
+  dbuf<uint8_t>& scratch = r.w_scratch;
   fg.ensure(cells + 1);
   pg.ensure(cells + 1);
   fr.ensure(cells + 1);
