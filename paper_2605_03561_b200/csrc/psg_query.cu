@@ -88,7 +88,7 @@ typedef unsigned __int128 u128;
 #define PSG_G 8
 #endif
 #ifndef PSG_FLUSH_UNROLL
-#define PSG_FLUSH_UNROLL 2
+#define PSG_FLUSH_UNROLL 1
 #endif
 constexpr int kFlushUnroll = PSG_FLUSH_UNROLL;
 
