@@ -91,6 +91,13 @@ typedef unsigned __int128 u128;
 #define PSG_FLUSH_UNROLL 1
 #endif
 constexpr int kFlushUnroll = PSG_FLUSH_UNROLL;
+#ifndef PSG_COPY_UNROLL
+#define PSG_COPY_UNROLL 4  // the flush's block copy (16-byte loads / zeroing / stores)
+#endif
+constexpr int kCopyUnroll = PSG_COPY_UNROLL;
+#ifndef PSG_GEN_ALL
+#define PSG_GEN_ALL 1  // general path: specialisations for interior block steps
+#endif
 
 #ifndef PSG_RB
 #define PSG_RB 16
@@ -797,9 +804,9 @@ __device__ __forceinline__ void run_block_il(int wm, u64 (&tv)[RM + 1], uint32_t
                                              const run_ctx& R, run_state& st,
                                              const warp_tables& T, const rot_src& rs) {
   const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
-  if (!CWIDE && all && wm == WIN_FULL)
+  if (PSG_GEN_ALL && !CWIDE && all && wm == WIN_FULL)
     run_events_il<WIN, CUBE, WIN_FULL, false, true>(tv, cv, lane, R, st, T, rs);
-  else if (!CWIDE && all && wm == WIN_NONE)
+  else if (PSG_GEN_ALL && !CWIDE && all && wm == WIN_NONE)
     run_events_il<WIN, CUBE, WIN_NONE, false, true>(tv, cv, lane, R, st, T, rs);
   else if (wm == WIN_FULL)
     run_events_il<WIN, CUBE, WIN_FULL, CWIDE, false>(tv, cv, lane, R, st, T, rs);
@@ -1074,7 +1081,7 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
   uint4* z = reinterpret_cast<uint4*>(rows);
   if (p.cube32) {
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.cube_incl) + ob);
-#pragma unroll 4
+#pragma unroll kCopyUnroll
     for (uint32_t i = lane; i < nq; i += 32) {
       const uint4 v = src[i];
       z[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -1082,7 +1089,7 @@ __device__ __forceinline__ void flush_fast(const query_params& p, uint32_t* rows
     }
   } else {
     ulonglong2* dst = reinterpret_cast<ulonglong2*>(p.cube_incl + ob);
-#pragma unroll 4
+#pragma unroll kCopyUnroll
     for (uint32_t i = lane; i < nq; i += 32) {
       const uint4 v = src[i];
       z[i] = make_uint4(0u, 0u, 0u, 0u);
