@@ -98,6 +98,9 @@ constexpr int kCopyUnroll = PSG_COPY_UNROLL;
 #ifndef PSG_GEN_ALL
 #define PSG_GEN_ALL 1  // general path: specialisations for interior block steps
 #endif
+#ifndef PSG_GEN_RT
+#define PSG_GEN_RT 1  // general path: one copy with the window class at run time (-20 % code, A/B neutral)
+#endif
 
 #ifndef PSG_RB
 #define PSG_RB 16
@@ -738,7 +741,8 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
 template <bool WIN, bool CUBE, int WM, bool CWIDE, bool ALL>
 __device__ __forceinline__ void run_events_il(u64 (&tv)[RM + 1], uint32_t (&cv)[RM], int lane,
                                               const run_ctx& R, run_state& st,
-                                              const warp_tables& T, const rot_src& rs) {
+                                              const warp_tables& T, const rot_src& rs, int wm_rt = 0) {
+  const int wmx = WM >= 0 ? WM : wm_rt;  // WM < 0: the window class is a (warp-uniform) runtime value
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
     const int li = lane + 32 * j;
@@ -772,9 +776,9 @@ __device__ __forceinline__ void run_events_il(u64 (&tv)[RM + 1], uint32_t (&cv)[
         }
       }
     }
-    if (WIN && WM == WIN_FULL) {
+    if (WIN && wmx == WIN_FULL) {
       if (valid) win_row32(T, cj, static_cast<uint32_t>(nts) - static_cast<uint32_t>(tsj));
-    } else if (WIN && WM == WIN_PART) {
+    } else if (WIN && wmx == WIN_PART) {
       if (valid) {
         if (tsj >= R.t0) {
           if (tsj < R.t1w)
@@ -783,7 +787,7 @@ __device__ __forceinline__ void run_events_il(u64 (&tv)[RM + 1], uint32_t (&cv)[
           carry_in(T, cj, tsj, min(nts, R.t1w), R.t0);
         }
       }
-    } else if (WIN && WM == WIN_WIDE) {
+    } else if (WIN && wmx == WIN_WIDE) {
       if (valid) {
         const bool last = li == R.last_li;
         const u64 e2 = last ? R.t1w : min(nts, R.t1w);
@@ -804,6 +808,10 @@ __device__ __forceinline__ void run_block_il(int wm, u64 (&tv)[RM + 1], uint32_t
                                              const run_ctx& R, run_state& st,
                                              const warp_tables& T, const rot_src& rs) {
   const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
+  if (PSG_GEN_RT) {  // one copy of the general path (less code in the step loop)
+    run_events_il<WIN, CUBE, -1, CWIDE, false>(tv, cv, lane, R, st, T, rs, wm);
+    return;
+  }
   if (PSG_GEN_ALL && !CWIDE && all && wm == WIN_FULL)
     run_events_il<WIN, CUBE, WIN_FULL, false, true>(tv, cv, lane, R, st, T, rs);
   else if (PSG_GEN_ALL && !CWIDE && all && wm == WIN_NONE)
