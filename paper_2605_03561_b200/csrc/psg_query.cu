@@ -678,7 +678,9 @@ struct run_ctx {
 // (the common interior step): no per-event range or end checks.
 template <bool WIN, bool CUBE, int WM, bool CWIDE, bool ALL>
 __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
-                                           const run_ctx& R, run_state& st, const warp_tables& T) {
+                                           const run_ctx& R, run_state& st, const warp_tables& T,
+                                           int wm_rt = 0) {
+  const int wmx = WM >= 0 ? WM : wm_rt;  // WM < 0: the window class is a (warp-uniform) runtime value
 #pragma unroll
   for (int j = 0; j < RM; ++j) {
     const int li = R.lb + j;
@@ -709,9 +711,9 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
         }
       }
     }
-    if (WIN && WM == WIN_FULL) {  // the block spans < 2^32 ns
+    if (WIN && wmx == WIN_FULL) {  // the block spans < 2^32 ns
       if (valid) win_row32(T, cj, static_cast<uint32_t>(nts) - static_cast<uint32_t>(tsj));
-    } else if (WIN && WM == WIN_PART) {  // no trace end in this block step
+    } else if (WIN && wmx == WIN_PART) {  // no trace end in this block step
       if (valid) {
         if (tsj >= R.t0) {
           if (tsj < R.t1w)
@@ -720,7 +722,7 @@ __device__ __forceinline__ void run_events(const u64 (&tv)[RM + 1], const uint32
           carry_in(T, cj, tsj, min(nts, R.t1w), R.t0);
         }
       }
-    } else if (WIN && WM == WIN_WIDE) {
+    } else if (WIN && wmx == WIN_WIDE) {
       if (valid) {
         const bool last = li == R.last_li;
         const u64 e2 = last ? R.t1w : min(nts, R.t1w);
@@ -829,6 +831,10 @@ __device__ __forceinline__ void run_block_il(int wm, u64 (&tv)[RM + 1], uint32_t
 template <bool WIN, bool CUBE, bool CWIDE>
 __device__ __forceinline__ void run_block(int wm, const u64 (&tv)[RM + 1], const uint32_t (&cv)[RM],
                                           const run_ctx& R, run_state& st, const warp_tables& T) {
+  if (PSG_GEN_RT) {  // one copy of the general path (less code in the step loop)
+    run_events<WIN, CUBE, -1, CWIDE, false>(tv, cv, R, st, T, wm);
+    return;
+  }
   const bool all = R.lo == 0 && R.hi == STEP_M && R.last_li < 0;  // warp-uniform
   if (!CWIDE && all && wm == WIN_FULL)
     run_events<WIN, CUBE, WIN_FULL, false, true>(tv, cv, R, st, T);
