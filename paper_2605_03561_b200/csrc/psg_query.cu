@@ -1320,6 +1320,11 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
   // to the aligned trace base b0 = b - d0 every step position is 32-bit
   const u64 b0 = b & ~static_cast<u64>(SOFF);
   const uint32_t d0 = static_cast<uint32_t>(b - b0), n32 = static_cast<uint32_t>(n_t);
+  const uint64_t* ts_b0 = p.tr.ts + b0;
+  const uint32_t* cx_b0 = p.tr.ctx + b0;
+  const unsigned long long* ts_lane = reinterpret_cast<const unsigned long long*>(ts_b0) + lane;
+  const unsigned int* cx_lane = reinterpret_cast<const unsigned int*>(cx_b0) + lane;
+  uint32_t pf_rel = 0xFFFFFFFFu;  // step (relative to b0) whose events sit in tv / cv (interleaved layout)
   u64 wspan = 0;  // time span added to the 32-bit pending window sums since the last fold
   uint32_t mybw = 0xFFFFFFFFu;  // lane j <= 2G: relative event index of boundary kb + j
 
@@ -1408,13 +1413,15 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
 #endif
       if (PSG_Q_PF_DIST > 0) {
         const bool pf = lane == 0 && static_cast<u64>(sr) + (PSG_Q_PF_DIST + 1) * STEP_M <= static_cast<u64>(n32) + d0;
-        prefetch_l2_lane0(p.tr.ts + s_abs + PSG_Q_PF_DIST * STEP_M, 8 * STEP_M, pf);
-        prefetch_l2_lane0(p.tr.ctx + s_abs + PSG_Q_PF_DIST * STEP_M, 4 * STEP_M, pf);
+        prefetch_l2_lane0(ts_b0 + sr + PSG_Q_PF_DIST * STEP_M, 8 * STEP_M, pf);
+        prefetch_l2_lane0(cx_b0 + sr + PSG_Q_PF_DIST * STEP_M, 4 * STEP_M, pf);
       }
       rot_src rs{};
       if constexpr (IL) {
       {
-        if (pf_pos != s_abs) {  // first step (or the pipeline did not run ahead): load now
+        // step positions relative to the aligned trace base b0 (32-bit), on
+        // per-trace lane base pointers: no 64-bit address arithmetic per step
+        if (pf_rel != sr) {  // first step (or the pipeline did not run ahead): load now
           u64 nf = 0;
           u64 t8[RM];
           load_step_il(p.tr, s_abs, lane, t8, cv, nf);
@@ -1423,11 +1430,11 @@ __global__ void __launch_bounds__(ONE ? 32 : PSG_WIDE_THREADS, ONE ? ((!WIN && !
           tv[RM] = nf;
         }
         const bool more = lim < n32 && (PSG_PIPE_CROSS || lim < E1);
-        const u64 nxt = b0 + ((lim + d0) & ~static_cast<uint32_t>(SOFF));
-        const u64 lp = more ? nxt : s_abs;
-        pf_pos = more ? nxt : ~0ull;
-        rs.ts = reinterpret_cast<const unsigned long long*>(p.tr.ts + lp) + lane;
-        rs.ctx = reinterpret_cast<const unsigned int*>(p.tr.ctx + lp) + lane;
+        const uint32_t nxt = (lim + d0) & ~static_cast<uint32_t>(SOFF);
+        const uint32_t lp = more ? nxt : sr;
+        pf_rel = more ? nxt : 0xFFFFFFFFu;
+        rs.ts = ts_lane + lp;
+        rs.ctx = cx_lane + lp;
       }
       } else {
       // software pipeline: this block step's events were loaded into registers
