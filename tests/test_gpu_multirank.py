@@ -27,7 +27,8 @@ def _gpus() -> int:
 
 
 @pytest.mark.parametrize("world,mode", [(2, "gen"), (3, "gen"), (2, "dup"), (3, "dup"), (2, "auto"),
-                                        (3, "auto_empty"), (2, "nccl"), (8, "nccl")])
+                                        (3, "auto_empty"), (2, "nccl"), (8, "nccl"), (2, "gen_units"),
+                                        (3, "dup_units")])
 def test_sharded_query_equals_single_context(tmp_path, world, mode):
     """mode "dup": one rank's traces make the optimistic pass 1 miss; the
     verdict is all-reduced, so every rank re-runs both passes exactly.
@@ -35,10 +36,13 @@ def test_sharded_query_equals_single_context(tmp_path, world, mode):
     (psg_comm_init); runs where the box has that many GPUs."""
     if mode == "nccl" and _gpus() < world:
         pytest.skip(f"NCCL data plane needs {world} GPUs (this box has {_gpus()})")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
+    if mode.endswith("_units"):  # every trace split into work units, on every rank and the single context
+        mode = mode[: -len("_units")]
+        env["PSG_UNIT_EVENTS"] = "300"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
            f"--nproc-per-node={world}", os.path.join(ROOT, "tests", "mp_shard_worker.py"),
            str(tmp_path), mode]
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     one = dict(np.load(tmp_path / "single.npz"))
