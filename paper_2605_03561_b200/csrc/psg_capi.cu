@@ -195,6 +195,10 @@ struct psg_context {
   uint8_t* pinned[3] = {nullptr, nullptr, nullptr};  // pageable-source staging ring
   cudaEvent_t pinned_ev[3] = {nullptr, nullptr, nullptr};
   cudaStream_t copy_stream = nullptr;  // H2D of pinned trace bodies (load_aos)
+  // side stream of a speculative single-rank query: the pass-1 verification
+  // runs there, concurrently with the cross-rank statistics
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_in = nullptr, side_out = nullptr;
   cudaEvent_t stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
   // nodes / topology
@@ -893,6 +897,12 @@ void psg_close(psg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->side_stream) {
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaStreamDestroy(ctx->side_stream);
+    cudaEventDestroy(ctx->side_in);
+    cudaEventDestroy(ctx->side_out);
+  }
   if (ctx->d2h_stream) {
     cudaStreamSynchronize(ctx->d2h_stream);
     cudaStreamDestroy(ctx->d2h_stream);
@@ -1620,6 +1630,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
     uint32_t k_cap = 0;  // K the statistics accumulators are laid out for
     for (;;) {
     const bool sp = spec && do_cube && !exact_bounds;
+    bool side_pending = false;
     PSG_CUDA(cudaMemsetAsync(qs, 0, QS_WORDS * sizeof(unsigned long long), s));
     if (do_cube) {
       compute_subtree(c, anchor);
@@ -1782,7 +1793,23 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       // the optimistic pass 1 (and its 32-bit cells) against the boundary
       // timestamps pass 2 recorded; a miss re-runs both passes exactly
       unsigned long long* v = qs + QS_VERIFY;
-      launch_verify_bounds(c->view(), c->d_cap_off.p, c->d_bts.p, c->d_nbounds.p, c->iter_count.p, v, s);
+      // speculative single-rank query: the verdict is read at the end, so the
+      // (latency-bound) verification overlaps k_cross_stats on a side stream
+      if (sp && !c->multi() && !std::getenv("PSG_NO_SIDE_STREAM")) {
+        if (!c->side_stream) {
+          PSG_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+          PSG_CUDA(cudaEventCreateWithFlags(&c->side_in, cudaEventDisableTiming));
+          PSG_CUDA(cudaEventCreateWithFlags(&c->side_out, cudaEventDisableTiming));
+        }
+        PSG_CUDA(cudaEventRecord(c->side_in, s));
+        PSG_CUDA(cudaStreamWaitEvent(c->side_stream, c->side_in, 0));
+        launch_verify_bounds(c->view(), c->d_cap_off.p, c->d_bts.p, c->d_nbounds.p, c->iter_count.p, v,
+                             c->side_stream);
+        PSG_CUDA(cudaEventRecord(c->side_out, c->side_stream));
+        side_pending = true;
+      } else {
+        launch_verify_bounds(c->view(), c->d_cap_off.p, c->d_bts.p, c->d_nbounds.p, c->iter_count.p, v, s);
+      }
       if (!sp) {
         if (c->multi()) c->allreduce(v, 1, ncclUint64, ncclMax);  // every rank re-runs together
         PSG_CUDA(cudaMemcpyAsync(&hq[QS_VERIFY], v, 8, cudaMemcpyDeviceToHost, s));
@@ -1876,6 +1903,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
       c->allreduce(qs + QS_CAP_MISS, 1, ncclUint64, ncclMax);
       c->group_end();
     }
+    if (side_pending) PSG_CUDA(cudaStreamWaitEvent(s, c->side_out, 0));
     PSG_CUDA(cudaEventRecord(c->ev[3], s));
     // the query's one host round trip: the status block
     PSG_CUDA(cudaMemcpyAsync(hq, qs, sizeof(hq), cudaMemcpyDeviceToHost, s));
