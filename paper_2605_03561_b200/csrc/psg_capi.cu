@@ -1645,6 +1645,7 @@ ps_status psg_query(psg_context* c, const psg_query_spec* q, psg_query_info* inf
         bp.ctx8 = c->ctx8_valid ? c->d_ctx8.p : nullptr;
         bp.sub_lo = static_cast<uint32_t>(c->cct_po.pre[anchor]);
         bp.sub_size = static_cast<uint32_t>(c->cct_po.size[anchor]);
+        bp.ctx7 = (c->n_ctx <= 128 && !std::getenv("PSG_NO_CTX7")) ? 1u : 0u;
         bp.contains = c->d_contains.p;
         bp.words = c->contains_words;
         bp.cap_off = c->d_cap_off.p;

@@ -110,6 +110,7 @@ struct bound_params {
   // byte range [sub_lo, sub_lo + sub_size) and membership is a SIMD compare
   const uint8_t* ctx8;
   uint32_t sub_lo, sub_size;
+  uint32_t ctx7;             // every preorder byte < 128 (n_ctx <= 128): the 3-op SWAR test
   const uint32_t* contains;  // [ceil(n_ctx/32)] bit c set iff ctx c is in the anchor subtree
   uint32_t words;
   const uint64_t* cap_off;   // [n+1] offsets of the per-trace boundary regions in bidx

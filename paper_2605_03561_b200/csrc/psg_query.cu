@@ -318,6 +318,8 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
   const u64 cap = p.cap_off[t + 1] - p.cap_off[t];
   const uint32_t lo4 = p.sub_lo * 0x01010101u, sz4 = p.sub_size * 0x01010101u;
   const bool sub_all = p.sub_size >= 256;
+  const uint32_t c7lo = (128u - p.sub_lo) * 0x01010101u;                // ctx7: bytes >= lo
+  const uint32_t c7hi = (128u - (p.sub_lo + p.sub_size)) * 0x01010101u;  // ctx7: bytes >= hi
 #define BTS(i) ldg64(p.tr.ts + (i))
   uint32_t* out = p.bidx + p.cap_off[t];
   uint64_t* out_ts = p.bts + p.cap_off[t];
@@ -376,7 +378,22 @@ __global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
       real = run_mask(lo, hi);
     }
     uint32_t inm = 0;
-    if (C8) {
+    if (C8 && p.ctx7) {
+      // every preorder byte x < 128 (the top bit is free): x + (128 - lo) has
+      // its top bit set iff x >= lo, x + (128 - hi) iff x >= hi, and neither
+      // sum carries into the next byte (bytes past the trace may carry, but
+      // only into later bytes, which are masked too) -- three ops per four
+      // events.  Two words' top bits, interleaved by a shift, fold into eight
+      // in-order bits with one high multiply (every partial product lands on
+      // its own bit: no carries).
+#pragma unroll
+      for (int q = 0; q < RR / 8; ++q) {
+        const uint32_t x0 = w[2 * q], x1 = w[2 * q + 1];
+        const uint32_t m0 = (x0 + c7lo) & ~(x0 + c7hi) & 0x80808080u;
+        const uint32_t m1 = (x1 + c7lo) & ~(x1 + c7hi) & 0x80808080u;
+        inm |= (__umulhi((m0 >> 4) | m1, 0x20408100u) & 0xFFu) << (8 * q);
+      }
+    } else if (C8) {
       // preorder bytes: in the subtree iff (b - lo) mod 256 < size, four
       // events per SIMD compare; the four 0xff/0 bytes fold into a nibble
       // (bit k of byte k, summed into the top byte by one multiply)
