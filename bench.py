@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--traces", type=int, default=N_TRACES)
     ap.add_argument("--iters", type=int, default=N_ITERS)
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_TRACES)
@@ -339,7 +339,28 @@ def main():
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         secs = [float(tt.item())]
+        # the e2e roofline: PCIe.  Pinned H2D rate measured here on 4 GiB of the
+        # same pinned buffer (one copy, CUDA events); the step cannot beat
+        # h2d_bytes / that rate (the D2H runs on the other direction)
+        hb = 4 << 30
+        if host.numel() >= hb:
+            dbuf = torch.empty(hb, dtype=torch.uint8, device="cuda")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            dbuf.copy_(host[:hb], non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            h2d_gbs = hb / (e0.elapsed_time(e1) / 1000.0) / 1e9
+            del dbuf
+        else:
+            h2d_gbs = None
+        h2d_b = int(events_local * 12 + 8 * (n_local + 1) + 12 * n_local)
+        e2e_bound = {"bound": "pcie_h2d", "h2d_gbs": h2d_gbs,
+                     "min_s_per_step": h2d_b / (h2d_gbs * 1e9) if h2d_gbs else None,
+                     "frac": (h2d_b / (h2d_gbs * 1e9)) / statistics.mean(secs) if h2d_gbs else None}
         e2e = {"value": total_events / statistics.mean(secs), "unit": "events/s",
+               "roofline": e2e_bound,
                "h2d_bytes_per_step": int(events_local * 12 + 8 * (n_local + 1) + 12 * n_local),
                "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                "s_per_step": statistics.mean(secs),

@@ -493,3 +493,20 @@ def test_flush_tail_columns_with_large_cells(gpu_ctx_factory):
     ctx.set_cct(parent)
     ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
     check_cube(ctx, tr, parent, 1)
+
+
+@pytest.mark.parametrize("n_ctx", [127, 128, 129, 256])
+def test_pass1_membership_at_ctx8_edges(gpu_ctx_factory, n_ctx):
+    """Pass 1 on the 1-byte preorder mirror at the edges of its two subtree
+    tests: the 3-op SWAR test (every preorder byte < 128: n_ctx <= 128, incl.
+    the root's subtree [0, 128) whose upper bound has no headroom) and the
+    SIMD-compare test above it (129..256 contexts); anchors at the first and
+    last preorder positions and a random one.  GPU == oracle bit for bit."""
+    rng = np.random.default_rng(1000 + n_ctx)
+    ctx = gpu_ctx_factory()
+    parent = random_cct(rng, n_ctx)
+    tr = random_traces(rng, 12, n_ctx, 3000, ctx_pool=n_ctx, dup_prob=0.3)
+    ctx.set_cct(parent)
+    ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
+    for anchor in sorted({0, 1, n_ctx - 1, int(rng.integers(0, n_ctx))}):
+        check_cube(ctx, tr, parent, anchor, stats=False)

@@ -45,7 +45,7 @@ marks = [("run_events (general path)", find("__device__ __forceinline__ void run
          ("step: fast-path setup", find("if (CUBE && kept && all && !cwide")),
          ("step: general setup", find("if (!done) {")),
          ("chunk flush (other)", find("// ---- phase 2")),
-         ("epilogue", find("if (!active) return;")),
+         ("epilogue", find("if (!active) return;", find("// ---- phase 2"))),
          ("end", len(src) + 1)]
 print(f"total {ti} warp inst = {ti / events * 256:.0f} per 256-event step; stall samples {ts}")
 for (name, a), (_, b) in zip(marks, marks[1:]):
