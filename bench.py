@@ -304,6 +304,12 @@ def main():
         except Exception as e:  # host RAM too small to pin it: say so in the line
             cube_pin, cube_err = None, f"{type(e).__name__}: {e}"
         off_pin = torch.empty(8 * n_local + 8, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint64)
+        # pinned buffers for the cube's dense per-trace outputs (iteration
+        # counts, block offsets, gap rows: ~0.1 GB at configs[1])
+        cmeta = {"iter_counts": torch.empty(4 * n_local + 4, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint32),
+                 "block_offset": torch.empty(8 * n_local + 8, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint64),
+                 "gap_incl": torch.empty(8 * n_local * nn + 8, dtype=torch.uint8, pin_memory=True).numpy().view(np.int64),
+                 "gap_excl": torch.empty(8 * n_local * nn + 8, dtype=torch.uint8, pin_memory=True).numpy().view(np.int64)}
         d2h = 0
 
         def e2e_step():
@@ -318,7 +324,7 @@ def main():
             w = ctx.window(wout)
             st = ctx.stats(1.0)
             ou = ctx.outliers(n_nodes)
-            cb = ctx.cube(with_cells=False)
+            cb = ctx.cube(with_cells=False, out=cmeta)
             cs = ctx.cube_stored(*cube_np, wait=False, off_out=off_pin) if cube_pin is not None else None
             return (sum(a.nbytes for a in w.values()) + sum(a.nbytes for a in st.values())
                     + sum(a.nbytes for a in ou.values())

@@ -236,17 +236,31 @@ class Context:
                                      _ptr(cx, C.c_uint32)))
         return {"has": has, "ts": ts, "ctx": cx}
 
-    def cube(self, with_cells: bool = True) -> dict:
+    def cube(self, with_cells: bool = True, out: Optional[dict] = None) -> dict:
+        """The dense cube (reference layout, itermodel.hpp:97-101).  `out` may
+        supply host arrays (e.g. views of pinned buffers, for a fast copy-out)
+        for "iter_counts", "block_offset", "gap_incl" and "gap_excl" (at least
+        n_traces / n_kept / n_kept * n_nodes entries; views of their leading
+        parts are returned)."""
         info = self.info
         n = self.shard()["n_traces"]
         nn, kept, cells = info["n_nodes"], info["n_kept"], info["n_cells"]
+        out = out or {}
+
+        def arr(key, size, dt):
+            a = out.get(key)
+            if a is None:
+                return np.empty(size, dt)
+            assert a.dtype == dt and a.size >= size and a.flags.c_contiguous, key
+            return a.reshape(-1)[:size]
+
         node_ids = np.empty(nn, np.uint32)
-        ic = np.empty(n, np.uint32)
-        bo = np.empty(kept, np.uint64)
+        ic = arr("iter_counts", n, np.uint32)
+        bo = arr("block_offset", kept, np.uint64)
         incl = np.empty(cells, np.int64) if with_cells else None
         excl = np.empty(cells, np.int64) if with_cells else None
-        gi = np.empty(kept * nn, np.int64)
-        ge = np.empty(kept * nn, np.int64)
+        gi = arr("gap_incl", kept * nn, np.int64)
+        ge = arr("gap_excl", kept * nn, np.int64)
         check(self.lib.psg_get_cube(self.h, _ptr(node_ids, C.c_uint32), _ptr(ic, C.c_uint32),
                                     _ptr(bo, C.c_uint64), _ptr(incl, C.c_int64),
                                     _ptr(excl, C.c_int64), _ptr(gi, C.c_int64),
