@@ -75,6 +75,16 @@ ps_status psg_set_cct(psg_context* ctx, const uint32_t* parent, uint32_t n_ctx);
 ps_status psg_load_traces_aos(psg_context* ctx, const void* body, uint64_t n_events,
                               const uint64_t* event_off, const uint32_t* profile_ids,
                               const uint64_t* t_end_ns, uint32_t n_traces);
+
+/* Starts the host->device copy of the first staging chunks (up to 1.5 GB) of
+ * the NEXT psg_load_traces_aos call's body while the device works on the
+ * current traces (PCIe is otherwise idle during a query): call it after
+ * loading, before querying.  Only pinned bodies are prefetched (pageable ones:
+ * a no-op).  The bytes are read at prefetch time; a later
+ * psg_load_traces_aos with the same body pointer and n_events uses them, any
+ * other staging user drops them.  No reference counterpart: a pipelining
+ * hint under the drop-in of store.cpp:678-692 / ingest.cpp:178-208. */
+ps_status psg_prefetch_aos(psg_context* ctx, const void* body, uint64_t n_events);
 /* The mmap reader path: opens <dir>/meta.bin + trace.db (format store.hpp:5-23)
  * and loads the traces whose profile id is listed (NULL = every trace),
  * setting the CCT and the rank->host mapping from meta.bin as well. */

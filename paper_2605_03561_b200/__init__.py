@@ -103,6 +103,13 @@ class Context:
         check(self.lib.psg_load_traces_aos(self.h, C.c_void_p(addr), n_ev, _ptr(off, C.c_uint64),
                                            _ptr(pid, C.c_uint32), _ptr(te, C.c_uint64), len(pid)))
 
+    def prefetch_aos(self, body, n_events: int):
+        """Start copying the first staging chunks of the next load_aos(body, ...)
+        (same body, n_events events) while the device works on the current
+        traces; pinned bodies only (else a no-op)."""
+        addr = body if isinstance(body, int) else (body.ctypes.data if n_events else 0)
+        check(self.lib.psg_prefetch_aos(self.h, C.c_void_p(addr), int(n_events)))
+
     def load_trace_db(self, path: str, pids=None):
         if pids is None:
             check(self.lib.psg_load_trace_db(self.h, path.encode(), None, 0))

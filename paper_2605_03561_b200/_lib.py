@@ -102,6 +102,7 @@ _SIGS = {
     "psg_comm_init_host": (C.c_int, [P, C.c_int, C.c_int, ALLREDUCE_FN, P]),
     "psg_set_cct": (C.c_int, [P, U32P, C.c_uint32]),
     "psg_load_traces_aos": (C.c_int, [P, P, C.c_uint64, U64P, U32P, U64P, C.c_uint32]),
+    "psg_prefetch_aos": (C.c_int, [P, P, C.c_uint64]),
     "psg_load_trace_db": (C.c_int, [P, C.c_char_p, U32P, C.c_uint32]),
     "psg_generate_iterative": (C.c_int, [P, C.POINTER(IterScenario), C.c_uint32, C.c_uint32]),
     "psg_set_nodes": (C.c_int, [P, U32P, C.c_uint32, U32P, U32P]),

@@ -195,6 +195,11 @@ struct psg_context {
   uint8_t* pinned[3] = {nullptr, nullptr, nullptr};  // pageable-source staging ring
   cudaEvent_t pinned_ev[3] = {nullptr, nullptr, nullptr};
   cudaStream_t copy_stream = nullptr;  // H2D of pinned trace bodies (load_aos)
+  // psg_prefetch_aos: the first staging chunks of the NEXT pinned load, copied
+  // while the device works on the current one (pf_chunks chunks of pf_body)
+  const uint8_t* pf_body = nullptr;
+  uint64_t pf_events = 0;
+  int pf_chunks = 0;
   // side stream of a speculative single-rank query: the pass-1 verification
   // runs there, concurrently with the cross-rank statistics
   cudaStream_t side_stream = nullptr;
@@ -300,6 +305,7 @@ struct psg_context {
       if (pinned_ev[i]) cudaEventDestroy(pinned_ev[i]);
       if (pinned[i]) cudaFreeHost(pinned[i]);
     }
+    if (copy_stream) cudaStreamSynchronize(copy_stream);  // a prefetch into d_stage
     for (auto& e : stage_ev)
       if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -517,10 +523,28 @@ void ensure_pinned_ring(psg_context* c) {
   }
 }
 
+constexpr uint64_t kPinnedChunkEvents = 4ull << 24;  // 64 Mi events = 768 MB per staging chunk
+
+void ensure_copy_stream(psg_context* c) {
+  if (c->copy_stream) return;
+  PSG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : c->stage_ev) PSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+// Every other user of the staging buffer first lets an unclaimed prefetch land
+// (its copies may still be writing there) and forgets it.
+void drop_prefetch(psg_context* c) {
+  if (c->pf_chunks > 0) PSG_CUDA(cudaStreamSynchronize(c->copy_stream));
+  c->pf_body = nullptr;
+  c->pf_events = 0;
+  c->pf_chunks = 0;
+}
+
 void load_aos_pageable(psg_context* c, const uint8_t* body, uint64_t n_events) {
   constexpr uint64_t kBufEv = kRingEvents, kBufBytes = kRingBytes;
   constexpr int kBufs = kRingBufs;
   ensure_pinned_ring(c);
+  drop_prefetch(c);
   uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, 2 * kBufBytes));
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const unsigned nthreads = std::min(8u, hw);
@@ -561,6 +585,7 @@ void load_aos_file(psg_context* c, const std::string& path, uint64_t offset, uin
     int fd;
     ~fd_closer() { ::close(fd); }
   } closer{fd};
+  drop_prefetch(c);
   uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, 2 * kRingBytes));
   const unsigned nthreads = std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
   uint64_t done = 0;
@@ -612,30 +637,37 @@ void load_aos(psg_context* c, const uint8_t* body, uint64_t n_events) {
   if (attr.type != cudaMemoryTypeHost && attr.type != cudaMemoryTypeDevice &&
       attr.type != cudaMemoryTypeManaged)
     return load_aos_pageable(c, body, n_events);
-  const uint64_t chunk_ev = 4ull << 24;  // 64 Mi events = 768 MB per chunk
+  const uint64_t chunk_ev = kPinnedChunkEvents;
   const uint64_t chunk_bytes = chunk_ev * 12;
-  uint8_t* stage = c->d_stage.ensure(std::min<uint64_t>(2 * chunk_bytes, n_events * 12 + 64));
+  // chunks a psg_prefetch_aos of this very body already put in flight
+  const int pf = (c->pf_body == body && c->pf_events == n_events) ? c->pf_chunks : 0;
+  if (!pf) drop_prefetch(c);
+  c->pf_body = nullptr;
+  c->pf_chunks = 0;
+  uint8_t* stage = pf ? c->d_stage.p
+                      : c->d_stage.ensure(std::min<uint64_t>(2 * chunk_bytes, n_events * 12 + 64));
   const bool two = c->d_stage.n >= 2 * chunk_bytes;
   // H2D copies on their own stream, transposes on the context's stream: copy
   // i + 1 runs while transpose i does (two staging slots, events in between),
   // so the copy engine stays busy at the PCIe rate
-  if (!c->copy_stream) {
-    PSG_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    for (auto& e : c->stage_ev) PSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
+  ensure_copy_stream(c);
   cudaEvent_t* copied = c->stage_ev;      // [2] slot filled
   cudaEvent_t* consumed = c->stage_ev + 2;  // [2] slot transposed
-  PSG_CUDA(cudaEventRecord(consumed[0], c->stream));  // earlier work on the staging buffer
-  PSG_CUDA(cudaEventRecord(consumed[1], c->stream));
+  if (!pf) {
+    PSG_CUDA(cudaEventRecord(consumed[0], c->stream));  // earlier work on the staging buffer
+    PSG_CUDA(cudaEventRecord(consumed[1], c->stream));
+  }
   uint64_t done = 0;
   int slot = 0;
-  while (done < n_events) {
+  for (int i = 0; done < n_events; ++i) {
     uint64_t ev = std::min(chunk_ev, n_events - done);
     const int sl = two ? slot : 0;
     uint8_t* dst = stage + sl * chunk_bytes;
-    PSG_CUDA(cudaStreamWaitEvent(c->copy_stream, consumed[sl], 0));
-    PSG_CUDA(cudaMemcpyAsync(dst, body + done * 12, ev * 12, cudaMemcpyHostToDevice, c->copy_stream));
-    PSG_CUDA(cudaEventRecord(copied[sl], c->copy_stream));
+    if (i >= pf) {  // (the prefetch issued chunk i < pf into slot i, and recorded copied[i])
+      PSG_CUDA(cudaStreamWaitEvent(c->copy_stream, consumed[sl], 0));
+      PSG_CUDA(cudaMemcpyAsync(dst, body + done * 12, ev * 12, cudaMemcpyHostToDevice, c->copy_stream));
+      PSG_CUDA(cudaEventRecord(copied[sl], c->copy_stream));
+    }
     PSG_CUDA(cudaStreamWaitEvent(c->stream, copied[sl], 0));
     launch_aos_to_soa(dst, ev, c->d_ts.p + done, c->d_ctx.p + done, c->stream);
     PSG_CUDA(cudaEventRecord(consumed[sl], c->stream));
@@ -994,6 +1026,44 @@ ps_status psg_load_traces_aos(psg_context* c, const void* body, uint64_t n_event
   });
 }
 
+ps_status psg_prefetch_aos(psg_context* c, const void* body, uint64_t n_events) {
+  if (!c) return PS_E_INVALID_ARGUMENT;
+  return guarded([&] {
+    require(n_events == 0 || body, "body is required");
+    ensure_device(c);
+    drop_prefetch(c);
+    if (n_events == 0) return;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, body) != cudaSuccess) {
+      cudaGetLastError();
+      return;  // pageable memory: nothing to prefetch (psg_load_traces_aos stages it itself)
+    }
+    if (attr.type != cudaMemoryTypeHost) return;
+    const uint64_t chunk_ev = kPinnedChunkEvents, chunk_bytes = chunk_ev * 12;
+    uint8_t* stage = c->d_stage.ensure(std::min<uint64_t>(2 * chunk_bytes, n_events * 12 + 64));
+    const int slots = c->d_stage.n >= 2 * chunk_bytes ? 2 : 1;
+    ensure_copy_stream(c);
+    cudaEvent_t* copied = c->stage_ev;
+    cudaEvent_t* consumed = c->stage_ev + 2;
+    // the slots are free once the earlier transposes (and any other staging
+    // work on the context's stream) are done
+    PSG_CUDA(cudaEventRecord(consumed[0], c->stream));
+    PSG_CUDA(cudaEventRecord(consumed[1], c->stream));
+    const uint8_t* src = static_cast<const uint8_t*>(body);
+    int k = 0;
+    for (uint64_t done = 0; k < slots && done < n_events; ++k, done += chunk_ev) {
+      const uint64_t ev = std::min(chunk_ev, n_events - done);
+      PSG_CUDA(cudaStreamWaitEvent(c->copy_stream, consumed[k], 0));
+      PSG_CUDA(cudaMemcpyAsync(stage + k * chunk_bytes, src + done * 12, ev * 12, cudaMemcpyHostToDevice,
+                               c->copy_stream));
+      PSG_CUDA(cudaEventRecord(copied[k], c->copy_stream));
+    }
+    c->pf_body = src;
+    c->pf_events = n_events;
+    c->pf_chunks = k;
+  });
+}
+
 ps_status psg_set_nodes(psg_context* c, const uint32_t* node_of_trace, uint32_t n_nodes,
                         const uint32_t* node_rack, const uint32_t* node_chassis) {
   if (!c) return PS_E_INVALID_ARGUMENT;
@@ -1035,6 +1105,7 @@ void load_profiles_impl(psg_context* c, const uint8_t* records, const uint64_t* 
   cudaStream_t s = c->stream;
   PSG_CUDA(cudaMemcpyAsync(c->prof_off.ensure(n + 1), off.data(), 8ull * (n + 1), cudaMemcpyHostToDevice, s));
   PSG_CUDA(cudaMemcpyAsync(c->prof_pid.ensure(n + 1), pid, 4ull * n, cudaMemcpyHostToDevice, s));
+  drop_prefetch(c);
   uint8_t* stage = c->d_stage.ensure(n_rec * 14 + 16);
   if (n_rec)
     PSG_CUDA(cudaMemcpyAsync(stage, records, n_rec * 14, cudaMemcpyDefault, s));
@@ -2376,6 +2447,7 @@ ps_status psg_export_aos_range(psg_context* c, uint32_t t_lo, uint32_t t_hi, voi
     const uint64_t e0 = c->h_off[t_lo], e1 = c->h_off[t_hi];
     require(e1 == e0 || body != nullptr, "body is required");
     const uint64_t chunk_ev = 4ull << 24;
+    drop_prefetch(c);
     uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, chunk_ev * 12 + 64));
     // K1's inverse works on groups of 4 events from a 16-byte aligned start:
     // export from the aligned-down event and skip the head on the copy
@@ -2396,6 +2468,7 @@ ps_status psg_export_aos(psg_context* c, void* body) {
   return guarded([&] {
     ensure_device(c);
     const uint64_t chunk_ev = 4ull << 24;
+    drop_prefetch(c);
     uint8_t* stage = c->d_stage.ensure(std::max<uint64_t>(c->d_stage.n, chunk_ev * 12));
     for (uint64_t done = 0; done < c->n_events; done += chunk_ev) {
       uint64_t ev = std::min(chunk_ev, c->n_events - done);

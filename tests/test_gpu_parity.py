@@ -510,3 +510,54 @@ def test_pass1_membership_at_ctx8_edges(gpu_ctx_factory, n_ctx):
     ctx.load_aos(to_aos(tr), tr["off"], tr["pid"], tr["t_end"])
     for anchor in sorted({0, 1, n_ctx - 1, int(rng.integers(0, n_ctx))}):
         check_cube(ctx, tr, parent, anchor, stats=False)
+
+
+def test_prefetched_loads_equal_plain_loads(gpu_ctx_factory):
+    """psg_prefetch_aos (the e2e pipelining hint): a pinned load whose first two
+    768 MB staging chunks were copied while a query ran equals the plain load
+    (a third chunk follows the prefetched two: 150 M events); a prefetch of
+    another length, or one followed by another staging user (export), is
+    dropped and the load is still exact.  Checked on the loaded events and on
+    a full query's window and cube."""
+    import torch
+    ctx = gpu_ctx_factory()
+    ctx.generate_iterative(scenarios.device_scenario(3000, 746, seed=6))  # 149.9 M events
+    n_ev = ctx.shard()["n_events"]
+    assert n_ev > 2 * (64 << 20)
+    idx = ctx.index()
+    host = torch.empty(n_ev * 12, dtype=torch.uint8, pin_memory=True)
+    ctx.export_aos(host.data_ptr())
+    parent = np.array([0xFFFFFFFF, 0] + [1] * 64 + [0], np.uint32)
+    ctx.set_cct(parent)
+    T = int(ctx.shard()["t_max"])
+
+    def run():
+        ctx.query(Q_WINDOW | Q_CUBE | Q_STATS, t0=T // 4, t1=3 * T // 4, anchor=1)
+        return ctx.window(), ctx.cube()
+
+    ctx.load_aos(host.data_ptr(), idx["off"], idx["pid"], idx["t_end"])
+    want_ev = ctx.traces()
+    want_w, want_c = run()
+    # prefetched (query in between), then loaded
+    ctx.prefetch_aos(host.data_ptr(), n_ev)
+    run()
+    ctx.load_aos(host.data_ptr(), idx["off"], idx["pid"], idx["t_end"])
+    got = ctx.traces()
+    for k in ("ts", "ctx", "off"):
+        assert np.array_equal(got[k], want_ev[k]), k
+    w, c = run()
+    for k in WINDOW_KEYS:
+        assert np.array_equal(w[k], want_w[k]), k
+    for k in ("iter_counts", "incl", "excl", "gap_incl"):
+        assert np.array_equal(c[k], want_c[k]), k
+    # a prefetch that does not match the load, and one another staging user drops
+    ctx.prefetch_aos(host.data_ptr(), n_ev - 5)
+    ctx.load_aos(host.data_ptr(), idx["off"], idx["pid"], idx["t_end"])
+    assert np.array_equal(ctx.traces()["ts"], want_ev["ts"])
+    ctx.prefetch_aos(host.data_ptr(), n_ev)
+    out = torch.empty(n_ev * 12, dtype=torch.uint8, pin_memory=True)
+    ctx.export_aos(out.data_ptr())
+    assert torch.equal(out, host)
+    ctx.load_aos(host.data_ptr(), idx["off"], idx["pid"], idx["t_end"])
+    got = ctx.traces()
+    assert np.array_equal(got["ts"], want_ev["ts"]) and np.array_equal(got["ctx"], want_ev["ctx"])
