@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--iters", type=int, default=N_ITERS)
     ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-prefetch", action="store_true", help="e2e without psg_prefetch_aos (A/B)")
+    ap.add_argument("--prefetch", action="store_true",
+                    help="e2e with psg_prefetch_aos (A/B: neutral, profiles/r2o_ab_e2e_prefetch.txt)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_TRACES)
     return ap.parse_args()
@@ -321,9 +322,9 @@ def main():
             # the last one landed (ctx.wait_copies below).
             ctx.load_aos(host.data_ptr(), off, pids, tend)
             ctx.set_nodes(node_of, n_nodes, 4000 + node // 32, (node // 8) % 4)
-            # the next step's first 1.5 GB of trace bytes cross PCIe while this
-            # step's query and copy-out run (the H2D link is idle otherwise)
-            if not args.no_prefetch:
+            # optionally the next step's first 1.5 GB of trace bytes cross PCIe
+            # while this step's query and copy-out run (measured neutral)
+            if args.prefetch:
                 ctx.prefetch_aos(host.data_ptr(), events_local)
             ctx.query(**q)
             w = ctx.window(wout)

@@ -1,5 +1,5 @@
 #!/usr/bin/env bash
-# A/B of bench.py e2e flags in one box: ARGSETS="-;--no-prefetch" (';'-separated,
+# A/B of bench.py e2e flags in one box: ARGSETS="-;--prefetch" (';'-separated,
 # "-" = none), REPS rounds interleaved; prints e2e s/step and the H2D rate.
 cd "${GRAFT_REPO_ROOT:-$(pwd)}"; mkdir -p gpurun_out
 : > gpurun_out/ab_e2e.txt
