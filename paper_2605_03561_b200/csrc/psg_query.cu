@@ -72,6 +72,13 @@ typedef unsigned __int128 u128;
 #ifndef PSG_B_MINB
 #define PSG_B_MINB 1  // k_bounds: resident 256-thread CTAs per SM the registers must allow
 #endif
+#ifndef PSG_B8_MINB
+#define PSG_B8_MINB 8  // k_bounds, optimistic 1-byte-mirror pass: 8 CTAs (64 warps) per SM at 32
+                       // registers, no spills (A/B: 0.862 -> 0.797 ms; 6 CTAs at 40: 0.824)
+#endif
+#ifndef PSG_X_MINB
+#define PSG_X_MINB 2  // k_cross_stats: resident 512-thread CTAs per SM the registers must allow
+#endif
 #ifndef PSG_X_U
 #define PSG_X_U 16  // k_cross_stats: 32-bit cell pairs in flight per thread (the batch size)
 #endif
@@ -302,7 +309,7 @@ __device__ __forceinline__ uint32_t run_mask(int lo, int hi) {
 }
 
 template <bool SMALL, bool EXACT, bool C8>  // SMALL: <= 128 contexts, membership bits live in registers
-__global__ void __launch_bounds__(256, PSG_B_MINB) k_bounds(bound_params p) {
+__global__ void __launch_bounds__(256, (C8 && !EXACT) ? PSG_B8_MINB : PSG_B_MINB) k_bounds(bound_params p) {
   typedef bounds_geom<C8> GM;
   constexpr int RR = GM::R, STEP = GM::STEP, NV = GM::NV;
   extern __shared__ uint32_t s_bits[];
@@ -2065,7 +2072,7 @@ struct cell_acc {
 };
 
 template <typename CELL>
-__global__ void __launch_bounds__(512, 2) k_cross_stats(const CELL* __restrict__ incl,
+__global__ void __launch_bounds__(512, PSG_X_MINB) k_cross_stats(const CELL* __restrict__ incl,
                                                         const uint64_t* __restrict__ kept_bo,
                                                         uint32_t n_kept, uint32_t nn, uint32_t nnp,
                                                         uint32_t K, uint32_t kt, uint32_t per_tile,
